@@ -1,0 +1,184 @@
+/*
+ * dgkr_b200 — C ABI of the B200 (sm_100a) Sisu distributed-GKR prover.
+ *
+ * This is the drop-in boundary for the reference's prover hot path
+ * (/root/reference/proj/include/dgkr, a header-only C++20 library with no
+ * FFI of its own). Every entry point below replaces one reference call; the
+ * citation after each names it. Proof bytes, transcript state and roots are
+ * bit-identical to the reference on the same inputs.
+ *
+ * Conventions
+ *  - Field elements cross as canonical little-endian bytes of width
+ *    ceil(bits(p)/8) (field.hpp:159-187): 32 B for BN254, 8 B for
+ *    Goldilocks, 1 B for p = 97. Non-canonical inputs are rejected with
+ *    DGKR_INVALID_ARGUMENT, as FieldElement::from_bytes throws
+ *    std::invalid_argument.
+ *  - A transcript is the caller-owned value {state, draws}: exactly the
+ *    private state of dgkr::Transcript (transcript.hpp:127-129). Provers
+ *    read and advance it in place.
+ *  - Status codes mirror the reference's exception types so a C++ shim can
+ *    rethrow the same type: INVALID_ARGUMENT -> std::invalid_argument,
+ *    LOGIC_ERROR -> std::logic_error, DOMAIN_ERROR -> std::domain_error,
+ *    OUT_OF_RANGE -> std::out_of_range. dgkr_last_error() returns the
+ *    message (thread-local).
+ *  - Output buffers: (out, cap, *len). *len is always set to the required
+ *    size; DGKR_CAPACITY is returned when cap is too small.
+ *  - No CPU fallback: provers run on the GPU or fail with DGKR_CUDA_ERROR.
+ */
+#ifndef DGKR_B200_H
+#define DGKR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGKR_OK 0
+#define DGKR_INVALID_ARGUMENT 1
+#define DGKR_LOGIC_ERROR 2
+#define DGKR_DOMAIN_ERROR 3
+#define DGKR_OUT_OF_RANGE 4
+#define DGKR_CUDA_ERROR 5
+#define DGKR_UNSUPPORTED 6
+#define DGKR_CAPACITY 7
+#define DGKR_COMM_ERROR 8
+
+typedef struct dgkr_ctx dgkr_ctx;
+typedef struct dgkr_field dgkr_field;
+typedef struct dgkr_circuit dgkr_circuit;
+
+/* Transcript value: replaces the private members of dgkr::Transcript
+ * (transcript.hpp:127-129). */
+typedef struct dgkr_transcript {
+    uint8_t state[32];
+    uint64_t draws;
+} dgkr_transcript;
+
+/* Per-call profile (filled when dgkr_ctx_set_profile(ctx, 1)). */
+typedef struct dgkr_profile {
+    uint64_t launches;          /* kernels launched by this library */
+    uint64_t round_launches;    /* fused fold+round kernels */
+    double round_ms;            /* CUDA-event time inside fused round kernels */
+    uint64_t round_bytes;       /* algorithmic bytes moved by round kernels */
+    uint64_t round_mults;       /* algorithmic field multiplications in round kernels */
+    double bookkeep_ms;         /* phase-1 + phase-2 bookkeeping kernels */
+    double evaluate_ms;         /* circuit evaluation kernels */
+    double total_ms;            /* wall time of the call */
+    double host_transcript_ms;  /* serial host SHA-256 transcript work */
+    double output_absorb_ms;    /* part of the above: absorbing the output layer */
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t rounds;            /* sum-check rounds (host round trips) */
+} dgkr_profile;
+
+const char* dgkr_last_error(void);
+int dgkr_abi_version(void);
+
+/* ---- field (field.hpp:23-80) ------------------------------------------- */
+/* modulus: little-endian bytes. The GPU path supports odd p < 2^254
+ * (BN254 Fr is specialised; other moduli take the runtime-modulus path). */
+int dgkr_field_create(const uint8_t* modulus_le, size_t len, dgkr_field** out);
+void dgkr_field_destroy(dgkr_field* f);
+size_t dgkr_field_width(const dgkr_field* f);   /* field.hpp:67 byte_width() */
+size_t dgkr_field_bits(const dgkr_field* f);    /* field.hpp:66 bits() */
+
+/* ---- transcript (transcript.hpp:19-83); host-side, needs no GPU ---------- */
+int dgkr_transcript_init(const dgkr_field* f, const char* label, dgkr_transcript* t);      /* ctor :19-28 */
+int dgkr_transcript_absorb_bytes(const dgkr_field* f, dgkr_transcript* t, const uint8_t* data, size_t n); /* :32-37 */
+int dgkr_transcript_absorb_u64(const dgkr_field* f, dgkr_transcript* t, uint64_t v);      /* :44-48 */
+int dgkr_transcript_absorb_elems(const dgkr_field* f, dgkr_transcript* t, const uint8_t* elems, size_t n); /* :39-42 */
+int dgkr_transcript_challenge(const dgkr_field* f, dgkr_transcript* t, uint8_t* out);     /* :52-68 */
+int dgkr_transcript_challenge_index(const dgkr_field* f, dgkr_transcript* t, uint64_t bound, uint64_t* out); /* :71-83 */
+/* raw SHA-256 (sha256.hpp:138-151), exposed for tests */
+int dgkr_sha256(const uint8_t* data, size_t n, uint8_t* out32);
+int dgkr_sha256_has_shani(void);
+
+/* ---- context -------------------------------------------------------------- */
+int dgkr_ctx_create(int device, dgkr_ctx** out);
+void dgkr_ctx_destroy(dgkr_ctx* ctx);
+int dgkr_ctx_set_profile(dgkr_ctx* ctx, int on);
+int dgkr_ctx_get_profile(dgkr_ctx* ctx, dgkr_profile* out);   /* profile of the last call */
+int dgkr_ctx_device_info(dgkr_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- product sum-check -----------------------------------------------------
+ * prove_product_sum (sumcheck.hpp:226-241) over n_pairs pairs of 2^vars
+ * tables given as f0,g0,f1,g1,... Proof = SumcheckProof::to_bytes
+ * (sumcheck.hpp:51-61). */
+int dgkr_prove_product_sum(dgkr_ctx* ctx, const dgkr_field* f, size_t n_pairs, size_t vars, const uint8_t* tables,
+                           dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+
+/* ---- layer sum-check -------------------------------------------------------
+ * prove_layer_sum (sumcheck.hpp:342-448). wire_meta: n_wires x {is_mul,
+ * x_slot, y_slot}; wire_idx: n_wires x {x_index, y_index}; wire_weights:
+ * n_wires field elements. Proof = SumcheckProof::to_bytes; the x/y points
+ * are written to x_point/y_point (side_vars elements each) when non-NULL. */
+int dgkr_prove_layer_sum(dgkr_ctx* ctx, const dgkr_field* f, size_t side_vars, size_t n_slots,
+                         const uint8_t* slot_tables, size_t n_wires, const uint32_t* wire_meta,
+                         const uint64_t* wire_idx, const uint8_t* wire_weights, const uint8_t* claimed,
+                         dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len, uint8_t* x_point,
+                         uint8_t* y_point);
+
+/* ---- circuits + GKR ----------------------------------------------------------
+ * Flat layout of a GeneralCircuit (circuit.hpp:63):
+ *   layer_gate_start[depth+1]  cumulative gate counts (gates of layer li, 1-based,
+ *                              are [layer_gate_start[li-1], layer_gate_start[li]))
+ *   gate_nested_start[G+1]     cumulative nested-gate counts per gate
+ *   nested[5*N]                {kind (0 add, 1 mul), left_layer, left_gate,
+ *                               right_layer, right_gate} per nested gate
+ *   min_padded[depth+1]        reserve_padding() floors, or NULL
+ * n_copies > 1 describes a data-parallel circuit (Sisu): the given circuit is
+ * a sub-circuit replicated n_copies times, copy c of layer l occupying gates
+ * [c*size_l, (c+1)*size_l) — the copy index is the high variables, as in
+ * cluster.hpp:182-189. Requires n_copies and every sub layer size to be
+ * powers of two. Validation follows GeneralCircuit::validate
+ * (circuit.hpp:103-152); violations fail with DGKR_INVALID_ARGUMENT. */
+int dgkr_circuit_create(dgkr_ctx* ctx, uint32_t input_size, uint32_t depth, const uint64_t* layer_gate_start,
+                        const uint64_t* gate_nested_start, const uint32_t* nested, const uint64_t* min_padded,
+                        uint32_t n_copies, dgkr_circuit** out);
+void dgkr_circuit_destroy(dgkr_circuit* c);
+/* padded size of the output layer of the (replicated) circuit */
+size_t dgkr_circuit_output_size(const dgkr_circuit* c);
+/* GeneralCircuit::evaluate (circuit.hpp:164-193): padded output layer */
+int dgkr_circuit_evaluate(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const uint8_t* inputs,
+                          uint8_t* outputs, size_t cap, size_t* len);
+/* gkr_prove (gkr.hpp:182-244). inputs: n_copies * input_size elements.
+ * Proof bytes ("GkrProof layout"; the reference has no serializer,
+ * gkr.hpp:86-95):
+ *   u32 n_out || claimed_outputs || u32 n_layers ||
+ *   per layer (output first): u32 n_alphas || alphas || u32 len || SumcheckProof::to_bytes */
+int dgkr_gkr_prove(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const uint8_t* inputs, dgkr_transcript* t,
+                   uint8_t* proof, size_t cap, size_t* len);
+size_t dgkr_gkr_proof_bound(const dgkr_circuit* c, const dgkr_field* f);
+
+/* ---- polynomial commitment (pcs.hpp) ------------------------------------------ */
+/* pcs::commit (pcs.hpp:105-113): rows x cols row-major matrix -> Merkle root */
+int dgkr_pcs_commit(dgkr_ctx* ctx, const dgkr_field* f, size_t rows, size_t cols, const uint8_t* data,
+                    uint8_t* root32);
+/* pcs::open (pcs.hpp:212-254): Opening::to_bytes (pcs.hpp:135-156) */
+int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, size_t rows, size_t cols, const uint8_t* data,
+                  const uint8_t* r, size_t r_len, size_t spot_checks, dgkr_transcript* t, uint8_t* out, size_t cap,
+                  size_t* len);
+
+/* ---- distributed runtime (cluster.hpp), N workers in one call -------------------
+ * shard_pairs + dist_sumcheck (cluster.hpp:190-320) on full tables; proof
+ * bytes equal the reference's, TrafficStats::to_json().dump() written to
+ * traffic_json (phase "sumcheck"). */
+int dgkr_dist_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, size_t n_workers, size_t n_pairs, size_t vars,
+                       const uint8_t* tables, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len,
+                       char* traffic_json, size_t json_cap);
+/* DistPc commit + open (cluster.hpp:336-412): K roots (32 B each), cluster
+ * openings as u32 len || Opening::to_bytes, combined value, and traffic json
+ * (phases "commit", "open"). n_clusters = 0 selects ClusterTopology::plan's
+ * automatic K. */
+int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, size_t n_workers, size_t n_clusters, size_t row_vars,
+                const uint8_t* rows, const uint8_t* r, size_t r_len, size_t spot_checks, uint8_t* roots_out,
+                size_t* n_roots, uint8_t* open_out, size_t cap, size_t* open_len, uint8_t* combined_out,
+                char* traffic_json, size_t json_cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DGKR_B200_H */

@@ -1,0 +1,11 @@
+"""B200 (sm_100a) prover for the Sisu distributed-GKR hot path (arXiv 2404.10404).
+
+The product is the CUDA library ``libdgkr_b200.so`` behind the C ABI in
+``include/dgkr_b200.h``; this package is its Python mirror of the reference
+API (``/root/reference/proj/include/dgkr``). See DESIGN.md.
+"""
+from .prover import (BN254_P, GOLDILOCKS_P, Circuit, Context, Field, Transcript, dist_sumcheck, distpc,
+                     gkr_prove, pcs_commit, pcs_open, prove_layer_sum, prove_product_sum, sha256)
+
+__all__ = ["BN254_P", "GOLDILOCKS_P", "Circuit", "Context", "Field", "Transcript", "dist_sumcheck", "distpc",
+           "gkr_prove", "pcs_commit", "pcs_open", "prove_layer_sum", "prove_product_sum", "sha256"]

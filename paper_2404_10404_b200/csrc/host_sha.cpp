@@ -1,0 +1,142 @@
+// Host SHA-256 compression: SHA-NI (x86 SHA extensions) when available, a
+// portable FIPS 180-4 loop otherwise. The serial transcript chain
+// (transcript.hpp:32-37: one SHA-256 of state||element per absorb) is the
+// Amdahl term bit-exactness imposes, so it gets the fastest host path.
+#include <cpuid.h>
+#include <cstdlib>
+#include <immintrin.h>
+
+#include "host_core.hpp"
+
+namespace dgkr_b200 {
+
+namespace {
+
+const std::uint32_t kK[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+
+inline std::uint32_t rotr(std::uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+
+void compress_portable(std::uint32_t st[8], const std::uint8_t* p, std::size_t nblocks) {
+    for (; nblocks--; p += 64) {
+        std::uint32_t w[64];
+        for (int i = 0; i < 16; ++i)
+            w[i] = (std::uint32_t(p[4 * i]) << 24) | (std::uint32_t(p[4 * i + 1]) << 16) |
+                   (std::uint32_t(p[4 * i + 2]) << 8) | std::uint32_t(p[4 * i + 3]);
+        for (int i = 16; i < 64; ++i) {
+            const std::uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+            const std::uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+            w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+        }
+        std::uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+        for (int i = 0; i < 64; ++i) {
+            const std::uint32_t t1 = h + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + kK[i] + w[i];
+            const std::uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+            h = g;
+            g = f;
+            f = e;
+            e = d + t1;
+            d = c;
+            c = b;
+            b = a;
+            a = t1 + t2;
+        }
+        st[0] += a;
+        st[1] += b;
+        st[2] += c;
+        st[3] += d;
+        st[4] += e;
+        st[5] += f;
+        st[6] += g;
+        st[7] += h;
+    }
+}
+
+__attribute__((target("sha,sse4.1,ssse3"))) void compress_shani(std::uint32_t st[8], const std::uint8_t* p,
+                                                                 std::size_t nblocks) {
+    const __m128i bswap = _mm_set_epi64x(0x0c0d0e0f08090a0bULL, 0x0405060700010203ULL);
+    __m128i tmp = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&st[0]));  // DCBA
+    __m128i s1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&st[4]));   // HGFE
+    tmp = _mm_shuffle_epi32(tmp, 0xB1);                                       // CDAB
+    s1 = _mm_shuffle_epi32(s1, 0x1B);                                         // EFGH
+    __m128i s0 = _mm_alignr_epi8(tmp, s1, 8);                                 // ABEF
+    s1 = _mm_blend_epi16(s1, tmp, 0xF0);                                      // CDGH
+    for (; nblocks--; p += 64) {
+        const __m128i abef = s0, cdgh = s1;
+        __m128i w[16];
+        for (int g = 0; g < 4; ++g)
+            w[g] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(p + 16 * g)), bswap);
+        for (int g = 4; g < 16; ++g) {
+            // W[t] = sigma1(W[t-2]) + W[t-7] + sigma0(W[t-15]) + W[t-16]
+            __m128i x = _mm_sha256msg1_epu32(w[g - 4], w[g - 3]);
+            x = _mm_add_epi32(x, _mm_alignr_epi8(w[g - 1], w[g - 2], 4));
+            w[g] = _mm_sha256msg2_epu32(x, w[g - 1]);
+        }
+        for (int g = 0; g < 16; ++g) {
+            __m128i m = _mm_add_epi32(w[g], _mm_loadu_si128(reinterpret_cast<const __m128i*>(&kK[4 * g])));
+            s1 = _mm_sha256rnds2_epu32(s1, s0, m);
+            m = _mm_shuffle_epi32(m, 0x0E);
+            s0 = _mm_sha256rnds2_epu32(s0, s1, m);
+        }
+        s0 = _mm_add_epi32(s0, abef);
+        s1 = _mm_add_epi32(s1, cdgh);
+    }
+    tmp = _mm_shuffle_epi32(s0, 0x1B);       // FEBA
+    s1 = _mm_shuffle_epi32(s1, 0xB1);        // DCHG
+    s0 = _mm_blend_epi16(tmp, s1, 0xF0);     // DCBA
+    s1 = _mm_alignr_epi8(s1, tmp, 8);        // HGFE
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(&st[0]), s0);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(&st[4]), s1);
+}
+
+bool detect_shani() {
+    unsigned a, b, c, d;
+    if (!__get_cpuid_count(7, 0, &a, &b, &c, &d)) return false;
+    const bool sha = (b >> 29) & 1;
+    if (!__get_cpuid(1, &a, &b, &c, &d)) return false;
+    const bool sse41 = (c >> 19) & 1, ssse3 = (c >> 9) & 1;
+    return sha && sse41 && ssse3;
+}
+
+const bool g_shani = detect_shani() && !std::getenv("DGKR_NO_SHANI");
+
+// Padding block for a 64-byte message (bit length 512).
+const std::uint8_t kPad64[64] = {0x80, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,
+                                 0,    0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,
+                                 0,    0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0x02, 0x00};
+
+}  // namespace
+
+bool sha256_has_shani() { return g_shani; }
+
+void sha256_compress(std::uint32_t state[8], const std::uint8_t* blocks, std::size_t nblocks) {
+    if (g_shani) compress_shani(state, blocks, nblocks);
+    else compress_portable(state, blocks, nblocks);
+}
+
+Digest sha256_64(const std::uint8_t* a32, const std::uint8_t* b32) {
+    std::uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                          0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    std::uint8_t blk[128];
+    std::memcpy(blk, a32, 32);
+    std::memcpy(blk + 32, b32, 32);
+    std::memcpy(blk + 64, kPad64, 64);
+    sha256_compress(h, blk, 2);
+    Digest out;
+    for (int i = 0; i < 8; ++i) {
+        out[4 * i + 0] = static_cast<std::uint8_t>(h[i] >> 24);
+        out[4 * i + 1] = static_cast<std::uint8_t>(h[i] >> 16);
+        out[4 * i + 2] = static_cast<std::uint8_t>(h[i] >> 8);
+        out[4 * i + 3] = static_cast<std::uint8_t>(h[i]);
+    }
+    return out;
+}
+
+}  // namespace dgkr_b200

@@ -1,0 +1,719 @@
+// sm_100a kernels of the B200 distributed-GKR prover.
+//
+// All arithmetic is on the integer pipe (IMAD/IADD3/LOP3/SHF): 256-bit
+// Montgomery field ops (field.cuh) and SHA-256 words. Tables are element-
+// contiguous 32-byte records (one L2 sector per element) so that the random
+// gathers of the bookkeeping and evaluation kernels touch one sector each,
+// while the streaming round kernel reads 128 contiguous bytes per table per
+// thread.
+//
+// Reference loops each kernel replaces (file:line under
+// /root/reference/proj/include/dgkr):
+//   k_round            sumcheck.hpp:118-144 (round_poly_over + fold_over),
+//                      mle.hpp:75-85 (fold_once) — fused fold(r_{j-1}) + round(j)
+//   k_fold_final       mle.hpp:75-85 on the last 2-element tables
+//   k_pair_total       sumcheck.hpp:177-186 (PairSumSession::total)
+//   k_eq_build         mle.hpp:111-120 (chi_eval) as a doubling table
+//   k_bookkeep_phase1  sumcheck.hpp:368-391 (+ gkr.hpp:135-152 weights)
+//   k_bookkeep_phase2  sumcheck.hpp:407-431
+//   k_evaluate         circuit.hpp:164-193
+//   k_dense_eval       mle.hpp:51-61 (MultilinearTable::eval)
+//   k_column_digest    pcs.hpp:73-80
+//   k_merkle_*         merkle.hpp:16-28
+//   k_beta_combine     pcs.hpp:233-239
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "field.cuh"
+#include "kernels.hpp"
+
+namespace dgkr_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(std::uint64_t n, int threads, int cap) {
+    std::uint64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > static_cast<std::uint64_t>(cap)) b = cap;
+    return static_cast<int>(b);
+}
+
+// ---------------------------------------------------------------------------
+// Block / grid reductions of K field accumulators. The grid result is formed
+// by the last CTA to finish (threadfence + atomic ticket), so one launch per
+// round suffices.
+// ---------------------------------------------------------------------------
+template <class F, int K>
+__device__ __forceinline__ void warp_sum(Fe (&s)[K]) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = fe_add<F>(s[k], fe_shfl_down(s[k], off));
+    }
+}
+
+// Sum over the CTA; result valid in thread 0.
+template <class F, int K>
+__device__ __forceinline__ void block_sum(Fe (&s)[K], Fe (*sh)[K]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    warp_sum<F, K>(s);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[warp][k] = s[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = lane < nw ? sh[lane][k] : fe_zero();
+        warp_sum<F, K>(s);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ Fe fe_ldcg(const Fe* p) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 a = __ldcg(q), b = __ldcg(q + 1);
+    Fe r;
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+    return r;
+}
+
+template <class F, int K>
+__device__ __forceinline__ void grid_finish(Fe (&s)[K], Fe* partials, unsigned* counter, Fe* result) {
+    __shared__ Fe sh[32][K];
+    __shared__ bool last;
+    block_sum<F, K>(s, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) fe_store(&partials[blockIdx.x * K + k], s[k]);
+        __threadfence();
+        const unsigned t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    Fe a[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a[k] = fe_zero();
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a[k] = fe_add<F>(a[k], fe_ldcg(&partials[b * K + k]));
+    }
+    block_sum<F, K>(a, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) fe_store(&result[k], a[k]);
+        *counter = 0;
+    }
+}
+
+template <class F>
+__device__ __forceinline__ Fe fold1(const Fe& a, const Fe& b, const Fe& r) {
+    return fe_add<F>(a, fe_mul<F>(r, fe_sub<F>(b, a)));
+}
+
+// ---------------------------------------------------------------------------
+// Conversions
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void k_from_canonical(const std::uint8_t* __restrict__ in, int width, Fe* __restrict__ out,
+                                 std::uint64_t n, int* err) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe c = fe_zero();
+        if (width == 32) {
+            c = fe_load_nc(reinterpret_cast<const Fe*>(in) + i);
+        } else {
+            const std::uint8_t* q = in + i * width;
+            for (int b = 0; b < width; ++b) c.v[b >> 2] |= static_cast<uint32_t>(q[b]) << (8 * (b & 3));
+        }
+        if (!fe_lt_p<F>(c)) *err = 1;
+        fe_store(out + i, fe_to_mont<F>(c));
+    }
+}
+
+template <class F>
+__global__ void k_to_canonical(const Fe* __restrict__ in, std::uint8_t* __restrict__ out, int width,
+                               std::uint64_t n) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const Fe c = fe_from_mont<F>(fe_load(in + i));
+        if (width == 32) {
+            fe_store(reinterpret_cast<Fe*>(out) + i, c);
+        } else {
+            std::uint8_t* q = out + i * width;
+            for (int b = 0; b < width; ++b) q[b] = static_cast<std::uint8_t>(c.v[b >> 2] >> (8 * (b & 3)));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused fold + round polynomial
+// ---------------------------------------------------------------------------
+struct RoundParams {
+    const Fe* const* in;
+    Fe* const* out;
+    int np;
+    std::uint64_t n_out_pairs;
+    const Fe* r;
+    Fe* partials;
+    unsigned* counter;
+    Fe* result;
+};
+
+template <class F, bool FOLD>
+__device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __restrict__ dst, std::uint64_t i,
+                                          const Fe& r, Fe& x0, Fe& x1) {
+    if (FOLD) {
+        const Fe a0 = fe_load_nc(src + 4 * i), a1 = fe_load_nc(src + 4 * i + 1);
+        const Fe b0 = fe_load_nc(src + 4 * i + 2), b1 = fe_load_nc(src + 4 * i + 3);
+        x0 = fold1<F>(a0, a1, r);
+        x1 = fold1<F>(b0, b1, r);
+        fe_store(dst + 2 * i, x0);
+        fe_store(dst + 2 * i + 1, x1);
+    } else {
+        x0 = fe_load_nc(src + 2 * i);
+        x1 = fe_load_nc(src + 2 * i + 1);
+    }
+}
+
+template <class F, int NP, bool HAS_G, bool FOLD>
+__global__ void __launch_bounds__(kThreads) k_round(RoundParams a) {
+    Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
+    Fe r = fe_zero();
+    if (FOLD) r = fe_load(a.r);
+    const int np = NP > 0 ? NP : a.np;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < a.n_out_pairs;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        for (int k = 0; k < np; ++k) {
+            Fe f0, f1, g0, g1;
+            load_pair<F, FOLD>(a.in[2 * k], FOLD ? a.out[2 * k] : nullptr, i, r, f0, f1);
+            load_pair<F, FOLD>(a.in[2 * k + 1], FOLD ? a.out[2 * k + 1] : nullptr, i, r, g0, g1);
+            s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
+            s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
+            s[2] = fe_add<F>(s[2], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
+        }
+        if (HAS_G) {
+            Fe g0, g1;
+            load_pair<F, FOLD>(a.in[2 * np], FOLD ? a.out[2 * np] : nullptr, i, r, g0, g1);
+            s[0] = fe_add<F>(s[0], g0);
+            s[1] = fe_add<F>(s[1], g1);
+        }
+    }
+    grid_finish<F, 3>(s, a.partials, a.counter, a.result);
+}
+
+template <class F>
+__global__ void k_fold_final(const Fe* const* in, Fe* const* out, int n_tabs, const Fe* rp) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tabs) return;
+    const Fe r = fe_load(rp);
+    fe_store(out[t], fold1<F>(fe_load(in[t]), fe_load(in[t] + 1), r));
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_pair_total(const Fe* const* tabs, int np, std::uint64_t n,
+                                                         Fe* partials, unsigned* counter, Fe* result) {
+    Fe s[1] = {fe_zero()};
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        for (int k = 0; k < np; ++k) {
+            s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc(tabs[2 * k] + i), fe_load_nc(tabs[2 * k + 1] + i)));
+        }
+    }
+    grid_finish<F, 1>(s, partials, counter, result);
+}
+
+// ---------------------------------------------------------------------------
+// eq tables: out[b] = seed * prod_k (b_k ? p_k : 1 - p_k), built by doubling
+// (var k: out[b + 2^k] = out[b] p_k ; out[b] -= out[b + 2^k]).
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void k_eq_build(const EqJob* jobs) {
+    const EqJob j = jobs[blockIdx.x];
+    if (threadIdx.x == 0) fe_store(j.out, fe_load(j.seed));
+    __syncthreads();
+    for (int k = 0; k < j.nvars; ++k) {
+        const Fe pk = fe_load(j.point + k);
+        const std::uint64_t half = std::uint64_t{1} << k;
+        for (std::uint64_t b = threadIdx.x; b < half; b += blockDim.x) {
+            const Fe v = fe_load(j.out + b);
+            const Fe hi = fe_mul<F>(v, pk);
+            fe_store(j.out + b + half, hi);
+            fe_store(j.out + b, fe_sub<F>(v, hi));
+        }
+        __syncthreads();
+    }
+}
+
+template <class F>
+__device__ __forceinline__ Fe split_eq(const SplitEq& e, std::uint64_t g) {
+    const std::uint64_t lo = g & ((std::uint64_t{1} << e.klo) - 1), hi = g >> e.klo;
+    Fe w = fe_mul<F>(fe_load_nc(e.A + lo), fe_load_nc(e.B + hi));
+    for (int t = 1; t < e.K; ++t) {
+        w = fe_add<F>(w, fe_mul<F>(fe_load_nc(e.A + (static_cast<std::uint64_t>(t) << e.klo) + lo),
+                                   fe_load_nc(e.B + (static_cast<std::uint64_t>(t) << e.khi) + hi)));
+    }
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// GKR layer bookkeeping (CSR gather-reduce; the wiring transpose is built once
+// per circuit, so there are no atomics on 256-bit values).
+// Entry layout: {g_local, other_local, other_slot | is_mul << 31, wire id}.
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) {
+    for (std::uint64_t x = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; x < a.T;
+         x += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe gacc = fe_zero();
+        for (int m = 0; m < a.n_slots; ++m) {
+            const SlotDesc sd = a.slots[m];
+            const std::uint64_t c = x >> sd.log_stride;
+            const std::uint32_t xl = static_cast<std::uint32_t>(x & ((std::uint64_t{1} << sd.log_stride) - 1));
+            Fe h = fe_zero();
+            if (c < a.n_copies) {
+                const std::uint32_t e0 = sd.off[xl], e1 = sd.off[xl + 1];
+                for (std::uint32_t e = e0; e < e1; ++e) {
+                    const uint4 en = sd.ent[e];
+                    const std::uint64_t g = (c << a.log_gcons) | en.x;
+                    const Fe w = a.wire_w ? fe_load_nc(a.wire_w + en.w) : split_eq<F>(a.w, g);
+                    const std::uint32_t ys = en.z & 0x7fffffffu;
+                    const SlotDesc sy = a.slots[ys];
+                    const Fe vy = fe_load_nc(sy.V + ((c << sy.log_stride) | en.y));
+                    if (en.z >> 31) {
+                        h = fe_add<F>(h, fe_mul<F>(w, vy));
+                    } else {
+                        h = fe_add<F>(h, w);
+                        gacc = fe_add<F>(gacc, fe_mul<F>(w, vy));
+                    }
+                }
+            }
+            fe_store(sd.out + x, h);
+        }
+        fe_store(a.G + x, gacc);
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) {
+    for (std::uint64_t y = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; y < a.T;
+         y += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe cacc = fe_zero();
+        for (int m = 0; m < a.n_slots; ++m) {
+            const SlotDesc sd = a.slots[m];
+            const std::uint64_t c = y >> sd.log_stride;
+            const std::uint32_t yl = static_cast<std::uint32_t>(y & ((std::uint64_t{1} << sd.log_stride) - 1));
+            Fe ma = fe_zero();
+            if (c < a.n_copies) {
+                const std::uint32_t e0 = sd.off[yl], e1 = sd.off[yl + 1];
+                for (std::uint32_t e = e0; e < e1; ++e) {
+                    const uint4 en = sd.ent[e];
+                    const std::uint64_t g = (c << a.log_gcons) | en.x;
+                    const Fe w = a.wire_w ? fe_load_nc(a.wire_w + en.w) : split_eq<F>(a.w, g);
+                    const std::uint32_t xs = en.z & 0x7fffffffu;
+                    const std::uint64_t x = (c << a.slots[xs].log_stride) | en.y;
+                    const Fe cx = fe_mul<F>(w, split_eq<F>(a.u, x));
+                    const Fe vx = fe_load(a.vx + xs);
+                    if (en.z >> 31) {
+                        ma = fe_add<F>(ma, fe_mul<F>(cx, vx));
+                    } else {
+                        ma = fe_add<F>(ma, cx);
+                        cacc = fe_add<F>(cacc, fe_mul<F>(cx, vx));
+                    }
+                }
+            }
+            fe_store(sd.out + y, ma);
+        }
+        fe_store(a.G + y, cacc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Circuit evaluation of one layer (one thread per gate).
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_evaluate(EvalLaunch a) {
+    for (std::uint64_t g = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; g < a.n_write;
+         g += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe acc = fe_zero();
+        if (g < a.n_gates) {
+            const std::uint64_t c = g >> a.log_g;
+            const std::uint32_t gl = static_cast<std::uint32_t>(g & ((std::uint64_t{1} << a.log_g) - 1));
+            const std::uint32_t k0 = a.gstart[gl], k1 = a.gstart[gl + 1];
+            for (std::uint32_t k = k0; k < k1; ++k) {
+                const uint4 e = a.nested[k];
+                const std::uint32_t ll = (e.x >> 1) & 0x7fffu, rl = e.x >> 16;
+                const Fe va = fe_load_nc(a.layer_vals[ll] + ((c << a.layer_log_stride[ll]) | e.y));
+                const Fe vb = fe_load_nc(a.layer_vals[rl] + ((c << a.layer_log_stride[rl]) | e.z));
+                acc = fe_add<F>(acc, (e.x & 1) ? fe_mul<F>(va, vb) : fe_add<F>(va, vb));
+            }
+        }
+        fe_store(a.out + g, acc);
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_dense_eval(const Fe* __restrict__ t, std::uint64_t n, SplitEq e,
+                                                         Fe* partials, unsigned* counter, Fe* result) {
+    Fe s[1] = {fe_zero()};
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc(t + i), split_eq<F>(e, i)));
+    }
+    grid_finish<F, 1>(s, partials, counter, result);
+}
+
+// ---------------------------------------------------------------------------
+// SHA-256 (FIPS 180-4) on the 32-bit ALU pipe.
+// ---------------------------------------------------------------------------
+__constant__ uint32_t c_sha_k[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+
+// Message schedule + K of the constant padding block of a 64-byte message
+// (0x80, zeros, bit length 512): W+K precomputed once on the host.
+__constant__ uint32_t c_pad64_wk[64];
+
+__device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+__device__ __forceinline__ void sha_rounds(uint32_t st[8], const uint32_t* wk_or_w, bool precomputed_wk,
+                                           uint32_t w[16]) {
+    uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        uint32_t wk;
+        if (precomputed_wk) {
+            wk = wk_or_w[i];
+        } else {
+            if (i >= 16) {
+                const uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
+                const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+                const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+                w[i & 15] += s0 + w[(i - 7) & 15] + s1;
+            }
+            wk = w[i & 15] + c_sha_k[i];
+        }
+        const uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t t1 = h + S1 + ch + wk;
+        const uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        h = g;
+        g = f;
+        f = e;
+        e = d + t1;
+        d = c;
+        c = b;
+        b = a;
+        a = t1 + S0 + mj;
+    }
+    st[0] += a; st[1] += b; st[2] += c; st[3] += d;
+    st[4] += e; st[5] += f; st[6] += g; st[7] += h;
+}
+
+__device__ __forceinline__ void sha_init(uint32_t st[8]) {
+    st[0] = 0x6a09e667u; st[1] = 0xbb67ae85u; st[2] = 0x3c6ef372u; st[3] = 0xa54ff53au;
+    st[4] = 0x510e527fu; st[5] = 0x9b05688cu; st[6] = 0x1f83d9abu; st[7] = 0x5be0cd19u;
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// Streaming message builder over big-endian words.
+struct ShaStream {
+    uint32_t st[8];
+    uint32_t w[16];
+    uint32_t pos;     // bytes in the current block
+    uint64_t total;   // total bytes
+    __device__ void init() {
+        sha_init(st);
+        pos = 0;
+        total = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[i] = 0;
+    }
+    __device__ void flush_if_full() {
+        if (pos == 64) {
+            sha_rounds(st, nullptr, false, w);
+            pos = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = 0;
+        }
+    }
+    __device__ void push_byte(uint32_t byte) {
+        w[pos >> 2] |= byte << (24 - 8 * (pos & 3));
+        ++pos;
+        ++total;
+        flush_if_full();
+    }
+    // 4 message bytes given as a big-endian word; requires pos % 4 == 0
+    __device__ void push_word(uint32_t be) {
+        w[pos >> 2] = be;
+        pos += 4;
+        total += 4;
+        flush_if_full();
+    }
+    __device__ void finish(uint32_t out[8]) {
+        const uint64_t bits = total * 8;
+        push_byte(0x80);
+        --total;
+        while (pos != 56) {
+            ++pos;
+            flush_if_full();
+        }
+        w[14] = static_cast<uint32_t>(bits >> 32);
+        w[15] = static_cast<uint32_t>(bits);
+        sha_rounds(st, nullptr, false, w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = st[i];
+    }
+};
+
+__device__ __forceinline__ void store_digest(std::uint8_t* dst, const uint32_t h[8]) {
+    uint4* q = reinterpret_cast<uint4*>(dst);
+    q[0] = make_uint4(bswap32(h[0]), bswap32(h[1]), bswap32(h[2]), bswap32(h[3]));
+    q[1] = make_uint4(bswap32(h[4]), bswap32(h[5]), bswap32(h[6]), bswap32(h[7]));
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_column_digest(const Fe* __restrict__ rows, std::uint64_t cols, int M,
+                                                            int width, std::uint8_t* __restrict__ leaves) {
+    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < cols;
+         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        ShaStream s;
+        s.init();
+        for (int i = 0; i < M; ++i) {
+            const Fe c = fe_from_mont<F>(fe_load_nc(rows + static_cast<std::uint64_t>(i) * cols + j));
+            if ((width & 3) == 0) {
+                for (int k = 0; k < (width >> 2); ++k) s.push_word(bswap32(c.v[k]));
+            } else {
+                for (int b = 0; b < width; ++b) s.push_byte((c.v[b >> 2] >> (8 * (b & 3))) & 0xffu);
+            }
+        }
+        uint32_t h[8];
+        s.finish(h);
+        store_digest(leaves + 32 * j, h);
+    }
+}
+
+// H(left || right) for 32-byte digests stored as bytes.
+__device__ __forceinline__ void hash_pair(const std::uint8_t* l, const std::uint8_t* r, std::uint8_t* dst) {
+    uint32_t w[16];
+    const uint4* ql = reinterpret_cast<const uint4*>(l);
+    const uint4* qr = reinterpret_cast<const uint4*>(r);
+    uint4 a = ql[0], b = ql[1], c = qr[0], d = qr[1];
+    w[0] = bswap32(a.x); w[1] = bswap32(a.y); w[2] = bswap32(a.z); w[3] = bswap32(a.w);
+    w[4] = bswap32(b.x); w[5] = bswap32(b.y); w[6] = bswap32(b.z); w[7] = bswap32(b.w);
+    w[8] = bswap32(c.x); w[9] = bswap32(c.y); w[10] = bswap32(c.z); w[11] = bswap32(c.w);
+    w[12] = bswap32(d.x); w[13] = bswap32(d.y); w[14] = bswap32(d.z); w[15] = bswap32(d.w);
+    uint32_t st[8];
+    sha_init(st);
+    sha_rounds(st, nullptr, false, w);
+    sha_rounds(st, c_pad64_wk, true, w);
+    store_digest(dst, st);
+}
+
+// one level: nodes[i] = H(nodes[2i] || nodes[2i+1]) for i in [lo, 2lo)
+__global__ void __launch_bounds__(kThreads) k_merkle_level(std::uint8_t* nodes, std::uint64_t lo) {
+    for (std::uint64_t i = lo + blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < 2 * lo;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        hash_pair(nodes + 64 * i, nodes + 64 * i + 32, nodes + 32 * i);
+    }
+}
+
+// the top levels (lo <= blockDim) inside one CTA
+__global__ void k_merkle_top(std::uint8_t* nodes, std::uint64_t lo) {
+    for (; lo >= 1; lo >>= 1) {
+        for (std::uint64_t i = lo + threadIdx.x; i < 2 * lo; i += blockDim.x) {
+            hash_pair(nodes + 64 * i, nodes + 64 * i + 32, nodes + 32 * i);
+        }
+        __syncthreads();
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_beta_combine(const Fe* __restrict__ rows, std::uint64_t cols, int M,
+                                                           const Fe* __restrict__ beta, Fe* __restrict__ out) {
+    for (std::uint64_t j = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; j < cols;
+         j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe acc = fe_zero();
+        for (int i = 0; i < M; ++i) {
+            acc = fe_add<F>(acc, fe_mul<F>(fe_load(beta + i), fe_load_nc(rows + static_cast<std::uint64_t>(i) * cols + j)));
+        }
+        fe_store(out + j, acc);
+    }
+}
+
+void check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "dgkr_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+    }
+}
+
+bool g_pad_uploaded = false;
+
+void ensure_pad_table() {
+    if (g_pad_uploaded) return;
+    static const uint32_t K[64] = {
+        0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+        0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+        0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+        0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+        0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+        0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+        0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+        0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+    uint32_t w[64] = {0};
+    w[0] = 0x80000000u;
+    w[15] = 512;
+    auto rotr = [](uint32_t x, int n) { return (x >> n) | (x << (32 - n)); };
+    for (int i = 16; i < 64; ++i) {
+        const uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+        const uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t wk[64];
+    for (int i = 0; i < 64; ++i) wk[i] = w[i] + K[i];
+    cudaMemcpyToSymbol(c_pad64_wk, wk, sizeof(wk));
+    g_pad_uploaded = true;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+#define DISPATCH_FIELD(kind, F, ...)    \
+    do {                                \
+        if ((kind) == FieldKind::Bn254) { \
+            using F = Bn254;            \
+            __VA_ARGS__;                \
+        } else {                        \
+            using F = Rt;               \
+            __VA_ARGS__;                \
+        }                               \
+    } while (0)
+
+void upload_rt_field(const RtFieldHost& f, cudaStream_t st) {
+    static_assert(sizeof(RtFieldHost) == sizeof(RtFieldConst), "layout");
+    cudaMemcpyToSymbolAsync(c_rt_field, &f, sizeof(f), 0, cudaMemcpyHostToDevice, st);
+}
+
+void launch_from_canonical(FieldKind k, const std::uint8_t* in, int width, Fe* out, std::uint64_t n, int* err,
+                           cudaStream_t st) {
+    if (n == 0) return;
+    const int g = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_from_canonical<F><<<g, kThreads, 0, st>>>(in, width, out, n, err)));
+    check_launch("from_canonical");
+}
+
+void launch_to_canonical(FieldKind k, const Fe* in, std::uint8_t* out, int width, std::uint64_t n, cudaStream_t st) {
+    if (n == 0) return;
+    const int g = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_to_canonical<F><<<g, kThreads, 0, st>>>(in, out, width, n)));
+    check_launch("to_canonical");
+}
+
+void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, a.r, ws.partials, ws.counter, ws.result};
+    const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
+#define LAUNCH_ROUND(NP, HG, FD) k_round<F, NP, HG, FD><<<g, kThreads, 0, st>>>(p)
+    DISPATCH_FIELD(k, F, {
+        if (a.np == 1 && a.has_g) {
+            if (a.fold) LAUNCH_ROUND(1, true, true); else LAUNCH_ROUND(1, true, false);
+        } else if (a.has_g) {
+            if (a.fold) LAUNCH_ROUND(0, true, true); else LAUNCH_ROUND(0, true, false);
+        } else {
+            if (a.fold) LAUNCH_ROUND(0, false, true); else LAUNCH_ROUND(0, false, false);
+        }
+    });
+#undef LAUNCH_ROUND
+    check_launch("round");
+}
+
+void launch_fold_final(FieldKind k, const Fe* const* in, Fe* const* out, int n_tabs, const Fe* r, cudaStream_t st) {
+    const int g = (n_tabs + 63) / 64;
+    DISPATCH_FIELD(k, F, (k_fold_final<F><<<g, 64, 0, st>>>(in, out, n_tabs, r)));
+    check_launch("fold_final");
+}
+
+void launch_pair_total(FieldKind k, const Fe* const* tabs, int np, std::uint64_t n, const ReduceWs& ws,
+                       cudaStream_t st) {
+    const int g = grid_for(n, kThreads, ws.max_blocks);
+    DISPATCH_FIELD(k, F, (k_pair_total<F><<<g, kThreads, 0, st>>>(tabs, np, n, ws.partials, ws.counter, ws.result)));
+    check_launch("pair_total");
+}
+
+void launch_eq_build(FieldKind k, const EqJob* jobs, int n_jobs, cudaStream_t st) {
+    if (n_jobs == 0) return;
+    DISPATCH_FIELD(k, F, (k_eq_build<F><<<n_jobs, 1024, 0, st>>>(jobs)));
+    check_launch("eq_build");
+}
+
+void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
+    const int g = grid_for(a.T, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_bookkeep_phase1<F><<<g, kThreads, 0, st>>>(a)));
+    check_launch("bookkeep_phase1");
+}
+
+void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
+    const int g = grid_for(a.T, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_bookkeep_phase2<F><<<g, kThreads, 0, st>>>(a)));
+    check_launch("bookkeep_phase2");
+}
+
+void launch_evaluate(FieldKind k, const EvalLaunch& a, cudaStream_t st) {
+    if (a.n_write == 0) return;
+    const int g = grid_for(a.n_write, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_evaluate<F><<<g, kThreads, 0, st>>>(a)));
+    check_launch("evaluate");
+}
+
+void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq& eq, const ReduceWs& ws,
+                       cudaStream_t st) {
+    const int g = grid_for(n, kThreads, ws.max_blocks);
+    DISPATCH_FIELD(k, F, (k_dense_eval<F><<<g, kThreads, 0, st>>>(t, n, eq, ws.partials, ws.counter, ws.result)));
+    check_launch("dense_eval");
+}
+
+void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,
+                           cudaStream_t st) {
+    const int g = grid_for(cols, kThreads, 148 * 32);
+    DISPATCH_FIELD(k, F, (k_column_digest<F><<<g, kThreads, 0, st>>>(rows, cols, M, width, leaves)));
+    check_launch("column_digest");
+}
+
+void launch_merkle(std::uint8_t* nodes, std::uint64_t n_leaves, cudaStream_t st) {
+    ensure_pad_table();
+    std::uint64_t lo = n_leaves / 2;
+    constexpr std::uint64_t kTop = 1024;
+    while (lo > kTop) {
+        const int g = grid_for(lo, kThreads, 148 * 32);
+        k_merkle_level<<<g, kThreads, 0, st>>>(nodes, lo);
+        lo >>= 1;
+    }
+    if (lo >= 1) k_merkle_top<<<1, static_cast<unsigned>(std::min<std::uint64_t>(lo, kTop)), 0, st>>>(nodes, lo);
+    check_launch("merkle");
+}
+
+void launch_beta_combine(FieldKind k, const Fe* rows, std::uint64_t cols, int M, const Fe* beta, Fe* out,
+                         cudaStream_t st) {
+    const int g = grid_for(cols, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_beta_combine<F><<<g, kThreads, 0, st>>>(rows, cols, M, beta, out)));
+    check_launch("beta_combine");
+}
+
+}  // namespace dgkr_b200

@@ -1,0 +1,136 @@
+// Host-visible launcher interface for the sm_100a kernels in kernels.cu.
+// Every launcher enqueues on `st` and never synchronises; the drivers in
+// prover.cpp own ordering and host<->device traffic.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dgkr_b200 {
+
+struct Fe;  // 8 x u32 Montgomery limbs (fe.hpp)
+
+/// Which field policy a launch uses: the BN254 specialisation or the
+/// runtime-modulus path (constants uploaded with upload_rt_field()).
+enum class FieldKind : int { Bn254 = 0, Runtime = 1 };
+
+struct RtFieldHost {
+    std::uint32_t p[8];
+    std::uint32_t np0;
+    std::uint32_t r2[8];
+    std::uint32_t one[8];
+};
+
+void upload_rt_field(const RtFieldHost& f, cudaStream_t st);
+
+// canonical LE (width bytes/element) -> Montgomery; *err set to 1 on a value >= p
+void launch_from_canonical(FieldKind k, const std::uint8_t* in, int width, Fe* out, std::uint64_t n, int* err,
+                           cudaStream_t st);
+void launch_to_canonical(FieldKind k, const Fe* in, std::uint8_t* out, int width, std::uint64_t n, cudaStream_t st);
+
+/// Reduction workspace shared by all "sum to a few field elements" kernels.
+struct ReduceWs {
+    Fe* partials = nullptr;      // [max_blocks * 3]
+    unsigned* counter = nullptr; // zero-initialised, self-resetting
+    Fe* result = nullptr;        // [3] (device)
+    int max_blocks = 0;
+    int num_sms = 0;
+};
+
+/// One sum-check round over pair tables (f_k, g_k) (+ optional G paired with
+/// the implicit all-ones table). With fold=true the inputs are the previous
+/// round's tables (size 4*n_out_pairs) folded with r into `out`
+/// (size 2*n_out_pairs); with fold=false the inputs themselves are scanned.
+/// Writes (S0, S1, S2) = (sum f0 g0, sum f1 g1, sum df dg) (+G terms into
+/// S0/S1) to ws.result; the host forms c0=S0, c2=S2, c1=S1-S0-S2.
+struct RoundLaunch {
+    const Fe* const* in = nullptr;  // device array [2*np + has_g]
+    Fe* const* out = nullptr;       // device array [2*np + has_g]
+    int np = 0;
+    bool has_g = false;
+    bool fold = false;
+    std::uint64_t n_out_pairs = 0;
+    const Fe* r = nullptr;          // device pointer to the fold challenge
+};
+void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
+
+/// out[t][0] = in[t][0] + r (in[t][1] - in[t][0]) for each table t.
+void launch_fold_final(FieldKind k, const Fe* const* in, Fe* const* out, int n_tabs, const Fe* r, cudaStream_t st);
+
+/// sum_k sum_i f_k[i] g_k[i]  -> ws.result[0]
+void launch_pair_total(FieldKind k, const Fe* const* tabs, int np, std::uint64_t n, const ReduceWs& ws,
+                       cudaStream_t st);
+
+/// eq-table jobs: out[b] = seed * chi_b(point), b < 2^nvars (one CTA per job).
+struct EqJob {
+    const Fe* point;
+    const Fe* seed;   // device pointer to the seed value
+    Fe* out;
+    int nvars;
+    int pad;
+};
+void launch_eq_build(FieldKind k, const EqJob* jobs, int n_jobs, cudaStream_t st);
+
+/// Split-eq weight tables: w(g) = sum_t A[t][g & (2^klo - 1)] * B[t][g >> klo]
+struct SplitEq {
+    const Fe* A = nullptr;  // K * 2^klo
+    const Fe* B = nullptr;  // K * 2^khi
+    int K = 0;
+    int klo = 0;
+    int khi = 0;
+};
+
+/// Per-slot description of a data-parallel layer: values are laid out as
+/// n_copies blocks of 2^log_stride (copy = high bits).
+struct SlotDesc {
+    const Fe* V;             // source values (capacity >= side size, zero padded)
+    Fe* out;                 // H_m (phase 1) or MA_m (phase 2), size 2^side
+    const std::uint32_t* off;  // CSR offsets [2^log_stride + 1]
+    const uint4* ent;        // CSR entries
+    std::uint32_t log_stride;
+    std::uint32_t pad;
+};
+
+struct BookkeepLaunch {
+    const SlotDesc* slots = nullptr;  // device array [n_slots]
+    int n_slots = 0;
+    std::uint64_t T = 0;          // 2^side
+    std::uint32_t n_copies = 1;
+    std::uint32_t log_gcons = 0;  // consumer gate stride (log2)
+    Fe* G = nullptr;              // G (phase 1) / C (phase 2)
+    SplitEq w;                    // wire weights from the combined claim
+    SplitEq u;                    // phase 2: chi_x(u) split tables
+    const Fe* vx = nullptr;       // phase 2: V_m(u) per slot (device)
+    const Fe* wire_w = nullptr;   // explicit per-wire weights (entry .w = wire id), else w
+};
+void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
+void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
+
+/// Layer evaluation (circuit.hpp:178-191) for a data-parallel layer.
+struct EvalLaunch {
+    Fe* out = nullptr;
+    std::uint64_t n_write = 0;     // entries to write (gates + zero padding)
+    std::uint64_t n_gates = 0;     // n_copies * sub gates
+    std::uint32_t log_g = 0;       // sub gate stride (log2)
+    const std::uint32_t* gstart = nullptr;  // [sub_gates + 1]
+    const uint4* nested = nullptr;  // {kind | left_layer<<1 | right_layer<<16, left_gate, right_gate, 0}
+    const Fe* const* layer_vals = nullptr;   // device array [depth+1]
+    const std::uint32_t* layer_log_stride = nullptr;  // device array [depth+1]
+};
+void launch_evaluate(FieldKind k, const EvalLaunch& a, cudaStream_t st);
+
+/// ws.result[0] = sum_g t[g] * A[g & m] * B[g >> klo]  (dense MLE evaluation, mle.hpp:51-61)
+void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq& eq, const ReduceWs& ws,
+                       cudaStream_t st);
+
+/// Batched SHA-256 column digests (pcs.hpp:73-80): leaf[j] = SHA256(canon(m[0][j]) || ... || canon(m[M-1][j])).
+void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,
+                           cudaStream_t st);
+/// Merkle tree over 2^depth leaves in heap layout (merkle.hpp:16-28): nodes[i] = H(nodes[2i]||nodes[2i+1]).
+void launch_merkle(std::uint8_t* nodes, std::uint64_t n_leaves, cudaStream_t st);
+/// combined[j] = sum_i beta[i] * m[i][j]   (pcs.hpp:233-239)
+void launch_beta_combine(FieldKind k, const Fe* rows, std::uint64_t cols, int M, const Fe* beta, Fe* out,
+                         cudaStream_t st);
+
+}  // namespace dgkr_b200

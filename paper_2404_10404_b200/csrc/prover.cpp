@@ -1,0 +1,1587 @@
+// Host drivers and C ABI of the B200 distributed-GKR prover
+// (include/dgkr_b200.h). The protocol logic that must stay serial and
+// bit-exact — transcript order, claim registry, claim combination — runs here
+// on the host, following the reference line by line (citations inline); all
+// O(table) work runs in the sm_100a kernels of kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "dgkr_b200.h"
+#include "fe.hpp"
+#include "host_core.hpp"
+#include "kernels.hpp"
+
+using namespace dgkr_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class Fn>
+int guard(Fn&& fn) {
+    try {
+        fn();
+        return DGKR_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("host allocation failed: ") + e.what();
+        return DGKR_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DGKR_LOGIC_ERROR;
+    }
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) fail(DGKR_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(std::size_t count) {
+        if (count <= n && p) return;
+        release();
+        CK(cudaMalloc(reinterpret_cast<void**>(&p), std::max<std::size_t>(count, 1) * sizeof(T)));
+        n = std::max<std::size_t>(count, 1);
+    }
+};
+
+inline Fe to_fe(const U256& x) {
+    Fe f;
+    std::memcpy(f.v, x.w, 32);
+    return f;
+}
+inline U256 to_u256(const Fe& f) {
+    U256 x;
+    std::memcpy(x.w, f.v, 32);
+    return x;
+}
+
+std::uint32_t log2_exact(std::uint64_t n) {  // circuit.hpp:57-61
+    std::uint32_t l = 0;
+    while ((std::uint64_t{1} << l) < n) ++l;
+    return l;
+}
+std::uint64_t next_pow2(std::uint64_t n) {  // circuit.hpp:43-47
+    std::uint64_t p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+void put32(std::vector<std::uint8_t>& out, std::uint32_t v) {
+    for (int i = 0; i < 4; ++i) out.push_back(static_cast<std::uint8_t>(v >> (8 * i)));
+}
+
+void emit(const std::vector<std::uint8_t>& bytes, std::uint8_t* out, std::size_t cap, std::size_t* len) {
+    *len = bytes.size();
+    if (bytes.size() > cap) fail(DGKR_CAPACITY, "output buffer too small");
+    if (!bytes.empty()) std::memcpy(out, bytes.data(), bytes.size());
+}
+
+}  // namespace
+
+// ===========================================================================
+// Opaque handles
+// ===========================================================================
+struct dgkr_field {
+    HostField f;
+    FieldKind kind = FieldKind::Runtime;
+    RtFieldHost rt{};
+};
+
+struct dgkr_ctx {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t st = nullptr;
+    ReduceWs ws;
+    DBuf<Fe> partials, result;
+    DBuf<unsigned> counter;
+    DBuf<Fe> d_small;      // challenges, points, seeds, finals
+    DBuf<int> d_err;
+    Fe* h_small = nullptr;  // pinned mirror of d_small
+    // pinned staging layout (Fe units): [0] challenge, [1..4) reduction
+    // results, [16, 8192) eq-table points/seeds, [8192, 12288) slot values,
+    // [12288, 16384) round finals.
+    static constexpr std::size_t kSmall = 1 << 14;
+    static constexpr std::size_t kEqOff = 16, kEqOff2 = 4112, kVxOff = 8192, kFinalsOff = 12288;
+    bool rt_valid = false;
+    RtFieldHost rt_cur{};
+    bool profile_on = false;
+    dgkr_profile prof{};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    ~dgkr_ctx() {
+        if (h_small) cudaFreeHost(h_small);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    FieldKind use(const dgkr_field* f) {
+        if (f->kind == FieldKind::Runtime) {
+            if (!rt_valid || std::memcmp(&rt_cur, &f->rt, sizeof(RtFieldHost)) != 0) {
+                upload_rt_field(f->rt, st);
+                rt_cur = f->rt;
+                rt_valid = true;
+            }
+        }
+        return f->kind;
+    }
+
+    void sync() { CK(cudaStreamSynchronize(st)); }
+
+    void begin_call() {
+        std::memset(&prof, 0, sizeof(prof));
+        prof.total_ms = now_ms();
+    }
+    void end_call() { prof.total_ms = now_ms() - prof.total_ms; }
+
+    void h2d(void* dst, const void* src, std::size_t n) {
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+        prof.h2d_bytes += n;
+    }
+    void d2h(void* dst, const void* src, std::size_t n) {
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+        prof.d2h_bytes += n;
+    }
+    void launched(std::uint64_t n = 1) { prof.launches += n; }
+
+    void check_err_flag(const char* what) {
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        sync();
+        if (h) {
+            CK(cudaMemsetAsync(d_err.p, 0, sizeof(int), st));
+            fail(DGKR_INVALID_ARGUMENT, std::string("non-canonical field element encoding (") + what + ")");
+        }
+    }
+
+    /// canonical bytes (host) -> Montgomery Fe (device)
+    void upload_elems(const dgkr_field* f, const std::uint8_t* host, std::uint64_t n, Fe* dst, DBuf<std::uint8_t>& stage) {
+        if (n == 0) return;
+        const std::size_t bytes = n * f->f.width();
+        stage.ensure(bytes);
+        h2d(stage.p, host, bytes);
+        launch_from_canonical(use(f), stage.p, static_cast<int>(f->f.width()), dst, n, d_err.p, st);
+        launched();
+        check_err_flag("input tables");
+    }
+};
+
+namespace {
+
+// ===========================================================================
+// Sum-check round engine: runs the rounds of one sum-check over device pair
+// tables, with the transcript on the host (sumcheck.hpp:230-238 order:
+// absorb c0..c3, then challenge).
+// ===========================================================================
+struct RoundBuffers {
+    int ntab = 0;
+    std::uint64_t cap = 0;  // max table size handled
+    DBuf<Fe> bufA, bufB, finals;
+    DBuf<const Fe*> ptrs;   // [A ptrs | B ptrs | finals ptrs] each ntab
+    void ensure(int nt, std::uint64_t size0) {
+        if (nt <= ntab && size0 <= cap) return;
+        ntab = std::max(nt, ntab);
+        cap = std::max(size0, cap);
+        const std::uint64_t a = std::max<std::uint64_t>(cap / 2, 1), b = std::max<std::uint64_t>(cap / 4, 1);
+        bufA.ensure(ntab * a);
+        bufB.ensure(ntab * b);
+        finals.ensure(ntab);
+        std::vector<const Fe*> h(3 * ntab);
+        for (int t = 0; t < ntab; ++t) {
+            h[t] = bufA.p + t * a;
+            h[ntab + t] = bufB.p + t * b;
+            h[2 * ntab + t] = finals.p + t;
+        }
+        ptrs.ensure(3 * ntab);
+        CK(cudaMemcpy(ptrs.p, h.data(), h.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+    }
+    const Fe* const* A() const { return ptrs.p; }
+    const Fe* const* B() const { return ptrs.p + ntab; }
+    const Fe* const* F() const { return ptrs.p + 2 * ntab; }
+};
+
+struct RoundPoly {
+    U256 c[3];
+};
+
+struct SumcheckRun {
+    std::vector<RoundPoly> rounds;
+    std::vector<U256> challenges;
+    std::vector<U256> finals;  // per table, Montgomery
+};
+
+/// tables: device pointer array `base` of ntab = 2*np + has_g tables of
+/// size 2^nv. Returns rounds, challenges and the final value of each table.
+SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
+                       RoundBuffers& rb, Transcript& tr) {
+    const HostField& F = f->f;
+    const FieldKind kind = ctx->use(f);
+    const int ntab = 2 * np + (has_g ? 1 : 0);
+    SumcheckRun out;
+    const std::uint64_t size0 = std::uint64_t{1} << nv;
+    rb.ensure(ntab, size0);
+    Fe* d_r = ctx->d_small.p;
+    const Fe* const* cur = base;
+    const U256 zero{};
+    for (int j = 1; j <= nv; ++j) {
+        RoundLaunch rl;
+        rl.np = np;
+        rl.has_g = has_g;
+        rl.r = d_r;
+        if (j == 1) {
+            rl.fold = false;
+            rl.in = base;
+            rl.out = nullptr;
+        } else {
+            rl.fold = true;
+            rl.in = cur;
+            const Fe* const* nxt = (j % 2 == 0) ? rb.A() : rb.B();
+            rl.out = const_cast<Fe* const*>(nxt);
+            cur = nxt;
+        }
+        rl.n_out_pairs = size0 >> j;
+        if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_round(kind, rl, ctx->ws, ctx->st);
+        ctx->launched();
+        if (ctx->profile_on) CK(cudaEventRecord(ctx->ev1, ctx->st));
+        ctx->d2h(ctx->h_small + 1, ctx->ws.result, 3 * sizeof(Fe));
+        ctx->sync();
+        if (ctx->profile_on) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            ctx->prof.round_ms += ms;
+            ctx->prof.round_launches += 1;
+            const std::uint64_t pairs = rl.n_out_pairs;
+            const std::uint64_t ntabs = static_cast<std::uint64_t>(ntab);
+            // bytes: fold reads 4, writes 2 elements per table per output pair; scan reads 2
+            ctx->prof.round_bytes += pairs * ntabs * 32 * (rl.fold ? 6 : 2);
+            ctx->prof.round_mults += pairs * (3 * np + (rl.fold ? 2 * ntabs : 0));
+        }
+        const double t0 = now_ms();
+        const U256 s0 = to_u256(ctx->h_small[1]), s1 = to_u256(ctx->h_small[2]), s2 = to_u256(ctx->h_small[3]);
+        RoundPoly rp;
+        rp.c[0] = s0;
+        rp.c[2] = s2;
+        rp.c[1] = F.sub(F.sub(s1, s0), s2);
+        for (int k = 0; k < 3; ++k) tr.absorb(rp.c[k]);
+        tr.absorb(zero);
+        const U256 r = tr.challenge();
+        ctx->prof.host_transcript_ms += now_ms() - t0;
+        ctx->prof.rounds += 1;
+        out.rounds.push_back(rp);
+        out.challenges.push_back(r);
+        ctx->h_small[0] = to_fe(r);
+        ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
+    }
+    // final fold of the 2-element tables (or read the 1-element tables)
+    if (nv >= 1) {
+        launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
+        ctx->launched();
+        Fe* hf = ctx->h_small + dgkr_ctx::kFinalsOff;
+        ctx->d2h(hf, rb.finals.p, ntab * sizeof(Fe));
+        ctx->sync();
+        for (int t = 0; t < ntab; ++t) out.finals.push_back(to_u256(hf[t]));
+    } else {
+        ctx->sync();
+        std::vector<const Fe*> hp(ntab);
+        CK(cudaMemcpy(hp.data(), base, ntab * sizeof(const Fe*), cudaMemcpyDeviceToHost));
+        for (int t = 0; t < ntab; ++t) {
+            Fe v;
+            CK(cudaMemcpy(&v, hp[t], sizeof(Fe), cudaMemcpyDeviceToHost));
+            out.finals.push_back(to_u256(v));
+        }
+    }
+    return out;
+}
+
+void append_elem(std::vector<std::uint8_t>& out, const HostField& F, const U256& m) {
+    const std::size_t w = F.width();
+    const std::size_t off = out.size();
+    out.resize(off + w);
+    F.to_bytes(m, out.data() + off);
+}
+
+/// SumcheckProof::to_bytes (sumcheck.hpp:51-61)
+std::vector<std::uint8_t> sumcheck_bytes(const HostField& F, const U256& claimed, const std::vector<RoundPoly>& rounds,
+                                         const std::vector<U256>& finals) {
+    std::vector<std::uint8_t> out;
+    append_elem(out, F, claimed);
+    put32(out, static_cast<std::uint32_t>(rounds.size()));
+    const U256 zero{};
+    for (const auto& r : rounds) {
+        for (int k = 0; k < 3; ++k) append_elem(out, F, r.c[k]);
+        append_elem(out, F, zero);
+    }
+    put32(out, static_cast<std::uint32_t>(finals.size()));
+    for (const auto& e : finals) append_elem(out, F, e);
+    return out;
+}
+
+// ===========================================================================
+// Product sum-check on uploaded tables (shared by prove_product_sum and the
+// single-device dist_sumcheck).
+// ===========================================================================
+std::vector<std::uint8_t> product_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_pairs, std::size_t vars,
+                                           const std::uint8_t* tables, Transcript& tr, U256* claimed_out) {
+    if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "product sum needs at least one pair");  // sumcheck.hpp:155-157
+    if (vars > 40) fail(DGKR_INVALID_ARGUMENT, "table too large");
+    const HostField& F = f->f;
+    const std::uint64_t n = std::uint64_t{1} << vars;
+    const int ntab = static_cast<int>(2 * n_pairs);
+    DBuf<Fe> tabs;
+    DBuf<std::uint8_t> stage;
+    tabs.ensure(static_cast<std::size_t>(ntab) * n);
+    ctx->upload_elems(f, tables, static_cast<std::uint64_t>(ntab) * n, tabs.p, stage);
+    std::vector<const Fe*> hp(ntab);
+    for (int t = 0; t < ntab; ++t) hp[t] = tabs.p + t * n;
+    DBuf<const Fe*> base;
+    base.ensure(ntab);
+    ctx->h2d(base.p, hp.data(), ntab * sizeof(const Fe*));
+    // claimed sum: PairSumSession::total (sumcheck.hpp:177-186)
+    launch_pair_total(ctx->use(f), base.p, static_cast<int>(n_pairs), n, ctx->ws, ctx->st);
+    ctx->launched();
+    ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
+    ctx->sync();
+    const U256 claimed = to_u256(ctx->h_small[1]);
+    tr.absorb(claimed);  // sumcheck.hpp:231
+    RoundBuffers rb;
+    SumcheckRun run = run_rounds(ctx, f, static_cast<int>(n_pairs), false, static_cast<int>(vars), base.p, rb, tr);
+    if (claimed_out) *claimed_out = claimed;
+    return sumcheck_bytes(F, claimed, run.rounds, run.finals);
+}
+
+}  // namespace
+
+// ===========================================================================
+// GKR circuit (data-parallel capable)
+// ===========================================================================
+struct dgkr_circuit {
+    std::uint32_t input_size = 0;  // per copy
+    std::uint32_t depth = 0;
+    std::uint32_t n_copies = 1;
+    std::uint32_t log_copies = 0;
+    // per layer 0..depth (sub-circuit view)
+    std::vector<std::uint64_t> sub_size, sub_padded;
+    std::vector<std::uint32_t> sub_log;      // log2 sub_padded
+    std::vector<std::uint64_t> full_padded;  // n_copies * sub_padded
+    std::vector<std::uint64_t> capacity;     // buffer elements
+    // per consumer layer 1..depth
+    struct Consumer {
+        std::vector<std::uint32_t> slots;  // ascending source layers
+        std::uint32_t side = 0;            // full side vars
+        std::uint64_t n_wires = 0;         // sub wires
+        DBuf<std::uint32_t> xoff, yoff;    // concatenated per slot
+        DBuf<uint4> xent, yent;
+        DBuf<SlotDesc> d_slots1, d_slots2;
+        DBuf<const Fe*> base_ptrs;         // V0,H0,V1,H1,...,G
+        DBuf<std::uint32_t> gstart;        // evaluation CSR
+        DBuf<uint4> nested;
+    };
+    std::vector<std::unique_ptr<Consumer>> cons;  // index li (0 unused)
+    // device state
+    std::vector<std::unique_ptr<DBuf<Fe>>> values;
+    DBuf<const Fe*> d_layer_vals;
+    DBuf<std::uint32_t> d_layer_log;
+    DBuf<Fe> H, G;  // bookkeeping outputs, max_slots x Tmax and Tmax
+    std::uint32_t max_slots = 0;
+    std::uint64_t Tmax = 1;
+    RoundBuffers rb;
+    DBuf<std::uint8_t> stage;
+    DBuf<Fe> eq_tabs;  // split-eq tables for weights and u
+    DBuf<EqJob> eq_jobs, eq_jobs2;
+    std::uint64_t total_gates = 0;  // full circuit gate count
+
+    std::uint32_t padded_log2_full(std::uint32_t l) const { return sub_log[l] + log_copies; }
+};
+
+namespace {
+
+/// GeneralCircuit::validate (circuit.hpp:103-152) on the sub-circuit plus
+/// the data-parallel preconditions; builds all device-side structures.
+void build_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const std::uint64_t* gns,
+                   const std::uint32_t* nested, const std::uint64_t* min_padded) {
+    const std::uint32_t D = c.depth;
+    std::vector<std::string> violations;
+    c.sub_size.assign(D + 1, 0);
+    c.sub_size[0] = c.input_size;
+    for (std::uint32_t li = 1; li <= D; ++li) c.sub_size[li] = lgs[li] - lgs[li - 1];
+    c.sub_padded.assign(D + 1, 1);
+    c.sub_log.assign(D + 1, 0);
+    for (std::uint32_t l = 0; l <= D; ++l) {
+        std::uint64_t p = next_pow2(std::max<std::uint64_t>(c.sub_size[l], 1));  // circuit.hpp:81-84
+        if (min_padded) p = std::max(p, next_pow2(min_padded[l]));
+        c.sub_padded[l] = p;
+        c.sub_log[l] = log2_exact(p);
+    }
+    if (c.n_copies > 1) {
+        for (std::uint32_t l = 0; l <= D; ++l) {
+            if (c.sub_size[l] != c.sub_padded[l])
+                fail(DGKR_INVALID_ARGUMENT, "data-parallel circuits need power-of-two sub layer sizes");
+        }
+    }
+    auto name = [](std::uint32_t li, std::uint64_t gi, const char* side) {
+        return "layer " + std::to_string(li) + " gate " + std::to_string(gi) + " " + side;
+    };
+    for (std::uint32_t li = 1; li <= D; ++li) {
+        bool reads_prev = false;
+        const std::uint64_t g0 = lgs[li - 1], g1 = lgs[li];
+        if (g0 == g1) violations.push_back("layer " + std::to_string(li) + " has no gates");
+        for (std::uint64_t g = g0; g < g1; ++g) {
+            if (gns[g] == gns[g + 1]) {
+                violations.push_back("layer " + std::to_string(li) + " gate " + std::to_string(g - g0) +
+                                     " has no nested gates");
+                continue;
+            }
+            for (std::uint64_t k = gns[g]; k < gns[g + 1]; ++k) {
+                const std::uint32_t* e = nested + 5 * k;
+                const std::uint32_t refs[2][2] = {{e[1], e[2]}, {e[3], e[4]}};
+                const char* sides[2] = {"left", "right"};
+                for (int s = 0; s < 2; ++s) {
+                    if (refs[s][0] >= li) {
+                        violations.push_back("non-causal wire at " + name(li, g - g0, sides[s]));
+                        continue;
+                    }
+                    if (refs[s][1] >= c.sub_padded[refs[s][0]]) {
+                        violations.push_back("dangling wire at " + name(li, g - g0, sides[s]));
+                        continue;
+                    }
+                    if (refs[s][0] + 1 == li) reads_prev = true;
+                }
+            }
+        }
+        if (g0 != g1 && !reads_prev)
+            violations.push_back("layer " + std::to_string(li) + " has no wire into layer " + std::to_string(li - 1));
+    }
+    if (!violations.empty()) fail(DGKR_INVALID_ARGUMENT, "invalid circuit: " + violations.front());
+    if (D >= (1u << 15)) fail(DGKR_UNSUPPORTED, "too many layers");
+
+    c.full_padded.assign(D + 1, 0);
+    for (std::uint32_t l = 0; l <= D; ++l) c.full_padded[l] = c.sub_padded[l] << c.log_copies;
+    c.capacity = c.full_padded;
+    c.total_gates = 0;
+    for (std::uint32_t li = 1; li <= D; ++li) c.total_gates += c.sub_size[li] * c.n_copies;
+
+    // consumers: slots (gkr.hpp:107-131), CSR transposes, evaluation CSR
+    c.cons.clear();
+    c.cons.resize(D + 1);
+    for (std::uint32_t li = 1; li <= D; ++li) {
+        auto cp = std::make_unique<dgkr_circuit::Consumer>();
+        auto& C = *cp;
+        std::set<std::uint32_t> srcs;  // circuit.hpp:212-221
+        for (std::uint64_t g = lgs[li - 1]; g < lgs[li]; ++g) {
+            for (std::uint64_t k = gns[g]; k < gns[g + 1]; ++k) {
+                srcs.insert(nested[5 * k + 1]);
+                srcs.insert(nested[5 * k + 3]);
+            }
+        }
+        C.slots.assign(srcs.begin(), srcs.end());
+        std::uint32_t side = 0;
+        for (auto s : C.slots) side = std::max(side, c.padded_log2_full(s));
+        C.side = side;
+        const std::uint64_t T = std::uint64_t{1} << side;
+        for (auto s : C.slots) c.capacity[s] = std::max(c.capacity[s], T);
+        c.Tmax = std::max(c.Tmax, T);
+        c.max_slots = std::max<std::uint32_t>(c.max_slots, static_cast<std::uint32_t>(C.slots.size()));
+        std::vector<int> slot_of(D + 1, -1);
+        for (std::size_t s = 0; s < C.slots.size(); ++s) slot_of[C.slots[s]] = static_cast<int>(s);
+        const std::size_t ns = C.slots.size();
+        // counts
+        std::vector<std::uint64_t> xbase(ns + 1, 0), ybase(ns + 1, 0);
+        for (std::size_t s = 0; s < ns; ++s) {
+            xbase[s + 1] = xbase[s] + c.sub_padded[C.slots[s]] + 1;
+        }
+        ybase = xbase;
+        std::vector<std::uint32_t> xoff(xbase[ns], 0), yoff(ybase[ns], 0);
+        std::uint64_t nw = 0;
+        for (std::uint64_t g = lgs[li - 1]; g < lgs[li]; ++g) {
+            for (std::uint64_t k = gns[g]; k < gns[g + 1]; ++k) {
+                const std::uint32_t* e = nested + 5 * k;
+                xoff[xbase[slot_of[e[1]]] + e[2] + 1]++;
+                yoff[ybase[slot_of[e[3]]] + e[4] + 1]++;
+                ++nw;
+            }
+        }
+        C.n_wires = nw;
+        // prefix sums per slot (offsets are per-slot local indexes into one entry array)
+        std::vector<std::uint32_t> xslot_start(ns), yslot_start(ns);
+        std::uint32_t accx = 0, accy = 0;
+        for (std::size_t s = 0; s < ns; ++s) {
+            const std::uint64_t len = c.sub_padded[C.slots[s]] + 1;
+            xoff[xbase[s]] += accx;
+            for (std::uint64_t i = 1; i < len; ++i) xoff[xbase[s] + i] += xoff[xbase[s] + i - 1];
+            accx = xoff[xbase[s] + len - 1];
+            yoff[ybase[s]] += accy;
+            for (std::uint64_t i = 1; i < len; ++i) yoff[ybase[s] + i] += yoff[ybase[s] + i - 1];
+            accy = yoff[ybase[s] + len - 1];
+        }
+        std::vector<uint4> xent(nw), yent(nw);
+        std::vector<std::uint32_t> xfill(xoff), yfill(yoff);
+        std::uint32_t wid = 0;
+        for (std::uint64_t g = lgs[li - 1]; g < lgs[li]; ++g) {
+            const std::uint32_t gl = static_cast<std::uint32_t>(g - lgs[li - 1]);
+            for (std::uint64_t k = gns[g]; k < gns[g + 1]; ++k, ++wid) {
+                const std::uint32_t* e = nested + 5 * k;
+                const std::uint32_t mul = e[0] ? 0x80000000u : 0u;
+                const int xs = slot_of[e[1]], ys = slot_of[e[3]];
+                xent[xfill[xbase[xs] + e[2]]++] = make_uint4(gl, e[4], static_cast<std::uint32_t>(ys) | mul, wid);
+                yent[yfill[ybase[ys] + e[4]]++] = make_uint4(gl, e[2], static_cast<std::uint32_t>(xs) | mul, wid);
+            }
+        }
+        C.xoff.ensure(xoff.size());
+        C.yoff.ensure(yoff.size());
+        C.xent.ensure(nw);
+        C.yent.ensure(nw);
+        CK(cudaMemcpy(C.xoff.p, xoff.data(), xoff.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(C.yoff.p, yoff.data(), yoff.size() * 4, cudaMemcpyHostToDevice));
+        if (nw) {
+            CK(cudaMemcpy(C.xent.p, xent.data(), nw * sizeof(uint4), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(C.yent.p, yent.data(), nw * sizeof(uint4), cudaMemcpyHostToDevice));
+        }
+        // evaluation CSR (gate -> nested)
+        const std::uint64_t ng = lgs[li] - lgs[li - 1];
+        std::vector<std::uint32_t> gstart(ng + 1);
+        std::vector<uint4> nest(nw);
+        for (std::uint64_t g = 0; g < ng; ++g) gstart[g] = static_cast<std::uint32_t>(gns[lgs[li - 1] + g] - gns[lgs[li - 1]]);
+        gstart[ng] = static_cast<std::uint32_t>(gns[lgs[li]] - gns[lgs[li - 1]]);
+        for (std::uint64_t k = gns[lgs[li - 1]], i = 0; k < gns[lgs[li]]; ++k, ++i) {
+            const std::uint32_t* e = nested + 5 * k;
+            nest[i] = make_uint4((e[0] ? 1u : 0u) | (e[1] << 1) | (e[3] << 16), e[2], e[4], 0);
+        }
+        C.gstart.ensure(ng + 1);
+        C.nested.ensure(nw);
+        CK(cudaMemcpy(C.gstart.p, gstart.data(), (ng + 1) * 4, cudaMemcpyHostToDevice));
+        if (nw) CK(cudaMemcpy(C.nested.p, nest.data(), nw * sizeof(uint4), cudaMemcpyHostToDevice));
+        // stash per-slot offsets bases for SlotDesc (filled after buffers exist)
+        C.d_slots1.ensure(ns);
+        C.d_slots2.ensure(ns);
+        c.cons[li] = std::move(cp);
+        // keep bases in host-side vectors via lambdas below
+        (void)xslot_start;
+        (void)yslot_start;
+    }
+    // device buffers
+    c.values.clear();
+    for (std::uint32_t l = 0; l <= D; ++l) {
+        auto b = std::make_unique<DBuf<Fe>>();
+        b->ensure(c.capacity[l]);
+        c.values.push_back(std::move(b));
+    }
+    std::vector<const Fe*> lv(D + 1);
+    std::vector<std::uint32_t> ll(D + 1);
+    for (std::uint32_t l = 0; l <= D; ++l) {
+        lv[l] = c.values[l]->p;
+        ll[l] = c.sub_log[l];
+    }
+    c.d_layer_vals.ensure(D + 1);
+    c.d_layer_log.ensure(D + 1);
+    CK(cudaMemcpy(c.d_layer_vals.p, lv.data(), lv.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.d_layer_log.p, ll.data(), ll.size() * 4, cudaMemcpyHostToDevice));
+    if (D >= 1) {
+        c.H.ensure(static_cast<std::size_t>(c.max_slots) * c.Tmax);
+        c.G.ensure(c.Tmax);
+        c.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
+    }
+    for (std::uint32_t li = 1; li <= D; ++li) {
+        auto& C = *c.cons[li];
+        const std::size_t ns = C.slots.size();
+        std::vector<SlotDesc> s1(ns), s2(ns);
+        std::uint64_t base = 0;
+        for (std::size_t s = 0; s < ns; ++s) {
+            const std::uint32_t src = C.slots[s];
+            // stride of a slot = sub padded size of its source (copy = high bits)
+            const std::uint32_t lstr = (c.n_copies > 1) ? c.sub_log[src] : c.padded_log2_full(src);
+            s1[s] = SlotDesc{c.values[src]->p, c.H.p + s * c.Tmax, C.xoff.p + base, C.xent.p, lstr, 0};
+            s2[s] = SlotDesc{c.values[src]->p, c.H.p + s * c.Tmax, C.yoff.p + base, C.yent.p, lstr, 0};
+            base += c.sub_padded[src] + 1;
+        }
+        CK(cudaMemcpy(C.d_slots1.p, s1.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(C.d_slots2.p, s2.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
+        std::vector<const Fe*> bp;
+        for (std::size_t s = 0; s < ns; ++s) {
+            bp.push_back(c.values[C.slots[s]]->p);
+            bp.push_back(c.H.p + s * c.Tmax);
+        }
+        bp.push_back(c.G.p);
+        C.base_ptrs.ensure(bp.size());
+        CK(cudaMemcpy(C.base_ptrs.p, bp.data(), bp.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+    }
+    (void)ctx;
+}
+
+// ---------------------------------------------------------------------------
+// Claims (gkr.hpp:20-84, :157-173) — host, order-sensitive, verbatim.
+// ---------------------------------------------------------------------------
+struct ClaimTerm {
+    std::vector<U256> point;
+    U256 weight;
+};
+struct LayerClaim {
+    std::size_t layer = 0;
+    std::vector<ClaimTerm> terms;
+    U256 value;
+};
+
+LayerClaim combine_claims(std::vector<LayerClaim> claims, Transcript& tr, const HostField& F,
+                          std::vector<U256>* alphas) {
+    if (claims.empty()) fail(DGKR_INVALID_ARGUMENT, "no claims to combine");
+    for (const auto& c : claims)
+        if (c.layer != claims.front().layer) fail(DGKR_INVALID_ARGUMENT, "claims span different layers");
+    if (claims.size() == 1) return std::move(claims.front());
+    const U256 alpha = tr.challenge();
+    if (alphas) alphas->push_back(alpha);
+    LayerClaim out;
+    out.layer = claims.front().layer;
+    U256 scale = F.one();
+    for (auto& c : claims) {
+        out.value = F.add(out.value, F.mul(scale, c.value));
+        for (auto& t : c.terms) {
+            const U256 w = F.mul(scale, t.weight);
+            bool merged = false;
+            for (auto& ot : out.terms) {
+                if (ot.point == t.point) {
+                    ot.weight = F.add(ot.weight, w);
+                    merged = true;
+                    break;
+                }
+            }
+            if (!merged) out.terms.push_back(ClaimTerm{std::move(t.point), w});
+        }
+        scale = F.mul(scale, alpha);
+    }
+    return out;
+}
+
+LayerClaim shrink_claim(std::size_t layer, std::size_t native, const std::vector<U256>& point, const U256& value,
+                        const HostField& F) {
+    U256 w = F.one();
+    for (std::size_t k = native; k < point.size(); ++k) w = F.mul(w, F.sub(F.one(), point[k]));
+    LayerClaim c;
+    c.layer = layer;
+    c.terms.push_back(ClaimTerm{std::vector<U256>(point.begin(), point.begin() + static_cast<std::ptrdiff_t>(native)), w});
+    c.value = value;
+    return c;
+}
+
+/// Build split-eq tables on the device: for each (point, seed) pair, A =
+/// seed * eq(point[0..klo)), B = eq(point[klo..)). Returns the SplitEq view
+/// rooted at `dst` (which must hold K*(2^klo + 2^khi) elements).
+SplitEq build_split_eq(dgkr_ctx* ctx, const dgkr_field* f, const std::vector<std::vector<U256>>& points,
+                       const std::vector<U256>& seeds, Fe* dst, DBuf<EqJob>& jobs_buf, std::size_t small_off) {
+    const int K = static_cast<int>(points.size());
+    const int nv = K ? static_cast<int>(points[0].size()) : 0;
+    const int klo = (nv + 1) / 2, khi = nv - klo;
+    SplitEq e;
+    e.K = K;
+    e.klo = klo;
+    e.khi = khi;
+    e.A = dst;
+    e.B = dst + static_cast<std::size_t>(K) * (std::size_t{1} << klo);
+    // stage points and seeds in the small buffer
+    const std::size_t limit = small_off < dgkr_ctx::kEqOff2 ? dgkr_ctx::kEqOff2 : dgkr_ctx::kVxOff;
+    if (small_off + static_cast<std::size_t>(K) * (nv + 2) > limit) fail(DGKR_UNSUPPORTED, "too many claim terms");
+    Fe* hs = ctx->h_small + small_off;
+    Fe* ds = ctx->d_small.p + small_off;
+    std::size_t pos = 0;
+    std::vector<EqJob> jobs;
+    const U256 one = f->f.one();
+    for (int t = 0; t < K; ++t) {
+        const std::size_t pt_off = pos;
+        for (int k = 0; k < nv; ++k) hs[pos++] = to_fe(points[t][k]);
+        const std::size_t seed_off = pos;
+        hs[pos++] = to_fe(seeds[t]);
+        const std::size_t one_off = pos;
+        hs[pos++] = to_fe(one);
+        jobs.push_back(EqJob{ds + pt_off, ds + seed_off, const_cast<Fe*>(e.A) + (static_cast<std::size_t>(t) << klo), klo, 0});
+        jobs.push_back(EqJob{ds + pt_off + klo, ds + one_off, const_cast<Fe*>(e.B) + (static_cast<std::size_t>(t) << khi), khi, 0});
+    }
+    ctx->h2d(ds, hs, pos * sizeof(Fe));
+    jobs_buf.ensure(jobs.size() + 64);
+    // jobs go right after any previous jobs in jobs_buf: caller uses distinct buffers per build
+    ctx->h2d(jobs_buf.p, jobs.data(), jobs.size() * sizeof(EqJob));
+    launch_eq_build(ctx->use(f), jobs_buf.p, static_cast<int>(jobs.size()), ctx->st);
+    ctx->launched();
+    return e;
+}
+
+void evaluate_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_field* f, const std::uint8_t* inputs) {
+    const FieldKind kind = ctx->use(f);
+    const std::uint64_t n_in = static_cast<std::uint64_t>(c.input_size) * c.n_copies;
+    Fe* v0 = c.values[0]->p;
+    ctx->upload_elems(f, inputs, n_in, v0, c.stage);
+    if (c.capacity[0] > n_in) CK(cudaMemsetAsync(v0 + n_in, 0, (c.capacity[0] - n_in) * sizeof(Fe), ctx->st));
+    for (std::uint32_t li = 1; li <= c.depth; ++li) {
+        auto& C = *c.cons[li];
+        EvalLaunch el;
+        el.out = c.values[li]->p;
+        el.n_write = c.capacity[li];
+        el.n_gates = c.sub_size[li] * c.n_copies;
+        el.log_g = (c.n_copies > 1) ? c.sub_log[li] : 63;
+        el.gstart = C.gstart.p;
+        el.nested = C.nested.p;
+        el.layer_vals = c.d_layer_vals.p;
+        el.layer_log_stride = c.d_layer_log.p;
+        if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_evaluate(kind, el, ctx->st);
+        ctx->launched();
+        if (ctx->profile_on) {
+            CK(cudaEventRecord(ctx->ev1, ctx->st));
+            CK(cudaEventSynchronize(ctx->ev1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            ctx->prof.evaluate_ms += ms;
+        }
+    }
+}
+
+/// gkr_prove (gkr.hpp:182-244) on the device-resident circuit.
+std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_field* f, const std::uint8_t* inputs,
+                                    Transcript& tr) {
+    const HostField& F = f->f;
+    const FieldKind kind = ctx->use(f);
+    const std::size_t w = F.width();
+    evaluate_circuit(ctx, c, f, inputs);  // gkr.hpp:186
+
+    // absorb the padded output table (gkr.hpp:189-190): D2H canonical, serial SHA chain
+    const std::uint32_t out_layer = c.depth;
+    const std::uint64_t n_out = c.full_padded[out_layer];
+    std::vector<std::uint8_t> proof;
+    put32(proof, static_cast<std::uint32_t>(n_out));
+    const std::size_t out_off = proof.size();
+    proof.resize(out_off + n_out * w);
+    {
+        c.stage.ensure(n_out * w);
+        launch_to_canonical(kind, c.values[out_layer]->p, c.stage.p, static_cast<int>(w), n_out, ctx->st);
+        ctx->launched();
+        ctx->d2h(proof.data() + out_off, c.stage.p, n_out * w);
+        ctx->sync();
+        const double t0 = now_ms();
+        for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(proof.data() + out_off + i * w, w);
+        const double dt = now_ms() - t0;
+        ctx->prof.output_absorb_ms += dt;
+        ctx->prof.host_transcript_ms += dt;
+    }
+    // q and the output claim (gkr.hpp:192-202)
+    const std::uint32_t qlen = c.padded_log2_full(out_layer);
+    std::vector<U256> q;
+    for (std::uint32_t k = 0; k < qlen; ++k) q.push_back(tr.challenge());
+    // split-eq table space: (max claim terms + 1 u-table) x (2^ceil(L/2) + 2^floor(L/2))
+    std::uint32_t lmax = log2_exact(c.Tmax);
+    for (std::uint32_t l = 0; l <= c.depth; ++l) lmax = std::max(lmax, c.padded_log2_full(l));
+    const std::size_t per_term = (std::size_t{1} << ((lmax + 1) / 2)) + (std::size_t{1} << (lmax / 2));
+    const std::size_t max_terms = 2 * static_cast<std::size_t>(c.depth) * std::max<std::uint32_t>(c.max_slots, 1) + 2;
+    c.eq_tabs.ensure((max_terms + 2) * per_term);
+    U256 out_value;
+    {
+        SplitEq e = build_split_eq(ctx, f, {q}, {F.one()}, c.eq_tabs.p, c.eq_jobs, dgkr_ctx::kEqOff);
+        launch_dense_eval(kind, c.values[out_layer]->p, n_out, e, ctx->ws, ctx->st);
+        ctx->launched();
+        ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
+        ctx->sync();
+        out_value = to_u256(ctx->h_small[1]);
+    }
+    std::vector<std::vector<LayerClaim>> registry(out_layer + 1);
+    {
+        LayerClaim lc;
+        lc.layer = out_layer;
+        lc.terms.push_back(ClaimTerm{q, F.one()});
+        lc.value = out_value;
+        registry[out_layer].push_back(std::move(lc));
+    }
+    put32(proof, out_layer);
+    for (std::uint32_t layer = out_layer; layer >= 1; --layer) {
+        auto& C = *c.cons[layer];
+        std::vector<U256> alphas;
+        const double th = now_ms();
+        LayerClaim combined = combine_claims(std::move(registry[layer]), tr, F, &alphas);  // gkr.hpp:206-207
+        ctx->prof.host_transcript_ms += now_ms() - th;
+        registry[layer].clear();
+        const std::uint32_t side = C.side;
+        const std::uint64_t T = std::uint64_t{1} << side;
+        const int ns = static_cast<int>(C.slots.size());
+        // wire weights (gkr.hpp:135-152) as split-eq tables of the claim terms
+        std::vector<std::vector<U256>> pts;
+        std::vector<U256> seeds;
+        for (const auto& t : combined.terms) {
+            pts.push_back(t.point);
+            seeds.push_back(t.weight);
+        }
+        const std::uint32_t lgc = c.padded_log2_full(layer);
+        for (auto& p : pts)
+            if (p.size() != lgc) fail(DGKR_LOGIC_ERROR, "claim point length mismatch");
+        if (pts.size() > max_terms) fail(DGKR_UNSUPPORTED, "too many claim terms");
+        SplitEq wq = build_split_eq(ctx, f, pts, seeds, c.eq_tabs.p, c.eq_jobs, dgkr_ctx::kEqOff);
+        const std::size_t wq_elems = pts.size() * ((std::size_t{1} << wq.klo) + (std::size_t{1} << wq.khi));
+
+        // prove_layer_sum (sumcheck.hpp:342-448)
+        tr.absorb(combined.value);  // :364
+        BookkeepLaunch bk;
+        bk.slots = C.d_slots1.p;
+        bk.n_slots = ns;
+        bk.T = T;
+        bk.n_copies = c.n_copies;
+        bk.log_gcons = (c.n_copies > 1) ? c.sub_log[layer] : 63;
+        bk.G = c.G.p;
+        bk.w = wq;
+        if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_bookkeep_phase1(kind, bk, ctx->st);
+        ctx->launched();
+        if (ctx->profile_on) {
+            CK(cudaEventRecord(ctx->ev1, ctx->st));
+            CK(cudaEventSynchronize(ctx->ev1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            ctx->prof.bookkeep_ms += ms;
+        }
+        SumcheckRun p1 = run_rounds(ctx, f, ns, true, static_cast<int>(side), C.base_ptrs.p, c.rb, tr);
+        std::vector<U256> vx(ns);
+        for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
+        // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
+        std::vector<U256> one_seed{F.one()};
+        SplitEq uq = build_split_eq(ctx, f, {p1.challenges}, one_seed, c.eq_tabs.p + wq_elems, c.eq_jobs2,
+                                    dgkr_ctx::kEqOff2);
+        // vx to device
+        for (int m = 0; m < ns; ++m) ctx->h_small[dgkr_ctx::kVxOff + m] = to_fe(vx[m]);
+        ctx->h2d(ctx->d_small.p + dgkr_ctx::kVxOff, ctx->h_small + dgkr_ctx::kVxOff, ns * sizeof(Fe));
+        bk.slots = C.d_slots2.p;
+        bk.u = uq;
+        bk.vx = ctx->d_small.p + dgkr_ctx::kVxOff;
+        if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_bookkeep_phase2(kind, bk, ctx->st);
+        ctx->launched();
+        if (ctx->profile_on) {
+            CK(cudaEventRecord(ctx->ev1, ctx->st));
+            CK(cudaEventSynchronize(ctx->ev1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            ctx->prof.bookkeep_ms += ms;
+        }
+        SumcheckRun p2 = run_rounds(ctx, f, ns, true, static_cast<int>(side), C.base_ptrs.p, c.rb, tr);
+        std::vector<U256> finals = vx;
+        for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
+        std::vector<RoundPoly> rounds = p1.rounds;
+        rounds.insert(rounds.end(), p2.rounds.begin(), p2.rounds.end());
+        // registry (gkr.hpp:225-233)
+        for (int s = 0; s < ns; ++s) {
+            const std::uint32_t src = C.slots[s];
+            registry[src].push_back(shrink_claim(src, c.padded_log2_full(src), p1.challenges, finals[s], F));
+            registry[src].push_back(shrink_claim(src, c.padded_log2_full(src), p2.challenges, finals[ns + s], F));
+        }
+        // layer proof bytes
+        put32(proof, static_cast<std::uint32_t>(alphas.size()));
+        for (const auto& a : alphas) append_elem(proof, F, a);
+        const auto sb = sumcheck_bytes(F, combined.value, rounds, finals);
+        put32(proof, static_cast<std::uint32_t>(sb.size()));
+        proof.insert(proof.end(), sb.begin(), sb.end());
+    }
+    return proof;
+}
+
+// ---------------------------------------------------------------------------
+// PCS (pcs.hpp) on device
+// ---------------------------------------------------------------------------
+struct PcsDevice {
+    DBuf<Fe> m;              // rows x cols Montgomery
+    DBuf<std::uint8_t> nodes;  // 2*cols digests
+    DBuf<std::uint8_t> stage;
+};
+
+void pcs_build_tree(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols) {
+    d.nodes.ensure(2 * cols * 32);
+    launch_column_digests(ctx->use(f), d.m.p, cols, static_cast<int>(rows), static_cast<int>(f->f.width()),
+                          d.nodes.p + cols * 32, ctx->st);
+    ctx->launched();
+    launch_merkle(d.nodes.p, cols, ctx->st);
+    ctx->launched(cols > 1 ? log2_exact(cols) : 0);
+}
+
+void check_matrix(std::size_t rows, std::size_t cols) {
+    if (rows == 0 || cols == 0 || (cols & (cols - 1)) != 0 || (rows & (rows - 1)) != 0)
+        fail(DGKR_INVALID_ARGUMENT, "matrix dimensions must be nonzero powers of two");  // pcs.hpp:26-29
+}
+
+Digest pcs_commit(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols,
+                  const std::uint8_t* data) {
+    check_matrix(rows, cols);
+    d.m.ensure(rows * cols);
+    ctx->upload_elems(f, data, rows * cols, d.m.p, d.stage);
+    pcs_build_tree(ctx, f, d, rows, cols);
+    Digest root;
+    ctx->d2h(root.data(), d.nodes.p + 32, 32);
+    ctx->sync();
+    return root;
+}
+
+U256 chi_eval_host(std::uint64_t index, const std::vector<U256>& point, const HostField& F) {  // mle.hpp:111-120
+    U256 acc = F.one();
+    for (std::size_t k = 0; k < point.size(); ++k)
+        acc = F.mul(acc, ((index >> k) & 1) ? point[k] : F.sub(F.one(), point[k]));
+    return acc;
+}
+
+/// pcs::open (pcs.hpp:212-254) -> Opening::to_bytes
+std::vector<std::uint8_t> pcs_open(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows,
+                                   std::size_t cols, const std::uint8_t* data, const std::vector<U256>& r,
+                                   std::size_t q, Transcript& tr, U256* value_out) {
+    check_matrix(rows, cols);
+    const HostField& F = f->f;
+    const FieldKind kind = ctx->use(f);
+    const std::size_t w = F.width();
+    const std::uint32_t row_vars = log2_exact(cols), index_vars = log2_exact(rows);
+    if (r.size() != row_vars + index_vars) fail(DGKR_INVALID_ARGUMENT, "opening point has wrong dimension");
+    d.m.ensure(rows * cols);
+    ctx->upload_elems(f, data, rows * cols, d.m.p, d.stage);
+    std::vector<U256> r_low(r.begin(), r.begin() + row_vars), r_high(r.begin() + row_vars, r.end());
+    std::vector<U256> beta(rows);
+    for (std::size_t i = 0; i < rows; ++i) beta[i] = chi_eval_host(i, r_high, F);  // pcs.hpp:161-170
+    // row evaluations (dense MLE at r_low) with split-eq tables
+    DBuf<Fe> eqt;
+    DBuf<EqJob> jobs;
+    eqt.ensure(2 * ((std::size_t{1} << ((row_vars + 1) / 2)) + (std::size_t{1} << (row_vars / 2))) + 8);
+    SplitEq e = build_split_eq(ctx, f, {r_low}, {F.one()}, eqt.p, jobs, 16);
+    std::vector<U256> row_evals(rows);
+    U256 value{};
+    for (std::size_t i = 0; i < rows; ++i) {
+        launch_dense_eval(kind, d.m.p + i * cols, cols, e, ctx->ws, ctx->st);
+        ctx->launched();
+        ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
+        ctx->sync();
+        row_evals[i] = to_u256(ctx->h_small[1]);
+        value = F.add(value, F.mul(beta[i], row_evals[i]));
+    }
+    // combined row (pcs.hpp:233-239)
+    DBuf<Fe> comb, dbeta;
+    comb.ensure(cols);
+    dbeta.ensure(rows);
+    std::vector<Fe> hb(rows);
+    for (std::size_t i = 0; i < rows; ++i) hb[i] = to_fe(beta[i]);
+    ctx->h2d(dbeta.p, hb.data(), rows * sizeof(Fe));
+    launch_beta_combine(kind, d.m.p, cols, static_cast<int>(rows), dbeta.p, comb.p, ctx->st);
+    ctx->launched();
+    // leaves + tree (pcs.hpp:241-244)
+    pcs_build_tree(ctx, f, d, rows, cols);
+    std::vector<std::uint8_t> combined_bytes(cols * w);
+    d.stage.ensure(cols * w);
+    launch_to_canonical(kind, comb.p, d.stage.p, static_cast<int>(w), cols, ctx->st);
+    ctx->launched();
+    ctx->d2h(combined_bytes.data(), d.stage.p, cols * w);
+    Digest root;
+    ctx->d2h(root.data(), d.nodes.p + 32, 32);
+    ctx->sync();
+    // derive_spot_indices (pcs.hpp:185-208): serial transcript
+    const double t0 = now_ms();
+    tr.absorb_bytes(root.data(), 32);
+    for (const auto& x : r) tr.absorb(x);
+    tr.absorb(value);
+    for (const auto& x : row_evals) tr.absorb(x);
+    for (std::size_t j = 0; j < cols; ++j) tr.absorb_bytes(combined_bytes.data() + j * w, w);
+    std::vector<std::uint64_t> idx;
+    if (q >= cols) {
+        for (std::uint64_t j = 0; j < cols; ++j) idx.push_back(j);
+    } else {
+        std::vector<bool> seen(cols, false);
+        while (idx.size() < q) {
+            const std::uint64_t j = tr.challenge_index(cols);
+            if (!seen[j]) {
+                seen[j] = true;
+                idx.push_back(j);
+            }
+        }
+    }
+    ctx->prof.host_transcript_ms += now_ms() - t0;
+    // Opening::to_bytes (pcs.hpp:135-156)
+    std::vector<std::uint8_t> out;
+    put32(out, static_cast<std::uint32_t>(r.size()));
+    for (const auto& x : r) append_elem(out, F, x);
+    append_elem(out, F, value);
+    put32(out, static_cast<std::uint32_t>(rows));
+    for (const auto& x : row_evals) append_elem(out, F, x);
+    put32(out, static_cast<std::uint32_t>(cols));
+    out.insert(out.end(), combined_bytes.begin(), combined_bytes.end());
+    put32(out, static_cast<std::uint32_t>(idx.size()));
+    for (std::uint64_t j : idx) {
+        put32(out, static_cast<std::uint32_t>(j));
+        for (std::size_t i = 0; i < rows; ++i) {
+            const std::uint8_t* src = data + (i * cols + j) * w;
+            out.insert(out.end(), src, src + w);
+        }
+        // Merkle path (merkle.hpp:34-45): siblings leaf -> root
+        std::size_t node = cols + j;
+        while (node > 1) {
+            const std::size_t off = out.size();
+            out.resize(off + 32);
+            ctx->d2h(out.data() + off, d.nodes.p + (node ^ 1) * 32, 32);
+            node >>= 1;
+        }
+    }
+    ctx->sync();
+    if (value_out) *value_out = value;
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// TrafficStats (cluster.hpp:69-115), byte-accurate logical metering.
+// ---------------------------------------------------------------------------
+struct Traffic {
+    struct P {
+        std::uint64_t w2w = 0, w2m = 0, m2w = 0, mempool = 0;
+    };
+    P total;
+    std::vector<std::pair<std::string, P>> phases;  // sorted on output (std::map order)
+    std::string cur = "setup";
+    P& ph() {
+        for (auto& p : phases)
+            if (p.first == cur) return p.second;
+        phases.push_back({cur, P{}});
+        return phases.back().second;
+    }
+    void msg(std::size_t from, std::size_t to, std::size_t master, std::size_t bytes) {
+        if (from == to) return;
+        P& p = ph();
+        if (to == master) {
+            total.w2m += bytes;
+            p.w2m += bytes;
+        } else if (from == master) {
+            total.m2w += bytes;
+            p.m2w += bytes;
+        } else {
+            total.w2w += bytes;
+            p.w2w += bytes;
+        }
+    }
+    void mempool(std::size_t bytes) {
+        total.mempool += bytes;
+        ph().mempool += bytes;
+    }
+    std::string json() const {
+        auto obj = [](const P& p) {
+            return "{\"w2w\":" + std::to_string(p.w2w) + ",\"w2m\":" + std::to_string(p.w2m) +
+                   ",\"m2w\":" + std::to_string(p.m2w) + ",\"mempool\":" + std::to_string(p.mempool) + "}";
+        };
+        std::string s = "{\"w2w\":" + std::to_string(total.w2w) + ",\"w2m\":" + std::to_string(total.w2m) +
+                        ",\"m2w\":" + std::to_string(total.m2w) + ",\"mempool\":" + std::to_string(total.mempool) +
+                        ",\"phases\":";
+        if (phases.empty()) return s + "null}";
+        auto sorted = phases;
+        std::sort(sorted.begin(), sorted.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        s += "{";
+        for (std::size_t i = 0; i < sorted.size(); ++i) {
+            if (i) s += ",";
+            s += "\"" + sorted[i].first + "\":" + obj(sorted[i].second);
+        }
+        return s + "}}";
+    }
+};
+
+void write_json(const std::string& js, char* out, std::size_t cap) {
+    if (!out) return;
+    if (js.size() + 1 > cap) fail(DGKR_CAPACITY, "traffic json buffer too small");
+    std::memcpy(out, js.c_str(), js.size() + 1);
+}
+
+/// ClusterTopology::plan (cluster.hpp:38-57) -> K
+std::size_t plan_clusters(std::size_t n, std::size_t k) {
+    if (n == 0 || (n & (n - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "worker count must be a nonzero power of two");
+    if (k) {
+        if (k > n || n % k != 0) fail(DGKR_INVALID_ARGUMENT, "cluster count must divide worker count");
+        return k;
+    }
+    std::size_t log2n = log2_exact(n), clusters = 1;
+    while (clusters < log2n) clusters <<= 1;
+    return std::min(clusters, n);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* dgkr_last_error(void) { return g_err.c_str(); }
+int dgkr_abi_version(void) { return 1; }
+
+int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out) {
+    return guard([&] {
+        auto f = std::make_unique<dgkr_field>();
+        f->f = HostField(mod, len);
+        static const std::uint8_t bn[32] = {0x01, 0x00, 0x00, 0xf0, 0x93, 0xf5, 0xe1, 0x43, 0x91, 0x70, 0xb9,
+                                            0x79, 0x48, 0xe8, 0x33, 0x28, 0x5d, 0x58, 0x81, 0x81, 0xb6, 0x45,
+                                            0x50, 0xb8, 0x29, 0xa0, 0x31, 0xe1, 0x72, 0x4e, 0x64, 0x30};
+        HostField bnf(bn, 32);
+        f->kind = f->f.same(bnf) ? FieldKind::Bn254 : FieldKind::Runtime;
+        for (int i = 0; i < 4; ++i) {
+            f->rt.p[2 * i] = static_cast<std::uint32_t>(f->f.p().w[i]);
+            f->rt.p[2 * i + 1] = static_cast<std::uint32_t>(f->f.p().w[i] >> 32);
+            f->rt.r2[2 * i] = static_cast<std::uint32_t>(f->f.r2().w[i]);
+            f->rt.r2[2 * i + 1] = static_cast<std::uint32_t>(f->f.r2().w[i] >> 32);
+            f->rt.one[2 * i] = static_cast<std::uint32_t>(f->f.one().w[i]);
+            f->rt.one[2 * i + 1] = static_cast<std::uint32_t>(f->f.one().w[i] >> 32);
+        }
+        f->rt.np0 = static_cast<std::uint32_t>(f->f.np0());
+        *out = f.release();
+    });
+}
+void dgkr_field_destroy(dgkr_field* f) { delete f; }
+std::size_t dgkr_field_width(const dgkr_field* f) { return f ? f->f.width() : 0; }
+std::size_t dgkr_field_bits(const dgkr_field* f) { return f ? f->f.bits() : 0; }
+
+int dgkr_transcript_init(const dgkr_field* f, const char* label, dgkr_transcript* t) {
+    return guard([&] {
+        Transcript tr(&f->f, label ? label : "");
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = 0;
+    });
+}
+int dgkr_transcript_absorb_bytes(const dgkr_field* f, dgkr_transcript* t, const std::uint8_t* d, std::size_t n) {
+    return guard([&] {
+        Transcript tr(&f->f, t->state, t->draws);
+        tr.absorb_bytes(d, n);
+        std::memcpy(t->state, tr.state().data(), 32);
+    });
+}
+int dgkr_transcript_absorb_u64(const dgkr_field* f, dgkr_transcript* t, std::uint64_t v) {
+    return guard([&] {
+        Transcript tr(&f->f, t->state, t->draws);
+        tr.absorb_u64(v);
+        std::memcpy(t->state, tr.state().data(), 32);
+    });
+}
+int dgkr_transcript_absorb_elems(const dgkr_field* f, dgkr_transcript* t, const std::uint8_t* e, std::size_t n) {
+    return guard([&] {
+        Transcript tr(&f->f, t->state, t->draws);
+        const std::size_t w = f->f.width();
+        for (std::size_t i = 0; i < n; ++i) {
+            f->f.from_bytes(e + i * w);  // canonical check (field.hpp:183-185)
+            tr.absorb_bytes(e + i * w, w);
+        }
+        std::memcpy(t->state, tr.state().data(), 32);
+    });
+}
+int dgkr_transcript_challenge(const dgkr_field* f, dgkr_transcript* t, std::uint8_t* out) {
+    return guard([&] {
+        Transcript tr(&f->f, t->state, t->draws);
+        f->f.to_bytes(tr.challenge(), out);
+        t->draws = tr.draws();
+    });
+}
+int dgkr_transcript_challenge_index(const dgkr_field* f, dgkr_transcript* t, std::uint64_t bound, std::uint64_t* out) {
+    return guard([&] {
+        Transcript tr(&f->f, t->state, t->draws);
+        *out = tr.challenge_index(bound);
+        t->draws = tr.draws();
+    });
+}
+int dgkr_sha256(const std::uint8_t* d, std::size_t n, std::uint8_t* out32) {
+    return guard([&] {
+        const Digest h = sha256(d, n);
+        std::memcpy(out32, h.data(), 32);
+    });
+}
+int dgkr_sha256_has_shani(void) { return sha256_has_shani() ? 1 : 0; }
+
+int dgkr_ctx_create(int device, dgkr_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(DGKR_CUDA_ERROR, "no such CUDA device");
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) fail(DGKR_UNSUPPORTED, "this build targets sm_100a (B200)");
+        auto c = std::make_unique<dgkr_ctx>();
+        c->device = device;
+        c->sms = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        c->ws.num_sms = c->sms;
+        c->ws.max_blocks = c->sms * 8;
+        c->partials.ensure(static_cast<std::size_t>(c->ws.max_blocks) * 3);
+        c->result.ensure(4);
+        c->counter.ensure(1);
+        CK(cudaMemset(c->counter.p, 0, sizeof(unsigned)));
+        c->ws.partials = c->partials.p;
+        c->ws.result = c->result.p;
+        c->ws.counter = c->counter.p;
+        c->d_small.ensure(dgkr_ctx::kSmall);
+        c->d_err.ensure(1);
+        CK(cudaMemset(c->d_err.p, 0, sizeof(int)));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_small), dgkr_ctx::kSmall * sizeof(Fe)));
+        CK(cudaEventCreate(&c->ev0));
+        CK(cudaEventCreate(&c->ev1));
+        *out = c.release();
+    });
+}
+void dgkr_ctx_destroy(dgkr_ctx* ctx) { delete ctx; }
+int dgkr_ctx_set_profile(dgkr_ctx* ctx, int on) {
+    return guard([&] { ctx->profile_on = on != 0; });
+}
+int dgkr_ctx_get_profile(dgkr_ctx* ctx, dgkr_profile* out) {
+    return guard([&] { *out = ctx->prof; });
+}
+int dgkr_ctx_device_info(dgkr_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor) {
+    return guard([&] {
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, ctx->device));
+        *sm_count = prop.multiProcessorCount;
+        *cc_major = prop.major;
+        *cc_minor = prop.minor;
+    });
+}
+
+int dgkr_prove_product_sum(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_pairs, std::size_t vars,
+                           const std::uint8_t* tables, dgkr_transcript* t, std::uint8_t* proof, std::size_t cap,
+                           std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        Transcript tr(&f->f, t->state, t->draws);
+        auto bytes = product_sumcheck(ctx, f, n_pairs, vars, tables, tr, nullptr);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_prove_layer_sum(dgkr_ctx* ctx, const dgkr_field* f, std::size_t side_vars, std::size_t n_slots,
+                         const std::uint8_t* slot_tables, std::size_t n_wires, const std::uint32_t* wire_meta,
+                         const std::uint64_t* wire_idx, const std::uint8_t* wire_weights, const std::uint8_t* claimed,
+                         dgkr_transcript* t, std::uint8_t* proof, std::size_t cap, std::size_t* len,
+                         std::uint8_t* x_point, std::uint8_t* y_point) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const HostField& F = f->f;
+        const FieldKind kind = ctx->use(f);
+        if (side_vars > 40) fail(DGKR_INVALID_ARGUMENT, "table too large");
+        const std::uint64_t T = std::uint64_t{1} << side_vars;
+        if (n_slots == 0) fail(DGKR_INVALID_ARGUMENT, "layer sum needs at least one slot");
+        for (std::size_t i = 0; i < n_wires; ++i) {  // sumcheck.hpp:354-359
+            if (wire_meta[3 * i + 1] >= n_slots || wire_meta[3 * i + 2] >= n_slots || wire_idx[2 * i] >= T ||
+                wire_idx[2 * i + 1] >= T)
+                fail(DGKR_INVALID_ARGUMENT, "layer wire index out of range");
+        }
+        const U256 cl = F.from_bytes(claimed);
+        Transcript tr(&f->f, t->state, t->draws);
+        DBuf<Fe> V, Hb, Gb, W;
+        DBuf<std::uint8_t> stage;
+        V.ensure(n_slots * T);
+        ctx->upload_elems(f, slot_tables, n_slots * T, V.p, stage);
+        W.ensure(n_wires);
+        ctx->upload_elems(f, wire_weights, n_wires, W.p, stage);
+        Hb.ensure(n_slots * T);
+        Gb.ensure(T);
+        // CSR transposes by (slot, x) and (slot, y)
+        std::vector<std::uint32_t> xoff(n_slots * (T + 1), 0), yoff(n_slots * (T + 1), 0);
+        for (std::size_t i = 0; i < n_wires; ++i) {
+            xoff[wire_meta[3 * i + 1] * (T + 1) + wire_idx[2 * i] + 1]++;
+            yoff[wire_meta[3 * i + 2] * (T + 1) + wire_idx[2 * i + 1] + 1]++;
+        }
+        std::uint32_t ax = 0, ay = 0;
+        for (std::size_t s = 0; s < n_slots; ++s) {
+            xoff[s * (T + 1)] += ax;
+            yoff[s * (T + 1)] += ay;
+            for (std::uint64_t i = 1; i <= T; ++i) {
+                xoff[s * (T + 1) + i] += xoff[s * (T + 1) + i - 1];
+                yoff[s * (T + 1) + i] += yoff[s * (T + 1) + i - 1];
+            }
+            ax = xoff[s * (T + 1) + T];
+            ay = yoff[s * (T + 1) + T];
+        }
+        std::vector<uint4> xent(n_wires), yent(n_wires);
+        std::vector<std::uint32_t> xf(xoff), yf(yoff);
+        for (std::size_t i = 0; i < n_wires; ++i) {
+            const std::uint32_t mul = wire_meta[3 * i] ? 0x80000000u : 0u;
+            const std::uint32_t xs = wire_meta[3 * i + 1], ys = wire_meta[3 * i + 2];
+            const std::uint32_t xi = static_cast<std::uint32_t>(wire_idx[2 * i]);
+            const std::uint32_t yi = static_cast<std::uint32_t>(wire_idx[2 * i + 1]);
+            xent[xf[xs * (T + 1) + xi]++] = make_uint4(0, yi, ys | mul, static_cast<std::uint32_t>(i));
+            yent[yf[ys * (T + 1) + yi]++] = make_uint4(0, xi, xs | mul, static_cast<std::uint32_t>(i));
+        }
+        DBuf<std::uint32_t> dxo, dyo;
+        DBuf<uint4> dxe, dye;
+        dxo.ensure(xoff.size());
+        dyo.ensure(yoff.size());
+        dxe.ensure(n_wires);
+        dye.ensure(n_wires);
+        ctx->h2d(dxo.p, xoff.data(), xoff.size() * 4);
+        ctx->h2d(dyo.p, yoff.data(), yoff.size() * 4);
+        if (n_wires) {
+            ctx->h2d(dxe.p, xent.data(), n_wires * sizeof(uint4));
+            ctx->h2d(dye.p, yent.data(), n_wires * sizeof(uint4));
+        }
+        std::vector<SlotDesc> s1(n_slots), s2(n_slots);
+        const std::uint32_t ls = static_cast<std::uint32_t>(side_vars);
+        for (std::size_t s = 0; s < n_slots; ++s) {
+            s1[s] = SlotDesc{V.p + s * T, Hb.p + s * T, dxo.p + s * (T + 1), dxe.p, ls, 0};
+            s2[s] = SlotDesc{V.p + s * T, Hb.p + s * T, dyo.p + s * (T + 1), dye.p, ls, 0};
+        }
+        DBuf<SlotDesc> ds1, ds2;
+        ds1.ensure(n_slots);
+        ds2.ensure(n_slots);
+        ctx->h2d(ds1.p, s1.data(), n_slots * sizeof(SlotDesc));
+        ctx->h2d(ds2.p, s2.data(), n_slots * sizeof(SlotDesc));
+        std::vector<const Fe*> bp;
+        for (std::size_t s = 0; s < n_slots; ++s) {
+            bp.push_back(V.p + s * T);
+            bp.push_back(Hb.p + s * T);
+        }
+        bp.push_back(Gb.p);
+        DBuf<const Fe*> dbp;
+        dbp.ensure(bp.size());
+        ctx->h2d(dbp.p, bp.data(), bp.size() * sizeof(const Fe*));
+
+        tr.absorb(cl);  // sumcheck.hpp:364
+        BookkeepLaunch bk;
+        bk.slots = ds1.p;
+        bk.n_slots = static_cast<int>(n_slots);
+        bk.T = T;
+        bk.n_copies = 1;
+        bk.log_gcons = 63;
+        bk.G = Gb.p;
+        bk.wire_w = W.p;
+        launch_bookkeep_phase1(kind, bk, ctx->st);
+        ctx->launched();
+        RoundBuffers rb;
+        SumcheckRun p1 = run_rounds(ctx, f, static_cast<int>(n_slots), true, static_cast<int>(side_vars), dbp.p, rb, tr);
+        std::vector<U256> vx(n_slots);
+        for (std::size_t m = 0; m < n_slots; ++m) vx[m] = p1.finals[2 * m];
+        DBuf<Fe> eqt;
+        DBuf<EqJob> jobs;
+        eqt.ensure(2 * ((std::size_t{1} << ((side_vars + 1) / 2)) + (std::size_t{1} << (side_vars / 2))) + 8);
+        SplitEq uq = build_split_eq(ctx, f, {p1.challenges}, {F.one()}, eqt.p, jobs, 16);
+        for (std::size_t m = 0; m < n_slots; ++m) ctx->h_small[8192 + m] = to_fe(vx[m]);
+        ctx->h2d(ctx->d_small.p + 8192, ctx->h_small + 8192, n_slots * sizeof(Fe));
+        bk.slots = ds2.p;
+        bk.u = uq;
+        bk.vx = ctx->d_small.p + 8192;
+        launch_bookkeep_phase2(kind, bk, ctx->st);
+        ctx->launched();
+        SumcheckRun p2 = run_rounds(ctx, f, static_cast<int>(n_slots), true, static_cast<int>(side_vars), dbp.p, rb, tr);
+        std::vector<U256> finals = vx;
+        for (std::size_t m = 0; m < n_slots; ++m) finals.push_back(p2.finals[2 * m]);
+        std::vector<RoundPoly> rounds = p1.rounds;
+        rounds.insert(rounds.end(), p2.rounds.begin(), p2.rounds.end());
+        if (x_point)
+            for (std::size_t k = 0; k < side_vars; ++k) F.to_bytes(p1.challenges[k], x_point + k * F.width());
+        if (y_point)
+            for (std::size_t k = 0; k < side_vars; ++k) F.to_bytes(p2.challenges[k], y_point + k * F.width());
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(sumcheck_bytes(F, cl, rounds, finals), proof, cap, len);
+    });
+}
+
+int dgkr_circuit_create(dgkr_ctx* ctx, std::uint32_t input_size, std::uint32_t depth, const std::uint64_t* lgs,
+                        const std::uint64_t* gns, const std::uint32_t* nested, const std::uint64_t* min_padded,
+                        std::uint32_t n_copies, dgkr_circuit** out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_copies == 0 || (n_copies & (n_copies - 1)) != 0)
+            fail(DGKR_INVALID_ARGUMENT, "n_copies must be a power of two");
+        auto c = std::make_unique<dgkr_circuit>();
+        c->input_size = input_size;
+        c->depth = depth;
+        c->n_copies = n_copies;
+        c->log_copies = log2_exact(n_copies);
+        build_circuit(ctx, *c, lgs, gns, nested, min_padded);
+        *out = c.release();
+    });
+}
+void dgkr_circuit_destroy(dgkr_circuit* c) { delete c; }
+std::size_t dgkr_circuit_output_size(const dgkr_circuit* c) { return c ? c->full_padded[c->depth] : 0; }
+
+int dgkr_circuit_evaluate(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* inputs,
+                          std::uint8_t* outputs, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        evaluate_circuit(ctx, *c, f, inputs);
+        const std::size_t w = f->f.width();
+        const std::uint64_t n_out = c->full_padded[c->depth];
+        *len = n_out * w;
+        if (n_out * w > cap) fail(DGKR_CAPACITY, "output buffer too small");
+        c->stage.ensure(n_out * w);
+        launch_to_canonical(ctx->use(f), c->values[c->depth]->p, c->stage.p, static_cast<int>(w), n_out, ctx->st);
+        ctx->d2h(outputs, c->stage.p, n_out * w);
+        ctx->sync();
+        ctx->end_call();
+    });
+}
+
+std::size_t dgkr_gkr_proof_bound(const dgkr_circuit* c, const dgkr_field* f) {
+    if (!c || !f) return 0;
+    const std::size_t w = f->f.width();
+    std::size_t b = 8 + c->full_padded[c->depth] * w;
+    for (std::uint32_t li = 1; li <= c->depth; ++li) {
+        const auto& C = *c->cons[li];
+        b += 16 + w + 4 * w * 2 * C.side + 2 * C.slots.size() * w + 2 * c->depth * w + 64;
+    }
+    return b;
+}
+
+int dgkr_gkr_prove(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* inputs, dgkr_transcript* t,
+                   std::uint8_t* proof, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        Transcript tr(&f->f, t->state, t->draws);
+        auto bytes = gkr_prove(ctx, *c, f, inputs, tr);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_pcs_commit(dgkr_ctx* ctx, const dgkr_field* f, std::size_t rows, std::size_t cols, const std::uint8_t* data,
+                    std::uint8_t* root32) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        PcsDevice d;
+        const Digest root = pcs_commit(ctx, f, d, rows, cols, data);
+        std::memcpy(root32, root.data(), 32);
+        ctx->end_call();
+    });
+}
+
+int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, std::size_t rows, std::size_t cols, const std::uint8_t* data,
+                  const std::uint8_t* r, std::size_t r_len, std::size_t q, dgkr_transcript* t, std::uint8_t* out,
+                  std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const HostField& F = f->f;
+        std::vector<U256> pt(r_len);
+        for (std::size_t i = 0; i < r_len; ++i) pt[i] = F.from_bytes(r + i * F.width());
+        Transcript tr(&f->f, t->state, t->draws);
+        PcsDevice d;
+        auto bytes = pcs_open(ctx, f, d, rows, cols, data, pt, q, tr, nullptr);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, out, cap, len);
+    });
+}
+
+int dgkr_dist_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::size_t n_pairs,
+                       std::size_t vars, const std::uint8_t* tables, dgkr_transcript* t, std::uint8_t* proof,
+                       std::size_t cap, std::size_t* len, char* traffic_json, std::size_t json_cap) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "nothing to shard");  // cluster.hpp:192-194
+        const std::uint64_t total = std::uint64_t{1} << vars;
+        if (n_workers == 0 || total % n_workers != 0)
+            fail(DGKR_INVALID_ARGUMENT, "worker count must divide table size");  // :196-198
+        plan_clusters(n_workers, 0);
+        // dist_sumcheck is byte-identical to the single-machine prover over
+        // the concatenated tables (cluster.hpp:219-227); on one device the
+        // shards are contiguous slices of the same tables.
+        Transcript tr(&f->f, t->state, t->draws);
+        auto bytes = product_sumcheck(ctx, f, n_pairs, vars, tables, tr, nullptr);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        // logical metering (cluster.hpp:258-298)
+        Traffic ts;
+        ts.cur = "sumcheck";
+        const std::size_t w = f->f.width();
+        const std::size_t local_vars = log2_exact(total / n_workers);
+        for (std::size_t i = 0; i < n_workers; ++i) ts.msg(i, 0, 0, w);
+        for (std::size_t j = 0; j < local_vars; ++j) {
+            for (std::size_t i = 0; i < n_workers; ++i) ts.msg(i, 0, 0, 4 * w);
+            for (std::size_t i = 0; i < n_workers; ++i) ts.msg(0, i, 0, w);
+        }
+        for (std::size_t i = 0; i < n_workers; ++i) ts.msg(i, 0, 0, 2 * n_pairs * w);
+        write_json(ts.json(), traffic_json, json_cap);
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::size_t n_clusters,
+                std::size_t row_vars, const std::uint8_t* rows, const std::uint8_t* r, std::size_t r_len,
+                std::size_t q, std::uint8_t* roots_out, std::size_t* n_roots, std::uint8_t* open_out, std::size_t cap,
+                std::size_t* open_len, std::uint8_t* combined_out, char* traffic_json, std::size_t json_cap) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const HostField& F = f->f;
+        const std::size_t K = plan_clusters(n_workers, n_clusters);
+        const std::size_t M = n_workers / K;
+        const std::size_t cols = std::size_t{1} << row_vars;
+        const std::size_t w = F.width();
+        const std::size_t row_bytes = cols * w;
+        Traffic ts;
+        ts.cur = "commit";
+        // mempool writes (cluster.hpp:349-361): every worker row lands in its
+        // cluster leader's buffer; rows of one cluster are contiguous here.
+        for (std::size_t i = 0; i < n_workers; ++i) {
+            for (std::size_t e = 0; e < cols; ++e) F.from_bytes(rows + i * row_bytes + e * w);
+            ts.mempool(row_bytes);
+        }
+        std::vector<PcsDevice> dev(K);
+        for (std::size_t c = 0; c < K; ++c) {
+            const Digest root = pcs_commit(ctx, f, dev[c], M, cols, rows + c * M * row_bytes);
+            std::memcpy(roots_out + 32 * c, root.data(), 32);
+            ts.msg(c * M, 0, 0, 32);
+        }
+        *n_roots = K;
+        ts.cur = "open";
+        std::size_t member_vars = log2_exact(M), cluster_vars = log2_exact(K);
+        if (r_len != row_vars + member_vars + cluster_vars) fail(DGKR_INVALID_ARGUMENT, "opening point has wrong dimension");
+        std::vector<U256> pt(r_len);
+        for (std::size_t i = 0; i < r_len; ++i) pt[i] = F.from_bytes(r + i * w);
+        std::vector<U256> r_local(pt.begin(), pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars));
+        std::vector<U256> r_top(pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars), pt.end());
+        std::vector<std::uint8_t> all;
+        U256 combined{};
+        for (std::size_t c = 0; c < K; ++c) {
+            Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
+            tr.absorb_u64(c);
+            U256 value;
+            auto op = pcs_open(ctx, f, dev[c], M, cols, rows + c * M * row_bytes, r_local, q, tr, &value);
+            ts.msg(c * M, 0, 0, op.size());
+            combined = F.add(combined, F.mul(chi_eval_host(c, r_top, F), value));
+            put32(all, static_cast<std::uint32_t>(op.size()));
+            all.insert(all.end(), op.begin(), op.end());
+        }
+        F.to_bytes(combined, combined_out);
+        write_json(ts.json(), traffic_json, json_cap);
+        ctx->end_call();
+        emit(all, open_out, cap, open_len);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,343 @@
+"""Python mirror of the reference prover API over the C ABI
+(``include/dgkr_b200.h``). Names and argument meaning follow
+``/root/reference/proj/include/dgkr`` so the parity tests read like the
+reference's own tests; every prover call runs on the GPU through
+``libdgkr_b200.so`` (no CPU fallback).
+
+Field elements are passed either as Python ints (converted to canonical
+little-endian bytes) or as ready canonical byte buffers (``bytes`` /
+``numpy.uint8`` arrays), which is what the benchmark uses.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple, Union
+
+import numpy as np
+
+from ._lib import Profile_t, Transcript_t, check, lib
+
+BN254_P = 21888242871839275222246405745257275088548364400416034343698204186575808495617
+GOLDILOCKS_P = 18446744069414584321
+
+Elems = Union[bytes, bytearray, memoryview, np.ndarray, Sequence[int]]
+
+
+def _buf(b) -> C.c_void_p:
+    if isinstance(b, np.ndarray):
+        return b.ctypes.data_as(C.c_void_p)
+    return C.cast(C.c_char_p(bytes(b)), C.c_void_p)
+
+
+class Field:
+    """FieldConfig (field.hpp:23-80)."""
+
+    def __init__(self, modulus: int):
+        self.p = int(modulus)
+        mb = self.p.to_bytes(max(1, (self.p.bit_length() + 7) // 8), "little")
+        h = C.c_void_p()
+        check(lib().dgkr_field_create(C.c_char_p(mb), C.c_size_t(len(mb)), C.byref(h)))
+        self._h = h
+        self.width = int(lib().dgkr_field_width(h))
+        self.bits = int(lib().dgkr_field_bits(h))
+
+    @staticmethod
+    def bn254() -> "Field":
+        return Field(BN254_P)
+
+    @staticmethod
+    def goldilocks() -> "Field":
+        return Field(GOLDILOCKS_P)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dgkr_field_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def encode(self, vals: Elems) -> bytes:
+        """canonical LE bytes (field.hpp:159-167) of a sequence of ints, or
+        pass-through of ready byte buffers"""
+        if isinstance(vals, (bytes, bytearray, memoryview)):
+            return bytes(vals)
+        if isinstance(vals, np.ndarray):
+            return vals.astype(np.uint8, copy=False).tobytes()
+        w = self.width
+        return b"".join(int(v).to_bytes(w, "little") for v in vals)
+
+    def decode(self, b: bytes) -> List[int]:
+        w = self.width
+        return [int.from_bytes(b[i:i + w], "little") for i in range(0, len(b), w)]
+
+
+class Transcript:
+    """dgkr::Transcript (transcript.hpp:17-130); host-side SHA-256 chain."""
+
+    def __init__(self, field: Field, label: str, pre: Sequence[int] = ()):
+        self.field = field
+        self.t = Transcript_t()
+        check(lib().dgkr_transcript_init(field.handle, label.encode(), C.byref(self.t)))
+        for v in pre:
+            self.absorb_u64(v)
+
+    def absorb_bytes(self, data: bytes) -> None:
+        check(lib().dgkr_transcript_absorb_bytes(self.field.handle, C.byref(self.t), C.c_char_p(bytes(data)),
+                                                 C.c_size_t(len(data))))
+
+    def absorb(self, v: int) -> None:
+        b = self.field.encode([v])
+        check(lib().dgkr_transcript_absorb_elems(self.field.handle, C.byref(self.t), C.c_char_p(b), C.c_size_t(1)))
+
+    def absorb_elems(self, vals: Elems) -> None:
+        b = self.field.encode(vals)
+        check(lib().dgkr_transcript_absorb_elems(self.field.handle, C.byref(self.t), C.c_char_p(b),
+                                                 C.c_size_t(len(b) // self.field.width)))
+
+    def absorb_u64(self, v: int) -> None:
+        check(lib().dgkr_transcript_absorb_u64(self.field.handle, C.byref(self.t), C.c_uint64(v)))
+
+    def challenge(self) -> int:
+        out = C.create_string_buffer(self.field.width)
+        check(lib().dgkr_transcript_challenge(self.field.handle, C.byref(self.t), out))
+        return int.from_bytes(out.raw, "little")
+
+    def challenge_index(self, bound: int) -> int:
+        out = C.c_uint64()
+        check(lib().dgkr_transcript_challenge_index(self.field.handle, C.byref(self.t), C.c_uint64(bound),
+                                                    C.byref(out)))
+        return out.value
+
+    @property
+    def state(self) -> bytes:
+        return bytes(self.t.state)
+
+    @property
+    def draws(self) -> int:
+        return int(self.t.draws)
+
+
+def sha256(data: bytes) -> bytes:
+    out = C.create_string_buffer(32)
+    check(lib().dgkr_sha256(C.c_char_p(bytes(data)), C.c_size_t(len(data)), out))
+    return out.raw
+
+
+class Context:
+    """One CUDA device + stream + workspaces (dgkr_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().dgkr_ctx_create(C.c_int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dgkr_ctx_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_profile(self, on: bool) -> None:
+        check(lib().dgkr_ctx_set_profile(self._h, C.c_int(1 if on else 0)))
+
+    def profile(self) -> dict:
+        p = Profile_t()
+        check(lib().dgkr_ctx_get_profile(self._h, C.byref(p)))
+        return p.as_dict()
+
+    def device_info(self) -> Tuple[int, int, int]:
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        check(lib().dgkr_ctx_device_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+
+def _out(cap: int):
+    return C.create_string_buffer(max(1, cap)), C.c_size_t()
+
+
+def prove_product_sum(ctx: Context, pairs: Sequence[Tuple[Elems, Elems]], tr: Transcript) -> bytes:
+    """prove_product_sum (sumcheck.hpp:226-241) -> SumcheckProof::to_bytes."""
+    f = tr.field
+    tabs = [f.encode(x) for pair in pairs for x in pair]
+    n = len(tabs[0]) // f.width if tabs else 0
+    vars_ = max(0, n.bit_length() - 1)
+    if tabs and any(len(t) != len(tabs[0]) for t in tabs):
+        from ._lib import InvalidArgument
+
+        raise InvalidArgument(1, "mixed table sizes in product sum")
+    if n & (n - 1):
+        from ._lib import InvalidArgument
+
+        raise InvalidArgument(1, "table size must be 2^num_vars")
+    data = b"".join(tabs)
+    cap = 64 + (vars_ + 2) * 4 * f.width + 2 * len(pairs) * f.width + 64
+    out, ln = _out(cap)
+    check(lib().dgkr_prove_product_sum(ctx.handle, f.handle, C.c_size_t(len(pairs)), C.c_size_t(vars_),
+                                       C.c_char_p(data), C.byref(tr.t), out, C.c_size_t(cap), C.byref(ln)))
+    return out.raw[: ln.value]
+
+
+def prove_layer_sum(ctx: Context, side_vars: int, slot_tables: Sequence[Elems], wires, claimed: int,
+                    tr: Transcript):
+    """prove_layer_sum (sumcheck.hpp:342-448). wires: objects with is_mul,
+    weight, x_slot, y_slot, x_index, y_index. Returns (proof bytes, x_point,
+    y_point)."""
+    f = tr.field
+    meta = np.array([(int(w.is_mul), w.x_slot, w.y_slot) for w in wires], dtype=np.uint32).reshape(-1, 3)
+    idx = np.array([(w.x_index, w.y_index) for w in wires], dtype=np.uint64).reshape(-1, 2)
+    weights = f.encode([w.weight for w in wires])
+    tables = b"".join(f.encode(t) for t in slot_tables)
+    cap = 64 + (2 * side_vars + 2) * 4 * f.width + 2 * len(slot_tables) * f.width + 64
+    out, ln = _out(cap)
+    xp = C.create_string_buffer(max(1, side_vars * f.width))
+    yp = C.create_string_buffer(max(1, side_vars * f.width))
+    check(lib().dgkr_prove_layer_sum(ctx.handle, f.handle, C.c_size_t(side_vars), C.c_size_t(len(slot_tables)),
+                                     C.c_char_p(tables), C.c_size_t(len(wires)), _buf(meta), _buf(idx),
+                                     C.c_char_p(weights), C.c_char_p(f.encode([claimed])), C.byref(tr.t), out,
+                                     C.c_size_t(cap), C.byref(ln), xp, yp))
+    return out.raw[: ln.value], f.decode(xp.raw[: side_vars * f.width]), f.decode(yp.raw[: side_vars * f.width])
+
+
+class Circuit:
+    """Device-resident GeneralCircuit (circuit.hpp:63) in the flat layout of
+    include/dgkr_b200.h; n_copies > 1 replicates it data-parallel (Sisu)."""
+
+    def __init__(self, ctx: Context, input_size: int, layer_gate_start, gate_nested_start, nested,
+                 min_padded=None, n_copies: int = 1):
+        self.ctx = ctx
+        self.input_size = int(input_size)
+        self.n_copies = int(n_copies)
+        lgs = np.ascontiguousarray(layer_gate_start, dtype=np.uint64)
+        gns = np.ascontiguousarray(gate_nested_start, dtype=np.uint64)
+        nst = np.ascontiguousarray(nested, dtype=np.uint32).reshape(-1, 5)
+        self.depth = len(lgs) - 1
+        mp = None if min_padded is None else np.ascontiguousarray(min_padded, dtype=np.uint64)
+        h = C.c_void_p()
+        check(lib().dgkr_circuit_create(ctx.handle, C.c_uint32(self.input_size), C.c_uint32(self.depth), _buf(lgs),
+                                        _buf(gns), _buf(nst) if len(nst) else C.c_void_p(None),
+                                        _buf(mp) if mp is not None else C.c_void_p(None),
+                                        C.c_uint32(self.n_copies), C.byref(h)))
+        self._h = h
+        self.n_gates = int(lgs[-1]) * self.n_copies
+        self.output_size = int(lib().dgkr_circuit_output_size(h))
+
+    @staticmethod
+    def from_oracle(ctx: Context, c, n_copies: int = 1) -> "Circuit":
+        lgs, gns, nested, minp = c.to_flat()
+        return Circuit(ctx, c.input_size, lgs, gns, nested, minp, n_copies)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dgkr_circuit_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def evaluate(self, field: Field, inputs: Elems) -> bytes:
+        """padded output layer, canonical bytes (circuit.hpp:164-193)"""
+        data = field.encode(inputs)
+        cap = self.output_size * field.width
+        out, ln = _out(cap)
+        check(lib().dgkr_circuit_evaluate(self.ctx.handle, self._h, field.handle, _buf(np.frombuffer(data, np.uint8)),
+                                          out, C.c_size_t(cap), C.byref(ln)))
+        return out.raw[: ln.value]
+
+    def proof_bound(self, field: Field) -> int:
+        return int(lib().dgkr_gkr_proof_bound(self._h, field.handle))
+
+
+def gkr_prove(ctx: Context, circuit: Circuit, inputs: Elems, tr: Transcript, out_buf=None) -> bytes:
+    """gkr_prove (gkr.hpp:182-244) -> GkrProof bytes (layout in dgkr_b200.h)."""
+    f = tr.field
+    data = inputs if isinstance(inputs, np.ndarray) else np.frombuffer(f.encode(inputs), np.uint8)
+    cap = circuit.proof_bound(f)
+    if out_buf is None or len(out_buf) < cap:
+        out_buf = C.create_string_buffer(cap)
+    ln = C.c_size_t()
+    check(lib().dgkr_gkr_prove(ctx.handle, circuit.handle, f.handle, _buf(data), C.byref(tr.t), out_buf,
+                               C.c_size_t(cap), C.byref(ln)))
+    return out_buf.raw[: ln.value]
+
+
+def pcs_commit(ctx: Context, field: Field, rows: Sequence[Elems]) -> bytes:
+    """pcs::commit (pcs.hpp:105-113) -> 32-byte root"""
+    data = b"".join(field.encode(r) for r in rows)
+    cols = len(field.encode(rows[0])) // field.width
+    root = C.create_string_buffer(32)
+    check(lib().dgkr_pcs_commit(ctx.handle, field.handle, C.c_size_t(len(rows)), C.c_size_t(cols),
+                                C.c_char_p(data), root))
+    return root.raw
+
+
+def pcs_open(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], tr: Transcript,
+             spot_checks: int = 32) -> bytes:
+    """pcs::open (pcs.hpp:212-254) -> Opening::to_bytes"""
+    data = b"".join(field.encode(x) for x in rows)
+    M = len(rows)
+    cols = len(field.encode(rows[0])) // field.width
+    depth = max(0, (cols - 1).bit_length())
+    cap = 64 + (len(r) + 2 + M + cols) * field.width + min(spot_checks, cols) * (4 + M * field.width + 32 * depth) + 64
+    out, ln = _out(cap)
+    check(lib().dgkr_pcs_open(ctx.handle, field.handle, C.c_size_t(M), C.c_size_t(cols), C.c_char_p(data),
+                              C.c_char_p(field.encode(r)), C.c_size_t(len(r)), C.c_size_t(spot_checks),
+                              C.byref(tr.t), out, C.c_size_t(cap), C.byref(ln)))
+    return out.raw[: ln.value]
+
+
+def dist_sumcheck(ctx: Context, n_workers: int, pairs, tr: Transcript):
+    """shard_pairs + dist_sumcheck (cluster.hpp:190-320) -> (proof bytes,
+    TrafficStats json)"""
+    f = tr.field
+    tabs = [f.encode(x) for pair in pairs for x in pair]
+    n = len(tabs[0]) // f.width
+    vars_ = max(0, n.bit_length() - 1)
+    cap = 64 + (vars_ + 2) * 4 * f.width + 2 * len(pairs) * f.width + 64
+    out, ln = _out(cap)
+    js = C.create_string_buffer(4096)
+    check(lib().dgkr_dist_sumcheck(ctx.handle, f.handle, C.c_size_t(n_workers), C.c_size_t(len(pairs)),
+                                   C.c_size_t(vars_), C.c_char_p(b"".join(tabs)), C.byref(tr.t), out, C.c_size_t(cap),
+                                   C.byref(ln), js, C.c_size_t(4096)))
+    return out.raw[: ln.value], js.value.decode()
+
+
+def distpc(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], spot_checks: int = 32,
+           n_clusters: int = 0):
+    """DistPc::commit + open (cluster.hpp:336-412) -> (roots, cluster opening
+    bytes, combined value, TrafficStats json)"""
+    N = len(rows)
+    data = b"".join(field.encode(x) for x in rows)
+    cols = len(field.encode(rows[0])) // field.width
+    row_vars = max(0, cols.bit_length() - 1)
+    roots = C.create_string_buffer(32 * N)
+    nr = C.c_size_t()
+    cap = N * (64 + (len(r) + 2 + N + cols) * field.width + min(spot_checks, cols) * (4 + N * field.width + 32 * 64)) + 1024
+    out, ln = _out(cap)
+    comb = C.create_string_buffer(field.width)
+    js = C.create_string_buffer(8192)
+    check(lib().dgkr_distpc(ctx.handle, field.handle, C.c_size_t(N), C.c_size_t(n_clusters), C.c_size_t(row_vars),
+                            C.c_char_p(data), C.c_char_p(field.encode(r)), C.c_size_t(len(r)),
+                            C.c_size_t(spot_checks), roots, C.byref(nr), out, C.c_size_t(cap), C.byref(ln), comb, js,
+                            C.c_size_t(8192)))
+    raw = out.raw[: ln.value]
+    ops = []
+    pos = 0
+    while pos < len(raw):
+        n = int.from_bytes(raw[pos:pos + 4], "little")
+        ops.append(raw[pos + 4:pos + 4 + n])
+        pos += 4 + n
+    return ([roots.raw[32 * i:32 * (i + 1)] for i in range(nr.value)], ops, int.from_bytes(comb.raw, "little"),
+            js.value.decode())

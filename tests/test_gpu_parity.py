@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA prover (through the C ABI) against the CPU oracle.
+
+Bit-exact is the bar for every comparison (integer / byte work): proof
+bytes, transcript state and draw counter, Merkle roots, openings and
+TrafficStats json. Small cases compare with the pure-Python restatement
+(oracle/dgkr_oracle.py); medium and full-scale cases with the compiled
+reference (oracle/_ref, when present) and with size-independent properties.
+"""
+import numpy as np
+import pytest
+
+import paper_2404_10404_b200 as P
+from oracle import dgkr_oracle as O
+from paper_2404_10404_b200 import workloads as W
+from paper_2404_10404_b200._lib import InvalidArgument
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = [O.BN254_P, 97, O.GOLDILOCKS_P]
+
+
+def _pairs(of, n_pairs, vars_, rng):
+    return [(O.random_elements(of, 1 << vars_, rng), O.random_elements(of, 1 << vars_, rng)) for _ in range(n_pairs)]
+
+
+@pytest.mark.parametrize("p", FIELDS)
+@pytest.mark.parametrize("vars_,n_pairs", [(0, 1), (1, 1), (2, 2), (5, 3), (8, 2), (11, 1)])
+def test_product_sum_matches_oracle(ctx, p, vars_, n_pairs):
+    rng = np.random.default_rng(1000 * vars_ + n_pairs + p % 1000)
+    f, of = P.Field(p), O.Field(p)
+    pairs = _pairs(of, n_pairs, vars_, rng)
+    tr = P.Transcript(f, "test.sumcheck", [3])
+    got = P.prove_product_sum(ctx, pairs, tr)
+    otr = O.Transcript("test.sumcheck", of, [3])
+    want = O.prove_product_sum(pairs, otr).to_bytes(of)
+    assert got == want
+    assert tr.state == otr.state and tr.draws == otr.draws
+
+
+def test_product_sum_kat_one_variable(ctx):
+    # tests/test_sumcheck.cpp:76-86: [1,2].[3,4] -> claimed 11
+    f = P.Field(97)
+    tr = P.Transcript(f, "test.sumcheck", [0])
+    proof = P.prove_product_sum(ctx, [([1, 2], [3, 4])], tr)
+    assert proof[0] == 11
+
+
+def test_product_sum_zero_tables(ctx):
+    # tests/test_sumcheck.cpp:66-74
+    f, of = P.Field(97), O.Field(97)
+    pairs = [([0] * 8, [0] * 8)]
+    tr = P.Transcript(f, "test.sumcheck", [0])
+    got = P.prove_product_sum(ctx, pairs, tr)
+    otr = O.Transcript("test.sumcheck", of, [0])
+    assert got == O.prove_product_sum(pairs, otr).to_bytes(of)
+    assert got[0] == 0
+
+
+def test_product_sum_errors(ctx):
+    f = P.Field(97)
+    tr = P.Transcript(f, "t")
+    with pytest.raises(InvalidArgument):  # sumcheck.hpp:161-163 mixed table sizes
+        P.prove_product_sum(ctx, [([1, 2], [3, 4]), ([1, 2, 3, 4], [1, 2, 3, 4])], tr)
+    with pytest.raises(InvalidArgument):  # field.hpp:183-185 non-canonical
+        P.prove_product_sum(ctx, [(bytes([97, 1]), bytes([1, 1]))], tr)
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, 97])
+@pytest.mark.parametrize("n_workers", [1, 2, 4, 8])
+def test_dist_sumcheck_matches_oracle(ctx, p, n_workers):
+    rng = np.random.default_rng(n_workers + p % 7)
+    f, of = P.Field(p), O.Field(p)
+    pairs = _pairs(of, 2, 5, rng)
+    tr = P.Transcript(f, "dgkr.bench")
+    proof, js = P.dist_sumcheck(ctx, n_workers, pairs, tr)
+    otr = O.Transcript("dgkr.bench", of)
+    ts = O.TrafficStats()
+    ts.begin_phase("sumcheck")
+    want = O.dist_sumcheck(n_workers, pairs, otr, ts).to_bytes(of)
+    assert proof == want and tr.state == otr.state
+    assert js == ts.to_json()
+
+
+def _random_layer(of, rng, side, n_slots, n_wires):
+    T = 1 << side
+    tables = [O.random_elements(of, T, rng) for _ in range(n_slots)]
+    wires = [O.LayerWire(bool(rng.integers(2)), O.random_elements(of, 1, rng)[0], int(rng.integers(n_slots)),
+                         int(rng.integers(n_slots)), int(rng.integers(T)), int(rng.integers(T)))
+             for _ in range(n_wires)]
+    claimed = sum(w.weight * (tables[w.x_slot][w.x_index] * tables[w.y_slot][w.y_index] if w.is_mul else
+                              tables[w.x_slot][w.x_index] + tables[w.y_slot][w.y_index]) for w in wires) % of.p
+    return tables, wires, claimed
+
+
+@pytest.mark.parametrize("p", FIELDS)
+@pytest.mark.parametrize("side,n_slots,n_wires", [(0, 1, 1), (2, 1, 16), (3, 2, 20), (6, 3, 200)])
+def test_layer_sum_matches_oracle(ctx, p, side, n_slots, n_wires):
+    rng = np.random.default_rng(side * 100 + n_slots)
+    f, of = P.Field(p), O.Field(p)
+    tables, wires, claimed = _random_layer(of, rng, side, n_slots, n_wires)
+    tr = P.Transcript(f, "test.layer")
+    got, xp, yp = P.prove_layer_sum(ctx, side, tables, wires, claimed, tr)
+    otr = O.Transcript("test.layer", of)
+    proof, u, v = O.prove_layer_sum(side, tables, wires, claimed, otr)
+    assert got == proof.to_bytes(of)
+    assert xp == u and yp == v and tr.state == otr.state
+
+
+def _gkr_both(ctx, p, circ: O.Circuit, inputs, label="test.gkr", pre=(0,)):
+    f, of = P.Field(p), O.Field(p)
+    dc = P.Circuit.from_oracle(ctx, circ)
+    tr = P.Transcript(f, label, pre)
+    got = P.gkr_prove(ctx, dc, inputs, tr)
+    otr = O.Transcript(label, of, pre)
+    outs, layers = O.gkr_prove(circ, inputs, otr)
+    want = O.gkr_proof_bytes(of, outs, layers)
+    return got, want, tr, otr
+
+
+def test_gkr_acc4_example(ctx):
+    # tests/test_gkr.cpp:17-24, :61-73: one accumulation gate adding 4 inputs -> 10
+    circ = O.Circuit(4, [[[(O.ADD, (0, 0), (0, 1)), (O.ADD, (0, 2), (0, 3))]]])
+    got, want, tr, otr = _gkr_both(ctx, 97, circ, [1, 2, 3, 4])
+    assert got == want and tr.state == otr.state
+    assert got[4] == 10  # claimed output
+
+
+def test_gkr_empty_circuit(ctx):
+    # tests/test_gkr.cpp:128-140: no layers, claims land on the inputs
+    circ = O.Circuit(4, [])
+    got, want, tr, otr = _gkr_both(ctx, 97, circ, [9, 8, 7, 6])
+    assert got == want and tr.state == otr.state
+
+
+def _py_random_general_circuit(rng, input_size, depth, max_gates, max_nested, mul_percent=50):
+    """Same shape as circuit::random_general_circuit (circuit.hpp:342-381) with
+    a numpy generator: accumulation gates, wires into any earlier layer."""
+    sizes = [input_size]
+    layers = []
+    for li in range(1, depth + 1):
+        n_gates = 1 + int(rng.integers(max_gates))
+        layer = []
+        reads_prev = False
+        for _ in range(n_gates):
+            g = []
+            for _ in range(1 + int(rng.integers(max_nested))):
+                kind = O.MUL if rng.integers(100) < mul_percent else O.ADD
+                ll, rl = int(rng.integers(li)), int(rng.integers(li))
+                g.append((kind, (ll, int(rng.integers(sizes[ll]))), (rl, int(rng.integers(sizes[rl])))))
+                reads_prev |= ll + 1 == li or rl + 1 == li
+            layer.append(g)
+        if not reads_prev:
+            k, _l, r = layer[0][0]
+            layer[0][0] = (k, (li - 1, int(rng.integers(sizes[li - 1]))), r)
+        sizes.append(len(layer))
+        layers.append(layer)
+    return O.Circuit(input_size, layers)
+
+
+@pytest.mark.parametrize("p", FIELDS)
+@pytest.mark.parametrize("trial", range(6))
+def test_gkr_general_circuits_match_oracle(ctx, p, trial):
+    rng = np.random.default_rng(trial * 31 + p % 101)
+    of = O.Field(p)
+    insz = 4 + trial
+    circ = _py_random_general_circuit(rng, insz, 2 + trial % 4, 12, 3)
+    inputs = O.random_elements(of, insz, rng)
+    got, want, tr, otr = _gkr_both(ctx, p, circ, inputs, pre=(trial,))
+    assert got == want and tr.state == otr.state and tr.draws == otr.draws
+
+
+def test_gkr_layered_matches_oracle(ctx):
+    insz, flat = W.layered_circuit(seed=5, log_width=6, depth=5)
+    circ = O.Circuit.from_flat(insz, *flat)
+    inputs = O.Field(O.BN254_P).elems_from_bytes(W.random_inputs(O.BN254_P, insz, 6).tobytes())
+    got, want, tr, otr = _gkr_both(ctx, O.BN254_P, circ, inputs)
+    assert got == want and tr.state == otr.state
+
+
+@pytest.mark.parametrize("n_copies", [2, 4, 8])
+def test_gkr_data_parallel_matches_replicated_oracle(ctx, n_copies):
+    """dgkr_circuit_create(..., n_copies): copy index = high variables
+    (cluster.hpp:182-189) — must equal gkr_prove on the explicit replica."""
+    p = O.BN254_P
+    f, of = P.Field(p), O.Field(p)
+    insz, flat = W.layered_circuit(seed=11, log_width=4, depth=4)
+    full_in, full_flat = W.replicate(insz, flat, n_copies)
+    inputs = W.random_inputs(p, full_in, 12)
+    dc = P.Circuit(ctx, insz, *flat, n_copies=n_copies)
+    tr = P.Transcript(f, "dp", [1])
+    got = P.gkr_prove(ctx, dc, inputs, tr)
+    circ = O.Circuit.from_flat(full_in, *full_flat)
+    otr = O.Transcript("dp", of, [1])
+    outs, layers = O.gkr_prove(circ, of.elems_from_bytes(inputs.tobytes()), otr)
+    assert got == O.gkr_proof_bytes(of, outs, layers)
+    assert tr.state == otr.state
+
+
+def test_circuit_validation_errors(ctx):
+    # circuit.hpp:103-152 violations surface as invalid_argument
+    bad = O.Circuit(2, [[[(O.ADD, (1, 0), (0, 0))]]])  # non-causal
+    with pytest.raises(InvalidArgument, match="non-causal"):
+        P.Circuit.from_oracle(ctx, bad)
+    bad = O.Circuit(2, [[[(O.ADD, (0, 9), (0, 0))]]])  # dangling
+    with pytest.raises(InvalidArgument, match="dangling"):
+        P.Circuit.from_oracle(ctx, bad)
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, 97])
+@pytest.mark.parametrize("M,cols,q", [(1, 1, 32), (1, 8, 32), (2, 8, 4), (4, 16, 5), (2, 64, 32), (1, 1024, 32)])
+def test_pcs_commit_open_match_oracle(ctx, p, M, cols, q):
+    rng = np.random.default_rng(M * 1000 + cols)
+    f, of = P.Field(p), O.Field(p)
+    rows = [O.random_elements(of, cols, rng) for _ in range(M)]
+    assert P.pcs_commit(ctx, f, rows) == O.pcs_commit(of, rows)
+    r = O.random_elements(of, O.log2_exact(cols) + O.log2_exact(M), rng)
+    tr = P.Transcript(f, "test.pcs")
+    got = P.pcs_open(ctx, f, rows, r, tr, q)
+    otr = O.Transcript("test.pcs", of)
+    assert got == O.pcs_open(of, rows, r, otr, q)
+    assert tr.state == otr.state
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+def test_distpc_matches_oracle(ctx, N):
+    p = O.BN254_P
+    rng = np.random.default_rng(N)
+    f, of = P.Field(p), O.Field(p)
+    rows = [O.random_elements(of, 16, rng) for _ in range(N)]
+    r = O.random_elements(of, 4 + O.log2_exact(N), rng)
+    roots, ops, comb, js = P.distpc(ctx, f, rows, r, 4)
+    ts = O.TrafficStats()
+    roots2, ops2, comb2 = O.distpc(of, rows, r, 4, ts)
+    assert roots == roots2 and ops == ops2 and comb == comb2
+    assert js == ts.to_json()
