@@ -151,6 +151,35 @@ int dgkr_circuit_evaluate(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, c
 int dgkr_gkr_prove(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const uint8_t* inputs, dgkr_transcript* t,
                    uint8_t* proof, size_t cap, size_t* len);
 size_t dgkr_gkr_proof_bound(const dgkr_circuit* c, const dgkr_field* f);
+/* Split form of dgkr_gkr_prove for measurement with inputs resident in HBM:
+ * load_inputs uploads + converts the inputs (not a reference call);
+ * prove_resident then runs gkr_prove exactly as dgkr_gkr_prove does. */
+int dgkr_circuit_load_inputs(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const uint8_t* inputs);
+int dgkr_gkr_prove_resident(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, dgkr_transcript* t,
+                            uint8_t* proof, size_t cap, size_t* len);
+/* n independent gkr_prove calls on the same circuit, run concurrently: proof
+ * i on lane i (its own stream, workspace and host thread), so the serial
+ * host transcript of one proof overlaps the GPU work of the others. Each
+ * proof/transcript is exactly what dgkr_gkr_prove would produce for it.
+ * inputs == NULL proves the inputs loaded with dgkr_circuit_load_inputs_lane.
+ * All lanes must use the same field. */
+int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, size_t n,
+                         const uint8_t* const* inputs, dgkr_transcript* ts, uint8_t* const* proofs,
+                         const size_t* caps, size_t* lens);
+int dgkr_circuit_load_inputs_lane(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, int lane,
+                                  const uint8_t* inputs);
+int dgkr_ctx_get_profile_lane(dgkr_ctx* ctx, int lane, dgkr_profile* out);
+
+/* ---- measurement helpers (not reference calls) ------------------------------ */
+/* CUDA events on the context's stream (slots 0..7) */
+int dgkr_ctx_event_record(dgkr_ctx* ctx, int slot);
+int dgkr_ctx_event_elapsed(dgkr_ctx* ctx, int slot_a, int slot_b, float* ms);
+/* page-lock a caller buffer (cudaHostRegister) so proof D2H lands in place */
+int dgkr_host_register(void* ptr, size_t bytes);
+int dgkr_host_unregister(void* ptr);
+/* Montgomery-multiplication throughput of the device (BN254), as the
+ * measured integer-pipe roofline denominator: field mults per second. */
+int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
 
 /* ---- polynomial commitment (pcs.hpp) ------------------------------------------ */
 /* pcs::commit (pcs.hpp:105-113): rows x cols row-major matrix -> Merkle root */

@@ -160,53 +160,99 @@ struct RoundParams {
     const Fe* const* in;
     Fe* const* out;
     int np;
-    std::uint64_t n_out_pairs;
+    std::uint64_t n_out_pairs;  // P
+    int log_p;                  // log2 P
     const Fe* r;
     Fe* partials;
     unsigned* counter;
     Fe* result;
 };
 
-template <class F, bool FOLD>
+// Table layouts of the round engine (P = output pairs of this round):
+//   kScan      round 1: natural-order table of 2P, pair i = (t[2i], t[2i+1])
+//   kFoldNat   round 2: natural-order input of 4P (the bookkeeping / layer
+//              tables), fold pairs (4i..4i+3) and write the 2P outputs in
+//              bit-reversed order: logical 2i -> brev(i), 2i+1 -> brev(i)+P
+//   kFoldRev   rounds >= 3: bit-reversed input of 4P; the variable being
+//              bound is the top storage bit, so pair partners are s and
+//              s + 2P and every load/store is warp-contiguous.
+enum RoundMode : int { kScan = 0, kFoldNat = 1, kFoldRev = 2 };
+
+template <class F, int MODE>
 __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __restrict__ dst, std::uint64_t i,
-                                          const Fe& r, Fe& x0, Fe& x1) {
-    if (FOLD) {
+                                          std::uint64_t P, int log_p, const Fe& r, Fe& x0, Fe& x1) {
+    if (MODE == kScan) {
+        x0 = fe_load_nc(src + 2 * i);
+        x1 = fe_load_nc(src + 2 * i + 1);
+    } else if (MODE == kFoldNat) {
         const Fe a0 = fe_load_nc(src + 4 * i), a1 = fe_load_nc(src + 4 * i + 1);
         const Fe b0 = fe_load_nc(src + 4 * i + 2), b1 = fe_load_nc(src + 4 * i + 3);
         x0 = fold1<F>(a0, a1, r);
         x1 = fold1<F>(b0, b1, r);
-        fe_store(dst + 2 * i, x0);
-        fe_store(dst + 2 * i + 1, x1);
+        const std::uint64_t s = log_p ? (__brevll(i) >> (64 - log_p)) : 0;
+        fe_store(dst + s, x0);
+        fe_store(dst + s + P, x1);
     } else {
-        x0 = fe_load_nc(src + 2 * i);
-        x1 = fe_load_nc(src + 2 * i + 1);
+        const Fe a0 = fe_load_nc(src + i), a1 = fe_load_nc(src + i + 2 * P);
+        const Fe b0 = fe_load_nc(src + i + P), b1 = fe_load_nc(src + i + 3 * P);
+        x0 = fold1<F>(a0, a1, r);
+        x1 = fold1<F>(b0, b1, r);
+        fe_store(dst + i, x0);
+        fe_store(dst + i + P, x1);
     }
 }
 
-template <class F, int NP, bool HAS_G, bool FOLD>
+template <class F, int NP, bool HAS_G, int MODE>
+__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, const Fe& r, Fe (&s)[3]) {
+    const int np = NP > 0 ? NP : a.np;
+    const std::uint64_t P = a.n_out_pairs;
+    for (int k = 0; k < np; ++k) {
+        Fe f0, f1, g0, g1;
+        load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, r, f0, f1);
+        load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, r, g0, g1);
+        s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
+        s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
+        s[2] = fe_add<F>(s[2], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
+    }
+    if (HAS_G) {
+        Fe g0, g1;
+        load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, r, g0, g1);
+        s[0] = fe_add<F>(s[0], g0);
+        s[1] = fe_add<F>(s[1], g1);
+    }
+}
+
+template <class F, int NP, bool HAS_G, int MODE>
 __global__ void __launch_bounds__(kThreads) k_round(RoundParams a) {
     Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
     Fe r = fe_zero();
-    if (FOLD) r = fe_load(a.r);
-    const int np = NP > 0 ? NP : a.np;
+    if (MODE != kScan) r = fe_load(a.r);
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < a.n_out_pairs;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        for (int k = 0; k < np; ++k) {
-            Fe f0, f1, g0, g1;
-            load_pair<F, FOLD>(a.in[2 * k], FOLD ? a.out[2 * k] : nullptr, i, r, f0, f1);
-            load_pair<F, FOLD>(a.in[2 * k + 1], FOLD ? a.out[2 * k + 1] : nullptr, i, r, g0, g1);
-            s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
-            s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
-            s[2] = fe_add<F>(s[2], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
-        }
-        if (HAS_G) {
-            Fe g0, g1;
-            load_pair<F, FOLD>(a.in[2 * np], FOLD ? a.out[2 * np] : nullptr, i, r, g0, g1);
-            s[0] = fe_add<F>(s[0], g0);
-            s[1] = fe_add<F>(s[1], g1);
-        }
+        round_body<F, NP, HAS_G, MODE>(a, i, r, s);
     }
     grid_finish<F, 3>(s, a.partials, a.counter, a.result);
+}
+
+// Small-table variant: one CTA covers all pairs; the CTA sum is the result.
+template <class F, int NP, bool HAS_G, int MODE>
+__global__ void __launch_bounds__(kThreads) k_round_small(RoundParams a) {
+    __shared__ Fe sh[32][3];
+    Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
+    Fe r = fe_zero();
+    if (MODE != kScan) r = fe_load(a.r);
+    for (std::uint64_t i = threadIdx.x; i < a.n_out_pairs; i += blockDim.x) {
+        round_body<F, NP, HAS_G, MODE>(a, i, r, s);
+    }
+    if (blockDim.x <= 32) {
+        warp_sum<F, 3>(s);
+    } else {
+        block_sum<F, 3>(s, sh);
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) fe_store(&a.result[k], s[k]);
+    }
 }
 
 template <class F>
@@ -263,6 +309,14 @@ __device__ __forceinline__ Fe split_eq(const SplitEq& e, std::uint64_t g) {
     return w;
 }
 
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_split_eq_expand(SplitEq e, std::uint64_t n, Fe* __restrict__ out) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        fe_store(out + i, split_eq<F>(e, i));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // GKR layer bookkeeping (CSR gather-reduce; the wiring transpose is built once
 // per circuit, so there are no atomics on 256-bit values).
@@ -283,7 +337,9 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) 
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
-                    const Fe w = a.wire_w ? fe_load_nc(a.wire_w + en.w) : split_eq<F>(a.w, g);
+                    const Fe w = a.wire_w   ? fe_load_nc(a.wire_w + en.w)
+                                 : a.gate_w ? fe_load_nc(a.gate_w + g)
+                                            : split_eq<F>(a.w, g);
                     const std::uint32_t ys = en.z & 0x7fffffffu;
                     const SlotDesc sy = a.slots[ys];
                     const Fe vy = fe_load_nc(sy.V + ((c << sy.log_stride) | en.y));
@@ -316,10 +372,12 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
-                    const Fe w = a.wire_w ? fe_load_nc(a.wire_w + en.w) : split_eq<F>(a.w, g);
+                    const Fe w = a.wire_w   ? fe_load_nc(a.wire_w + en.w)
+                                 : a.gate_w ? fe_load_nc(a.gate_w + g)
+                                            : split_eq<F>(a.w, g);
                     const std::uint32_t xs = en.z & 0x7fffffffu;
                     const std::uint64_t x = (c << a.slots[xs].log_stride) | en.y;
-                    const Fe cx = fe_mul<F>(w, split_eq<F>(a.u, x));
+                    const Fe cx = fe_mul<F>(w, a.eq_u ? fe_load_nc(a.eq_u + x) : split_eq<F>(a.u, x));
                     const Fe vx = fe_load(a.vx + xs);
                     if (en.z >> 31) {
                         ma = fe_add<F>(ma, fe_mul<F>(cx, vx));
@@ -556,6 +614,23 @@ __global__ void __launch_bounds__(kThreads) k_beta_combine(const Fe* __restrict_
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_mul_peak(int iters, Fe* sink, unsigned never) {
+    Fe a[4], b;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[k].v[i] = (threadIdx.x * 0x9e3779b9u + k * 0x85ebca6bu + i) & 0x0fffffffu;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b.v[i] = (blockIdx.x * 0x27d4eb2fu + i) & 0x0fffffffu;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = fe_mul<Bn254>(a[k], b);
+    }
+    Fe s = fe_add<Bn254>(fe_add<Bn254>(a[0], a[1]), fe_add<Bn254>(a[2], a[3]));
+    if (s.v[0] == never) fe_store(sink, s);  // keep the chains live (never is a runtime 0xffffffff)
+}
+
 void check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -628,20 +703,46 @@ void launch_to_canonical(FieldKind k, const Fe* in, std::uint8_t* out, int width
 }
 
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
-    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, a.r, ws.partials, ws.counter, ws.result};
+    int lp = 0;
+    while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, a.r, ws.partials, ws.counter, ws.result};
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
-#define LAUNCH_ROUND(NP, HG, FD) k_round<F, NP, HG, FD><<<g, kThreads, 0, st>>>(p)
+#define LAUNCH_ROUND(NP, HG, MD) k_round<F, NP, HG, MD><<<g, kThreads, 0, st>>>(p)
+#define BY_MODE(NP, HG)                                   \
+    do {                                                  \
+        if (a.mode == kScan) LAUNCH_ROUND(NP, HG, kScan);  \
+        else if (a.mode == kFoldNat) LAUNCH_ROUND(NP, HG, kFoldNat); \
+        else LAUNCH_ROUND(NP, HG, kFoldRev);               \
+    } while (0)
     DISPATCH_FIELD(k, F, {
-        if (a.np == 1 && a.has_g) {
-            if (a.fold) LAUNCH_ROUND(1, true, true); else LAUNCH_ROUND(1, true, false);
-        } else if (a.has_g) {
-            if (a.fold) LAUNCH_ROUND(0, true, true); else LAUNCH_ROUND(0, true, false);
-        } else {
-            if (a.fold) LAUNCH_ROUND(0, false, true); else LAUNCH_ROUND(0, false, false);
-        }
+        if (a.np == 1 && a.has_g) BY_MODE(1, true);
+        else if (a.has_g) BY_MODE(0, true);
+        else BY_MODE(0, false);
     });
 #undef LAUNCH_ROUND
     check_launch("round");
+}
+
+void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
+    int lp = 0;
+    while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, a.r, ws.partials, ws.counter, ws.result};
+    const unsigned threads = a.n_out_pairs <= 32 ? 32u : (a.n_out_pairs <= 128 ? 128u : kThreads);
+#define LAUNCH_ROUND(NP, HG, MD) k_round_small<F, NP, HG, MD><<<1, threads, 0, st>>>(p)
+    DISPATCH_FIELD(k, F, {
+        if (a.np == 1 && a.has_g) BY_MODE(1, true);
+        else if (a.has_g) BY_MODE(0, true);
+        else BY_MODE(0, false);
+    });
+#undef LAUNCH_ROUND
+#undef BY_MODE
+    check_launch("round_small");
+}
+
+void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st) {
+    const int g = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_split_eq_expand<F><<<g, kThreads, 0, st>>>(e, n, out)));
+    check_launch("split_eq_expand");
 }
 
 void launch_fold_final(FieldKind k, const Fe* const* in, Fe* const* out, int n_tabs, const Fe* r, cudaStream_t st) {
@@ -687,6 +788,11 @@ void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq&
     const int g = grid_for(n, kThreads, ws.max_blocks);
     DISPATCH_FIELD(k, F, (k_dense_eval<F><<<g, kThreads, 0, st>>>(t, n, eq, ws.partials, ws.counter, ws.result)));
     check_launch("dense_eval");
+}
+
+void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st) {
+    k_mul_peak<<<n_blocks, kThreads, 0, st>>>(iters, sink, 0xffffffffu);
+    check_launch("mul_peak");
 }
 
 void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,

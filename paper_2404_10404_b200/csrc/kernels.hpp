@@ -49,11 +49,16 @@ struct RoundLaunch {
     Fe* const* out = nullptr;       // device array [2*np + has_g]
     int np = 0;
     bool has_g = false;
-    bool fold = false;
+    int mode = 0;  // 0 scan (round 1), 1 fold natural->bit-reversed (round 2), 2 fold bit-reversed (rounds >= 3)
     std::uint64_t n_out_pairs = 0;
     const Fe* r = nullptr;          // device pointer to the fold challenge
 };
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
+
+/// Same as launch_round, but for small tables: one CTA, no grid reduction
+/// (the tail rounds of every sum-check phase are latency-bound).
+void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
+constexpr std::uint64_t kSmallRoundPairs = 256;
 
 /// out[t][0] = in[t][0] + r (in[t][1] - in[t][0]) for each table t.
 void launch_fold_final(FieldKind k, const Fe* const* in, Fe* const* out, int n_tabs, const Fe* r, cudaStream_t st);
@@ -81,6 +86,10 @@ struct SplitEq {
     int khi = 0;
 };
 
+/// Dense expansion of a split-eq: out[i] = sum_t A[t][i & m] * B[t][i >> klo], i < n
+/// (coalesced; turns the per-wire split-eq lookups into one 32-byte gather).
+void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st);
+
 /// Per-slot description of a data-parallel layer: values are laid out as
 /// n_copies blocks of 2^log_stride (copy = high bits).
 struct SlotDesc {
@@ -102,7 +111,9 @@ struct BookkeepLaunch {
     SplitEq w;                    // wire weights from the combined claim
     SplitEq u;                    // phase 2: chi_x(u) split tables
     const Fe* vx = nullptr;       // phase 2: V_m(u) per slot (device)
-    const Fe* wire_w = nullptr;   // explicit per-wire weights (entry .w = wire id), else w
+    const Fe* wire_w = nullptr;   // explicit per-wire weights (entry .w = wire id), else gate_w / w
+    const Fe* gate_w = nullptr;   // dense per-gate weights (global gate index), else split-eq w
+    const Fe* eq_u = nullptr;     // phase 2: dense chi_x(u) table, else split-eq u
 };
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
@@ -123,6 +134,10 @@ void launch_evaluate(FieldKind k, const EvalLaunch& a, cudaStream_t st);
 /// ws.result[0] = sum_g t[g] * A[g & m] * B[g >> klo]  (dense MLE evaluation, mle.hpp:51-61)
 void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq& eq, const ReduceWs& ws,
                        cudaStream_t st);
+
+/// Microbenchmark: n_blocks x 256 threads, each running `iters` dependent
+/// steps of 4 independent BN254 Montgomery multiplication chains.
+void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st);
 
 /// Batched SHA-256 column digests (pcs.hpp:73-80): leaf[j] = SHA256(canon(m[0][j]) || ... || canon(m[M-1][j])).
 void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,

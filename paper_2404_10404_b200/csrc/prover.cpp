@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <set>
 #include <string>
 #include <vector>
@@ -117,9 +119,22 @@ struct dgkr_field {
     RtFieldHost rt{};
 };
 
-struct dgkr_ctx {
+/// Runtime-modulus constants live in one __constant__ block per device;
+/// lanes share it (concurrent lanes must use the same runtime field).
+struct RtState {
+    std::mutex mu;
+    bool valid = false;
+    RtFieldHost cur{};
+};
+
+/// One in-flight proof: a CUDA stream, its reduction workspace, pinned
+/// staging and profile counters. A context owns one lane per concurrent
+/// proof (lane 0 serves the single-call API).
+struct Lane {
     int device = 0;
     int sms = 0;
+    int index = 0;
+    RtState* rt = nullptr;
     cudaStream_t st = nullptr;
     ReduceWs ws;
     DBuf<Fe> partials, result;
@@ -132,13 +147,33 @@ struct dgkr_ctx {
     // [12288, 16384) round finals.
     static constexpr std::size_t kSmall = 1 << 14;
     static constexpr std::size_t kEqOff = 16, kEqOff2 = 4112, kVxOff = 8192, kFinalsOff = 12288;
-    bool rt_valid = false;
-    RtFieldHost rt_cur{};
     bool profile_on = false;
     dgkr_profile prof{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
-    ~dgkr_ctx() {
+    Lane(int dev, int sm_count, int idx, RtState* rts) : device(dev), sms(sm_count), index(idx), rt(rts) {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ws.num_sms = sms;
+        ws.max_blocks = sms * 8;
+        partials.ensure(static_cast<std::size_t>(ws.max_blocks) * 3);
+        result.ensure(4);
+        counter.ensure(1);
+        CK(cudaMemset(counter.p, 0, sizeof(unsigned)));
+        ws.partials = partials.p;
+        ws.result = result.p;
+        ws.counter = counter.p;
+        d_small.ensure(kSmall);
+        d_err.ensure(1);
+        CK(cudaMemset(d_err.p, 0, sizeof(int)));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
+        CK(cudaEventCreate(&ev0));
+        CK(cudaEventCreate(&ev1));
+    }
+    Lane(const Lane&) = delete;
+    Lane& operator=(const Lane&) = delete;
+
+    ~Lane() {
         if (h_small) cudaFreeHost(h_small);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -147,10 +182,12 @@ struct dgkr_ctx {
 
     FieldKind use(const dgkr_field* f) {
         if (f->kind == FieldKind::Runtime) {
-            if (!rt_valid || std::memcmp(&rt_cur, &f->rt, sizeof(RtFieldHost)) != 0) {
+            std::lock_guard<std::mutex> lk(rt->mu);
+            if (!rt->valid || std::memcmp(&rt->cur, &f->rt, sizeof(RtFieldHost)) != 0) {
                 upload_rt_field(f->rt, st);
-                rt_cur = f->rt;
-                rt_valid = true;
+                CK(cudaStreamSynchronize(st));
+                rt->cur = f->rt;
+                rt->valid = true;
             }
         }
         return f->kind;
@@ -193,6 +230,31 @@ struct dgkr_ctx {
         launch_from_canonical(use(f), stage.p, static_cast<int>(f->f.width()), dst, n, d_err.p, st);
         launched();
         check_err_flag("input tables");
+    }
+};
+
+/// The context is lane 0 itself; extra lanes (concurrent proofs) are
+/// created on demand and share the runtime-field state.
+struct dgkr_ctx : Lane {
+    std::unique_ptr<RtState> rt_owner;
+    std::mutex lanes_mu;
+    std::vector<std::unique_ptr<Lane>> extra;  // lanes 1..
+    cudaEvent_t user_ev[8] = {};
+
+    dgkr_ctx(int dev, int sm_count, std::unique_ptr<RtState> rts)
+        : Lane(dev, sm_count, 0, rts.get()), rt_owner(std::move(rts)) {}
+
+    Lane* lane(int i) {
+        if (i == 0) return this;
+        std::lock_guard<std::mutex> lk(lanes_mu);
+        while (static_cast<int>(extra.size()) < i)
+            extra.push_back(std::make_unique<Lane>(device, sms, static_cast<int>(extra.size()) + 1, rt_owner.get()));
+        return extra[i - 1].get();
+    }
+
+    ~dgkr_ctx() {
+        for (auto& e : user_ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -242,7 +304,7 @@ struct SumcheckRun {
 
 /// tables: device pointer array `base` of ntab = 2*np + has_g tables of
 /// size 2^nv. Returns rounds, challenges and the final value of each table.
-SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
+SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                        RoundBuffers& rb, Transcript& tr) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
@@ -259,11 +321,11 @@ SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, i
         rl.has_g = has_g;
         rl.r = d_r;
         if (j == 1) {
-            rl.fold = false;
+            rl.mode = 0;  // scan the natural-order base tables
             rl.in = base;
             rl.out = nullptr;
         } else {
-            rl.fold = true;
+            rl.mode = (j == 2) ? 1 : 2;  // fold natural -> bit-reversed, then bit-reversed -> bit-reversed
             rl.in = cur;
             const Fe* const* nxt = (j % 2 == 0) ? rb.A() : rb.B();
             rl.out = const_cast<Fe* const*>(nxt);
@@ -271,7 +333,8 @@ SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, i
         }
         rl.n_out_pairs = size0 >> j;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        launch_round(kind, rl, ctx->ws, ctx->st);
+        if (rl.n_out_pairs <= kSmallRoundPairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
+        else launch_round(kind, rl, ctx->ws, ctx->st);
         ctx->launched();
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev1, ctx->st));
         ctx->d2h(ctx->h_small + 1, ctx->ws.result, 3 * sizeof(Fe));
@@ -284,8 +347,8 @@ SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, i
             const std::uint64_t pairs = rl.n_out_pairs;
             const std::uint64_t ntabs = static_cast<std::uint64_t>(ntab);
             // bytes: fold reads 4, writes 2 elements per table per output pair; scan reads 2
-            ctx->prof.round_bytes += pairs * ntabs * 32 * (rl.fold ? 6 : 2);
-            ctx->prof.round_mults += pairs * (3 * np + (rl.fold ? 2 * ntabs : 0));
+            ctx->prof.round_bytes += pairs * ntabs * 32 * (rl.mode ? 6 : 2);
+            ctx->prof.round_mults += pairs * (3 * np + (rl.mode ? 2 * ntabs : 0));
         }
         const double t0 = now_ms();
         const U256 s0 = to_u256(ctx->h_small[1]), s1 = to_u256(ctx->h_small[2]), s2 = to_u256(ctx->h_small[3]);
@@ -307,7 +370,7 @@ SumcheckRun run_rounds(dgkr_ctx* ctx, const dgkr_field* f, int np, bool has_g, i
     if (nv >= 1) {
         launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
         ctx->launched();
-        Fe* hf = ctx->h_small + dgkr_ctx::kFinalsOff;
+        Fe* hf = ctx->h_small + Lane::kFinalsOff;
         ctx->d2h(hf, rb.finals.p, ntab * sizeof(Fe));
         ctx->sync();
         for (int t = 0; t < ntab; ++t) out.finals.push_back(to_u256(hf[t]));
@@ -351,7 +414,7 @@ std::vector<std::uint8_t> sumcheck_bytes(const HostField& F, const U256& claimed
 // Product sum-check on uploaded tables (shared by prove_product_sum and the
 // single-device dist_sumcheck).
 // ===========================================================================
-std::vector<std::uint8_t> product_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_pairs, std::size_t vars,
+std::vector<std::uint8_t> product_sumcheck(Lane* ctx, const dgkr_field* f, std::size_t n_pairs, std::size_t vars,
                                            const std::uint8_t* tables, Transcript& tr, U256* claimed_out) {
     if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "product sum needs at least one pair");  // sumcheck.hpp:155-157
     if (vars > 40) fail(DGKR_INVALID_ARGUMENT, "table too large");
@@ -385,6 +448,23 @@ std::vector<std::uint8_t> product_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, s
 // ===========================================================================
 // GKR circuit (data-parallel capable)
 // ===========================================================================
+struct CircuitWs {
+    std::vector<std::unique_ptr<DBuf<Fe>>> values;  // per layer, capacity-sized, zero padded
+    DBuf<const Fe*> d_layer_vals;
+    DBuf<Fe> H, G;      // bookkeeping outputs, max_slots x Tmax and Tmax
+    DBuf<Fe> Wg, EqU;   // dense per-gate weights and chi(u) tables
+    RoundBuffers rb;
+    DBuf<std::uint8_t> stage;
+    DBuf<Fe> eq_tabs;   // split-eq tables for weights and u
+    DBuf<EqJob> eq_jobs, eq_jobs2;
+    struct Cons {
+        DBuf<SlotDesc> d_slots1, d_slots2;
+        DBuf<const Fe*> base_ptrs;  // V0,H0,V1,H1,...,G
+    };
+    std::vector<std::unique_ptr<Cons>> cons;
+    bool inputs_loaded = false;
+};
+
 struct dgkr_circuit {
     std::uint32_t input_size = 0;  // per copy
     std::uint32_t depth = 0;
@@ -402,24 +482,16 @@ struct dgkr_circuit {
         std::uint64_t n_wires = 0;         // sub wires
         DBuf<std::uint32_t> xoff, yoff;    // concatenated per slot
         DBuf<uint4> xent, yent;
-        DBuf<SlotDesc> d_slots1, d_slots2;
-        DBuf<const Fe*> base_ptrs;         // V0,H0,V1,H1,...,G
         DBuf<std::uint32_t> gstart;        // evaluation CSR
         DBuf<uint4> nested;
     };
     std::vector<std::unique_ptr<Consumer>> cons;  // index li (0 unused)
-    // device state
-    std::vector<std::unique_ptr<DBuf<Fe>>> values;
-    DBuf<const Fe*> d_layer_vals;
     DBuf<std::uint32_t> d_layer_log;
-    DBuf<Fe> H, G;  // bookkeeping outputs, max_slots x Tmax and Tmax
     std::uint32_t max_slots = 0;
     std::uint64_t Tmax = 1;
-    RoundBuffers rb;
-    DBuf<std::uint8_t> stage;
-    DBuf<Fe> eq_tabs;  // split-eq tables for weights and u
-    DBuf<EqJob> eq_jobs, eq_jobs2;
     std::uint64_t total_gates = 0;  // full circuit gate count
+    std::mutex ws_mu;
+    std::vector<std::unique_ptr<CircuitWs>> ws;  // per lane
 
     std::uint32_t padded_log2_full(std::uint32_t l) const { return sub_log[l] + log_copies; }
 };
@@ -428,7 +500,7 @@ namespace {
 
 /// GeneralCircuit::validate (circuit.hpp:103-152) on the sub-circuit plus
 /// the data-parallel preconditions; builds all device-side structures.
-void build_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const std::uint64_t* gns,
+void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const std::uint64_t* gns,
                    const std::uint32_t* nested, const std::uint64_t* min_padded) {
     const std::uint32_t D = c.depth;
     std::vector<std::string> violations;
@@ -581,38 +653,46 @@ void build_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const std::uint64_t* lgs, con
         C.nested.ensure(nw);
         CK(cudaMemcpy(C.gstart.p, gstart.data(), (ng + 1) * 4, cudaMemcpyHostToDevice));
         if (nw) CK(cudaMemcpy(C.nested.p, nest.data(), nw * sizeof(uint4), cudaMemcpyHostToDevice));
-        // stash per-slot offsets bases for SlotDesc (filled after buffers exist)
-        C.d_slots1.ensure(ns);
-        C.d_slots2.ensure(ns);
         c.cons[li] = std::move(cp);
-        // keep bases in host-side vectors via lambdas below
         (void)xslot_start;
         (void)yslot_start;
     }
-    // device buffers
-    c.values.clear();
+    std::vector<std::uint32_t> ll(D + 1);
+    for (std::uint32_t l = 0; l <= D; ++l) ll[l] = c.sub_log[l];
+    c.d_layer_log.ensure(D + 1);
+    CK(cudaMemcpy(c.d_layer_log.p, ll.data(), ll.size() * 4, cudaMemcpyHostToDevice));
+    (void)ctx;
+}
+
+/// Per-lane device workspace of a circuit: layer values, bookkeeping and
+/// fold scratch, split-eq tables. Built on first use by a lane.
+CircuitWs& workspace(dgkr_circuit& c, int lane) {
+    std::lock_guard<std::mutex> lk(c.ws_mu);
+    if (static_cast<int>(c.ws.size()) <= lane) c.ws.resize(lane + 1);
+    if (c.ws[lane]) return *c.ws[lane];
+    auto wp = std::make_unique<CircuitWs>();
+    CircuitWs& W = *wp;
+    const std::uint32_t D = c.depth;
     for (std::uint32_t l = 0; l <= D; ++l) {
         auto b = std::make_unique<DBuf<Fe>>();
         b->ensure(c.capacity[l]);
-        c.values.push_back(std::move(b));
+        W.values.push_back(std::move(b));
     }
     std::vector<const Fe*> lv(D + 1);
-    std::vector<std::uint32_t> ll(D + 1);
-    for (std::uint32_t l = 0; l <= D; ++l) {
-        lv[l] = c.values[l]->p;
-        ll[l] = c.sub_log[l];
-    }
-    c.d_layer_vals.ensure(D + 1);
-    c.d_layer_log.ensure(D + 1);
-    CK(cudaMemcpy(c.d_layer_vals.p, lv.data(), lv.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c.d_layer_log.p, ll.data(), ll.size() * 4, cudaMemcpyHostToDevice));
+    for (std::uint32_t l = 0; l <= D; ++l) lv[l] = W.values[l]->p;
+    W.d_layer_vals.ensure(D + 1);
+    CK(cudaMemcpy(W.d_layer_vals.p, lv.data(), lv.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
     if (D >= 1) {
-        c.H.ensure(static_cast<std::size_t>(c.max_slots) * c.Tmax);
-        c.G.ensure(c.Tmax);
-        c.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
+        W.H.ensure(static_cast<std::size_t>(c.max_slots) * c.Tmax);
+        W.G.ensure(c.Tmax);
+        W.Wg.ensure(c.Tmax);
+        W.EqU.ensure(c.Tmax);
+        W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
     }
+    W.cons.resize(D + 1);
     for (std::uint32_t li = 1; li <= D; ++li) {
         auto& C = *c.cons[li];
+        auto wc = std::make_unique<CircuitWs::Cons>();
         const std::size_t ns = C.slots.size();
         std::vector<SlotDesc> s1(ns), s2(ns);
         std::uint64_t base = 0;
@@ -620,22 +700,26 @@ void build_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const std::uint64_t* lgs, con
             const std::uint32_t src = C.slots[s];
             // stride of a slot = sub padded size of its source (copy = high bits)
             const std::uint32_t lstr = (c.n_copies > 1) ? c.sub_log[src] : c.padded_log2_full(src);
-            s1[s] = SlotDesc{c.values[src]->p, c.H.p + s * c.Tmax, C.xoff.p + base, C.xent.p, lstr, 0};
-            s2[s] = SlotDesc{c.values[src]->p, c.H.p + s * c.Tmax, C.yoff.p + base, C.yent.p, lstr, 0};
+            s1[s] = SlotDesc{W.values[src]->p, W.H.p + s * c.Tmax, C.xoff.p + base, C.xent.p, lstr, 0};
+            s2[s] = SlotDesc{W.values[src]->p, W.H.p + s * c.Tmax, C.yoff.p + base, C.yent.p, lstr, 0};
             base += c.sub_padded[src] + 1;
         }
-        CK(cudaMemcpy(C.d_slots1.p, s1.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(C.d_slots2.p, s2.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
+        wc->d_slots1.ensure(ns);
+        wc->d_slots2.ensure(ns);
+        CK(cudaMemcpy(wc->d_slots1.p, s1.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(wc->d_slots2.p, s2.data(), ns * sizeof(SlotDesc), cudaMemcpyHostToDevice));
         std::vector<const Fe*> bp;
         for (std::size_t s = 0; s < ns; ++s) {
-            bp.push_back(c.values[C.slots[s]]->p);
-            bp.push_back(c.H.p + s * c.Tmax);
+            bp.push_back(W.values[C.slots[s]]->p);
+            bp.push_back(W.H.p + s * c.Tmax);
         }
-        bp.push_back(c.G.p);
-        C.base_ptrs.ensure(bp.size());
-        CK(cudaMemcpy(C.base_ptrs.p, bp.data(), bp.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+        bp.push_back(W.G.p);
+        wc->base_ptrs.ensure(bp.size());
+        CK(cudaMemcpy(wc->base_ptrs.p, bp.data(), bp.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+        W.cons[li] = std::move(wc);
     }
-    (void)ctx;
+    c.ws[lane] = std::move(wp);
+    return *c.ws[lane];
 }
 
 // ---------------------------------------------------------------------------
@@ -695,7 +779,7 @@ LayerClaim shrink_claim(std::size_t layer, std::size_t native, const std::vector
 /// Build split-eq tables on the device: for each (point, seed) pair, A =
 /// seed * eq(point[0..klo)), B = eq(point[klo..)). Returns the SplitEq view
 /// rooted at `dst` (which must hold K*(2^klo + 2^khi) elements).
-SplitEq build_split_eq(dgkr_ctx* ctx, const dgkr_field* f, const std::vector<std::vector<U256>>& points,
+SplitEq build_split_eq(Lane* ctx, const dgkr_field* f, const std::vector<std::vector<U256>>& points,
                        const std::vector<U256>& seeds, Fe* dst, DBuf<EqJob>& jobs_buf, std::size_t small_off) {
     const int K = static_cast<int>(points.size());
     const int nv = K ? static_cast<int>(points[0].size()) : 0;
@@ -707,7 +791,7 @@ SplitEq build_split_eq(dgkr_ctx* ctx, const dgkr_field* f, const std::vector<std
     e.A = dst;
     e.B = dst + static_cast<std::size_t>(K) * (std::size_t{1} << klo);
     // stage points and seeds in the small buffer
-    const std::size_t limit = small_off < dgkr_ctx::kEqOff2 ? dgkr_ctx::kEqOff2 : dgkr_ctx::kVxOff;
+    const std::size_t limit = small_off < Lane::kEqOff2 ? Lane::kEqOff2 : Lane::kVxOff;
     if (small_off + static_cast<std::size_t>(K) * (nv + 2) > limit) fail(DGKR_UNSUPPORTED, "too many claim terms");
     Fe* hs = ctx->h_small + small_off;
     Fe* ds = ctx->d_small.p + small_off;
@@ -733,22 +817,27 @@ SplitEq build_split_eq(dgkr_ctx* ctx, const dgkr_field* f, const std::vector<std
     return e;
 }
 
-void evaluate_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_field* f, const std::uint8_t* inputs) {
-    const FieldKind kind = ctx->use(f);
+void load_inputs(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs) {
     const std::uint64_t n_in = static_cast<std::uint64_t>(c.input_size) * c.n_copies;
-    Fe* v0 = c.values[0]->p;
-    ctx->upload_elems(f, inputs, n_in, v0, c.stage);
+    Fe* v0 = W.values[0]->p;
+    ctx->upload_elems(f, inputs, n_in, v0, W.stage);
     if (c.capacity[0] > n_in) CK(cudaMemsetAsync(v0 + n_in, 0, (c.capacity[0] - n_in) * sizeof(Fe), ctx->st));
+    W.inputs_loaded = true;
+}
+
+void evaluate_layers(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f) {
+    if (!W.inputs_loaded) fail(DGKR_LOGIC_ERROR, "circuit inputs not loaded");
+    const FieldKind kind = ctx->use(f);
     for (std::uint32_t li = 1; li <= c.depth; ++li) {
         auto& C = *c.cons[li];
         EvalLaunch el;
-        el.out = c.values[li]->p;
+        el.out = W.values[li]->p;
         el.n_write = c.capacity[li];
         el.n_gates = c.sub_size[li] * c.n_copies;
         el.log_g = (c.n_copies > 1) ? c.sub_log[li] : 63;
         el.gstart = C.gstart.p;
         el.nested = C.nested.p;
-        el.layer_vals = c.d_layer_vals.p;
+        el.layer_vals = W.d_layer_vals.p;
         el.layer_log_stride = c.d_layer_log.p;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
         launch_evaluate(kind, el, ctx->st);
@@ -763,29 +852,37 @@ void evaluate_circuit(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_field* f, const
     }
 }
 
-/// gkr_prove (gkr.hpp:182-244) on the device-resident circuit.
-std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_field* f, const std::uint8_t* inputs,
-                                    Transcript& tr) {
+void evaluate_circuit(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs) {
+    load_inputs(ctx, c, W, f, inputs);
+    evaluate_layers(ctx, c, W, f);
+}
+
+/// gkr_prove (gkr.hpp:182-244) on the device-resident circuit. The proof is
+/// written straight into the caller's buffer (the claimed outputs, by far
+/// its largest part, land there by D2H); returns the proof length.
+std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs,
+                      Transcript& tr, std::uint8_t* out, std::size_t cap) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
-    evaluate_circuit(ctx, c, f, inputs);  // gkr.hpp:186
+    if (inputs) evaluate_circuit(ctx, c, W, f, inputs);  // gkr.hpp:186
+    else evaluate_layers(ctx, c, W, f);
 
     // absorb the padded output table (gkr.hpp:189-190): D2H canonical, serial SHA chain
     const std::uint32_t out_layer = c.depth;
     const std::uint64_t n_out = c.full_padded[out_layer];
-    std::vector<std::uint8_t> proof;
-    put32(proof, static_cast<std::uint32_t>(n_out));
-    const std::size_t out_off = proof.size();
-    proof.resize(out_off + n_out * w);
+    if (cap < 4 + n_out * w) fail(DGKR_CAPACITY, "output buffer too small");
+    std::vector<std::uint8_t> proof;  // everything after the claimed outputs
+    for (int i = 0; i < 4; ++i) out[i] = static_cast<std::uint8_t>(n_out >> (8 * i));
     {
-        c.stage.ensure(n_out * w);
-        launch_to_canonical(kind, c.values[out_layer]->p, c.stage.p, static_cast<int>(w), n_out, ctx->st);
+        W.stage.ensure(n_out * w);
+        launch_to_canonical(kind, W.values[out_layer]->p, W.stage.p, static_cast<int>(w), n_out, ctx->st);
         ctx->launched();
-        ctx->d2h(proof.data() + out_off, c.stage.p, n_out * w);
+        ctx->d2h(out + 4, W.stage.p, n_out * w);
         ctx->sync();
         const double t0 = now_ms();
-        for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(proof.data() + out_off + i * w, w);
+        const std::uint8_t* o = out + 4;
+        for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(o + i * w, w);
         const double dt = now_ms() - t0;
         ctx->prof.output_absorb_ms += dt;
         ctx->prof.host_transcript_ms += dt;
@@ -799,11 +896,11 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
     for (std::uint32_t l = 0; l <= c.depth; ++l) lmax = std::max(lmax, c.padded_log2_full(l));
     const std::size_t per_term = (std::size_t{1} << ((lmax + 1) / 2)) + (std::size_t{1} << (lmax / 2));
     const std::size_t max_terms = 2 * static_cast<std::size_t>(c.depth) * std::max<std::uint32_t>(c.max_slots, 1) + 2;
-    c.eq_tabs.ensure((max_terms + 2) * per_term);
+    W.eq_tabs.ensure((max_terms + 2) * per_term);
     U256 out_value;
     {
-        SplitEq e = build_split_eq(ctx, f, {q}, {F.one()}, c.eq_tabs.p, c.eq_jobs, dgkr_ctx::kEqOff);
-        launch_dense_eval(kind, c.values[out_layer]->p, n_out, e, ctx->ws, ctx->st);
+        SplitEq e = build_split_eq(ctx, f, {q}, {F.one()}, W.eq_tabs.p, W.eq_jobs, Lane::kEqOff);
+        launch_dense_eval(kind, W.values[out_layer]->p, n_out, e, ctx->ws, ctx->st);
         ctx->launched();
         ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
         ctx->sync();
@@ -820,6 +917,7 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
     put32(proof, out_layer);
     for (std::uint32_t layer = out_layer; layer >= 1; --layer) {
         auto& C = *c.cons[layer];
+        auto& WC = *W.cons[layer];
         std::vector<U256> alphas;
         const double th = now_ms();
         LayerClaim combined = combine_claims(std::move(registry[layer]), tr, F, &alphas);  // gkr.hpp:206-207
@@ -839,20 +937,23 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
         for (auto& p : pts)
             if (p.size() != lgc) fail(DGKR_LOGIC_ERROR, "claim point length mismatch");
         if (pts.size() > max_terms) fail(DGKR_UNSUPPORTED, "too many claim terms");
-        SplitEq wq = build_split_eq(ctx, f, pts, seeds, c.eq_tabs.p, c.eq_jobs, dgkr_ctx::kEqOff);
+        SplitEq wq = build_split_eq(ctx, f, pts, seeds, W.eq_tabs.p, W.eq_jobs, Lane::kEqOff);
         const std::size_t wq_elems = pts.size() * ((std::size_t{1} << wq.klo) + (std::size_t{1} << wq.khi));
 
         // prove_layer_sum (sumcheck.hpp:342-448)
         tr.absorb(combined.value);  // :364
         BookkeepLaunch bk;
-        bk.slots = C.d_slots1.p;
+        bk.slots = WC.d_slots1.p;
         bk.n_slots = ns;
         bk.T = T;
         bk.n_copies = c.n_copies;
         bk.log_gcons = (c.n_copies > 1) ? c.sub_log[layer] : 63;
-        bk.G = c.G.p;
+        bk.G = W.G.p;
         bk.w = wq;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_split_eq_expand(kind, wq, c.sub_size[layer] * c.n_copies, W.Wg.p, ctx->st);  // w(g), gkr.hpp:140-148
+        ctx->launched();
+        bk.gate_w = W.Wg.p;
         launch_bookkeep_phase1(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -862,20 +963,23 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p1 = run_rounds(ctx, f, ns, true, static_cast<int>(side), C.base_ptrs.p, c.rb, tr);
+        SumcheckRun p1 = run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
         std::vector<U256> one_seed{F.one()};
-        SplitEq uq = build_split_eq(ctx, f, {p1.challenges}, one_seed, c.eq_tabs.p + wq_elems, c.eq_jobs2,
-                                    dgkr_ctx::kEqOff2);
+        SplitEq uq = build_split_eq(ctx, f, {p1.challenges}, one_seed, W.eq_tabs.p + wq_elems, W.eq_jobs2,
+                                    Lane::kEqOff2);
         // vx to device
-        for (int m = 0; m < ns; ++m) ctx->h_small[dgkr_ctx::kVxOff + m] = to_fe(vx[m]);
-        ctx->h2d(ctx->d_small.p + dgkr_ctx::kVxOff, ctx->h_small + dgkr_ctx::kVxOff, ns * sizeof(Fe));
-        bk.slots = C.d_slots2.p;
+        for (int m = 0; m < ns; ++m) ctx->h_small[Lane::kVxOff + m] = to_fe(vx[m]);
+        ctx->h2d(ctx->d_small.p + Lane::kVxOff, ctx->h_small + Lane::kVxOff, ns * sizeof(Fe));
+        bk.slots = WC.d_slots2.p;
         bk.u = uq;
-        bk.vx = ctx->d_small.p + dgkr_ctx::kVxOff;
+        bk.vx = ctx->d_small.p + Lane::kVxOff;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st);  // chi_x(u), sumcheck.hpp:415
+        ctx->launched();
+        bk.eq_u = W.EqU.p;
         launch_bookkeep_phase2(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -885,7 +989,7 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p2 = run_rounds(ctx, f, ns, true, static_cast<int>(side), C.base_ptrs.p, c.rb, tr);
+        SumcheckRun p2 = run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;
@@ -903,7 +1007,10 @@ std::vector<std::uint8_t> gkr_prove(dgkr_ctx* ctx, dgkr_circuit& c, const dgkr_f
         put32(proof, static_cast<std::uint32_t>(sb.size()));
         proof.insert(proof.end(), sb.begin(), sb.end());
     }
-    return proof;
+    const std::size_t total = 4 + n_out * w + proof.size();
+    if (total > cap) fail(DGKR_CAPACITY, "output buffer too small");
+    std::memcpy(out + 4 + n_out * w, proof.data(), proof.size());
+    return total;
 }
 
 // ---------------------------------------------------------------------------
@@ -915,7 +1022,7 @@ struct PcsDevice {
     DBuf<std::uint8_t> stage;
 };
 
-void pcs_build_tree(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols) {
+void pcs_build_tree(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols) {
     d.nodes.ensure(2 * cols * 32);
     launch_column_digests(ctx->use(f), d.m.p, cols, static_cast<int>(rows), static_cast<int>(f->f.width()),
                           d.nodes.p + cols * 32, ctx->st);
@@ -929,7 +1036,7 @@ void check_matrix(std::size_t rows, std::size_t cols) {
         fail(DGKR_INVALID_ARGUMENT, "matrix dimensions must be nonzero powers of two");  // pcs.hpp:26-29
 }
 
-Digest pcs_commit(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols,
+Digest pcs_commit(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols,
                   const std::uint8_t* data) {
     check_matrix(rows, cols);
     d.m.ensure(rows * cols);
@@ -949,7 +1056,7 @@ U256 chi_eval_host(std::uint64_t index, const std::vector<U256>& point, const Ho
 }
 
 /// pcs::open (pcs.hpp:212-254) -> Opening::to_bytes
-std::vector<std::uint8_t> pcs_open(dgkr_ctx* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows,
+std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows,
                                    std::size_t cols, const std::uint8_t* data, const std::vector<U256>& r,
                                    std::size_t q, Transcript& tr, U256* value_out) {
     check_matrix(rows, cols);
@@ -1218,25 +1325,7 @@ int dgkr_ctx_create(int device, dgkr_ctx** out) {
         cudaDeviceProp prop{};
         CK(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) fail(DGKR_UNSUPPORTED, "this build targets sm_100a (B200)");
-        auto c = std::make_unique<dgkr_ctx>();
-        c->device = device;
-        c->sms = prop.multiProcessorCount;
-        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-        c->ws.num_sms = c->sms;
-        c->ws.max_blocks = c->sms * 8;
-        c->partials.ensure(static_cast<std::size_t>(c->ws.max_blocks) * 3);
-        c->result.ensure(4);
-        c->counter.ensure(1);
-        CK(cudaMemset(c->counter.p, 0, sizeof(unsigned)));
-        c->ws.partials = c->partials.p;
-        c->ws.result = c->result.p;
-        c->ws.counter = c->counter.p;
-        c->d_small.ensure(dgkr_ctx::kSmall);
-        c->d_err.ensure(1);
-        CK(cudaMemset(c->d_err.p, 0, sizeof(int)));
-        CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_small), dgkr_ctx::kSmall * sizeof(Fe)));
-        CK(cudaEventCreate(&c->ev0));
-        CK(cudaEventCreate(&c->ev1));
+        auto c = std::make_unique<dgkr_ctx>(device, prop.multiProcessorCount, std::make_unique<RtState>());
         *out = c.release();
     });
 }
@@ -1426,14 +1515,15 @@ int dgkr_circuit_evaluate(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, c
     return guard([&] {
         ctx->begin_call();
         CK(cudaSetDevice(ctx->device));
-        evaluate_circuit(ctx, *c, f, inputs);
+        CircuitWs& W = workspace(*c, 0);
+        evaluate_circuit(ctx, *c, W, f, inputs);
         const std::size_t w = f->f.width();
         const std::uint64_t n_out = c->full_padded[c->depth];
         *len = n_out * w;
         if (n_out * w > cap) fail(DGKR_CAPACITY, "output buffer too small");
-        c->stage.ensure(n_out * w);
-        launch_to_canonical(ctx->use(f), c->values[c->depth]->p, c->stage.p, static_cast<int>(w), n_out, ctx->st);
-        ctx->d2h(outputs, c->stage.p, n_out * w);
+        W.stage.ensure(n_out * w);
+        launch_to_canonical(ctx->use(f), W.values[c->depth]->p, W.stage.p, static_cast<int>(w), n_out, ctx->st);
+        ctx->d2h(outputs, W.stage.p, n_out * w);
         ctx->sync();
         ctx->end_call();
     });
@@ -1455,12 +1545,132 @@ int dgkr_gkr_prove(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const st
     return guard([&] {
         ctx->begin_call();
         CK(cudaSetDevice(ctx->device));
+        if (!inputs) fail(DGKR_INVALID_ARGUMENT, "inputs must not be NULL");
+        *len = dgkr_gkr_proof_bound(c, f);
         Transcript tr(&f->f, t->state, t->draws);
-        auto bytes = gkr_prove(ctx, *c, f, inputs, tr);
+        *len = gkr_prove(ctx, *c, workspace(*c, 0), f, inputs, tr, proof, cap);
         std::memcpy(t->state, tr.state().data(), 32);
         t->draws = tr.draws();
         ctx->end_call();
-        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_circuit_load_inputs(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* inputs) {
+    return dgkr_circuit_load_inputs_lane(ctx, c, f, 0, inputs);
+}
+
+int dgkr_circuit_load_inputs_lane(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, int lane,
+                                  const std::uint8_t* inputs) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (lane < 0 || lane >= 64) fail(DGKR_OUT_OF_RANGE, "lane");
+        Lane* L = ctx->lane(lane);
+        load_inputs(L, *c, workspace(*c, lane), f, inputs);
+        L->sync();
+    });
+}
+
+int dgkr_gkr_prove_resident(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, dgkr_transcript* t,
+                            std::uint8_t* proof, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        *len = dgkr_gkr_proof_bound(c, f);
+        Transcript tr(&f->f, t->state, t->draws);
+        *len = gkr_prove(ctx, *c, workspace(*c, 0), f, nullptr, tr, proof, cap);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+    });
+}
+
+int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, std::size_t n,
+                         const std::uint8_t* const* inputs, dgkr_transcript* ts, std::uint8_t* const* proofs,
+                         const std::size_t* caps, std::size_t* lens) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n == 0 || n > 64) fail(DGKR_OUT_OF_RANGE, "batch size must be 1..64");
+        std::vector<Lane*> lanes(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            lanes[i] = ctx->lane(static_cast<int>(i));
+            workspace(*c, static_cast<int>(i));  // allocate before the threads start
+        }
+        ctx->use(f);  // upload runtime-field constants once, before concurrency
+        std::vector<std::string> errs(n);
+        std::vector<int> codes(n, DGKR_OK);
+        auto work = [&](std::size_t i) {
+            try {
+                CK(cudaSetDevice(ctx->device));
+                Lane* L = lanes[i];
+                L->begin_call();
+                Transcript tr(&f->f, ts[i].state, ts[i].draws);
+                lens[i] = gkr_prove(L, *c, workspace(*c, static_cast<int>(i)), f, inputs ? inputs[i] : nullptr, tr,
+                                    proofs[i], caps[i]);
+                std::memcpy(ts[i].state, tr.state().data(), 32);
+                ts[i].draws = tr.draws();
+                L->end_call();
+            } catch (const Error& e) {
+                codes[i] = e.code;
+                errs[i] = e.what();
+            } catch (const std::exception& e) {
+                codes[i] = DGKR_LOGIC_ERROR;
+                errs[i] = e.what();
+            }
+        };
+        std::vector<std::thread> th;
+        for (std::size_t i = 1; i < n; ++i) th.emplace_back(work, i);
+        work(0);
+        for (auto& t : th) t.join();
+        for (std::size_t i = 0; i < n; ++i)
+            if (codes[i] != DGKR_OK) fail(codes[i], "batch proof " + std::to_string(i) + ": " + errs[i]);
+    });
+}
+
+int dgkr_ctx_get_profile_lane(dgkr_ctx* ctx, int lane, dgkr_profile* out) {
+    return guard([&] {
+        if (lane < 0 || lane >= 64) fail(DGKR_OUT_OF_RANGE, "lane");
+        *out = ctx->lane(lane)->prof;
+    });
+}
+
+int dgkr_ctx_event_record(dgkr_ctx* ctx, int slot) {
+    return guard([&] {
+        if (slot < 0 || slot >= 8) fail(DGKR_OUT_OF_RANGE, "event slot");
+        if (!ctx->user_ev[slot]) CK(cudaEventCreate(&ctx->user_ev[slot]));
+        CK(cudaEventRecord(ctx->user_ev[slot], ctx->st));
+    });
+}
+
+int dgkr_ctx_event_elapsed(dgkr_ctx* ctx, int a, int b, float* ms) {
+    return guard([&] {
+        if (a < 0 || a >= 8 || b < 0 || b >= 8 || !ctx->user_ev[a] || !ctx->user_ev[b])
+            fail(DGKR_OUT_OF_RANGE, "event slot");
+        CK(cudaEventSynchronize(ctx->user_ev[b]));
+        CK(cudaEventElapsedTime(ms, ctx->user_ev[a], ctx->user_ev[b]));
+    });
+}
+
+int dgkr_host_register(void* ptr, std::size_t bytes) {
+    return guard([&] { CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault)); });
+}
+int dgkr_host_unregister(void* ptr) {
+    return guard([&] { CK(cudaHostUnregister(ptr)); });
+}
+
+int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        DBuf<Fe> sink;
+        sink.ensure(1);
+        const int blocks = ctx->sms * 8, iters = 4096;
+        launch_mul_peak(blocks, 64, sink.p, ctx->st);  // warm-up
+        CK(cudaEventRecord(ctx->ev0, ctx->st));
+        launch_mul_peak(blocks, iters, sink.p, ctx->st);
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *mults_per_s = static_cast<double>(blocks) * 256.0 * iters * 4.0 / (ms * 1e-3);
     });
 }
 

@@ -273,6 +273,40 @@ def gkr_prove(ctx: Context, circuit: Circuit, inputs: Elems, tr: Transcript, out
     return out_buf.raw[: ln.value]
 
 
+def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[Elems]], trs: Sequence[Transcript],
+                    out_bufs=None) -> List[bytes]:
+    """n independent gkr_prove calls run concurrently (one lane = stream +
+    workspace + host thread per proof); inputs=None proves the inputs loaded
+    per lane with load_inputs_lane. Transcripts are advanced in place."""
+    n = len(trs)
+    f = trs[0].field
+    cap = circuit.proof_bound(f)
+    if out_bufs is None:
+        out_bufs = [np.empty(cap, dtype=np.uint8) for _ in range(n)]
+    keep = []
+    in_ptrs = None
+    if inputs is not None:
+        arrs = [x if isinstance(x, np.ndarray) else np.frombuffer(f.encode(x), np.uint8) for x in inputs]
+        keep.extend(arrs)
+        in_ptrs = (C.c_void_p * n)(*[a.ctypes.data for a in arrs])
+    tarr = (Transcript_t * n)()
+    for i, t in enumerate(trs):
+        tarr[i] = t.t
+    outs = (C.c_void_p * n)(*[b.ctypes.data for b in out_bufs])
+    caps = (C.c_size_t * n)(*[len(b) for b in out_bufs])
+    lens = (C.c_size_t * n)()
+    check(lib().dgkr_gkr_prove_batch(ctx.handle, circuit.handle, f.handle, C.c_size_t(n), in_ptrs, tarr, outs, caps,
+                                     lens))
+    for i, t in enumerate(trs):
+        t.t = tarr[i]
+    return [out_bufs[i][: lens[i]].tobytes() for i in range(n)]
+
+
+def load_inputs_lane(ctx: Context, circuit: Circuit, field: Field, lane: int, inputs: Elems) -> None:
+    data = inputs if isinstance(inputs, np.ndarray) else np.frombuffer(field.encode(inputs), np.uint8)
+    check(lib().dgkr_circuit_load_inputs_lane(ctx.handle, circuit.handle, field.handle, C.c_int(lane), _buf(data)))
+
+
 def pcs_commit(ctx: Context, field: Field, rows: Sequence[Elems]) -> bytes:
     """pcs::commit (pcs.hpp:105-113) -> 32-byte root"""
     data = b"".join(field.encode(r) for r in rows)

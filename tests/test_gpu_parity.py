@@ -196,6 +196,31 @@ def test_gkr_data_parallel_matches_replicated_oracle(ctx, n_copies):
     assert tr.state == otr.state
 
 
+@pytest.mark.parametrize("n", [1, 3])
+def test_gkr_batch_equals_single_proofs(ctx, n):
+    """dgkr_gkr_prove_batch runs n proofs concurrently on n lanes; each must be
+    byte-identical to the oracle's proof of the same instance."""
+    p = O.BN254_P
+    f, of = P.Field(p), O.Field(p)
+    insz, flat = W.layered_circuit(seed=21, log_width=5, depth=4)
+    dc = P.Circuit(ctx, insz, *flat, n_copies=2)
+    full_in, full_flat = W.replicate(insz, flat, 2)
+    circ = O.Circuit.from_flat(full_in, *full_flat)
+    inputs = [W.random_inputs(p, full_in, 100 + i) for i in range(n)]
+    trs = [P.Transcript(f, "batch", [i]) for i in range(n)]
+    got = P.gkr_prove_batch(ctx, dc, inputs, trs)
+    for i in range(n):
+        otr = O.Transcript("batch", of, [i])
+        outs, layers = O.gkr_prove(circ, of.elems_from_bytes(inputs[i].tobytes()), otr)
+        assert got[i] == O.gkr_proof_bytes(of, outs, layers)
+        assert trs[i].state == otr.state
+    # resident inputs per lane
+    for i in range(n):
+        P.load_inputs_lane(ctx, dc, f, i, inputs[i])
+    trs2 = [P.Transcript(f, "batch", [i]) for i in range(n)]
+    assert P.gkr_prove_batch(ctx, dc, None, trs2) == got
+
+
 def test_circuit_validation_errors(ctx):
     # circuit.hpp:103-152 violations surface as invalid_argument
     bad = O.Circuit(2, [[[(O.ADD, (1, 0), (0, 0))]]])  # non-causal
