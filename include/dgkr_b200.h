@@ -170,6 +170,29 @@ int dgkr_circuit_load_inputs_lane(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_fie
                                   const uint8_t* inputs);
 int dgkr_ctx_get_profile_lane(dgkr_ctx* ctx, int lane, dgkr_profile* out);
 
+/* ---- multi-GPU data-parallel GKR (Sisu; cluster.hpp:182-320 generalised) ----
+ * One process per GPU. Rank r proves copies [r*n, (r+1)*n) of a uniform-width
+ * data-parallel circuit created with n_copies = n (the rank index is the top
+ * log2(world) variables of every layer). Per sum-check round the only
+ * traffic is an NCCL all-gather of 3 field elements per rank; at each phase
+ * boundary one all-gather of the final table values; the claimed outputs are
+ * all-gathered once. Every rank produces the identical proof and transcript,
+ * byte-equal to the single-GPU proof of the full circuit. */
+typedef struct dgkr_comm dgkr_comm;
+int dgkr_comm_nccl_unique_id(uint8_t* out128);
+int dgkr_comm_create_nccl(dgkr_ctx* ctx, const uint8_t* uid128, int rank, int world, dgkr_comm** out);
+void dgkr_comm_destroy(dgkr_comm* comm);
+/* inputs: this rank's n*input_size elements, or NULL for inputs already loaded
+ * with dgkr_circuit_load_inputs */
+int dgkr_gkr_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, dgkr_circuit* c, const dgkr_field* f,
+                        const uint8_t* inputs, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+/* The same protocol with `world` ranks emulated as host threads driving
+ * lanes of this one GPU (exchange through host memory); checks that every
+ * rank produced the identical proof. inputs_all: world*n*input_size elements. */
+int dgkr_gkr_prove_dist_emulated(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, int world,
+                                 const uint8_t* inputs_all, dgkr_transcript* t, uint8_t* proof, size_t cap,
+                                 size_t* len);
+
 /* ---- measurement helpers (not reference calls) ------------------------------ */
 /* CUDA events on the context's stream (slots 0..7) */
 int dgkr_ctx_event_record(dgkr_ctx* ctx, int slot);

@@ -300,6 +300,7 @@ __global__ void k_eq_build(const EqJob* jobs) {
 
 template <class F>
 __device__ __forceinline__ Fe split_eq(const SplitEq& e, std::uint64_t g) {
+    g += e.offset;
     const std::uint64_t lo = g & ((std::uint64_t{1} << e.klo) - 1), hi = g >> e.klo;
     Fe w = fe_mul<F>(fe_load_nc(e.A + lo), fe_load_nc(e.B + hi));
     for (int t = 1; t < e.K; ++t) {
@@ -323,6 +324,71 @@ __global__ void __launch_bounds__(kThreads) k_split_eq_expand(SplitEq e, std::ui
 // Entry layout: {g_local, other_local, other_slot | is_mul << 31, wire id}.
 // ---------------------------------------------------------------------------
 template <class F>
+__device__ __forceinline__ Fe fe_select(bool c, const Fe& a, const Fe& b) {
+    Fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.v[i] = c ? a.v[i] : b.v[i];
+    return r;
+}
+
+// Single-slot phase 1 (layered circuits): thread t visits row perm[t mod S]
+// of copy t / S; rows are degree-sorted so warps do not diverge on the CSR
+// row length, and the mul/add cases share one multiplication:
+//   mul: H += w*V[y]            add: H += w, G += w*V[y]
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bookkeep1_sorted(BookkeepLaunch a) {
+    const SlotDesc sd = a.slots[0];
+    const std::uint64_t smask = (std::uint64_t{1} << sd.log_stride) - 1;
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < a.T;
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t c = t >> sd.log_stride;
+        const std::uint32_t j = static_cast<std::uint32_t>(t & smask);
+        const std::uint64_t x = (c << sd.log_stride) | a.perm[j];
+        const uint2 sg = a.seg[j];
+        Fe h = fe_zero(), gacc = fe_zero();
+        for (std::uint32_t e = sg.x; e < sg.x + sg.y; ++e) {
+            const uint4 en = sd.ent[e];
+            const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
+            const Fe vy = fe_load_nc(sd.V + ((c << sd.log_stride) | en.y));
+            const Fe prod = fe_mul<F>(w, vy);
+            const bool mul = en.z >> 31;
+            h = fe_add<F>(h, fe_select<F>(mul, prod, w));
+            gacc = fe_select<F>(mul, gacc, fe_add<F>(gacc, prod));
+        }
+        fe_store(sd.out + x, h);
+        fe_store(a.G + x, gacc);
+    }
+}
+
+// Single-slot phase 2: cx = w * chi_x(u);  mul: MA += cx*V(u)   add: MA += cx, C += cx*V(u)
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(BookkeepLaunch a) {
+    const SlotDesc sd = a.slots[0];
+    const std::uint64_t smask = (std::uint64_t{1} << sd.log_stride) - 1;
+    const Fe vx = fe_load(a.vx);
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < a.T;
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t c = t >> sd.log_stride;
+        const std::uint32_t j = static_cast<std::uint32_t>(t & smask);
+        const std::uint64_t y = (c << sd.log_stride) | a.perm[j];
+        const uint2 sg = a.seg[j];
+        Fe ma = fe_zero(), cacc = fe_zero();
+        for (std::uint32_t e = sg.x; e < sg.x + sg.y; ++e) {
+            const uint4 en = sd.ent[e];
+            const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
+            const Fe eu = fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y));
+            const Fe cx = fe_mul<F>(w, eu);
+            const Fe prod = fe_mul<F>(cx, vx);
+            const bool mul = en.z >> 31;
+            ma = fe_add<F>(ma, fe_select<F>(mul, prod, cx));
+            cacc = fe_select<F>(mul, cacc, fe_add<F>(cacc, prod));
+        }
+        fe_store(sd.out + y, ma);
+        fe_store(a.G + y, cacc);
+    }
+}
+
+template <class F>
 __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) {
     for (std::uint64_t x = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; x < a.T;
          x += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -343,12 +409,10 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) 
                     const std::uint32_t ys = en.z & 0x7fffffffu;
                     const SlotDesc sy = a.slots[ys];
                     const Fe vy = fe_load_nc(sy.V + ((c << sy.log_stride) | en.y));
-                    if (en.z >> 31) {
-                        h = fe_add<F>(h, fe_mul<F>(w, vy));
-                    } else {
-                        h = fe_add<F>(h, w);
-                        gacc = fe_add<F>(gacc, fe_mul<F>(w, vy));
-                    }
+                    const Fe prod = fe_mul<F>(w, vy);
+                    const bool mul = en.z >> 31;
+                    h = fe_add<F>(h, fe_select<F>(mul, prod, w));
+                    gacc = fe_select<F>(mul, gacc, fe_add<F>(gacc, prod));
                 }
             }
             fe_store(sd.out + x, h);
@@ -379,12 +443,10 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
                     const std::uint64_t x = (c << a.slots[xs].log_stride) | en.y;
                     const Fe cx = fe_mul<F>(w, a.eq_u ? fe_load_nc(a.eq_u + x) : split_eq<F>(a.u, x));
                     const Fe vx = fe_load(a.vx + xs);
-                    if (en.z >> 31) {
-                        ma = fe_add<F>(ma, fe_mul<F>(cx, vx));
-                    } else {
-                        ma = fe_add<F>(ma, cx);
-                        cacc = fe_add<F>(cacc, fe_mul<F>(cx, vx));
-                    }
+                    const Fe prod = fe_mul<F>(cx, vx);
+                    const bool mul = en.z >> 31;
+                    ma = fe_add<F>(ma, fe_select<F>(mul, prod, cx));
+                    cacc = fe_select<F>(mul, cacc, fe_add<F>(cacc, prod));
                 }
             }
             fe_store(sd.out + y, ma);
@@ -766,13 +828,21 @@ void launch_eq_build(FieldKind k, const EqJob* jobs, int n_jobs, cudaStream_t st
 
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
-    DISPATCH_FIELD(k, F, (k_bookkeep_phase1<F><<<g, kThreads, 0, st>>>(a)));
+    if (a.perm && a.n_slots == 1 && a.gate_w) {
+        DISPATCH_FIELD(k, F, (k_bookkeep1_sorted<F><<<g, kThreads, 0, st>>>(a)));
+    } else {
+        DISPATCH_FIELD(k, F, (k_bookkeep_phase1<F><<<g, kThreads, 0, st>>>(a)));
+    }
     check_launch("bookkeep_phase1");
 }
 
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
-    DISPATCH_FIELD(k, F, (k_bookkeep_phase2<F><<<g, kThreads, 0, st>>>(a)));
+    if (a.perm && a.n_slots == 1 && a.gate_w && a.eq_u) {
+        DISPATCH_FIELD(k, F, (k_bookkeep2_sorted<F><<<g, kThreads, 0, st>>>(a)));
+    } else {
+        DISPATCH_FIELD(k, F, (k_bookkeep_phase2<F><<<g, kThreads, 0, st>>>(a)));
+    }
     check_launch("bookkeep_phase2");
 }
 

@@ -84,6 +84,7 @@ struct SplitEq {
     int K = 0;
     int klo = 0;
     int khi = 0;
+    std::uint64_t offset = 0;  // added to every index (a rank's slice of the global hypercube)
 };
 
 /// Dense expansion of a split-eq: out[i] = sum_t A[t][i & m] * B[t][i >> klo], i < n
@@ -114,6 +115,10 @@ struct BookkeepLaunch {
     const Fe* wire_w = nullptr;   // explicit per-wire weights (entry .w = wire id), else gate_w / w
     const Fe* gate_w = nullptr;   // dense per-gate weights (global gate index), else split-eq w
     const Fe* eq_u = nullptr;     // phase 2: dense chi_x(u) table, else split-eq u
+    // Single-slot fast path (layered circuits): CSR rows visited in a static
+    // degree-sorted order so the 32 rows of a warp have equal length.
+    const std::uint32_t* perm = nullptr;  // [2^log_stride] row (x or y local index) per position
+    const uint2* seg = nullptr;           // [2^log_stride] (entry start, entry count) per position
 };
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);

@@ -4,6 +4,10 @@
 // on the host, following the reference line by line (citations inline); all
 // O(table) work runs in the sm_100a kernels of kernels.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <condition_variable>
 
 #include <algorithm>
 #include <array>
@@ -147,6 +151,7 @@ struct Lane {
     // [12288, 16384) round finals.
     static constexpr std::size_t kSmall = 1 << 14;
     static constexpr std::size_t kEqOff = 16, kEqOff2 = 4112, kVxOff = 8192, kFinalsOff = 12288;
+    static constexpr std::size_t kGatherOff = 14336;  // [14336, 16384): all-gathered round sums (<= 682 ranks)
     bool profile_on = false;
     dgkr_profile prof{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -258,6 +263,182 @@ struct dgkr_ctx : Lane {
     }
 };
 
+// ===========================================================================
+// Communicators for the data-parallel (multi-GPU) prover. The protocol code
+// is shared; only the transport differs:
+//   NcclComm    one process per GPU, NCCL over NVLink/NVSwitch (production)
+//   ThreadComm  ranks as host threads driving lanes of ONE GPU, exchanging
+//               through host memory at barriers (tests the distributed
+//               protocol on a single device; no kernel ever waits on another)
+// Per sum-check round the only traffic is an all-gather of 3 field elements
+// per rank (cluster.hpp:272-286); at each phase boundary an all-gather of the
+// final table values (cluster.hpp:295-309).
+// ===========================================================================
+struct dgkr_comm {
+    int rank = 0;
+    int world = 1;
+    DBuf<std::uint8_t> scratch;
+    virtual ~dgkr_comm() = default;
+    /// d_recv (device) = concatenation over ranks of each rank's d_send
+    virtual void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) = 0;
+    /// h_recv (host) = concatenation over ranks of each rank's d_send
+    virtual void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) {
+        scratch.ensure(static_cast<std::size_t>(world) * bytes);
+        allgather(d_send, scratch.p, bytes, L);
+        L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
+        L->sync();
+    }
+    /// rank 0: h_recv (host) = concatenation over ranks of d_send; others: untouched
+    virtual void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) = 0;
+    /// every rank's h (host, `bytes`) = rank 0's h
+    virtual void broadcast_host(void* h, std::size_t bytes, Lane* L) = 0;
+};
+
+namespace {
+
+struct ThreadGroup {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    std::uint64_t gen = 0;
+    std::vector<std::uint8_t> buf;
+    bool aborted = false;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (aborted) fail(DGKR_COMM_ERROR, "thread group aborted");
+        const std::uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g || aborted; });
+            if (aborted) fail(DGKR_COMM_ERROR, "thread group aborted");
+        }
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
+    }
+};
+
+struct ThreadComm : dgkr_comm {
+    ThreadGroup* g = nullptr;
+    void stage(std::size_t bytes) {
+        g->barrier();  // everyone is done with the previous contents
+        if (rank == 0 && g->buf.size() < static_cast<std::size_t>(world) * bytes) g->buf.resize(world * bytes);
+        g->barrier();
+    }
+    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
+        stage(bytes);
+        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        g->barrier();
+        CK(cudaMemcpyAsync(d_recv, g->buf.data(), world * bytes, cudaMemcpyHostToDevice, L->st));
+        L->sync();
+    }
+    void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+        stage(bytes);
+        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        g->barrier();
+        std::memcpy(h_recv, g->buf.data(), world * bytes);
+    }
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+        stage(bytes);
+        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        g->barrier();
+        if (rank == 0) std::memcpy(h_recv, g->buf.data(), world * bytes);
+    }
+    void broadcast_host(void* h, std::size_t bytes, Lane*) override {
+        stage(bytes);
+        if (rank == 0) std::memcpy(g->buf.data(), h, bytes);
+        g->barrier();
+        if (rank != 0) std::memcpy(h, g->buf.data(), bytes);
+    }
+};
+
+// NCCL is resolved at run time (dlopen) so the library loads without it;
+// torch's bundled libnccl.so.2 is picked up when already loaded.
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    bool load() {
+        if (h) return true;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(h, "ncclCommInitRank"));
+        allGather = reinterpret_cast<decltype(allGather)>(dlsym(h, "ncclAllGather"));
+        commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        errStr = reinterpret_cast<decltype(errStr)>(dlsym(h, "ncclGetErrorString"));
+        send = reinterpret_cast<decltype(send)>(dlsym(h, "ncclSend"));
+        recv = reinterpret_cast<decltype(recv)>(dlsym(h, "ncclRecv"));
+        bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
+        groupStart = reinterpret_cast<decltype(groupStart)>(dlsym(h, "ncclGroupStart"));
+        groupEnd = reinterpret_cast<decltype(groupEnd)>(dlsym(h, "ncclGroupEnd"));
+        return getUniqueId && commInitRank && allGather && commDestroy && errStr && send && recv && bcast &&
+               groupStart && groupEnd;
+    }
+};
+NcclApi g_nccl;
+
+#define NCK(x)                                                                                         \
+    do {                                                                                               \
+        ncclResult_t r_ = (x);                                                                         \
+        if (r_ != ncclSuccess) fail(DGKR_COMM_ERROR, std::string(#x) + ": " + g_nccl.errStr(r_));     \
+    } while (0)
+
+struct NcclComm : dgkr_comm {
+    ncclComm_t comm = nullptr;
+    ~NcclComm() override {
+        if (comm) g_nccl.commDestroy(comm);
+    }
+    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
+        NCK(g_nccl.allGather(d_send, d_recv, bytes, ncclUint8, comm, L->st));
+    }
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+        if (rank == 0) scratch.ensure(static_cast<std::size_t>(world) * bytes);
+        NCK(g_nccl.groupStart());
+        if (rank == 0) {
+            for (int r = 1; r < world; ++r) NCK(g_nccl.recv(scratch.p + r * bytes, bytes, ncclUint8, r, comm, L->st));
+        } else {
+            NCK(g_nccl.send(d_send, bytes, ncclUint8, 0, comm, L->st));
+        }
+        NCK(g_nccl.groupEnd());
+        if (rank == 0) {
+            CK(cudaMemcpyAsync(scratch.p, d_send, bytes, cudaMemcpyDeviceToDevice, L->st));
+            L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
+        }
+        L->sync();
+    }
+    void broadcast_host(void* h, std::size_t bytes, Lane* L) override {
+        bc.ensure(bytes);
+        if (rank == 0) L->h2d(bc.p, h, bytes);
+        NCK(g_nccl.bcast(bc.p, bc.p, bytes, ncclUint8, 0, comm, L->st));
+        if (rank != 0) L->d2h(h, bc.p, bytes);
+        L->sync();
+    }
+    DBuf<std::uint8_t> bc;
+};
+
+}  // namespace
+
 namespace {
 
 // ===========================================================================
@@ -305,7 +486,51 @@ struct SumcheckRun {
 /// tables: device pointer array `base` of ntab = 2*np + has_g tables of
 /// size 2^nv. Returns rounds, challenges and the final value of each table.
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                       RoundBuffers& rb, Transcript& tr) {
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr);
+
+/// Distributed form (cluster.hpp:228-320 generalised to the layer
+/// sum-check): `nv` local variables per rank, rank = high variables. Local
+/// rounds sum every rank's (S0,S1,S2) after an all-gather (the reference's
+/// worker->master round messages); at the boundary the per-rank finals are
+/// all-gathered and every rank finishes the log2(world) top rounds on the
+/// rebuilt world-sized tables — identical on all ranks, so the transcript
+/// equals the single-GPU one byte for byte.
+SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
+                            RoundBuffers& rb, Transcript& tr, dgkr_comm* comm) {
+    const int ntab = 2 * np + (has_g ? 1 : 0);
+    const int world = comm->world;
+    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm);
+    // boundary: gather every rank's final table values
+    std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
+    for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
+    DBuf<Fe> dmine;
+    dmine.ensure(ntab);
+    ctx->h2d(dmine.p, mine.data(), ntab * sizeof(Fe));
+    comm->allgather_to_host(dmine.p, all.data(), ntab * sizeof(Fe), ctx);
+    // world-sized tables, rank index = position (natural order)
+    DBuf<Fe> tabs;
+    tabs.ensure(static_cast<std::size_t>(ntab) * world);
+    std::vector<Fe> h(static_cast<std::size_t>(ntab) * world);
+    for (int t = 0; t < ntab; ++t)
+        for (int r = 0; r < world; ++r) h[static_cast<std::size_t>(t) * world + r] = all[static_cast<std::size_t>(r) * ntab + t];
+    ctx->h2d(tabs.p, h.data(), h.size() * sizeof(Fe));
+    std::vector<const Fe*> hp(ntab);
+    for (int t = 0; t < ntab; ++t) hp[t] = tabs.p + static_cast<std::size_t>(t) * world;
+    DBuf<const Fe*> dp;
+    dp.ensure(ntab);
+    ctx->h2d(dp.p, hp.data(), ntab * sizeof(const Fe*));
+    int lw = 0;
+    while ((1 << lw) < world) ++lw;
+    RoundBuffers tail_rb;
+    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dp.p, tail_rb, tr, nullptr);
+    loc.rounds.insert(loc.rounds.end(), tail.rounds.begin(), tail.rounds.end());
+    loc.challenges.insert(loc.challenges.end(), tail.challenges.begin(), tail.challenges.end());
+    loc.finals = tail.finals;
+    return loc;
+}
+
+SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const int ntab = 2 * np + (has_g ? 1 : 0);
@@ -337,8 +562,18 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         else launch_round(kind, rl, ctx->ws, ctx->st);
         ctx->launched();
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev1, ctx->st));
-        ctx->d2h(ctx->h_small + 1, ctx->ws.result, 3 * sizeof(Fe));
-        ctx->sync();
+        if (comm) {
+            // every rank's partial round sums (cluster.hpp:272-278), summed on every rank
+            const std::size_t W = static_cast<std::size_t>(comm->world);
+            comm->allgather_to_host(ctx->ws.result, ctx->h_small + Lane::kGatherOff, 3 * sizeof(Fe), ctx);
+            U256 acc[3] = {};
+            for (std::size_t r = 0; r < W; ++r)
+                for (int k = 0; k < 3; ++k) acc[k] = F.add(acc[k], to_u256(ctx->h_small[Lane::kGatherOff + 3 * r + k]));
+            for (int k = 0; k < 3; ++k) ctx->h_small[1 + k] = to_fe(acc[k]);
+        } else {
+            ctx->d2h(ctx->h_small + 1, ctx->ws.result, 3 * sizeof(Fe));
+            ctx->sync();
+        }
         if (ctx->profile_on) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
@@ -484,6 +719,8 @@ struct dgkr_circuit {
         DBuf<uint4> xent, yent;
         DBuf<std::uint32_t> gstart;        // evaluation CSR
         DBuf<uint4> nested;
+        DBuf<std::uint32_t> xperm, yperm;  // single-slot: degree-sorted rows
+        DBuf<uint2> xseg, yseg;
     };
     std::vector<std::unique_ptr<Consumer>> cons;  // index li (0 unused)
     DBuf<std::uint32_t> d_layer_log;
@@ -628,6 +865,25 @@ void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const s
                 xent[xfill[xbase[xs] + e[2]]++] = make_uint4(gl, e[4], static_cast<std::uint32_t>(ys) | mul, wid);
                 yent[yfill[ybase[ys] + e[4]]++] = make_uint4(gl, e[2], static_cast<std::uint32_t>(xs) | mul, wid);
             }
+        }
+        if (ns == 1) {
+            // degree-sorted row order for the single-slot bookkeeping kernels
+            const std::uint64_t S = c.sub_padded[C.slots[0]];
+            auto sorted = [&](const std::vector<std::uint32_t>& off, DBuf<std::uint32_t>& dperm, DBuf<uint2>& dseg) {
+                std::vector<std::uint32_t> perm(S);
+                for (std::uint64_t i = 0; i < S; ++i) perm[i] = static_cast<std::uint32_t>(i);
+                std::stable_sort(perm.begin(), perm.end(), [&](std::uint32_t a, std::uint32_t b) {
+                    return off[a + 1] - off[a] > off[b + 1] - off[b];
+                });
+                std::vector<uint2> seg(S);
+                for (std::uint64_t i = 0; i < S; ++i) seg[i] = make_uint2(off[perm[i]], off[perm[i] + 1] - off[perm[i]]);
+                dperm.ensure(S);
+                dseg.ensure(S);
+                CK(cudaMemcpy(dperm.p, perm.data(), S * 4, cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(dseg.p, seg.data(), S * sizeof(uint2), cudaMemcpyHostToDevice));
+            };
+            sorted(xoff, C.xperm, C.xseg);
+            sorted(yoff, C.yperm, C.yseg);
         }
         C.xoff.ensure(xoff.size());
         C.yoff.ensure(yoff.size());
@@ -861,50 +1117,90 @@ void evaluate_circuit(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
 /// written straight into the caller's buffer (the claimed outputs, by far
 /// its largest part, land there by D2H); returns the proof length.
 std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs,
-                      Transcript& tr, std::uint8_t* out, std::size_t cap) {
+                      Transcript& tr, std::uint8_t* out, std::size_t cap, dgkr_comm* comm = nullptr) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
+    // distributed: this rank holds copies [rank*n, (rank+1)*n) of a
+    // uniform-width data-parallel circuit; the rank index is the top log2(world)
+    // variables of every layer (cluster.hpp:182-189).
+    const std::uint64_t world = comm ? static_cast<std::uint64_t>(comm->world) : 1;
+    const std::uint64_t rank = comm ? static_cast<std::uint64_t>(comm->rank) : 0;
+    const std::uint32_t lw = log2_exact(world);
+    if (comm) {
+        if ((world & (world - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "world size must be a power of two");
+        for (std::uint32_t l = 0; l <= c.depth; ++l)
+            if (c.sub_size[l] != c.sub_size[0] || c.sub_size[l] != c.sub_padded[l])
+                fail(DGKR_INVALID_ARGUMENT, "distributed proving needs a uniform power-of-two layer width");
+    }
     if (inputs) evaluate_circuit(ctx, c, W, f, inputs);  // gkr.hpp:186
     else evaluate_layers(ctx, c, W, f);
 
     // absorb the padded output table (gkr.hpp:189-190): D2H canonical, serial SHA chain
     const std::uint32_t out_layer = c.depth;
-    const std::uint64_t n_out = c.full_padded[out_layer];
+    const std::uint64_t n_out_local = c.full_padded[out_layer];
+    const std::uint64_t n_out = n_out_local * world;
     if (cap < 4 + n_out * w) fail(DGKR_CAPACITY, "output buffer too small");
     std::vector<std::uint8_t> proof;  // everything after the claimed outputs
     for (int i = 0; i < 4; ++i) out[i] = static_cast<std::uint8_t>(n_out >> (8 * i));
     {
-        W.stage.ensure(n_out * w);
-        launch_to_canonical(kind, W.values[out_layer]->p, W.stage.p, static_cast<int>(w), n_out, ctx->st);
+        W.stage.ensure(n_out_local * w);
+        launch_to_canonical(kind, W.values[out_layer]->p, W.stage.p, static_cast<int>(w), n_out_local, ctx->st);
         ctx->launched();
-        ctx->d2h(out + 4, W.stage.p, n_out * w);
-        ctx->sync();
-        const double t0 = now_ms();
-        const std::uint8_t* o = out + 4;
-        for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(o + i * w, w);
-        const double dt = now_ms() - t0;
-        ctx->prof.output_absorb_ms += dt;
-        ctx->prof.host_transcript_ms += dt;
+        if (comm) {
+            // outputs in global order on rank 0 only: it alone runs the serial absorb
+            comm->gather_to_root_host(W.stage.p, out + 4, n_out_local * w, ctx);
+        } else {
+            ctx->d2h(out + 4, W.stage.p, n_out * w);
+            ctx->sync();
+        }
+        if (!comm || comm->rank == 0) {
+            const double t0 = now_ms();
+            const std::uint8_t* o = out + 4;
+            for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(o + i * w, w);
+            const double dt = now_ms() - t0;
+            ctx->prof.output_absorb_ms += dt;
+            ctx->prof.host_transcript_ms += dt;
+        }
+        if (comm) {
+            // the absorbed transcript state goes to every rank (40 bytes)
+            std::uint8_t st[40];
+            std::memcpy(st, tr.state().data(), 32);
+            const std::uint64_t draws = tr.draws();
+            std::memcpy(st + 32, &draws, 8);
+            comm->broadcast_host(st, 40, ctx);
+            std::uint64_t d2;
+            std::memcpy(&d2, st + 32, 8);
+            tr = Transcript(&F, st, d2);
+            if (comm->rank != 0) std::memset(out + 4, 0, n_out * w);  // only rank 0 holds the outputs
+        }
     }
     // q and the output claim (gkr.hpp:192-202)
-    const std::uint32_t qlen = c.padded_log2_full(out_layer);
+    const std::uint32_t qlen = c.padded_log2_full(out_layer) + lw;
     std::vector<U256> q;
     for (std::uint32_t k = 0; k < qlen; ++k) q.push_back(tr.challenge());
     // split-eq table space: (max claim terms + 1 u-table) x (2^ceil(L/2) + 2^floor(L/2))
-    std::uint32_t lmax = log2_exact(c.Tmax);
-    for (std::uint32_t l = 0; l <= c.depth; ++l) lmax = std::max(lmax, c.padded_log2_full(l));
+    std::uint32_t lmax = log2_exact(c.Tmax) + lw;
+    for (std::uint32_t l = 0; l <= c.depth; ++l) lmax = std::max(lmax, c.padded_log2_full(l) + lw);
     const std::size_t per_term = (std::size_t{1} << ((lmax + 1) / 2)) + (std::size_t{1} << (lmax / 2));
     const std::size_t max_terms = 2 * static_cast<std::size_t>(c.depth) * std::max<std::uint32_t>(c.max_slots, 1) + 2;
     W.eq_tabs.ensure((max_terms + 2) * per_term);
     U256 out_value;
     {
         SplitEq e = build_split_eq(ctx, f, {q}, {F.one()}, W.eq_tabs.p, W.eq_jobs, Lane::kEqOff);
-        launch_dense_eval(kind, W.values[out_layer]->p, n_out, e, ctx->ws, ctx->st);
+        e.offset = rank * n_out_local;
+        launch_dense_eval(kind, W.values[out_layer]->p, n_out_local, e, ctx->ws, ctx->st);
         ctx->launched();
-        ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
-        ctx->sync();
-        out_value = to_u256(ctx->h_small[1]);
+        if (comm) {
+            comm->allgather_to_host(ctx->ws.result, ctx->h_small + Lane::kGatherOff, sizeof(Fe), ctx);
+            U256 acc{};
+            for (std::uint64_t r = 0; r < world; ++r) acc = F.add(acc, to_u256(ctx->h_small[Lane::kGatherOff + r]));
+            out_value = acc;
+        } else {
+            ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
+            ctx->sync();
+            out_value = to_u256(ctx->h_small[1]);
+        }
     }
     std::vector<std::vector<LayerClaim>> registry(out_layer + 1);
     {
@@ -933,11 +1229,12 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             pts.push_back(t.point);
             seeds.push_back(t.weight);
         }
-        const std::uint32_t lgc = c.padded_log2_full(layer);
+        const std::uint32_t lgc = c.padded_log2_full(layer) + lw;
         for (auto& p : pts)
             if (p.size() != lgc) fail(DGKR_LOGIC_ERROR, "claim point length mismatch");
         if (pts.size() > max_terms) fail(DGKR_UNSUPPORTED, "too many claim terms");
         SplitEq wq = build_split_eq(ctx, f, pts, seeds, W.eq_tabs.p, W.eq_jobs, Lane::kEqOff);
+        wq.offset = rank * (c.sub_size[layer] * c.n_copies);  // global gate index of local gate 0
         const std::size_t wq_elems = pts.size() * ((std::size_t{1} << wq.klo) + (std::size_t{1} << wq.khi));
 
         // prove_layer_sum (sumcheck.hpp:342-448)
@@ -954,6 +1251,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         launch_split_eq_expand(kind, wq, c.sub_size[layer] * c.n_copies, W.Wg.p, ctx->st);  // w(g), gkr.hpp:140-148
         ctx->launched();
         bk.gate_w = W.Wg.p;
+        bk.perm = C.xperm.p;
+        bk.seg = C.xseg.p;
         launch_bookkeep_phase1(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -963,13 +1262,15 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p1 = run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
+        SumcheckRun p1 = comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm)
+                              : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
         std::vector<U256> one_seed{F.one()};
         SplitEq uq = build_split_eq(ctx, f, {p1.challenges}, one_seed, W.eq_tabs.p + wq_elems, W.eq_jobs2,
                                     Lane::kEqOff2);
+        uq.offset = rank * T;  // this rank's slice of the x hypercube
         // vx to device
         for (int m = 0; m < ns; ++m) ctx->h_small[Lane::kVxOff + m] = to_fe(vx[m]);
         ctx->h2d(ctx->d_small.p + Lane::kVxOff, ctx->h_small + Lane::kVxOff, ns * sizeof(Fe));
@@ -980,6 +1281,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st);  // chi_x(u), sumcheck.hpp:415
         ctx->launched();
         bk.eq_u = W.EqU.p;
+        bk.perm = C.yperm.p;
+        bk.seg = C.yseg.p;
         launch_bookkeep_phase2(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -989,7 +1292,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p2 = run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
+        SumcheckRun p2 = comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm)
+                              : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;
@@ -997,8 +1301,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         // registry (gkr.hpp:225-233)
         for (int s = 0; s < ns; ++s) {
             const std::uint32_t src = C.slots[s];
-            registry[src].push_back(shrink_claim(src, c.padded_log2_full(src), p1.challenges, finals[s], F));
-            registry[src].push_back(shrink_claim(src, c.padded_log2_full(src), p2.challenges, finals[ns + s], F));
+            const std::uint32_t native = c.padded_log2_full(src) + lw;
+            registry[src].push_back(shrink_claim(src, native, p1.challenges, finals[s], F));
+            registry[src].push_back(shrink_claim(src, native, p2.challenges, finals[ns + s], F));
         }
         // layer proof bytes
         put32(proof, static_cast<std::uint32_t>(alphas.size()));
@@ -1623,6 +1928,115 @@ int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, st
         for (auto& t : th) t.join();
         for (std::size_t i = 0; i < n; ++i)
             if (codes[i] != DGKR_OK) fail(codes[i], "batch proof " + std::to_string(i) + ": " + errs[i]);
+    });
+}
+
+int dgkr_comm_nccl_unique_id(std::uint8_t* out128) {
+    return guard([&] {
+        if (!g_nccl.load()) fail(DGKR_COMM_ERROR, "libnccl.so.2 not found");
+        ncclUniqueId id;
+        NCK(g_nccl.getUniqueId(&id));
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+int dgkr_comm_create_nccl(dgkr_ctx* ctx, const std::uint8_t* uid128, int rank, int world, dgkr_comm** out) {
+    return guard([&] {
+        if (!g_nccl.load()) fail(DGKR_COMM_ERROR, "libnccl.so.2 not found");
+        if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
+        CK(cudaSetDevice(ctx->device));
+        auto c = std::make_unique<NcclComm>();
+        c->rank = rank;
+        c->world = world;
+        ncclUniqueId id;
+        std::memcpy(&id, uid128, sizeof(id));
+        NCK(g_nccl.commInitRank(&c->comm, world, id, rank));
+        *out = c.release();
+    });
+}
+
+void dgkr_comm_destroy(dgkr_comm* c) { delete c; }
+
+int dgkr_gkr_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, dgkr_circuit* c, const dgkr_field* f,
+                        const std::uint8_t* inputs, dgkr_transcript* t, std::uint8_t* proof, std::size_t cap,
+                        std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        Transcript tr(&f->f, t->state, t->draws);
+        *len = gkr_prove(ctx, *c, workspace(*c, 0), f, inputs, tr, proof, cap, comm);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+    });
+}
+
+int dgkr_gkr_prove_dist_emulated(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, int world,
+                                 const std::uint8_t* inputs_all, dgkr_transcript* t, std::uint8_t* proof,
+                                 std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (world < 1 || world > 64 || (world & (world - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "world must be 1..64, pow2");
+        if (!inputs_all) fail(DGKR_INVALID_ARGUMENT, "inputs must not be NULL");
+        const std::size_t in_bytes = static_cast<std::size_t>(c->input_size) * c->n_copies * f->f.width();
+        std::vector<Lane*> lanes(world);
+        for (int r = 0; r < world; ++r) {
+            lanes[r] = ctx->lane(r);
+            workspace(*c, r);
+        }
+        ctx->use(f);
+        ThreadGroup group;
+        group.world = world;
+        std::vector<ThreadComm> comms(world);
+        std::vector<std::vector<std::uint8_t>> bufs(world);
+        std::vector<std::size_t> lens(world, 0);
+        std::vector<dgkr_transcript> ts(world, *t);
+        std::vector<int> codes(world, DGKR_OK);
+        std::vector<std::string> errs(world);
+        for (int r = 0; r < world; ++r) {
+            comms[r].rank = r;
+            comms[r].world = world;
+            comms[r].g = &group;
+            if (r) bufs[r].resize(cap);
+        }
+        auto work = [&](int r) {
+            try {
+                CK(cudaSetDevice(ctx->device));
+                Lane* L = lanes[r];
+                L->begin_call();
+                Transcript tr(&f->f, ts[r].state, ts[r].draws);
+                std::uint8_t* dst = r ? bufs[r].data() : proof;
+                lens[r] = gkr_prove(L, *c, workspace(*c, r), f, inputs_all + r * in_bytes, tr, dst, cap, &comms[r]);
+                std::memcpy(ts[r].state, tr.state().data(), 32);
+                ts[r].draws = tr.draws();
+                L->end_call();
+            } catch (const Error& e) {
+                codes[r] = e.code;
+                errs[r] = e.what();
+                group.abort();
+            } catch (const std::exception& e) {
+                codes[r] = DGKR_LOGIC_ERROR;
+                errs[r] = e.what();
+                group.abort();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int r = 1; r < world; ++r) th.emplace_back(work, r);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int r = 0; r < world; ++r)
+            if (codes[r] != DGKR_OK) fail(codes[r], "rank " + std::to_string(r) + ": " + errs[r]);
+        // every rank must hold the identical proof (outside the claimed-output
+        // block, which only rank 0 gathers) and transcript
+        const std::size_t ob = 4 + c->full_padded[c->depth] * static_cast<std::size_t>(world) * f->f.width();
+        for (int r = 1; r < world; ++r) {
+            if (lens[r] != lens[0] || std::memcmp(bufs[r].data(), proof, 4) != 0 ||
+                std::memcmp(bufs[r].data() + ob, proof + ob, lens[0] - ob) != 0 ||
+                std::memcmp(ts[r].state, ts[0].state, 32) != 0 || ts[r].draws != ts[0].draws)
+                fail(DGKR_LOGIC_ERROR, "ranks disagree on the proof");
+        }
+        *len = lens[0];
+        *t = ts[0];
     });
 }
 

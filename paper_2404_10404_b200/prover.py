@@ -302,6 +302,65 @@ def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[El
     return [out_bufs[i][: lens[i]].tobytes() for i in range(n)]
 
 
+def gkr_prove_dist_emulated(ctx: Context, circuit: Circuit, world: int, inputs_all: Elems, tr: Transcript) -> bytes:
+    """The multi-GPU data-parallel prover with `world` ranks emulated as host
+    threads on one GPU (circuit = one rank's share, n_copies = total/world).
+    Returns the proof, which every rank must have produced identically."""
+    f = tr.field
+    data = inputs_all if isinstance(inputs_all, np.ndarray) else np.frombuffer(f.encode(inputs_all), np.uint8)
+    cap = circuit.proof_bound(f) + (world - 1) * circuit.output_size * f.width + 4096 * world
+    out = np.empty(cap, dtype=np.uint8)
+    ln = C.c_size_t()
+    check(lib().dgkr_gkr_prove_dist_emulated(ctx.handle, circuit.handle, f.handle, C.c_int(world), _buf(data),
+                                             C.byref(tr.t), _buf(out), C.c_size_t(cap), C.byref(ln)))
+    return out[: ln.value].tobytes()
+
+
+class Comm:
+    """NCCL communicator for one rank (dgkr_comm); uid from nccl_unique_id()."""
+
+    def __init__(self, ctx: Context, uid: bytes, rank: int, world: int):
+        h = C.c_void_p()
+        check(lib().dgkr_comm_create_nccl(ctx.handle, C.c_char_p(bytes(uid)), C.c_int(rank), C.c_int(world),
+                                          C.byref(h)))
+        self._h = h
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        out = C.create_string_buffer(128)
+        check(lib().dgkr_comm_nccl_unique_id(out))
+        return out.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dgkr_comm_destroy(self._h)
+        except Exception:
+            pass
+
+
+def gkr_prove_dist(ctx: Context, comm: Comm, circuit: Circuit, inputs: Optional[Elems], tr: Transcript,
+                   out_buf=None) -> bytes:
+    """One rank of the multi-GPU prover (inputs = this rank's share, or None
+    for inputs loaded with load_inputs_lane(..., lane=0, ...))."""
+    f = tr.field
+    cap = circuit.proof_bound(f) + (comm.world - 1) * circuit.output_size * f.width + 4096 * comm.world
+    if out_buf is None or len(out_buf) < cap:
+        out_buf = np.empty(cap, dtype=np.uint8)
+    data = None if inputs is None else (inputs if isinstance(inputs, np.ndarray) else
+                                        np.frombuffer(f.encode(inputs), np.uint8))
+    ln = C.c_size_t()
+    check(lib().dgkr_gkr_prove_dist(ctx.handle, comm.handle, circuit.handle, f.handle,
+                                    _buf(data) if data is not None else C.c_void_p(None), C.byref(tr.t),
+                                    _buf(out_buf), C.c_size_t(cap), C.byref(ln)))
+    return out_buf[: ln.value].tobytes()
+
+
 def load_inputs_lane(ctx: Context, circuit: Circuit, field: Field, lane: int, inputs: Elems) -> None:
     data = inputs if isinstance(inputs, np.ndarray) else np.frombuffer(field.encode(inputs), np.uint8)
     check(lib().dgkr_circuit_load_inputs_lane(ctx.handle, circuit.handle, field.handle, C.c_int(lane), _buf(data)))
