@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "field.cuh"
 #include "kernels.hpp"
@@ -222,8 +223,8 @@ __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i
     }
 }
 
-template <class F, int NP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kThreads) k_round(RoundParams a) {
+template <class F, int NP, bool HAS_G, int MODE, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_round(RoundParams a) {
     Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
     Fe r = fe_zero();
     if (MODE != kScan) r = fe_load(a.r);
@@ -769,7 +770,15 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
     RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, a.r, ws.partials, ws.counter, ws.result};
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
-#define LAUNCH_ROUND(NP, HG, MD) k_round<F, NP, HG, MD><<<g, kThreads, 0, st>>>(p)
+    static const int minb = [] {
+        const char* e = std::getenv("DGKR_ROUND_MINB");
+        return (e && e[0] == '3') ? 3 : 2;
+    }();
+#define LAUNCH_ROUND(NP, HG, MD)                                             \
+    do {                                                                     \
+        if (minb == 3) k_round<F, NP, HG, MD, 3><<<g, kThreads, 0, st>>>(p); \
+        else k_round<F, NP, HG, MD, 2><<<g, kThreads, 0, st>>>(p);           \
+    } while (0)
 #define BY_MODE(NP, HG)                                   \
     do {                                                  \
         if (a.mode == kScan) LAUNCH_ROUND(NP, HG, kScan);  \

@@ -174,11 +174,14 @@ struct Lane {
         CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
         CK(cudaEventCreate(&ev0));
         CK(cudaEventCreate(&ev1));
+        CK(cudaEventCreateWithFlags(&ev_sync, cudaEventBlockingSync | cudaEventDisableTiming));
+        if (const char* e = std::getenv("DGKR_SPIN_US")) spin_ms = std::atof(e) * 1e-3;
     }
     Lane(const Lane&) = delete;
     Lane& operator=(const Lane&) = delete;
 
     ~Lane() {
+        if (ev_sync) cudaEventDestroy(ev_sync);
         if (h_small) cudaFreeHost(h_small);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -198,7 +201,22 @@ struct Lane {
         return f->kind;
     }
 
-    void sync() { CK(cudaStreamSynchronize(st)); }
+    /// Wait for the stream: poll briefly (round kernels on small tables finish
+    /// in microseconds), then block on an event so that waiting lanes leave
+    /// the host cores to the lanes running their serial SHA-256 chains.
+    void sync() {
+        CK(cudaEventRecord(ev_sync, st));
+        const double t0 = now_ms();
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(ev_sync);
+            if (q == cudaSuccess) return;
+            if (q != cudaErrorNotReady) CK(q);
+            if (now_ms() - t0 > spin_ms) break;
+        }
+        CK(cudaEventSynchronize(ev_sync));
+    }
+    cudaEvent_t ev_sync = nullptr;
+    double spin_ms = 1e12;  // measured: polling beats blocking even with 16 lanes (DGKR_SPIN_US to change)
 
     void begin_call() {
         std::memset(&prof, 0, sizeof(prof));
@@ -941,7 +959,11 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
     if (D >= 1) {
         W.H.ensure(static_cast<std::size_t>(c.max_slots) * c.Tmax);
         W.G.ensure(c.Tmax);
-        W.Wg.ensure(c.Tmax);
+        // per-gate weights are indexed by consumer gate: a layer may have more
+        // gates than its (padded) source tables have entries
+        std::uint64_t gmax = 1;
+        for (std::uint32_t l = 1; l <= D; ++l) gmax = std::max(gmax, c.full_padded[l]);
+        W.Wg.ensure(gmax);
         W.EqU.ensure(c.Tmax);
         W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
     }

@@ -169,6 +169,25 @@ def test_gkr_general_circuits_match_oracle(ctx, p, trial):
     assert got == want and tr.state == otr.state and tr.draws == otr.draws
 
 
+@pytest.mark.parametrize("seed", [1, 4, 10, 18, 21, 25, 40, 77])
+def test_gkr_reference_generated_wide_consumers(ctx, seed):
+    """Reference-generated circuits (circuit::random_general_circuit) whose
+    consumer layers have more gates than their source tables (regression:
+    the per-gate weight buffer was sized by the source tables)."""
+    from oracle import refbind as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    fld = O.BN254
+    insz, depth = 5 + seed % 8, 2 + seed % 4
+    c = R.random_general_circuit(1000 + seed, insz, depth, 24, 3)
+    inputs = O.random_elements(fld, insz, np.random.default_rng(seed))
+    want, st = R.gkr_prove(fld, "h", [seed], c, inputs)
+    tr = P.Transcript(P.Field(fld.p), "h", [seed])
+    assert P.gkr_prove(ctx, P.Circuit.from_oracle(ctx, c), inputs, tr) == want
+    assert tr.state == st
+
+
 def test_gkr_layered_matches_oracle(ctx):
     insz, flat = W.layered_circuit(seed=5, log_width=6, depth=5)
     circ = O.Circuit.from_flat(insz, *flat)
