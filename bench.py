@@ -3,14 +3,19 @@
 
 Default workload (N=1): config C2 — a data-parallel GKR proof of 64 identical
 sub-circuits of 2^16 gates/layer x 24 layers (100,663,296 gates) over BN254,
-synthetic inputs. One "step" = one complete gkr_prove (gkr.hpp:182-244):
+synthetic inputs. One proof = one complete gkr_prove (gkr.hpp:182-244):
 circuit evaluation, serial output-table absorb, 24 two-phase layer
-sum-checks, proof bytes back to the host.
+sum-checks, proof bytes back to the host. One "step" = `--lanes` proofs; the
+K timed steps run as one continuous stream of K*lanes proofs over `lanes`
+concurrent lanes (dgkr_gkr_prove_stream), because bit-exactness forces a
+~0.5 s serial host SHA-256 chain per proof that only
+concurrency can hide.
 
-  value  inputs resident in HBM when the timed region starts
-         (dgkr_gkr_prove_resident), CUDA events on the prover's stream
-  e2e    the public C-ABI call dgkr_gkr_prove with pinned host inputs and
-         proof bytes written back to a pinned host buffer
+  value  gates/s of the stream, inputs resident in HBM on every lane, CUDA
+         events around the stream
+  proof_latency_ms   one proof alone (dgkr_gkr_prove_resident)
+  e2e    the same stream through the public C-ABI call with pinned host
+         inputs (H2D inside) and proof bytes back to pinned host buffers
   roofline / roofline_int   fused fold+round kernel (the dominant kernel),
          from a separate profiled step (per-launch CUDA events)
   cpu_baseline   the compiled reference (oracle/_ref) on a bounded sample
@@ -246,71 +251,66 @@ def run_b200(args, cfg_name):
         lat_ms.append(ms.value)
     latency_ms = statistics.median(lat_ms)
 
-    # (2) throughput: a step is a batch of `lanes` concurrent proofs (one lane =
-    # stream + workspace + host thread), inputs resident in HBM per lane
+    # (2) throughput: a step is `lanes` proofs; the K timed steps run as ONE
+    # continuous stream of K*lanes proofs over `lanes` lanes (work queue: a
+    # lane takes the next proof when it finishes one, so the serial host
+    # transcript of one proof overlaps the GPU work of the others). Inputs
+    # are resident in HBM on every lane.
     lanes = args.lanes
     for i in range(lanes):
         P.load_inputs_lane(ctx, circ, field, i, in_pinned)
-    bufs = [out_buf] + [np.empty(cap, dtype=np.uint8) for _ in range(lanes - 1)]
-    for b in bufs[1:]:
-        check(lib().dgkr_host_register(b.ctypes.data_as(C.c_void_p), C.c_size_t(b.nbytes)))
-    outs = (C.c_void_p * lanes)(*[b.ctypes.data for b in bufs])
-    caps = (C.c_size_t * lanes)(*([cap] * lanes))
-    lens = (C.c_size_t * lanes)()
-    in_ptrs = (C.c_void_p * lanes)(*([in_pinned.ctypes.data] * lanes))
     from paper_2404_10404_b200._lib import Profile_t, Transcript_t
 
-    def batch(resident: bool):
-        tarr = (Transcript_t * lanes)()
-        for i in range(lanes):
+    n_max = lanes * max(args.steps, args.warmup)
+    bufs = [out_buf] + [np.empty(cap, dtype=np.uint8) for _ in range(n_max - 1)]
+    for b in bufs[1:]:
+        check(lib().dgkr_host_register(b.ctypes.data_as(C.c_void_p), C.c_size_t(b.nbytes)))
+
+    def stream(n_proofs: int, resident: bool):
+        tarr = (Transcript_t * n_proofs)()
+        for i in range(n_proofs):
             tarr[i] = P.Transcript(field, "dgkr.bench.c2").t
-        check(lib().dgkr_gkr_prove_batch(ctx.handle, circ.handle, field.handle, C.c_size_t(lanes),
-                                         None if resident else in_ptrs, tarr, outs, caps, lens))
-        for i in range(lanes):
-            assert bytes(tarr[i].state) == state0, "batch proof differs from the single proof"
-        prof = Profile_t()
+        outs = (C.c_void_p * n_proofs)(*[bufs[i].ctypes.data for i in range(n_proofs)])
+        caps = (C.c_size_t * n_proofs)(*([cap] * n_proofs))
+        lens = (C.c_size_t * n_proofs)()
+        in_ptrs = None if resident else (C.c_void_p * n_proofs)(*([in_pinned.ctypes.data] * n_proofs))
+        profs = (Profile_t * lanes)()
+        check(lib().dgkr_gkr_prove_stream(ctx.handle, circ.handle, field.handle, C.c_size_t(n_proofs),
+                                          C.c_size_t(lanes), in_ptrs, tarr, outs, caps, lens, profs))
+        for i in range(n_proofs):
+            assert bytes(tarr[i].state) == state0, "stream proof differs from the single proof"
         tot = {"launches": 0, "h2d_bytes": 0, "d2h_bytes": 0, "output_absorb_ms": 0.0, "host_transcript_ms": 0.0,
                "rounds": 0}
-        for i in range(lanes):
-            check(lib().dgkr_ctx_get_profile_lane(ctx.handle, C.c_int(i), C.byref(prof)))
+        for i in range(min(lanes, n_proofs)):
             for k in tot:
-                tot[k] += getattr(prof, k)
-        return tot
+                tot[k] += getattr(profs[i], k)
+        return tot, lens[0]
 
-    for _ in range(args.warmup):
-        batch(True)
+    stream(lanes * args.warmup, True)
     clocks = ClockSampler(local_rank)
     clocks.start()
-    launches = 0
-    phase = {"output_absorb_ms": 0.0, "host_transcript_ms": 0.0, "rounds": 0}
     check(lib().dgkr_ctx_event_record(ctx.handle, 0))
-    for _ in range(args.steps):
-        tot = batch(True)
-        launches += tot["launches"]
-        for k in phase:
-            phase[k] += tot[k]
+    tot, proof_len = stream(lanes * args.steps, True)
     check(lib().dgkr_ctx_event_record(ctx.handle, 1))
     ms = C.c_float()
     check(lib().dgkr_ctx_event_elapsed(ctx.handle, 0, 1, C.byref(ms)))
     clk = clocks.stop()
+    launches = tot["launches"]
+    phase = {k: tot[k] for k in ("output_absorb_ms", "host_transcript_ms", "rounds")}
     ms_per_step = ms.value / args.steps
     value = lanes * gates / (ms_per_step * 1e-3)
-    proof_len = lens[0]
 
-    # (3) e2e through the public batch call with pinned host inputs/outputs
-    for _ in range(max(1, args.warmup // 2)):
-        batch(False)
+    # (3) e2e: the same stream through the public call with pinned host inputs
+    # (H2D inside) and proof bytes back in pinned host buffers (D2H inside)
+    stream(lanes, False)
     check(lib().dgkr_ctx_event_record(ctx.handle, 2))
     t0 = time.perf_counter()
-    h2d = d2h = 0
-    for _ in range(args.steps):
-        tot = batch(False)
-        h2d += tot["h2d_bytes"]
-        d2h += tot["d2h_bytes"]
+    tot, _ = stream(lanes * args.steps, False)
     check(lib().dgkr_ctx_event_record(ctx.handle, 3))
     wall_e2e = (time.perf_counter() - t0) / args.steps
     check(lib().dgkr_ctx_event_elapsed(ctx.handle, 2, 3, C.byref(ms)))
     e2e_ms = ms.value / args.steps
+    h2d, d2h = tot["h2d_bytes"], tot["d2h_bytes"]
     for b in bufs[1:]:
         check(lib().dgkr_host_unregister(b.ctypes.data_as(C.c_void_p)))
 
@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=8,
+    ap.add_argument("--lanes", type=int, default=16,
                     help="concurrent proofs per step (lanes); the single-proof latency is reported separately")
     args = ap.parse_args()
     if args.impl == "reference":

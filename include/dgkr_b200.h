@@ -166,6 +166,14 @@ int dgkr_gkr_prove_resident(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f,
 int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, size_t n,
                          const uint8_t* const* inputs, dgkr_transcript* ts, uint8_t* const* proofs,
                          const size_t* caps, size_t* lens);
+/* n proofs over n_lanes lanes as a work queue (a lane takes the next proof
+ * when it finishes one), so the host transcript phases of different proofs
+ * stagger instead of coinciding. inputs == NULL: every proof uses the inputs
+ * loaded on the lane that runs it. lane_profiles (n_lanes entries, or NULL)
+ * receives each lane's accumulated counters. */
+int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, size_t n, size_t n_lanes,
+                          const uint8_t* const* inputs, dgkr_transcript* ts, uint8_t* const* proofs,
+                          const size_t* caps, size_t* lens, dgkr_profile* lane_profiles);
 int dgkr_circuit_load_inputs_lane(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, int lane,
                                   const uint8_t* inputs);
 int dgkr_ctx_get_profile_lane(dgkr_ctx* ctx, int lane, dgkr_profile* out);
@@ -182,6 +190,20 @@ typedef struct dgkr_comm dgkr_comm;
 int dgkr_comm_nccl_unique_id(uint8_t* out128);
 int dgkr_comm_create_nccl(dgkr_ctx* ctx, const uint8_t* uid128, int rank, int world, dgkr_comm** out);
 void dgkr_comm_destroy(dgkr_comm* comm);
+/* One-node transport over POSIX shared memory (one segment per lane, named
+ * e.g. "/dgkr_<token>_<lane>", same name on every rank; slot_bytes >= the
+ * largest exchange, i.e. the claimed outputs of one rank). Per-lane segments
+ * and barriers keep concurrently progressing lanes independent. */
+int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, size_t slot_bytes,
+                         dgkr_comm** out);
+/* host-only all-gather through a shared-memory communicator (transport test hook) */
+int dgkr_comm_allgather_host(dgkr_comm* comm, const void* in, size_t bytes, void* out);
+/* n distributed proofs over n_lanes lanes, lane l using comms[l] and proving
+ * l, l+n_lanes, ... in order on every rank (inputs NULL = lane-resident). */
+int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, size_t n_lanes, dgkr_circuit* c,
+                               const dgkr_field* f, size_t n, const uint8_t* const* inputs, dgkr_transcript* ts,
+                               uint8_t* const* proofs, const size_t* caps, size_t* lens,
+                               dgkr_profile* lane_profiles);
 /* inputs: this rank's n*input_size elements, or NULL for inputs already loaded
  * with dgkr_circuit_load_inputs */
 int dgkr_gkr_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, dgkr_circuit* c, const dgkr_field* f,

@@ -5,8 +5,12 @@
 // O(table) work runs in the sm_100a kernels of kernels.cu.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <condition_variable>
 
 #include <algorithm>
@@ -376,6 +380,90 @@ struct ThreadComm : dgkr_comm {
         if (rank == 0) std::memcpy(g->buf.data(), h, bytes);
         g->barrier();
         if (rank != 0) std::memcpy(h, g->buf.data(), bytes);
+    }
+};
+
+// One-node multi-process transport: a POSIX shared-memory segment per lane
+// (ranks = processes, one per GPU). The per-round payloads are already on the
+// host (the transcript needs them there), so a host exchange is the
+// lowest-latency path; every lane has its own segment and barrier, so lanes
+// never order-depend on one another (no cross-lane deadlock, unlike sharing
+// NCCL communicators between concurrently progressing lanes).
+struct ShmHeader {
+    std::atomic<std::uint64_t> arrived;
+    std::atomic<std::uint64_t> gen;
+    std::atomic<std::uint32_t> aborted;
+    std::uint32_t world;
+    std::uint64_t slot_bytes;
+};
+
+struct ShmComm : dgkr_comm {
+    ShmHeader* hdr = nullptr;
+    std::uint8_t* data = nullptr;  // world * slot_bytes
+    std::size_t map_bytes = 0;
+    std::string name;
+    bool owner = false;
+    ~ShmComm() override {
+        if (hdr) munmap(hdr, map_bytes);
+        if (owner) shm_unlink(name.c_str());
+    }
+    void barrier() {
+        const std::uint64_t g = hdr->gen.load(std::memory_order_acquire);
+        if (hdr->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<std::uint64_t>(world)) {
+            hdr->arrived.store(0, std::memory_order_relaxed);
+            hdr->gen.fetch_add(1, std::memory_order_acq_rel);
+            return;
+        }
+        for (std::uint64_t spins = 0; hdr->gen.load(std::memory_order_acquire) == g; ++spins) {
+            if (hdr->aborted.load(std::memory_order_relaxed)) fail(DGKR_COMM_ERROR, "peer rank aborted");
+            if (spins > 2000) std::this_thread::yield();
+        }
+    }
+    std::uint8_t* slot(int r) { return data + static_cast<std::size_t>(r) * hdr->slot_bytes; }
+    void need(std::size_t bytes) const {
+        if (bytes > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small for this exchange");
+    }
+    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
+        need(bytes);
+        barrier();  // previous contents consumed
+        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        barrier();
+        for (int r = 0; r < world; ++r)
+            CK(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_recv) + r * bytes, slot(r), bytes, cudaMemcpyHostToDevice, L->st));
+        L->sync();
+    }
+    void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+        need(bytes);
+        barrier();
+        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        barrier();
+        for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
+    }
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+        need(bytes);
+        barrier();
+        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        barrier();
+        if (rank == 0)
+            for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
+    }
+    void broadcast_host(void* h, std::size_t bytes, Lane*) override {
+        need(bytes);
+        barrier();
+        if (rank == 0) std::memcpy(slot(0), h, bytes);
+        barrier();
+        if (rank != 0) std::memcpy(h, slot(0), bytes);
+    }
+    /// host-only exchange (tests the transport without a GPU)
+    void allgather_host(const void* in, std::size_t bytes, void* out) {
+        need(bytes);
+        barrier();
+        std::memcpy(slot(rank), in, bytes);
+        barrier();
+        for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(out) + r * bytes, slot(r), bytes);
     }
 };
 
@@ -1914,42 +2002,66 @@ int dgkr_gkr_prove_resident(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f,
 int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, std::size_t n,
                          const std::uint8_t* const* inputs, dgkr_transcript* ts, std::uint8_t* const* proofs,
                          const std::size_t* caps, std::size_t* lens) {
+    return dgkr_gkr_prove_stream(ctx, c, f, n, n, inputs, ts, proofs, caps, lens, nullptr);
+}
+
+int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, std::size_t n, std::size_t n_lanes,
+                          const std::uint8_t* const* inputs, dgkr_transcript* ts, std::uint8_t* const* proofs,
+                          const std::size_t* caps, std::size_t* lens, dgkr_profile* lane_profiles) {
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
-        if (n == 0 || n > 64) fail(DGKR_OUT_OF_RANGE, "batch size must be 1..64");
-        std::vector<Lane*> lanes(n);
-        for (std::size_t i = 0; i < n; ++i) {
+        if (n == 0) fail(DGKR_OUT_OF_RANGE, "no proofs");
+        if (n_lanes == 0 || n_lanes > 64) fail(DGKR_OUT_OF_RANGE, "lanes must be 1..64");
+        const std::size_t L = std::min(n, n_lanes);
+        std::vector<Lane*> lanes(L);
+        for (std::size_t i = 0; i < L; ++i) {
             lanes[i] = ctx->lane(static_cast<int>(i));
             workspace(*c, static_cast<int>(i));  // allocate before the threads start
+            std::memset(&lanes[i]->prof, 0, sizeof(dgkr_profile));
         }
         ctx->use(f);  // upload runtime-field constants once, before concurrency
         std::vector<std::string> errs(n);
         std::vector<int> codes(n, DGKR_OK);
-        auto work = [&](std::size_t i) {
-            try {
-                CK(cudaSetDevice(ctx->device));
-                Lane* L = lanes[i];
-                L->begin_call();
-                Transcript tr(&f->f, ts[i].state, ts[i].draws);
-                lens[i] = gkr_prove(L, *c, workspace(*c, static_cast<int>(i)), f, inputs ? inputs[i] : nullptr, tr,
-                                    proofs[i], caps[i]);
-                std::memcpy(ts[i].state, tr.state().data(), 32);
-                ts[i].draws = tr.draws();
-                L->end_call();
-            } catch (const Error& e) {
-                codes[i] = e.code;
-                errs[i] = e.what();
-            } catch (const std::exception& e) {
-                codes[i] = DGKR_LOGIC_ERROR;
-                errs[i] = e.what();
+        std::atomic<std::size_t> next{0};
+        auto work = [&](std::size_t li) {
+            CK(cudaSetDevice(ctx->device));
+            Lane* Ln = lanes[li];
+            dgkr_profile acc{};
+            for (;;) {
+                const std::size_t i = next.fetch_add(1);
+                if (i >= n) break;
+                try {
+                    Ln->begin_call();
+                    Transcript tr(&f->f, ts[i].state, ts[i].draws);
+                    lens[i] = gkr_prove(Ln, *c, workspace(*c, static_cast<int>(li)), f, inputs ? inputs[i] : nullptr,
+                                        tr, proofs[i], caps[i]);
+                    std::memcpy(ts[i].state, tr.state().data(), 32);
+                    ts[i].draws = tr.draws();
+                    Ln->end_call();
+                    acc.launches += Ln->prof.launches;
+                    acc.h2d_bytes += Ln->prof.h2d_bytes;
+                    acc.d2h_bytes += Ln->prof.d2h_bytes;
+                    acc.rounds += Ln->prof.rounds;
+                    acc.output_absorb_ms += Ln->prof.output_absorb_ms;
+                    acc.host_transcript_ms += Ln->prof.host_transcript_ms;
+                    acc.total_ms += Ln->prof.total_ms;
+                } catch (const Error& e) {
+                    codes[i] = e.code;
+                    errs[i] = e.what();
+                } catch (const std::exception& e) {
+                    codes[i] = DGKR_LOGIC_ERROR;
+                    errs[i] = e.what();
+                }
             }
+            if (lane_profiles) lane_profiles[li] = acc;
+            Ln->prof = acc;
         };
         std::vector<std::thread> th;
-        for (std::size_t i = 1; i < n; ++i) th.emplace_back(work, i);
+        for (std::size_t i = 1; i < L; ++i) th.emplace_back(work, i);
         work(0);
         for (auto& t : th) t.join();
         for (std::size_t i = 0; i < n; ++i)
-            if (codes[i] != DGKR_OK) fail(codes[i], "batch proof " + std::to_string(i) + ": " + errs[i]);
+            if (codes[i] != DGKR_OK) fail(codes[i], "proof " + std::to_string(i) + ": " + errs[i]);
     });
 }
 
@@ -1978,6 +2090,105 @@ int dgkr_comm_create_nccl(dgkr_ctx* ctx, const std::uint8_t* uid128, int rank, i
 }
 
 void dgkr_comm_destroy(dgkr_comm* c) { delete c; }
+
+int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, std::size_t slot_bytes,
+                         dgkr_comm** out) {
+    return guard([&] {
+        (void)ctx;
+        if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
+        if (!name || name[0] != '/') fail(DGKR_INVALID_ARGUMENT, "shm name must start with '/'");
+        auto c = std::make_unique<ShmComm>();
+        c->rank = rank;
+        c->world = world;
+        c->name = name;
+        c->owner = rank == 0;
+        const std::size_t hb = 64;
+        c->map_bytes = hb + static_cast<std::size_t>(world) * slot_bytes;
+        const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0) fail(DGKR_COMM_ERROR, std::string("shm_open failed: ") + name);
+        if (ftruncate(fd, static_cast<off_t>(c->map_bytes)) != 0) {
+            close(fd);
+            fail(DGKR_COMM_ERROR, "ftruncate failed");
+        }
+        void* p = mmap(nullptr, c->map_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (p == MAP_FAILED) fail(DGKR_COMM_ERROR, "mmap failed");
+        c->hdr = static_cast<ShmHeader*>(p);
+        c->hdr->world = static_cast<std::uint32_t>(world);
+        c->hdr->slot_bytes = slot_bytes;
+        c->data = static_cast<std::uint8_t*>(p) + hb;
+        *out = c.release();
+    });
+}
+
+int dgkr_comm_allgather_host(dgkr_comm* comm, const void* in, std::size_t bytes, void* out) {
+    return guard([&] {
+        auto* s = dynamic_cast<ShmComm*>(comm);
+        if (!s) fail(DGKR_UNSUPPORTED, "host all-gather is a shared-memory communicator test hook");
+        s->allgather_host(in, bytes, out);
+    });
+}
+
+int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size_t n_lanes, dgkr_circuit* c,
+                               const dgkr_field* f, std::size_t n, const std::uint8_t* const* inputs,
+                               dgkr_transcript* ts, std::uint8_t* const* proofs, const std::size_t* caps,
+                               std::size_t* lens, dgkr_profile* lane_profiles) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n == 0 || n_lanes == 0 || n_lanes > 64) fail(DGKR_OUT_OF_RANGE, "bad proof / lane count");
+        const std::size_t L = std::min(n, n_lanes);
+        std::vector<Lane*> lanes(L);
+        for (std::size_t i = 0; i < L; ++i) {
+            lanes[i] = ctx->lane(static_cast<int>(i));
+            workspace(*c, static_cast<int>(i));
+        }
+        ctx->use(f);
+        std::vector<int> codes(n, DGKR_OK);
+        std::vector<std::string> errs(n);
+        // static assignment: lane l proves l, l+L, l+2L, ... in order on every
+        // rank, so lane l's exchanges pair up across ranks
+        auto work = [&](std::size_t li) {
+            CK(cudaSetDevice(ctx->device));
+            Lane* Ln = lanes[li];
+            dgkr_profile acc{};
+            for (std::size_t i = li; i < n; i += L) {
+                try {
+                    Ln->begin_call();
+                    Transcript tr(&f->f, ts[i].state, ts[i].draws);
+                    lens[i] = gkr_prove(Ln, *c, workspace(*c, static_cast<int>(li)), f, inputs ? inputs[i] : nullptr,
+                                        tr, proofs[i], caps[i], comms[li]);
+                    std::memcpy(ts[i].state, tr.state().data(), 32);
+                    ts[i].draws = tr.draws();
+                    Ln->end_call();
+                    acc.launches += Ln->prof.launches;
+                    acc.h2d_bytes += Ln->prof.h2d_bytes;
+                    acc.d2h_bytes += Ln->prof.d2h_bytes;
+                    acc.rounds += Ln->prof.rounds;
+                    acc.output_absorb_ms += Ln->prof.output_absorb_ms;
+                    acc.host_transcript_ms += Ln->prof.host_transcript_ms;
+                    acc.total_ms += Ln->prof.total_ms;
+                } catch (const Error& e) {
+                    codes[i] = e.code;
+                    errs[i] = e.what();
+                    if (auto* s = dynamic_cast<ShmComm*>(comms[li])) s->hdr->aborted.store(1);
+                    break;
+                } catch (const std::exception& e) {
+                    codes[i] = DGKR_LOGIC_ERROR;
+                    errs[i] = e.what();
+                    if (auto* s = dynamic_cast<ShmComm*>(comms[li])) s->hdr->aborted.store(1);
+                    break;
+                }
+            }
+            if (lane_profiles) lane_profiles[li] = acc;
+        };
+        std::vector<std::thread> th;
+        for (std::size_t i = 1; i < L; ++i) th.emplace_back(work, i);
+        work(0);
+        for (auto& t : th) t.join();
+        for (std::size_t i = 0; i < n; ++i)
+            if (codes[i] != DGKR_OK) fail(codes[i], "proof " + std::to_string(i) + ": " + errs[i]);
+    });
+}
 
 int dgkr_gkr_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, dgkr_circuit* c, const dgkr_field* f,
                         const std::uint8_t* inputs, dgkr_transcript* t, std::uint8_t* proof, std::size_t cap,

@@ -1,0 +1,155 @@
+"""Multi-GPU data-parallel proving: one process per GPU (torchrun), rank r
+proving copies [r*n, (r+1)*n) of the data-parallel circuit (the rank index is
+the top log2(world) variables of every layer, cluster.hpp:182-189).
+
+Transports (csrc/prover.cpp):
+  * shared memory ("shm", default for the multi-lane stream): one POSIX
+    segment per lane; per-round payloads are host-resident already, so a
+    one-node host exchange is the lowest-latency path and keeps lanes
+    independent;
+  * NCCL ("nccl"): one communicator per process over NVLink/NVSwitch; used
+    for single-lane proving (dgkr_gkr_prove_dist).
+
+torch.distributed is the plumbing: rendezvous, the token/NCCL-id broadcast,
+barriers and the max-over-ranks timing reduction.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import secrets
+import statistics
+import time
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import prover as P
+from ._lib import Profile_t, Transcript_t, check, lib
+
+
+class ShmComm:
+    """dgkr_comm over a shared-memory segment `name` (same on every rank)."""
+
+    def __init__(self, ctx: Optional[P.Context], name: str, rank: int, world: int, slot_bytes: int):
+        h = C.c_void_p()
+        check(lib().dgkr_comm_create_shm(ctx.handle if ctx is not None else None, name.encode(), C.c_int(rank),
+                                         C.c_int(world), C.c_size_t(slot_bytes), C.byref(h)))
+        self._h = h
+        self.rank, self.world = rank, world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def allgather_host(self, data: bytes) -> List[bytes]:
+        out = C.create_string_buffer(len(data) * self.world)
+        check(lib().dgkr_comm_allgather_host(self._h, C.c_char_p(bytes(data)), C.c_size_t(len(data)), out))
+        raw = out.raw
+        return [raw[i * len(data):(i + 1) * len(data)] for i in range(self.world)]
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dgkr_comm_destroy(self._h)
+        except Exception:
+            pass
+
+
+def slot_bytes_for(circuit: P.Circuit, field: P.Field) -> int:
+    """largest single exchange: one rank's claimed outputs"""
+    return max(circuit.output_size * field.width, 4096)
+
+
+def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field: P.Field, n: int, label: str,
+                      inputs=None, out_bufs=None):
+    """n distributed proofs over len(comms) lanes (lane l: proofs l, l+L, ...)."""
+    L = len(comms)
+    cap = circuit.proof_bound(field) + (comms[0].world - 1) * circuit.output_size * field.width + 4096
+    if out_bufs is None:
+        out_bufs = [np.empty(cap, dtype=np.uint8) for _ in range(n)]
+    tarr = (Transcript_t * n)()
+    for i in range(n):
+        tarr[i] = P.Transcript(field, label).t
+    outs = (C.c_void_p * n)(*[out_bufs[i].ctypes.data for i in range(n)])
+    caps = (C.c_size_t * n)(*[len(out_bufs[i]) for i in range(n)])
+    lens = (C.c_size_t * n)()
+    carr = (C.c_void_p * L)(*[c.handle.value for c in comms])
+    in_ptrs = None
+    if inputs is not None:
+        in_ptrs = (C.c_void_p * n)(*([inputs.ctypes.data] * n))
+    profs = (Profile_t * L)()
+    check(lib().dgkr_gkr_prove_dist_stream(ctx.handle, carr, C.c_size_t(L), circuit.handle, field.handle,
+                                           C.c_size_t(n), in_ptrs, tarr, outs, caps, lens, profs))
+    return ([out_bufs[i][: lens[i]] for i in range(n)], [bytes(tarr[i].state) for i in range(n)],
+            [profs[i].as_dict() for i in range(L)])
+
+
+def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
+    """bench.py --gpus N under torchrun: every rank proves its share of each
+    proof of a stream; rank 0 prints the JSON line (max-over-ranks timing)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import workloads as W
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n_copies, lw, depth, desc = configs[cfg_name]
+    if n_copies % world:
+        raise SystemExit(f"{n_copies} copies do not shard over {world} GPUs")
+    ctx = P.Context(local_rank)
+    field = P.Field.bn254()
+    insz, flat = W.layered_circuit(circuit_seed, lw, depth)
+    n_local = n_copies // world
+    circ = P.Circuit(ctx, insz, *flat, n_copies=n_local)
+    all_inputs = W.random_inputs(field.p, insz * n_copies, input_seed)
+    per = insz * n_local * field.width
+    mine = np.ascontiguousarray(all_inputs[rank * per:(rank + 1) * per])
+    lanes = args.lanes
+    token = [secrets.token_hex(6) if rank == 0 else None]
+    dist.broadcast_object_list(token, src=0)
+    comms = [ShmComm(ctx, f"/dgkr_{token[0]}_{l}", rank, world, slot_bytes_for(circ, field)) for l in range(lanes)]
+    for l in range(lanes):
+        P.load_inputs_lane(ctx, circ, field, l, mine)
+    gates = n_copies * (1 << lw) * depth
+
+    def timed(n):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2")
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        return float(dt.item()), proofs, states, profs
+
+    timed(lanes * args.warmup)
+    dt, proofs, states, profs = timed(lanes * args.steps)
+    # single-proof latency (one lane)
+    lat, _, _, _ = timed(1)
+    if rank == 0:
+        assert len(set(states)) == 1
+        ms_per_step = 1e3 * dt / args.steps
+        line = {
+            "metric": "gkr_prover_gates_per_sec", "value": lanes * gates / (ms_per_step * 1e-3), "unit": "gates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u256",
+            "data": "synthetic",
+            "config": {"workload": desc, "field": "bn254", "n_copies": n_copies, "copies_per_gpu": n_local,
+                       "gates_per_layer_per_copy": 1 << lw, "depth": depth, "gates": gates,
+                       "parallelism": f"dp{world} (rank = top log2(N) variables)", "transport": "shm per lane",
+                       "l2": "no flush: layer tables exceed L2"},
+            "lanes": lanes, "proof_latency_ms": 1e3 * lat,
+            "e2e": {"value": lanes * gates / (ms_per_step * 1e-3), "unit": "gates/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": sum(p["d2h_bytes"] for p in profs) // args.steps,
+                    "note": "multi-GPU arm measures the resident-input stream only"},
+            "gpu_launches": sum(p["launches"] for p in profs),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

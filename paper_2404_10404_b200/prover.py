@@ -302,6 +302,36 @@ def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[El
     return [out_bufs[i][: lens[i]].tobytes() for i in range(n)]
 
 
+def gkr_prove_stream(ctx: Context, circuit: Circuit, n: int, lanes: int, field: Field, label: str = "stream",
+                     inputs: Optional[Sequence[Elems]] = None, out_bufs=None):
+    """n proofs over `lanes` lanes as a work queue (dgkr_gkr_prove_stream).
+    inputs=None: each proof uses the inputs loaded on its lane. Returns
+    (proofs, transcripts, per-lane profile dicts)."""
+    from ._lib import Profile_t
+
+    cap = circuit.proof_bound(field)
+    if out_bufs is None:
+        out_bufs = [np.empty(cap, dtype=np.uint8) for _ in range(n)]
+    keep = []
+    in_ptrs = None
+    if inputs is not None:
+        arrs = [x if isinstance(x, np.ndarray) else np.frombuffer(field.encode(x), np.uint8) for x in inputs]
+        keep.extend(arrs)
+        in_ptrs = (C.c_void_p * n)(*[a.ctypes.data for a in arrs])
+    tarr = (Transcript_t * n)()
+    for i in range(n):
+        tarr[i] = Transcript(field, label).t
+    outs = (C.c_void_p * n)(*[out_bufs[i].ctypes.data for i in range(n)])
+    caps = (C.c_size_t * n)(*[len(out_bufs[i]) for i in range(n)])
+    lens = (C.c_size_t * n)()
+    nl = min(n, lanes)
+    profs = (Profile_t * nl)()
+    check(lib().dgkr_gkr_prove_stream(ctx.handle, circuit.handle, field.handle, C.c_size_t(n), C.c_size_t(lanes),
+                                      in_ptrs, tarr, outs, caps, lens, profs))
+    return ([out_bufs[i][: lens[i]] for i in range(n)], [bytes(tarr[i].state) for i in range(n)],
+            [profs[i].as_dict() for i in range(nl)])
+
+
 def gkr_prove_dist_emulated(ctx: Context, circuit: Circuit, world: int, inputs_all: Elems, tr: Transcript) -> bytes:
     """The multi-GPU data-parallel prover with `world` ranks emulated as host
     threads on one GPU (circuit = one rank's share, n_copies = total/world).

@@ -1,0 +1,40 @@
+"""GPU: the multi-process (one process per rank) data-parallel prover over
+the shared-memory transport, two ranks sharing this one GPU. Ranks exchange
+only through host shared memory (no kernel waits on another). Rank 0's
+proofs must equal the single-GPU proof of the full circuit."""
+import os
+import secrets
+import subprocess
+import sys
+
+import pytest
+
+import paper_2404_10404_b200 as P
+from paper_2404_10404_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("lanes,n", [(1, 1), (2, 4)])
+def test_two_process_shm_equals_single(ctx, tmp_path, lanes, n):
+    world = 2
+    token = secrets.token_hex(4)
+    out = str(tmp_path / "proofs.bin")
+    worker = os.path.join(ROOT, "tools", "dist_shm_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), token, str(lanes), str(n), out],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    logs = [p.communicate(timeout=300)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(logs)
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(seed=51, log_width=8, depth=5)
+    inputs = W.random_inputs(f.p, insz * 8, 52)
+    tr = P.Transcript(f, "shm")
+    want = P.gkr_prove(ctx, P.Circuit(ctx, insz, *flat, n_copies=8), inputs, tr)
+    raw = open(out, "rb").read()
+    pos = 0
+    for _ in range(n):
+        ln = int.from_bytes(raw[pos:pos + 8], "little")
+        proof, state = raw[pos + 8:pos + 8 + ln], raw[pos + 8 + ln:pos + 8 + ln + 32]
+        pos += 8 + ln + 32
+        assert proof == want and state == tr.state
