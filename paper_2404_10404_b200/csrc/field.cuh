@@ -255,6 +255,73 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
     return r;
 }
 
+/// Multiplication by a per-launch constant r (the sum-check challenge of a
+/// fold), BN254 only. With c_k = r * 2^(32k+64) * R^-1 mod p precomputed on
+/// the host,  mont(x, r) = x r R^-1 = 2^-64 * sum_k x_k c_k  (mod p):
+/// 64 32x32 products + 2 Montgomery steps instead of CIOS's 8 (~40% fewer
+/// IMADs). S = sum < 8 * 2^32 * p < 2^289, so after the two steps the value
+/// is < 2^225 + p < 2p (needs p > 2^253 + 2^224, true for BN254 Fr).
+struct FoldConst {
+    Fe c[8];  // c_k above (fully reduced)
+    Fe r;     // r itself (Montgomery form), for the generic path
+};
+
+__device__ __forceinline__ Fe fe_mul_const_bn254(const Fe& x, const FoldConst& K) {
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(x.v[k]) * K.c[k].v[j] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        const uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] += static_cast<uint32_t>(s >> 32);
+    }
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+        const uint32_t m = t[0] * Bn254::np0();
+        uint64_t c = (static_cast<uint64_t>(m) * Bn254::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(m) * Bn254::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        s = static_cast<uint64_t>(t[9]) + (s >> 32);
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = 0;
+    }
+    Fe r;
+    uint32_t d[8];
+    uint64_t br = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint64_t s = static_cast<uint64_t>(t[j]) - Bn254::p(j) - br;
+        d[j] = static_cast<uint32_t>(s);
+        br = s >> 63;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = br ? t[j] : d[j];
+    return r;
+}
+
+/// mont(x, r) for a fold challenge: constant-multiplier path for BN254,
+/// CIOS for runtime moduli.
+template <class F>
+__device__ __forceinline__ Fe fe_mul_fold(const Fe& x, const FoldConst& K) {
+    if constexpr (F::kRuntime) {
+        return fe_mul<F>(x, K.r);
+    } else {
+        return fe_mul_const_bn254(x, K);
+    }
+}
+
 template <class F>
 __device__ __forceinline__ Fe fe_to_mont(const Fe& canonical) {
     Fe r2;

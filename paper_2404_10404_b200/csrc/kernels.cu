@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "field.cuh"
 #include "kernels.hpp"
@@ -163,10 +164,10 @@ struct RoundParams {
     int np;
     std::uint64_t n_out_pairs;  // P
     int log_p;                  // log2 P
-    const Fe* r;
     Fe* partials;
     unsigned* counter;
     Fe* result;
+    FoldConst k;                // fold challenge (kernel-parameter space: IMAD constant operands)
 };
 
 // Table layouts of the round engine (P = output pairs of this round):
@@ -179,71 +180,72 @@ struct RoundParams {
 //              s + 2P and every load/store is warp-contiguous.
 enum RoundMode : int { kScan = 0, kFoldNat = 1, kFoldRev = 2 };
 
+template <class F>
+__device__ __forceinline__ Fe foldk(const Fe& a, const Fe& b, const FoldConst& K) {
+    return fe_add<F>(a, fe_mul_fold<F>(fe_sub<F>(b, a), K));
+}
+
 template <class F, int MODE>
 __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __restrict__ dst, std::uint64_t i,
-                                          std::uint64_t P, int log_p, const Fe& r, Fe& x0, Fe& x1) {
+                                          std::uint64_t P, int log_p, const FoldConst& K, Fe& x0, Fe& x1) {
     if (MODE == kScan) {
         x0 = fe_load_nc(src + 2 * i);
         x1 = fe_load_nc(src + 2 * i + 1);
     } else if (MODE == kFoldNat) {
         const Fe a0 = fe_load_nc(src + 4 * i), a1 = fe_load_nc(src + 4 * i + 1);
         const Fe b0 = fe_load_nc(src + 4 * i + 2), b1 = fe_load_nc(src + 4 * i + 3);
-        x0 = fold1<F>(a0, a1, r);
-        x1 = fold1<F>(b0, b1, r);
+        x0 = foldk<F>(a0, a1, K);
+        x1 = foldk<F>(b0, b1, K);
         const std::uint64_t s = log_p ? (__brevll(i) >> (64 - log_p)) : 0;
         fe_store(dst + s, x0);
         fe_store(dst + s + P, x1);
     } else {
         const Fe a0 = fe_load_nc(src + i), a1 = fe_load_nc(src + i + 2 * P);
         const Fe b0 = fe_load_nc(src + i + P), b1 = fe_load_nc(src + i + 3 * P);
-        x0 = fold1<F>(a0, a1, r);
-        x1 = fold1<F>(b0, b1, r);
+        x0 = foldk<F>(a0, a1, K);
+        x1 = foldk<F>(b0, b1, K);
         fe_store(dst + i, x0);
         fe_store(dst + i + P, x1);
     }
 }
 
 template <class F, int NP, bool HAS_G, int MODE>
-__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, const Fe& r, Fe (&s)[3]) {
+__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, Fe (&s)[3]) {
     const int np = NP > 0 ? NP : a.np;
     const std::uint64_t P = a.n_out_pairs;
     for (int k = 0; k < np; ++k) {
         Fe f0, f1, g0, g1;
-        load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, r, f0, f1);
-        load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, r, g0, g1);
+        load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, a.k, f0, f1);
+        load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
         s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
         s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
         s[2] = fe_add<F>(s[2], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
     }
     if (HAS_G) {
         Fe g0, g1;
-        load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, r, g0, g1);
+        load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, a.k, g0, g1);
         s[0] = fe_add<F>(s[0], g0);
         s[1] = fe_add<F>(s[1], g1);
     }
 }
 
 template <class F, int NP, bool HAS_G, int MODE, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_round(RoundParams a) {
+__global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant__ RoundParams a) {
     Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
-    Fe r = fe_zero();
-    if (MODE != kScan) r = fe_load(a.r);
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < a.n_out_pairs;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        round_body<F, NP, HAS_G, MODE>(a, i, r, s);
+        round_body<F, NP, HAS_G, MODE>(a, i, s);
     }
     grid_finish<F, 3>(s, a.partials, a.counter, a.result);
 }
 
 // Small-table variant: one CTA covers all pairs; the CTA sum is the result.
 template <class F, int NP, bool HAS_G, int MODE>
-__global__ void __launch_bounds__(kThreads) k_round_small(RoundParams a) {
+__global__ void __launch_bounds__(kThreads) k_round_small(const __grid_constant__ RoundParams a) {
     __shared__ Fe sh[32][3];
     Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
-    Fe r = fe_zero();
-    if (MODE != kScan) r = fe_load(a.r);
     for (std::uint64_t i = threadIdx.x; i < a.n_out_pairs; i += blockDim.x) {
-        round_body<F, NP, HAS_G, MODE>(a, i, r, s);
+        round_body<F, NP, HAS_G, MODE>(a, i, s);
     }
     if (blockDim.x <= 32) {
         warp_sum<F, 3>(s);
@@ -768,7 +770,9 @@ void launch_to_canonical(FieldKind k, const Fe* in, std::uint8_t* out, int width
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
-    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, a.r, ws.partials, ws.counter, ws.result};
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}};
+    static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
+    if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
     static const int minb = [] {
         const char* e = std::getenv("DGKR_ROUND_MINB");
@@ -797,7 +801,9 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
 void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
-    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, a.r, ws.partials, ws.counter, ws.result};
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}};
+    static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
+    if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const unsigned threads = a.n_out_pairs <= 32 ? 32u : (a.n_out_pairs <= 128 ? 128u : kThreads);
 #define LAUNCH_ROUND(NP, HG, MD) k_round_small<F, NP, HG, MD><<<1, threads, 0, st>>>(p)
     DISPATCH_FIELD(k, F, {

@@ -51,8 +51,12 @@ struct RoundLaunch {
     bool has_g = false;
     int mode = 0;  // 0 scan (round 1), 1 fold natural->bit-reversed (round 2), 2 fold bit-reversed (rounds >= 3)
     std::uint64_t n_out_pairs = 0;
-    const Fe* r = nullptr;          // device pointer to the fold challenge
+    const Fe* r = nullptr;          // device pointer to the fold challenge (unused by the round kernels)
+    // host pointer to the fold constants {c_0..c_7, r} (9 x 32 bytes, field.cuh
+    // FoldConst): c_k = r * 2^(32k+64) * R^-1 mod p; passed as kernel parameters
+    const void* fold_const = nullptr;
 };
+constexpr std::size_t kFoldConstBytes = 9 * 32;
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
 
 /// Same as launch_round, but for small tables: one CTA, no grid reduction

@@ -125,6 +125,13 @@ struct dgkr_field {
     HostField f;
     FieldKind kind = FieldKind::Runtime;
     RtFieldHost rt{};
+    U256 fold_pow[8];  // canonical 2^(32k+64) mod p, for the fold constants
+
+    /// {c_0..c_7, r} with c_k = mont(r, 2^(32k+64)) (field.cuh FoldConst)
+    void fold_const(const U256& r, U256 out[9]) const {
+        for (int k = 0; k < 8; ++k) out[k] = f.mul(r, fold_pow[k]);
+        out[8] = r;
+    }
 };
 
 /// Runtime-modulus constants live in one __constant__ block per device;
@@ -646,11 +653,13 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     Fe* d_r = ctx->d_small.p;
     const Fe* const* cur = base;
     const U256 zero{};
+    U256 fk[9] = {};
     for (int j = 1; j <= nv; ++j) {
         RoundLaunch rl;
         rl.np = np;
         rl.has_g = has_g;
         rl.r = d_r;
+        rl.fold_const = fk;
         if (j == 1) {
             rl.mode = 0;  // scan the natural-order base tables
             rl.in = base;
@@ -704,6 +713,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         ctx->prof.rounds += 1;
         out.rounds.push_back(rp);
         out.challenges.push_back(r);
+        f->fold_const(r, fk);  // next round's fold constants (kernel parameters)
         ctx->h_small[0] = to_fe(r);
         ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
     }
@@ -1670,6 +1680,12 @@ int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out
             f->rt.one[2 * i + 1] = static_cast<std::uint32_t>(f->f.one().w[i] >> 32);
         }
         f->rt.np0 = static_cast<std::uint32_t>(f->f.np0());
+        U256 x{{1, 0, 0, 0}};  // canonical powers of two by modular doubling
+        for (int b = 0; b < 64; ++b) x = f->f.add(x, x);
+        for (int k = 0; k < 8; ++k) {
+            f->fold_pow[k] = x;
+            for (int b = 0; b < 32; ++b) x = f->f.add(x, x);
+        }
         *out = f.release();
     });
 }

@@ -85,7 +85,7 @@ def main():
             if k == "kernel":
                 continue
             lines.append(f"- {k}: {vu[0]} {vu[1]}")
-        if d["kernel"] == "k_round" and "dram__bytes_read.sum" in d:
+        if d["kernel"].startswith("k_round<") and "dram__bytes_read.sum" in d:
             rb = to_bytes(*d["dram__bytes_read.sum"])
             wb = to_bytes(*d["dram__bytes_write.sum"])
             traffic.append({"grid": d.get("launch__grid_size", ("", ""))[0], "dram_bytes": rb + wb})
