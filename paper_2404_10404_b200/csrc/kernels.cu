@@ -365,10 +365,10 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep1_sorted(BookkeepLaunch a)
 
 // Single-slot phase 2: cx = w * chi_x(u);  mul: MA += cx*V(u)   add: MA += cx, C += cx*V(u)
 template <class F>
-__global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(BookkeepLaunch a) {
+__global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(const __grid_constant__ BookkeepLaunch a,
+                                                               const __grid_constant__ FoldConst vxk) {
     const SlotDesc sd = a.slots[0];
     const std::uint64_t smask = (std::uint64_t{1} << sd.log_stride) - 1;
-    const Fe vx = fe_load(a.vx);
     for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < a.T;
          t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         const std::uint64_t c = t >> sd.log_stride;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(BookkeepLaunch a)
             const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
             const Fe eu = fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y));
             const Fe cx = fe_mul<F>(w, eu);
-            const Fe prod = fe_mul<F>(cx, vx);
+            const Fe prod = fe_mul_fold<F>(cx, vxk);  // V(u) is a per-launch constant
             const bool mul = en.z >> 31;
             ma = fe_add<F>(ma, fe_select<F>(mul, prod, cx));
             cacc = fe_select<F>(mul, cacc, fe_add<F>(cacc, prod));
@@ -853,8 +853,10 @@ void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t s
 
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
-    if (a.perm && a.n_slots == 1 && a.gate_w && a.eq_u) {
-        DISPATCH_FIELD(k, F, (k_bookkeep2_sorted<F><<<g, kThreads, 0, st>>>(a)));
+    if (a.perm && a.n_slots == 1 && a.gate_w && a.eq_u && a.vx_const) {
+        FoldConst vk{};
+        std::memcpy(&vk, a.vx_const, sizeof(FoldConst));
+        DISPATCH_FIELD(k, F, (k_bookkeep2_sorted<F><<<g, kThreads, 0, st>>>(a, vk)));
     } else {
         DISPATCH_FIELD(k, F, (k_bookkeep_phase2<F><<<g, kThreads, 0, st>>>(a)));
     }

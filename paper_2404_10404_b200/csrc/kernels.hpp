@@ -116,6 +116,7 @@ struct BookkeepLaunch {
     SplitEq w;                    // wire weights from the combined claim
     SplitEq u;                    // phase 2: chi_x(u) split tables
     const Fe* vx = nullptr;       // phase 2: V_m(u) per slot (device)
+    const void* vx_const = nullptr;  // phase 2, single slot: host FoldConst of V_0(u) (kernel parameter)
     const Fe* wire_w = nullptr;   // explicit per-wire weights (entry .w = wire id), else gate_w / w
     const Fe* gate_w = nullptr;   // dense per-gate weights (global gate index), else split-eq w
     const Fe* eq_u = nullptr;     // phase 2: dense chi_x(u) table, else split-eq u

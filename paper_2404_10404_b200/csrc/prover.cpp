@@ -1397,6 +1397,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.slots = WC.d_slots2.p;
         bk.u = uq;
         bk.vx = ctx->d_small.p + Lane::kVxOff;
+        U256 vxk[9];
+        f->fold_const(vx[0], vxk);
+        bk.vx_const = vxk;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
         launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st);  // chi_x(u), sumcheck.hpp:415
         ctx->launched();
