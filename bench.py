@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=16,
+    ap.add_argument("--lanes", type=int, default=24,
                     help="concurrent proofs per step (lanes); the single-proof latency is reported separately")
     args = ap.parse_args()
     if args.impl == "reference":

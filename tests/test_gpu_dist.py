@@ -58,3 +58,18 @@ def test_dist_requires_uniform_width(ctx):
     local = P.Circuit(ctx, insz, *flat, n_copies=2)
     with pytest.raises(InvalidArgument):
         P.gkr_prove_dist_emulated(ctx, local, 2, W.random_inputs(p, insz * 4, 1), P.Transcript(f, "x"))
+
+
+def test_nccl_transport_world1(ctx):
+    """The NCCL communicator path (dlopen'd libnccl, all-gather / send-recv
+    group / broadcast) with the one rank a single GPU allows."""
+    p = O.BN254_P
+    f = P.Field(p)
+    insz, flat = W.layered_circuit(seed=61, log_width=6, depth=4)
+    inputs = W.random_inputs(p, insz * 4, 62)
+    tr1 = P.Transcript(f, "nccl")
+    want = P.gkr_prove(ctx, P.Circuit(ctx, insz, *flat, n_copies=4), inputs, tr1)
+    comm = P.Comm(ctx, P.Comm.nccl_unique_id(), 0, 1)
+    tr2 = P.Transcript(f, "nccl")
+    got = P.gkr_prove_dist(ctx, comm, P.Circuit(ctx, insz, *flat, n_copies=4), inputs, tr2)
+    assert got == want and tr2.state == tr1.state
