@@ -235,6 +235,29 @@ int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, size_t rows, size_t cols, 
                   const uint8_t* r, size_t r_len, size_t spot_checks, dgkr_transcript* t, uint8_t* out, size_t cap,
                   size_t* len);
 
+/* ---- Reed-Solomon encoding and FRI (north-star "Virgo/FRI" commitment) ------------
+ * No reference implementation exists: the reference replaced Virgo's VPD with
+ * the Merkle column commitment above. These entry points are
+ * our own specification, pinned by oracle/fri_oracle.py.
+ *   two-adic data: p - 1 = 2^s t; w = z^t has order 2^s where z is the smallest
+ *   quadratic non-residue, which is also the coset shift g.
+ *   dgkr_ntt:  out[i] = sum_j in[j] w_N^(ij)  (inverse: w^-1 and 1/N), natural order
+ *   dgkr_rs_encode: out[i] = f(g w_N^i), f = coeffs (n), N = n << blowup_log
+ *   dgkr_fri_prove: L = log2(N) - final_log folds of the RS codeword of coeffs;
+ *     per layer l: root_l = Merkle(SHA256(canon(f_l[j]))), absorb root_l,
+ *     beta_l = challenge, f_{l+1}[i] = (f_l[i] + f_l[i+h]) / 2
+ *                                       + beta_l (f_l[i] - f_l[i+h]) / (2 x_i),
+ *     x_i = g^(2^l) w_N^(2^l i), h = N_l / 2; absorb every element of f_L;
+ *     Q = min(queries, N/2) distinct challenge_index(N/2) positions.
+ *   proof = u32 L || L roots || u32 |f_L| || f_L || u32 Q || per query:
+ *     u32 i || per layer l: f_l[i mod h_l] || f_l[i mod h_l + h_l] || their two Merkle paths */
+int dgkr_field_ntt_info(const dgkr_field* f, unsigned* two_adicity, uint8_t* root, uint8_t* coset);
+int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* in, unsigned log_n, int inverse, uint8_t* out);
+int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, size_t n, unsigned blowup_log,
+                   uint8_t* out);
+int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, size_t n, unsigned blowup_log,
+                   unsigned final_log, size_t queries, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+
 /* ---- distributed runtime (cluster.hpp), N workers in one call -------------------
  * shard_pairs + dist_sumcheck (cluster.hpp:190-320) on full tables; proof
  * bytes equal the reference's, TrafficStats::to_json().dump() written to

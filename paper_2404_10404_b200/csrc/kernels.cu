@@ -696,6 +696,156 @@ __global__ void __launch_bounds__(kThreads) k_mul_peak(int iters, Fe* sink, unsi
     if (s.v[0] == never) fe_store(sink, s);  // keep the chains live (never is a runtime 0xffffffff)
 }
 
+// ---------------------------------------------------------------------------
+// Reed-Solomon encoding (radix-2 NTT) and FRI folding. No reference
+// counterpart (the reference replaced Virgo's VPD/FRI with the Merkle column
+// commitment); pinned by tests against a Python restatement
+// and algebraic properties (NTT o iNTT = id, folds of RS codewords stay RS).
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ Fe fe_pow_small(Fe b, std::uint64_t e) {
+    Fe r = fe_one<F>();
+    while (e) {
+        if (e & 1) r = fe_mul<F>(r, b);
+        b = fe_mul<F>(b, b);
+        e >>= 1;
+    }
+    return r;
+}
+
+// scratch: [0, 2^k) = base^j, [2^k, 2^k + ceil(n/2^k)) = base^(m 2^k)
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_pow_parts(const Fe* base, int k, std::uint64_t nb, Fe* scratch) {
+    const Fe b = fe_load(base);
+    const std::uint64_t na = std::uint64_t{1} << k;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < na + nb;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        fe_store(scratch + i, i < na ? fe_pow_small<F>(b, i) : fe_pow_small<F>(b, (i - na) << k));
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_pow_expand(const Fe* scratch, int k, std::uint64_t n, Fe* out) {
+    const std::uint64_t na = std::uint64_t{1} << k;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        fe_store(out + i, fe_mul<F>(fe_load_nc(scratch + (i & (na - 1))), fe_load_nc(scratch + na + (i >> k))));
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bitrev_scale(const Fe* __restrict__ in, const Fe* __restrict__ scale,
+                                                           Fe* __restrict__ out, int log_n, std::uint64_t n_in) {
+    const std::uint64_t n = std::uint64_t{1} << log_n;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        Fe v = fe_zero();
+        if (i < n_in) {
+            v = fe_load_nc(in + i);
+            if (scale) v = fe_mul<F>(v, fe_load_nc(scale + i));
+        }
+        const std::uint64_t r = log_n ? (__brevll(i) >> (64 - log_n)) : 0;
+        fe_store(out + r, v);
+    }
+}
+
+// Stages 1..b inside one CTA: the 2^b consecutive (bit-reversed) elements of
+// a chunk are exactly the inputs of its first b butterfly levels.
+constexpr int kNttLocalLog = 10;
+
+template <class F>
+__global__ void __launch_bounds__(512) k_ntt_local(Fe* a, int log_n, int b, const Fe* __restrict__ tw) {
+    extern __shared__ Fe sm[];
+    const std::uint64_t m = std::uint64_t{1} << b;
+    Fe* chunk = a + blockIdx.x * m;
+    for (std::uint64_t i = threadIdx.x; i < m; i += blockDim.x) sm[i] = fe_load(chunk + i);
+    __syncthreads();
+    for (int s = 1; s <= b; ++s) {
+        const std::uint64_t half = std::uint64_t{1} << (s - 1);
+        for (std::uint64_t t = threadIdx.x; t < m / 2; t += blockDim.x) {
+            const std::uint64_t j = t & (half - 1);
+            const std::uint64_t i0 = ((t >> (s - 1)) << s) + j, i1 = i0 + half;
+            const Fe w = fe_load_nc(tw + (j << (log_n - s)));
+            const Fe u = sm[i0], v = fe_mul<F>(w, sm[i1]);
+            sm[i0] = fe_add<F>(u, v);
+            sm[i1] = fe_sub<F>(u, v);
+        }
+        __syncthreads();
+    }
+    for (std::uint64_t i = threadIdx.x; i < m; i += blockDim.x) fe_store(chunk + i, sm[i]);
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_ntt_stage(Fe* a, int log_n, int s, const Fe* __restrict__ tw) {
+    const std::uint64_t half = std::uint64_t{1} << (s - 1);
+    const std::uint64_t nb = std::uint64_t{1} << (log_n - 1);
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < nb;
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t j = t & (half - 1);
+        const std::uint64_t i0 = ((t >> (s - 1)) << s) + j, i1 = i0 + half;
+        const Fe w = fe_load_nc(tw + (j << (log_n - s)));
+        const Fe u = fe_load(a + i0), v = fe_mul<F>(w, fe_load(a + i1));
+        fe_store(a + i0, fe_add<F>(u, v));
+        fe_store(a + i1, fe_sub<F>(u, v));
+    }
+}
+
+// (a + b) / 2 without a multiplication: halve a + b (or a + b + p if odd)
+template <class F>
+__device__ __forceinline__ Fe fe_half(const Fe& x) {
+    Fe s = x;
+    uint32_t carry = 0;
+    if (x.v[0] & 1) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t t = static_cast<uint64_t>(x.v[i]) + F::p(i) + c;
+            s.v[i] = static_cast<uint32_t>(t);
+            c = t >> 32;
+        }
+        carry = static_cast<uint32_t>(c);
+    }
+    Fe r;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) r.v[i] = (s.v[i] >> 1) | (s.v[i + 1] << 31);
+    r.v[7] = (s.v[7] >> 1) | (carry << 31);
+    return r;
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_fri_fold(const Fe* __restrict__ f, std::uint64_t n,
+                                                       const Fe* __restrict__ twinv, std::uint64_t step,
+                                                       const __grid_constant__ Fe ginv,
+                                                       const __grid_constant__ FoldConst beta, Fe* __restrict__ out) {
+    const std::uint64_t h = n / 2;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < h;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const Fe f0 = fe_load_nc(f + i), f1 = fe_load_nc(f + i + h);
+        const Fe xinv = fe_mul<F>(ginv, fe_load_nc(twinv + i * step));
+        const Fe odd = fe_mul_fold<F>(fe_mul<F>(xinv, fe_sub<F>(f0, f1)), beta);
+        // Montgomery form is linear, so halving the Montgomery value halves the element
+        fe_store(out + i, fe_half<F>(fe_add<F>(fe_add<F>(f0, f1), odd)));
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_scale(Fe* a, std::uint64_t n, const __grid_constant__ FoldConst c) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        fe_store(a + i, fe_mul_fold<F>(fe_load(a + i), c));
+    }
+}
+
+__global__ void k_gather32(const uint4* __restrict__ src, const std::uint64_t* __restrict__ idx, std::uint64_t n,
+                           uint4* __restrict__ dst) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t j = idx[i];
+        dst[2 * i] = src[2 * j];
+        dst[2 * i + 1] = src[2 * j + 1];
+    }
+}
+
 void check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -880,6 +1030,73 @@ void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq&
 void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st) {
     k_mul_peak<<<n_blocks, kThreads, 0, st>>>(iters, sink, 0xffffffffu);
     check_launch("mul_peak");
+}
+
+void launch_pow_table(FieldKind k, const Fe* base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st) {
+    int kk = 0;
+    while ((std::uint64_t{1} << (2 * (kk + 1))) <= n) ++kk;  // 2^kk ~ sqrt(n)
+    const std::uint64_t na = std::uint64_t{1} << kk, nb = (n + na - 1) >> kk;
+    const int g1 = grid_for(na + nb, kThreads, 148 * 8);
+    const int g2 = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, {
+        k_pow_parts<F><<<g1, kThreads, 0, st>>>(base, kk, nb, scratch);
+        k_pow_expand<F><<<g2, kThreads, 0, st>>>(scratch, kk, n, out);
+    });
+    check_launch("pow_table");
+}
+
+void launch_bitrev_scale(FieldKind k, const Fe* in, const Fe* scale, Fe* out, int log_n, std::uint64_t n_in,
+                         cudaStream_t st) {
+    const int g = grid_for(std::uint64_t{1} << log_n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_bitrev_scale<F><<<g, kThreads, 0, st>>>(in, scale, out, log_n, n_in)));
+    check_launch("bitrev_scale");
+}
+
+void launch_ntt(FieldKind k, Fe* a, int log_n, const Fe* tw, cudaStream_t st) {
+    if (log_n == 0) return;
+    const int b = std::min(log_n, kNttLocalLog);
+    const std::uint64_t chunks = std::uint64_t{1} << (log_n - b);
+    const std::size_t smem = (std::size_t{1} << b) * sizeof(Fe);
+    DISPATCH_FIELD(k, F, {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_ntt_local<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>((std::size_t{1} << kNttLocalLog) * sizeof(Fe)));
+            attr = true;
+        }
+        k_ntt_local<F><<<static_cast<unsigned>(chunks), 512, smem, st>>>(a, log_n, b, tw);
+        for (int s = b + 1; s <= log_n; ++s) {
+            const int g = grid_for(std::uint64_t{1} << (log_n - 1), kThreads, 148 * 16);
+            k_ntt_stage<F><<<g, kThreads, 0, st>>>(a, log_n, s, tw);
+        }
+    });
+    check_launch("ntt");
+}
+
+void launch_fri_fold(FieldKind k, const Fe* f, std::uint64_t n, const Fe* twinv, std::uint64_t step,
+                     const void* ginv, const void* beta_const, Fe* out, cudaStream_t st) {
+    Fe gi;
+    std::memcpy(&gi, ginv, sizeof(Fe));
+    FoldConst bk{};
+    std::memcpy(&bk, beta_const, sizeof(FoldConst));
+    const int g = grid_for(n / 2, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_fri_fold<F><<<g, kThreads, 0, st>>>(f, n, twinv, step, gi, bk, out)));
+    check_launch("fri_fold");
+}
+
+void launch_scale(FieldKind k, Fe* a, std::uint64_t n, const void* c_const, cudaStream_t st) {
+    FoldConst c{};
+    std::memcpy(&c, c_const, sizeof(FoldConst));
+    const int g = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_scale<F><<<g, kThreads, 0, st>>>(a, n, c)));
+    check_launch("scale");
+}
+
+void launch_gather32(const void* src, const std::uint64_t* idx, std::uint64_t n, void* dst, cudaStream_t st) {
+    if (n == 0) return;
+    const int g = grid_for(n, kThreads, 148 * 4);
+    k_gather32<<<g, kThreads, 0, st>>>(static_cast<const uint4*>(src), idx, n, static_cast<uint4*>(dst));
+    check_launch("gather32");
 }
 
 void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,

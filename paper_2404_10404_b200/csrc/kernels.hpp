@@ -149,6 +149,26 @@ void launch_dense_eval(FieldKind k, const Fe* t, std::uint64_t n, const SplitEq&
 /// steps of 4 independent BN254 Montgomery multiplication chains.
 void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st);
 
+// ---- Reed-Solomon encoding (NTT) and FRI folding ------------------------
+/// out[i] = A[i & (2^k - 1)] * B[i >> k] for i < n, where A[j] = base^j and
+/// B[m] = base^(m 2^k) are built per thread by square-and-multiply.
+void launch_pow_table(FieldKind k, const Fe* base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st);
+/// out[brev(i)] = in[i] * (scale ? scale[i] : 1), i < 2^log_n  (scale: coset powers)
+void launch_bitrev_scale(FieldKind k, const Fe* in, const Fe* scale, Fe* out, int log_n, std::uint64_t n_in,
+                         cudaStream_t st);
+/// in-place radix-2 DIT NTT stages on bit-reversed input; tw[i] = w_N^i, i < N/2
+void launch_ntt(FieldKind k, Fe* a, int log_n, const Fe* tw, cudaStream_t st);
+/// one FRI fold: out[i] = (f[i] + f[i+h] + beta * xinv_i * (f[i] - f[i+h])) / 2, h = n/2,
+/// xinv_i = ginv * twinv[i * step]  (beta_const: host FoldConst of beta; ginv: host Fe
+/// (32 bytes) of the layer's inverse coset shift)
+void launch_fri_fold(FieldKind k, const Fe* f, std::uint64_t n, const Fe* twinv, std::uint64_t step,
+                     const void* ginv, const void* beta_const, Fe* out, cudaStream_t st);
+
+/// a[i] = a[i] * c for a per-launch constant (host FoldConst of c)
+void launch_scale(FieldKind k, Fe* a, std::uint64_t n, const void* c_const, cudaStream_t st);
+/// dst[i] = 32-byte record src[idx[i]] (Merkle nodes, field elements)
+void launch_gather32(const void* src, const std::uint64_t* idx, std::uint64_t n, void* dst, cudaStream_t st);
+
 /// Batched SHA-256 column digests (pcs.hpp:73-80): leaf[j] = SHA256(canon(m[0][j]) || ... || canon(m[M-1][j])).
 void launch_column_digests(FieldKind k, const Fe* rows, std::uint64_t cols, int M, int width, std::uint8_t* leaves,
                            cudaStream_t st);

@@ -126,6 +126,18 @@ struct dgkr_field {
     FieldKind kind = FieldKind::Runtime;
     RtFieldHost rt{};
     U256 fold_pow[8];  // canonical 2^(32k+64) mod p, for the fold constants
+    // NTT data (Montgomery): two-adicity s, w of order 2^s, coset shift g =
+    // smallest quadratic non-residue (not in any 2-power subgroup), g^-1
+    unsigned two_adicity = 0;
+    U256 root{}, coset{}, coset_inv{};
+
+    /// w_N for N = 2^log_n (log_n <= two_adicity)
+    U256 root_of_unity(unsigned log_n) const {
+        if (log_n > two_adicity) fail(DGKR_UNSUPPORTED, "domain larger than the field's 2-adic subgroup");
+        U256 w = root;
+        for (unsigned i = log_n; i < two_adicity; ++i) w = f.mul(w, w);
+        return w;
+    }
 
     /// {c_0..c_7, r} with c_k = mont(r, 2^(32k+64)) (field.cuh FoldConst)
     void fold_const(const U256& r, U256 out[9]) const {
@@ -1584,6 +1596,167 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
 }
 
 // ---------------------------------------------------------------------------
+// Reed-Solomon / NTT / FRI (north-star "Virgo/FRI"; no reference exists, see
+// pinned by the Python restatement oracle/fri_oracle.py).
+// ---------------------------------------------------------------------------
+void pow_table(Lane* ctx, const dgkr_field* f, const U256& base, std::uint64_t n, Fe* out, DBuf<Fe>& scratch) {
+    std::uint64_t na = 1;
+    while (na * na < n) na <<= 1;
+    scratch.ensure(na + n / na + 2);
+    Fe* db = ctx->d_small.p + Lane::kEqOff;  // one staged element
+    ctx->h_small[Lane::kEqOff] = to_fe(base);
+    ctx->h2d(db, ctx->h_small + Lane::kEqOff, sizeof(Fe));
+    launch_pow_table(ctx->use(f), db, n, out, scratch.p, ctx->st);
+    ctx->launched(2);
+}
+
+/// evaluations (natural order) on c * <w_N> of the polynomial with
+/// coefficients `coeff` (n_in <= N entries, rest zero): a := NTT(coset-scaled, bit-reversed coeff)
+void coset_ntt(Lane* ctx, const dgkr_field* f, const Fe* coeff, std::uint64_t n_in, unsigned log_n, const U256& c,
+               bool apply_coset, Fe* a, DBuf<Fe>& tw, DBuf<Fe>& cpow, DBuf<Fe>& scratch) {
+    const FieldKind kind = ctx->use(f);
+    const std::uint64_t N = std::uint64_t{1} << log_n;
+    const U256 w = f->root_of_unity(log_n);
+    tw.ensure(std::max<std::uint64_t>(N / 2, 1));
+    if (N >= 2) pow_table(ctx, f, w, N / 2, tw.p, scratch);
+    const Fe* scale = nullptr;
+    if (apply_coset) {
+        cpow.ensure(n_in);
+        pow_table(ctx, f, c, n_in, cpow.p, scratch);
+        scale = cpow.p;
+    }
+    launch_bitrev_scale(kind, coeff, scale, a, static_cast<int>(log_n), n_in, ctx->st);
+    launch_ntt(kind, a, static_cast<int>(log_n), tw.p, ctx->st);
+    ctx->launched(2 + log_n);
+}
+
+/// FRI over the RS codeword of `coeffs` (protocol in include/dgkr_b200.h)
+std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::uint64_t n,
+                                    unsigned blowup_log, unsigned final_log, std::size_t q, Transcript& tr) {
+    const HostField& F = f->f;
+    const FieldKind kind = ctx->use(f);
+    const std::size_t w = F.width();
+    if (n == 0 || (n & (n - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "coefficient count must be a power of two");
+    const unsigned log_n0 = log2_exact(n) + blowup_log;
+    if (final_log > log_n0) fail(DGKR_INVALID_ARGUMENT, "final layer larger than the codeword");
+    const unsigned L = log_n0 - final_log;
+    const std::uint64_t N0 = std::uint64_t{1} << log_n0;
+    DBuf<std::uint8_t> stage;
+    DBuf<Fe> cf, tw, cpow, scratch, twinv;
+    cf.ensure(n);
+    ctx->upload_elems(f, coeffs, n, cf.p, stage);
+    // layer 0: RS encoding on the coset g<w_N0>
+    std::vector<std::unique_ptr<DBuf<Fe>>> layer(L + 1);
+    std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree(L);
+    for (unsigned l = 0; l <= L; ++l) {
+        layer[l] = std::make_unique<DBuf<Fe>>();
+        layer[l]->ensure(N0 >> l);
+    }
+    coset_ntt(ctx, f, cf.p, n, log_n0, f->coset, true, layer[0]->p, tw, cpow, scratch);
+    // inverse twiddles w^-i for the fold's 1/x
+    twinv.ensure(std::max<std::uint64_t>(N0 / 2, 1));
+    if (N0 >= 2) pow_table(ctx, f, F.inv(f->root_of_unity(log_n0)), N0 / 2, twinv.p, scratch);
+    std::vector<Digest> roots(L);
+    U256 ginv = f->coset_inv;  // (g^(2^l))^-1
+    for (unsigned l = 0; l < L; ++l) {
+        const std::uint64_t Nl = N0 >> l;
+        tree[l] = std::make_unique<DBuf<std::uint8_t>>();
+        tree[l]->ensure(2 * Nl * 32);
+        launch_column_digests(kind, layer[l]->p, Nl, 1, static_cast<int>(w), tree[l]->p + Nl * 32, ctx->st);
+        launch_merkle(tree[l]->p, Nl, ctx->st);
+        ctx->launched(2);
+        ctx->d2h(roots[l].data(), tree[l]->p + 32, 32);
+        ctx->sync();
+        tr.absorb_bytes(roots[l].data(), 32);
+        const U256 beta = tr.challenge();
+        U256 bk[9];
+        f->fold_const(beta, bk);
+        Fe gi = to_fe(ginv);
+        launch_fri_fold(kind, layer[l]->p, Nl, twinv.p, std::uint64_t{1} << l, &gi, bk, layer[l + 1]->p, ctx->st);
+        ctx->launched();
+        ginv = F.mul(ginv, ginv);
+    }
+    // final layer, absorbed element by element
+    const std::uint64_t NL = N0 >> L;
+    std::vector<std::uint8_t> fin(NL * w);
+    stage.ensure(NL * w);
+    launch_to_canonical(kind, layer[L]->p, stage.p, static_cast<int>(w), NL, ctx->st);
+    ctx->d2h(fin.data(), stage.p, NL * w);
+    ctx->sync();
+    for (std::uint64_t i = 0; i < NL; ++i) tr.absorb_bytes(fin.data() + i * w, w);
+    // queries on the first layer's half domain (distinct, like pcs.hpp:199-206)
+    const std::uint64_t H = N0 / 2;
+    std::vector<std::uint64_t> qi;
+    if (L > 0) {
+        if (q >= H) {
+            for (std::uint64_t i = 0; i < H; ++i) qi.push_back(i);
+        } else {
+            std::vector<bool> seen(H, false);
+            while (qi.size() < q) {
+                const std::uint64_t j = tr.challenge_index(H);
+                if (!seen[j]) {
+                    seen[j] = true;
+                    qi.push_back(j);
+                }
+            }
+        }
+    }
+    // gather opened values and Merkle paths on the device, one D2H per layer
+    std::vector<std::uint8_t> out;
+    put32(out, L);
+    for (const auto& r : roots) out.insert(out.end(), r.begin(), r.end());
+    put32(out, static_cast<std::uint32_t>(NL));
+    out.insert(out.end(), fin.begin(), fin.end());
+    put32(out, static_cast<std::uint32_t>(qi.size()));
+    std::vector<std::vector<std::uint8_t>> vals(L), paths(L);
+    std::vector<unsigned> depth(L);
+    DBuf<std::uint64_t> didx;
+    DBuf<std::uint8_t> dbuf;
+    for (unsigned l = 0; l < L; ++l) {
+        const std::uint64_t Nl = N0 >> l, hl = Nl / 2;
+        depth[l] = log2_exact(Nl);
+        std::vector<std::uint64_t> vidx, pidx;
+        for (std::uint64_t i : qi) {
+            const std::uint64_t il = i % hl;
+            vidx.push_back(il);
+            vidx.push_back(il + hl);
+            for (std::uint64_t leaf : {il, il + hl}) {
+                std::uint64_t node = Nl + leaf;
+                while (node > 1) {
+                    pidx.push_back(node ^ 1);
+                    node >>= 1;
+                }
+            }
+        }
+        const std::size_t nv = vidx.size(), np = pidx.size();
+        didx.ensure(nv + np);
+        dbuf.ensure((nv + np) * 32 + nv * w + 32);
+        ctx->h2d(didx.p, vidx.data(), nv * 8);
+        if (np) ctx->h2d(didx.p + nv, pidx.data(), np * 8);
+        launch_gather32(layer[l]->p, didx.p, nv, dbuf.p, ctx->st);
+        launch_to_canonical(kind, reinterpret_cast<const Fe*>(dbuf.p), dbuf.p + (nv + np) * 32, static_cast<int>(w), nv,
+                            ctx->st);
+        launch_gather32(tree[l]->p, didx.p + nv, np, dbuf.p + nv * 32, ctx->st);
+        ctx->launched(3);
+        vals[l].resize(nv * w);
+        paths[l].resize(np * 32);
+        ctx->d2h(vals[l].data(), dbuf.p + (nv + np) * 32, nv * w);
+        if (np) ctx->d2h(paths[l].data(), dbuf.p + nv * 32, np * 32);
+    }
+    ctx->sync();
+    for (std::size_t k = 0; k < qi.size(); ++k) {
+        put32(out, static_cast<std::uint32_t>(qi[k]));
+        for (unsigned l = 0; l < L; ++l) {
+            const std::uint8_t* v = vals[l].data() + 2 * k * w;
+            out.insert(out.end(), v, v + 2 * w);
+            const std::uint8_t* pth = paths[l].data() + 2 * k * depth[l] * 32;
+            out.insert(out.end(), pth, pth + 2 * depth[l] * 32);
+        }
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
 // TrafficStats (cluster.hpp:69-115), byte-accurate logical metering.
 // ---------------------------------------------------------------------------
 struct Traffic {
@@ -1688,6 +1861,30 @@ int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out
         for (int k = 0; k < 8; ++k) {
             f->fold_pow[k] = x;
             for (int b = 0; b < 32; ++b) x = f->f.add(x, x);
+        }
+        {  // 2-adic structure for the NTT / FRI (p - 1 = 2^s t, t odd)
+            const HostField& F = f->f;
+            U256 pm1, one{{1, 0, 0, 0}};
+            sub_to(pm1, F.p(), one);
+            U256 t = pm1;
+            unsigned s = 0;
+            while ((t.w[0] & 1) == 0 && !t.is_zero()) {
+                for (int i = 0; i < 4; ++i) t.w[i] = (t.w[i] >> 1) | (i < 3 ? t.w[i + 1] << 63 : 0);
+                ++s;
+            }
+            U256 half = pm1;  // (p-1)/2
+            for (int i = 0; i < 4; ++i) half.w[i] = (half.w[i] >> 1) | (i < 3 ? half.w[i + 1] << 63 : 0);
+            const U256 minus_one = F.neg(F.one());
+            for (std::uint64_t z = 2; z < 1000; ++z) {
+                const U256 zm = F.from_u64(z);
+                if (F.pow(zm, half) == minus_one) {  // Euler: z is a non-residue
+                    f->coset = zm;
+                    f->coset_inv = F.inv(zm);
+                    f->root = F.pow(zm, t);  // order exactly 2^s
+                    f->two_adicity = s;
+                    break;
+                }
+            }
         }
         *out = f.release();
     });
@@ -2081,6 +2278,84 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
         for (auto& t : th) t.join();
         for (std::size_t i = 0; i < n; ++i)
             if (codes[i] != DGKR_OK) fail(codes[i], "proof " + std::to_string(i) + ": " + errs[i]);
+    });
+}
+
+int dgkr_field_ntt_info(const dgkr_field* f, unsigned* two_adicity, std::uint8_t* root, std::uint8_t* coset) {
+    return guard([&] {
+        *two_adicity = f->two_adicity;
+        if (root) f->f.to_bytes(f->root, root);
+        if (coset) f->f.to_bytes(f->coset, coset);
+    });
+}
+
+int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* in, unsigned log_n, int inverse,
+             std::uint8_t* out) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const HostField& F = f->f;
+        const FieldKind kind = ctx->use(f);
+        const std::uint64_t N = std::uint64_t{1} << log_n;
+        const std::size_t w = F.width();
+        DBuf<std::uint8_t> stage;
+        DBuf<Fe> x, a, tw, scratch;
+        x.ensure(N);
+        a.ensure(N);
+        ctx->upload_elems(f, in, N, x.p, stage);
+        const U256 root = f->root_of_unity(log_n);
+        tw.ensure(std::max<std::uint64_t>(N / 2, 1));
+        if (N >= 2) pow_table(ctx, f, inverse ? F.inv(root) : root, N / 2, tw.p, scratch);
+        launch_bitrev_scale(kind, x.p, nullptr, a.p, static_cast<int>(log_n), N, ctx->st);
+        launch_ntt(kind, a.p, static_cast<int>(log_n), tw.p, ctx->st);
+        if (inverse) {
+            U256 k[9];
+            f->fold_const(F.inv(F.from_u64(N)), k);
+            launch_scale(kind, a.p, N, k, ctx->st);
+        }
+        stage.ensure(N * w);
+        launch_to_canonical(kind, a.p, stage.p, static_cast<int>(w), N, ctx->st);
+        ctx->d2h(out, stage.p, N * w);
+        ctx->sync();
+        ctx->end_call();
+    });
+}
+
+int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::size_t n,
+                   unsigned blowup_log, std::uint8_t* out) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (n == 0 || (n & (n - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "coefficient count must be a power of two");
+        const unsigned log_n = log2_exact(n) + blowup_log;
+        const std::uint64_t N = std::uint64_t{1} << log_n;
+        const std::size_t w = f->f.width();
+        DBuf<std::uint8_t> stage;
+        DBuf<Fe> cf, a, tw, cpow, scratch;
+        cf.ensure(n);
+        a.ensure(N);
+        ctx->upload_elems(f, coeffs, n, cf.p, stage);
+        coset_ntt(ctx, f, cf.p, n, log_n, f->coset, true, a.p, tw, cpow, scratch);
+        stage.ensure(N * w);
+        launch_to_canonical(ctx->use(f), a.p, stage.p, static_cast<int>(w), N, ctx->st);
+        ctx->d2h(out, stage.p, N * w);
+        ctx->sync();
+        ctx->end_call();
+    });
+}
+
+int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::size_t n,
+                   unsigned blowup_log, unsigned final_log, std::size_t queries, dgkr_transcript* t,
+                   std::uint8_t* proof, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        Transcript tr(&f->f, t->state, t->draws);
+        auto bytes = fri_prove(ctx, f, coeffs, n, blowup_log, final_log, queries, tr);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
     });
 }
 

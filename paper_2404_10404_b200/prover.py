@@ -302,6 +302,43 @@ def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[El
     return [out_bufs[i][: lens[i]].tobytes() for i in range(n)]
 
 
+def ntt(ctx: Context, field: Field, data: Elems, inverse: bool = False) -> List[int]:
+    """dgkr_ntt: natural-order NTT of 2^k elements (inverse: w^-1, 1/N)."""
+    b = field.encode(data)
+    n = len(b) // field.width
+    out = C.create_string_buffer(len(b))
+    check(lib().dgkr_ntt(ctx.handle, field.handle, C.c_char_p(b), C.c_uint(n.bit_length() - 1),
+                         C.c_int(1 if inverse else 0), out))
+    return field.decode(out.raw)
+
+
+def rs_encode(ctx: Context, field: Field, coeffs: Elems, blowup_log: int) -> List[int]:
+    """dgkr_rs_encode: f(g w_N^i), N = n << blowup_log."""
+    b = field.encode(coeffs)
+    n = len(b) // field.width
+    out = C.create_string_buffer((n << blowup_log) * field.width)
+    check(lib().dgkr_rs_encode(ctx.handle, field.handle, C.c_char_p(b), C.c_size_t(n), C.c_uint(blowup_log), out))
+    return field.decode(out.raw)
+
+
+def fri_prove(ctx: Context, field: Field, coeffs: Elems, blowup_log: int, final_log: int, queries: int,
+              tr: Transcript) -> bytes:
+    """dgkr_fri_prove (proof layout in include/dgkr_b200.h)."""
+    b = field.encode(coeffs)
+    n = len(b) // field.width
+    log_n0 = n.bit_length() - 1 + blowup_log
+    L = max(log_n0 - final_log, 0)
+    H = (1 << log_n0) // 2
+    q = min(queries, H) if L else 0
+    cap = 64 + L * 32 + (1 << final_log) * field.width + q * (4 + L * (2 * field.width + 2 * 32 * log_n0))
+    out = C.create_string_buffer(cap)
+    ln = C.c_size_t()
+    check(lib().dgkr_fri_prove(ctx.handle, field.handle, C.c_char_p(b), C.c_size_t(n), C.c_uint(blowup_log),
+                               C.c_uint(final_log), C.c_size_t(queries), C.byref(tr.t), out, C.c_size_t(cap),
+                               C.byref(ln)))
+    return out.raw[: ln.value]
+
+
 def gkr_prove_stream(ctx: Context, circuit: Circuit, n: int, lanes: int, field: Field, label: str = "stream",
                      inputs: Optional[Sequence[Elems]] = None, out_bufs=None):
     """n proofs over `lanes` lanes as a work queue (dgkr_gkr_prove_stream).
