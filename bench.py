@@ -119,36 +119,55 @@ def cpu_model():
 # ---------------------------------------------------------------------------
 # Reference CPU prover (oracle/_ref) — the baseline, never the product.
 # ---------------------------------------------------------------------------
-def reference_sample(threads: int, log_width: int, depth: int):
-    """gates/s of the reference gkr_prove on `threads` independent copies of a
-    (2^log_width x depth) sub-circuit of the same family, run concurrently."""
-    from concurrent.futures import ThreadPoolExecutor
+_REF_CACHE = {}
 
+
+def _ref_worker(args):
+    """one reference gkr_prove (separate process: the reference keeps a
+    shared_ptr<FieldConfig> in every FieldElement, so threads would contend on
+    one atomic refcount). Circuit and inputs are generated once per worker
+    process (pool initializer) and cached; copies differ by transcript prefix."""
+    log_width, depth, t = args
+    sys.path.insert(0, ROOT)
     from oracle import dgkr_oracle as O
     from oracle import refbind as R
     from paper_2404_10404_b200 import workloads as W
 
     fld = O.BN254
-    insz, flat = W.layered_circuit(CIRCUIT_SEED, log_width, depth)
-    gates = (1 << log_width) * depth
+    key = (log_width, depth)
+    if key not in _REF_CACHE:
+        insz, flat = W.layered_circuit(CIRCUIT_SEED, log_width, depth)
 
-    class _Shape:  # minimal shape for refbind.gkr_prove's capacity math
-        input_size = insz
+        class _Shape:  # minimal shape for refbind.gkr_prove's capacity math
+            input_size = insz
 
-        @staticmethod
-        def padded_size(l):
-            return 1 << log_width
+            @staticmethod
+            def padded_size(l):
+                return 1 << log_width
 
-    inputs = [fld.elems_from_bytes(W.random_inputs(fld.p, insz, INPUT_SEED + t).tobytes()) for t in range(threads)]
-
-    def one(t):
-        R.gkr_prove(fld, "dgkr.bench", [t], _Shape, inputs[t], flat=flat)
-
+        inputs = fld.elems_from_bytes(W.random_inputs(fld.p, insz, INPUT_SEED).tobytes())
+        _REF_CACHE[key] = (_Shape, flat, inputs)
+    if t < 0:  # pool initializer: build the cache only
+        return 0.0
+    shape, flat, inputs = _REF_CACHE[key]
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(one, range(threads)))
-    dt = time.perf_counter() - t0
-    return threads * gates / dt, dt, gates
+    R.gkr_prove(fld, "dgkr.bench", [t], shape, inputs, flat=flat)
+    return time.perf_counter() - t0
+
+
+def reference_sample(workers: int, log_width: int, depth: int, pool=None):
+    """gates/s of the reference gkr_prove on `workers` independent copies of a
+    (2^log_width x depth) sub-circuit of the same family, run concurrently in
+    separate processes; wall time of the whole batch)."""
+    gates = (1 << log_width) * depth
+    if pool is None:
+        dt = _ref_worker((log_width, depth, 0))
+        workers = 1
+    else:
+        t0 = time.perf_counter()
+        pool.map(_ref_worker, [(log_width, depth, t) for t in range(workers)], chunksize=1)
+        dt = time.perf_counter() - t0
+    return workers * gates / dt, dt, gates
 
 
 def run_reference_arm(args, cfg_name):
@@ -161,18 +180,23 @@ def run_reference_arm(args, cfg_name):
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdgkr_ref.so not built"}))
         return 0
-    threads = os.cpu_count() or 1
-    s_depth = 4 if cfg_name == "c2" else depth
+    import multiprocessing as mp
+
+    threads = len(os.sched_getaffinity(0)) or 1
+    s_depth = 2 if cfg_name == "c2" else depth
     s_lw = lw
-    sample = (f"{threads} concurrent independent reference gkr_prove calls, each on one 2^{s_lw} x {s_depth}-layer "
-              f"sub-circuit of the {cfg_name.upper()} family (BN254); gates/s = total gates / wall time")
-    for _ in range(args.warmup):
-        reference_sample(threads, s_lw, s_depth)
+    sample = (f"{threads} concurrent independent reference gkr_prove calls (one process per host core), each on "
+              f"one 2^{s_lw} x {s_depth}-layer sub-circuit of the {cfg_name.upper()} family (BN254); "
+              f"gates/s = total gates / wall time")
     vals, times = [], []
-    for _ in range(args.steps):
-        v, dt, _g = reference_sample(threads, s_lw, s_depth)
-        vals.append(v)
-        times.append(dt)
+    with mp.get_context("spawn").Pool(threads, initializer=_ref_worker,
+                                      initargs=((s_lw, s_depth, -1),)) as pool:
+        for _ in range(args.warmup):
+            reference_sample(threads, s_lw, s_depth, pool)
+        for _ in range(args.steps):
+            v, dt, _g = reference_sample(threads, s_lw, s_depth, pool)
+            vals.append(v)
+            times.append(dt)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": "gkr_prover_gates_per_sec", "value": value, "unit": "gates/s",
@@ -204,7 +228,7 @@ def run_b200(args, cfg_name):
 
     rank, world, local_rank = env_rank()
     n_copies, lw, depth, desc = CONFIGS[cfg_name]
-    if world > 1:
+    if world > 1 or os.environ.get("DGKR_FORCE_DIST") == "1":
         from paper_2404_10404_b200 import dist
 
         return dist.run_bench_rank(args, cfg_name, CONFIGS, CIRCUIT_SEED, INPUT_SEED)

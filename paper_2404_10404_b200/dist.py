@@ -96,12 +96,19 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # DGKR_DEVICE / DGKR_DIST_BACKEND let tests run several ranks on one GPU
+    # (ranks exchange only through host shared memory; no kernel waits on another)
+    device = int(os.environ.get("DGKR_DEVICE", local_rank))
+    backend = os.environ.get("DGKR_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(device)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+    else:
+        dist.init_process_group(backend)
     n_copies, lw, depth, desc = configs[cfg_name]
     if n_copies % world:
         raise SystemExit(f"{n_copies} copies do not shard over {world} GPUs")
-    ctx = P.Context(local_rank)
+    ctx = P.Context(device)
     field = P.Field.bn254()
     insz, flat = W.layered_circuit(circuit_seed, lw, depth)
     n_local = n_copies // world
@@ -123,8 +130,8 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
         t0 = time.perf_counter()
         proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2")
         torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], device="cuda")
-        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)  # max over ranks
         return float(dt.item()), proofs, states, profs
 
     timed(lanes * args.warmup)
