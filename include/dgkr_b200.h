@@ -71,10 +71,13 @@ typedef struct dgkr_profile {
     uint64_t h2d_bytes;
     uint64_t d2h_bytes;
     uint64_t rounds;            /* sum-check rounds (host round trips) */
+    double ntt_ms;              /* NTT / RS-encode kernels (bit-reverse + butterflies) */
+    double merkle_ms;           /* leaf digests + Merkle tree kernels (PCS, FRI) */
+    double fold_ms;             /* FRI fold kernels */
 } dgkr_profile;
 
 const char* dgkr_last_error(void);
-int dgkr_abi_version(void);
+int dgkr_abi_version(void); /* 2 */
 
 /* ---- field (field.hpp:23-80) ------------------------------------------- */
 /* modulus: little-endian bytes. The GPU path supports odd p < 2^254

@@ -104,6 +104,9 @@ class Profile_t(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("rounds", C.c_uint64),
+        ("ntt_ms", C.c_double),
+        ("merkle_ms", C.c_double),
+        ("fold_ms", C.c_double),
     ]
 
     def as_dict(self):

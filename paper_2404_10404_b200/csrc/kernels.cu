@@ -209,8 +209,14 @@ __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __rest
     }
 }
 
-template <class F, int NP, bool HAS_G, int MODE>
-__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, Fe (&s)[3]) {
+// Round sums per output pair index: S0 = sum f0 g0 (+ G0), S2 = sum df dg and,
+// when S1, S1 = sum f1 g1 (+ G1). With !S1 the host recovers S1 = claim - S0
+// from the sum-check invariant p(0) + p(1) = claim (only where the claim is
+// the prover's own, i.e. inside gkr_prove), saving one Montgomery product and
+// one accumulator per index. Accumulators: s[0] = S0, s[NS-1] = S2, s[1] = S1.
+template <class F, int NP, bool HAS_G, int MODE, bool S1>
+__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, Fe (&s)[S1 ? 3 : 2]) {
+    constexpr int NS = S1 ? 3 : 2;
     const int np = NP > 0 ? NP : a.np;
     const std::uint64_t P = a.n_out_pairs;
     for (int k = 0; k < np; ++k) {
@@ -218,43 +224,49 @@ __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i
         load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, a.k, f0, f1);
         load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
         s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
-        s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
-        s[2] = fe_add<F>(s[2], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
+        if constexpr (S1) s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
+        s[NS - 1] = fe_add<F>(s[NS - 1], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
     }
     if (HAS_G) {
         Fe g0, g1;
         load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, a.k, g0, g1);
         s[0] = fe_add<F>(s[0], g0);
-        s[1] = fe_add<F>(s[1], g1);
+        if constexpr (S1) s[1] = fe_add<F>(s[1], g1);
     }
 }
 
-template <class F, int NP, bool HAS_G, int MODE, int MINB>
+template <class F, int NP, bool HAS_G, int MODE, bool S1, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant__ RoundParams a) {
-    Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
+    constexpr int NS = S1 ? 3 : 2;
+    Fe s[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = fe_zero();
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < a.n_out_pairs;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        round_body<F, NP, HAS_G, MODE>(a, i, s);
+        round_body<F, NP, HAS_G, MODE, S1>(a, i, s);
     }
-    grid_finish<F, 3>(s, a.partials, a.counter, a.result);
+    grid_finish<F, NS>(s, a.partials, a.counter, a.result);
 }
 
 // Small-table variant: one CTA covers all pairs; the CTA sum is the result.
-template <class F, int NP, bool HAS_G, int MODE>
+template <class F, int NP, bool HAS_G, int MODE, bool S1>
 __global__ void __launch_bounds__(kThreads) k_round_small(const __grid_constant__ RoundParams a) {
-    __shared__ Fe sh[32][3];
-    Fe s[3] = {fe_zero(), fe_zero(), fe_zero()};
+    constexpr int NS = S1 ? 3 : 2;
+    __shared__ Fe sh[32][NS];
+    Fe s[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = fe_zero();
     for (std::uint64_t i = threadIdx.x; i < a.n_out_pairs; i += blockDim.x) {
-        round_body<F, NP, HAS_G, MODE>(a, i, s);
+        round_body<F, NP, HAS_G, MODE, S1>(a, i, s);
     }
     if (blockDim.x <= 32) {
-        warp_sum<F, 3>(s);
+        warp_sum<F, NS>(s);
     } else {
-        block_sum<F, 3>(s, sh);
+        block_sum<F, NS>(s, sh);
     }
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) fe_store(&a.result[k], s[k]);
+        for (int k = 0; k < NS; ++k) fe_store(&a.result[k], s[k]);
     }
 }
 
@@ -924,14 +936,11 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
-    static const int minb = [] {
-        const char* e = std::getenv("DGKR_ROUND_MINB");
-        return (e && e[0] == '3') ? 3 : 2;
-    }();
-#define LAUNCH_ROUND(NP, HG, MD)                                             \
-    do {                                                                     \
-        if (minb == 3) k_round<F, NP, HG, MD, 3><<<g, kThreads, 0, st>>>(p); \
-        else k_round<F, NP, HG, MD, 2><<<g, kThreads, 0, st>>>(p);           \
+    // 2 CTAs/SM (<= 128 registers); forcing 3 (80 registers, small spill) measured no faster
+#define LAUNCH_ROUND(NP, HG, MD)                                                   \
+    do {                                                                           \
+        if (a.need_s1) k_round<F, NP, HG, MD, true, 2><<<g, kThreads, 0, st>>>(p); \
+        else k_round<F, NP, HG, MD, false, 2><<<g, kThreads, 0, st>>>(p);          \
     } while (0)
 #define BY_MODE(NP, HG)                                   \
     do {                                                  \
@@ -955,7 +964,11 @@ void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, c
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const unsigned threads = a.n_out_pairs <= 32 ? 32u : (a.n_out_pairs <= 128 ? 128u : kThreads);
-#define LAUNCH_ROUND(NP, HG, MD) k_round_small<F, NP, HG, MD><<<1, threads, 0, st>>>(p)
+#define LAUNCH_ROUND(NP, HG, MD)                                                        \
+    do {                                                                                \
+        if (a.need_s1) k_round_small<F, NP, HG, MD, true><<<1, threads, 0, st>>>(p);    \
+        else k_round_small<F, NP, HG, MD, false><<<1, threads, 0, st>>>(p);             \
+    } while (0)
     DISPATCH_FIELD(k, F, {
         if (a.np == 1 && a.has_g) BY_MODE(1, true);
         else if (a.has_g) BY_MODE(0, true);

@@ -55,6 +55,8 @@ struct RoundLaunch {
     // host pointer to the fold constants {c_0..c_7, r} (9 x 32 bytes, field.cuh
     // FoldConst): c_k = r * 2^(32k+64) * R^-1 mod p; passed as kernel parameters
     const void* fold_const = nullptr;
+    // false: compute only (S0, S2) into result[0..2) (S1 = claim - S0 on the host)
+    bool need_s1 = true;
 };
 constexpr std::size_t kFoldConstBytes = 9 * 32;
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);

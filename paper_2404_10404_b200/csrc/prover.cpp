@@ -157,6 +157,16 @@ struct RtState {
 /// One in-flight proof: a CUDA stream, its reduction workspace, pinned
 /// staging and profile counters. A context owns one lane per concurrent
 /// proof (lane 0 serves the single-call API).
+/// device buffers of the NTT / RS / FRI entry points, kept across calls
+/// (multi-GiB at C5 sizes: cudaMalloc/cudaFree per call would dominate)
+struct NttWs {
+    DBuf<std::uint8_t> stage, dbuf;
+    DBuf<Fe> x, a, tw, cpow, scratch, twinv;
+    std::vector<std::unique_ptr<DBuf<Fe>>> layer;
+    std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree;
+    DBuf<std::uint64_t> didx;
+};
+
 struct Lane {
     int device = 0;
     int sms = 0;
@@ -177,6 +187,23 @@ struct Lane {
     static constexpr std::size_t kGatherOff = 14336;  // [14336, 16384): all-gathered round sums (<= 682 ranks)
     bool profile_on = false;
     dgkr_profile prof{};
+    /// profile-only CUDA-event bracket around a kernel group: tbeg(); ...; tend(prof.x_ms)
+    void tbeg() {
+        if (profile_on) CK(cudaEventRecord(ev0, st));
+    }
+    void tend(double& acc) {
+        if (!profile_on) return;
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        acc += ms;
+    }
+    std::unique_ptr<NttWs> ntt_ws;
+    NttWs& nttws() {
+        if (!ntt_ws) ntt_ws = std::make_unique<NttWs>();
+        return *ntt_ws;
+    }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     Lane(int dev, int sm_count, int idx, RtState* rts) : device(dev), sms(sm_count), index(idx), rt(rts) {
@@ -606,12 +633,16 @@ struct SumcheckRun {
     std::vector<RoundPoly> rounds;
     std::vector<U256> challenges;
     std::vector<U256> finals;  // per table, Montgomery
+    U256 claim_end{};          // p_last(r_last) when run with a known claim
 };
 
 /// tables: device pointer array `base` of ntab = 2*np + has_g tables of
 /// size 2^nv. Returns rounds, challenges and the final value of each table.
+/// claim: the running sum-check claim when the caller produced it itself
+/// (then p(0) + p(1) = claim holds exactly and S1 = claim - S0 is not
+/// computed on the device); nullptr = derive every round from the tables.
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr);
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr, const U256* claim = nullptr);
 
 /// Distributed form (cluster.hpp:228-320 generalised to the layer
 /// sum-check): `nv` local variables per rank, rank = high variables. Local
@@ -621,10 +652,10 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
 /// rebuilt world-sized tables — identical on all ranks, so the transcript
 /// equals the single-GPU one byte for byte.
 SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                            RoundBuffers& rb, Transcript& tr, dgkr_comm* comm) {
+                            RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim = nullptr) {
     const int ntab = 2 * np + (has_g ? 1 : 0);
     const int world = comm->world;
-    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm);
+    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim);
     // boundary: gather every rank's final table values
     std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
     for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
@@ -647,16 +678,21 @@ SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, 
     int lw = 0;
     while ((1 << lw) < world) ++lw;
     RoundBuffers tail_rb;
-    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dp.p, tail_rb, tr, nullptr);
+    const U256 mid = (nv > 0 || !claim) ? loc.claim_end : *claim;
+    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dp.p, tail_rb, tr, nullptr, claim ? &mid : nullptr);
     loc.rounds.insert(loc.rounds.end(), tail.rounds.begin(), tail.rounds.end());
     loc.challenges.insert(loc.challenges.end(), tail.challenges.begin(), tail.challenges.end());
     loc.finals = tail.finals;
+    loc.claim_end = tail.claim_end;
     return loc;
 }
 
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm) {
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim) {
     const HostField& F = f->f;
+    const bool skip_s1 = claim != nullptr;
+    const int nres = skip_s1 ? 2 : 3;  // device sums per round: (S0, S2) or (S0, S1, S2)
+    U256 run_claim = skip_s1 ? *claim : U256{};
     const FieldKind kind = ctx->use(f);
     const int ntab = 2 * np + (has_g ? 1 : 0);
     SumcheckRun out;
@@ -672,6 +708,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         rl.has_g = has_g;
         rl.r = d_r;
         rl.fold_const = fk;
+        rl.need_s1 = !skip_s1;
         if (j == 1) {
             rl.mode = 0;  // scan the natural-order base tables
             rl.in = base;
@@ -692,13 +729,14 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         if (comm) {
             // every rank's partial round sums (cluster.hpp:272-278), summed on every rank
             const std::size_t W = static_cast<std::size_t>(comm->world);
-            comm->allgather_to_host(ctx->ws.result, ctx->h_small + Lane::kGatherOff, 3 * sizeof(Fe), ctx);
+            comm->allgather_to_host(ctx->ws.result, ctx->h_small + Lane::kGatherOff, nres * sizeof(Fe), ctx);
             U256 acc[3] = {};
             for (std::size_t r = 0; r < W; ++r)
-                for (int k = 0; k < 3; ++k) acc[k] = F.add(acc[k], to_u256(ctx->h_small[Lane::kGatherOff + 3 * r + k]));
-            for (int k = 0; k < 3; ++k) ctx->h_small[1 + k] = to_fe(acc[k]);
+                for (int k = 0; k < nres; ++k)
+                    acc[k] = F.add(acc[k], to_u256(ctx->h_small[Lane::kGatherOff + nres * r + k]));
+            for (int k = 0; k < nres; ++k) ctx->h_small[1 + k] = to_fe(acc[k]);
         } else {
-            ctx->d2h(ctx->h_small + 1, ctx->ws.result, 3 * sizeof(Fe));
+            ctx->d2h(ctx->h_small + 1, ctx->ws.result, nres * sizeof(Fe));
             ctx->sync();
         }
         if (ctx->profile_on) {
@@ -710,10 +748,12 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             const std::uint64_t ntabs = static_cast<std::uint64_t>(ntab);
             // bytes: fold reads 4, writes 2 elements per table per output pair; scan reads 2
             ctx->prof.round_bytes += pairs * ntabs * 32 * (rl.mode ? 6 : 2);
-            ctx->prof.round_mults += pairs * (3 * np + (rl.mode ? 2 * ntabs : 0));
+            ctx->prof.round_mults += pairs * (nres * np + (rl.mode ? 2 * ntabs : 0));
         }
         const double t0 = now_ms();
-        const U256 s0 = to_u256(ctx->h_small[1]), s1 = to_u256(ctx->h_small[2]), s2 = to_u256(ctx->h_small[3]);
+        const U256 s0 = to_u256(ctx->h_small[1]);
+        const U256 s1 = skip_s1 ? F.sub(run_claim, s0) : to_u256(ctx->h_small[2]);  // p(0) + p(1) = claim
+        const U256 s2 = to_u256(ctx->h_small[nres]);
         RoundPoly rp;
         rp.c[0] = s0;
         rp.c[2] = s2;
@@ -721,6 +761,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         for (int k = 0; k < 3; ++k) tr.absorb(rp.c[k]);
         tr.absorb(zero);
         const U256 r = tr.challenge();
+        if (skip_s1) run_claim = F.add(rp.c[0], F.mul(r, F.add(rp.c[1], F.mul(r, rp.c[2]))));  // p(r)
         ctx->prof.host_transcript_ms += now_ms() - t0;
         ctx->prof.rounds += 1;
         out.rounds.push_back(rp);
@@ -729,6 +770,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         ctx->h_small[0] = to_fe(r);
         ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
     }
+    out.claim_end = run_claim;
     // final fold of the 2-element tables (or read the 1-element tables)
     if (nv >= 1) {
         launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
@@ -801,7 +843,8 @@ std::vector<std::uint8_t> product_sumcheck(Lane* ctx, const dgkr_field* f, std::
     const U256 claimed = to_u256(ctx->h_small[1]);
     tr.absorb(claimed);  // sumcheck.hpp:231
     RoundBuffers rb;
-    SumcheckRun run = run_rounds(ctx, f, static_cast<int>(n_pairs), false, static_cast<int>(vars), base.p, rb, tr);
+    SumcheckRun run =
+        run_rounds(ctx, f, static_cast<int>(n_pairs), false, static_cast<int>(vars), base.p, rb, tr, nullptr, &claimed);
     if (claimed_out) *claimed_out = claimed;
     return sumcheck_bytes(F, claimed, run.rounds, run.finals);
 }
@@ -1394,8 +1437,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p1 = comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm)
-                              : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
+        SumcheckRun p1 =
+            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm,
+                                   &combined.value)
+                 : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
+                              &combined.value);
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
@@ -1427,8 +1473,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
-        SumcheckRun p2 = comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm)
-                              : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr);
+        SumcheckRun p2 =
+            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm,
+                                   &p1.claim_end)
+                 : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
+                              &p1.claim_end);
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;
@@ -1464,10 +1513,12 @@ struct PcsDevice {
 
 void pcs_build_tree(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols) {
     d.nodes.ensure(2 * cols * 32);
+    ctx->tbeg();
     launch_column_digests(ctx->use(f), d.m.p, cols, static_cast<int>(rows), static_cast<int>(f->f.width()),
                           d.nodes.p + cols * 32, ctx->st);
     ctx->launched();
     launch_merkle(d.nodes.p, cols, ctx->st);
+    ctx->tend(ctx->prof.merkle_ms);
     ctx->launched(cols > 1 ? log2_exact(cols) : 0);
 }
 
@@ -1625,8 +1676,10 @@ void coset_ntt(Lane* ctx, const dgkr_field* f, const Fe* coeff, std::uint64_t n_
         pow_table(ctx, f, c, n_in, cpow.p, scratch);
         scale = cpow.p;
     }
+    ctx->tbeg();
     launch_bitrev_scale(kind, coeff, scale, a, static_cast<int>(log_n), n_in, ctx->st);
     launch_ntt(kind, a, static_cast<int>(log_n), tw.p, ctx->st);
+    ctx->tend(ctx->prof.ntt_ms);
     ctx->launched(2 + log_n);
 }
 
@@ -1641,15 +1694,22 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     if (final_log > log_n0) fail(DGKR_INVALID_ARGUMENT, "final layer larger than the codeword");
     const unsigned L = log_n0 - final_log;
     const std::uint64_t N0 = std::uint64_t{1} << log_n0;
-    DBuf<std::uint8_t> stage;
-    DBuf<Fe> cf, tw, cpow, scratch, twinv;
+    NttWs& ws = ctx->nttws();
+    auto& stage = ws.stage;
+    auto& cf = ws.x;
+    auto& tw = ws.tw;
+    auto& cpow = ws.cpow;
+    auto& scratch = ws.scratch;
+    auto& twinv = ws.twinv;
     cf.ensure(n);
     ctx->upload_elems(f, coeffs, n, cf.p, stage);
     // layer 0: RS encoding on the coset g<w_N0>
-    std::vector<std::unique_ptr<DBuf<Fe>>> layer(L + 1);
-    std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree(L);
+    auto& layer = ws.layer;
+    auto& tree = ws.tree;
+    if (layer.size() < L + 1) layer.resize(L + 1);
+    if (tree.size() < L) tree.resize(L);
     for (unsigned l = 0; l <= L; ++l) {
-        layer[l] = std::make_unique<DBuf<Fe>>();
+        if (!layer[l]) layer[l] = std::make_unique<DBuf<Fe>>();
         layer[l]->ensure(N0 >> l);
     }
     coset_ntt(ctx, f, cf.p, n, log_n0, f->coset, true, layer[0]->p, tw, cpow, scratch);
@@ -1660,10 +1720,12 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     U256 ginv = f->coset_inv;  // (g^(2^l))^-1
     for (unsigned l = 0; l < L; ++l) {
         const std::uint64_t Nl = N0 >> l;
-        tree[l] = std::make_unique<DBuf<std::uint8_t>>();
+        if (!tree[l]) tree[l] = std::make_unique<DBuf<std::uint8_t>>();
         tree[l]->ensure(2 * Nl * 32);
+        ctx->tbeg();
         launch_column_digests(kind, layer[l]->p, Nl, 1, static_cast<int>(w), tree[l]->p + Nl * 32, ctx->st);
         launch_merkle(tree[l]->p, Nl, ctx->st);
+        ctx->tend(ctx->prof.merkle_ms);
         ctx->launched(2);
         ctx->d2h(roots[l].data(), tree[l]->p + 32, 32);
         ctx->sync();
@@ -1672,7 +1734,9 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
         U256 bk[9];
         f->fold_const(beta, bk);
         Fe gi = to_fe(ginv);
+        ctx->tbeg();
         launch_fri_fold(kind, layer[l]->p, Nl, twinv.p, std::uint64_t{1} << l, &gi, bk, layer[l + 1]->p, ctx->st);
+        ctx->tend(ctx->prof.fold_ms);
         ctx->launched();
         ginv = F.mul(ginv, ginv);
     }
@@ -1710,8 +1774,8 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     put32(out, static_cast<std::uint32_t>(qi.size()));
     std::vector<std::vector<std::uint8_t>> vals(L), paths(L);
     std::vector<unsigned> depth(L);
-    DBuf<std::uint64_t> didx;
-    DBuf<std::uint8_t> dbuf;
+    auto& didx = ws.didx;
+    auto& dbuf = ws.dbuf;
     for (unsigned l = 0; l < L; ++l) {
         const std::uint64_t Nl = N0 >> l, hl = Nl / 2;
         depth[l] = log2_exact(Nl);
@@ -1836,7 +1900,7 @@ std::size_t plan_clusters(std::size_t n, std::size_t k) {
 extern "C" {
 
 const char* dgkr_last_error(void) { return g_err.c_str(); }
-int dgkr_abi_version(void) { return 1; }
+int dgkr_abi_version(void) { return 2; }
 
 int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out) {
     return guard([&] {
@@ -2298,16 +2362,22 @@ int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* in, unsigne
         const FieldKind kind = ctx->use(f);
         const std::uint64_t N = std::uint64_t{1} << log_n;
         const std::size_t w = F.width();
-        DBuf<std::uint8_t> stage;
-        DBuf<Fe> x, a, tw, scratch;
+        NttWs& ws = ctx->nttws();
+        auto& stage = ws.stage;
+        auto& x = ws.x;
+        auto& a = ws.a;
+        auto& tw = ws.tw;
+        auto& scratch = ws.scratch;
         x.ensure(N);
         a.ensure(N);
         ctx->upload_elems(f, in, N, x.p, stage);
         const U256 root = f->root_of_unity(log_n);
         tw.ensure(std::max<std::uint64_t>(N / 2, 1));
         if (N >= 2) pow_table(ctx, f, inverse ? F.inv(root) : root, N / 2, tw.p, scratch);
+        ctx->tbeg();
         launch_bitrev_scale(kind, x.p, nullptr, a.p, static_cast<int>(log_n), N, ctx->st);
         launch_ntt(kind, a.p, static_cast<int>(log_n), tw.p, ctx->st);
+        ctx->tend(ctx->prof.ntt_ms);
         if (inverse) {
             U256 k[9];
             f->fold_const(F.inv(F.from_u64(N)), k);
@@ -2330,8 +2400,13 @@ int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeff
         const unsigned log_n = log2_exact(n) + blowup_log;
         const std::uint64_t N = std::uint64_t{1} << log_n;
         const std::size_t w = f->f.width();
-        DBuf<std::uint8_t> stage;
-        DBuf<Fe> cf, a, tw, cpow, scratch;
+        NttWs& ws = ctx->nttws();
+        auto& stage = ws.stage;
+        auto& cf = ws.x;
+        auto& a = ws.a;
+        auto& tw = ws.tw;
+        auto& cpow = ws.cpow;
+        auto& scratch = ws.scratch;
         cf.ensure(n);
         a.ensure(N);
         ctx->upload_elems(f, coeffs, n, cf.p, stage);
