@@ -261,6 +261,26 @@ int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, si
 int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, size_t n, unsigned blowup_log,
                    unsigned final_log, size_t queries, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
 
+/* ---- distinct indexes: associative array hash (distinct.hpp; config C4) ------------
+ * F(e) = three rounds of r <- (r + e + 2^32 - 1)^3 from r = 0; AH(list) = sum F(e_i),
+ * 0 for the empty list. Items cross as canonical bytes (width), non-canonical
+ * encodings fail with DGKR_INVALID_ARGUMENT (FieldElement::from_bytes).
+ *   dgkr_distinct_ah            distinct::ah                      distinct.hpp:37-44
+ *   dgkr_distinct_check         distinct::pairwise_distinct_check distinct.hpp:53-68
+ *                               (*ok = AH(a) == AH(a_sorted) and a_sorted strictly ascends)
+ *   dgkr_distinct_chain_update  distinct::chain_update            distinct.hpp:82-92
+ *                               (h_out = h + AH(items); DGKR_OUT_OF_RANGE if an item > n_max)
+ *   dgkr_distinct_bitchange     distinct::bitchange_experiment    distinct.hpp:112-145
+ *                               (set_counts[k], k < bits(p): #x in 1..count with bit k of
+ *                               canonical F(x+1) - F(x) set; probability = count_k / count;
+ *                               DGKR_INVALID_ARGUMENT if count < 10^4) */
+int dgkr_distinct_ah(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* items, size_t n, uint8_t* out);
+int dgkr_distinct_check(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* a, size_t n_a, const uint8_t* a_sorted,
+                        size_t n_sorted, int* ok);
+int dgkr_distinct_chain_update(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* h, uint64_t n_max,
+                               const uint8_t* items, size_t n, uint8_t* h_out);
+int dgkr_distinct_bitchange(dgkr_ctx* ctx, const dgkr_field* f, size_t count, uint64_t* set_counts);
+
 /* ---- distributed runtime (cluster.hpp), N workers in one call -------------------
  * shard_pairs + dist_sumcheck (cluster.hpp:190-320) on full tables; proof
  * bytes equal the reference's, TrafficStats::to_json().dump() written to

@@ -24,6 +24,7 @@
 
 #include "dgkr/circuit.hpp"
 #include "dgkr/cluster.hpp"
+#include "dgkr/distinct.hpp"
 #include "dgkr/field.hpp"
 #include "dgkr/gkr.hpp"
 #include "dgkr/pcs.hpp"
@@ -520,6 +521,56 @@ int ref_distpc(const std::uint8_t* mod, std::size_t mod_len, std::size_t n_worke
         if (js.size() + 1 > json_cap) throw std::invalid_argument("json buffer too small");
         std::memcpy(traffic_json, js.c_str(), js.size() + 1);
         return emit(bytes, open_out, cap, open_len);
+    });
+}
+
+/// distinct::ah (distinct.hpp:37-44)
+int ref_distinct_ah(const std::uint8_t* mod, std::size_t mod_len, const std::uint8_t* items, std::size_t n,
+                    std::uint8_t* out) {
+    return guard([&] {
+        auto cfg = field_from(mod, mod_len);
+        auto v = read_elems(items, n, cfg);
+        auto b = distinct::ah(std::span<const FieldElement>(v), cfg).to_bytes();
+        std::memcpy(out, b.data(), b.size());
+        return OK;
+    });
+}
+
+/// distinct::pairwise_distinct_check (distinct.hpp:53-68)
+int ref_distinct_check(const std::uint8_t* mod, std::size_t mod_len, const std::uint8_t* a, std::size_t n_a,
+                       const std::uint8_t* a_sorted, std::size_t n_sorted, int* ok) {
+    return guard([&] {
+        auto cfg = field_from(mod, mod_len);
+        auto va = read_elems(a, n_a, cfg);
+        auto vs = read_elems(a_sorted, n_sorted, cfg);
+        *ok = distinct::pairwise_distinct_check(va, vs, cfg) ? 1 : 0;
+        return OK;
+    });
+}
+
+/// distinct::chain_update (distinct.hpp:82-92)
+int ref_distinct_chain_update(const std::uint8_t* mod, std::size_t mod_len, const std::uint8_t* h,
+                              std::uint64_t n_max, const std::uint8_t* items, std::size_t n, std::uint8_t* h_out) {
+    return guard([&] {
+        auto cfg = field_from(mod, mod_len);
+        distinct::ChainState st{read_elems(h, 1, cfg)[0], n_max};
+        distinct::IndexList block{cfg, read_elems(items, n, cfg), n_max};
+        auto b = distinct::chain_update(st, block).h.to_bytes();
+        std::memcpy(h_out, b.data(), b.size());
+        return OK;
+    });
+}
+
+/// distinct::bitchange_experiment (distinct.hpp:112-145): per-bit set counts
+int ref_distinct_bitchange(const std::uint8_t* mod, std::size_t mod_len, std::size_t count, std::uint64_t* set_counts,
+                           std::size_t* bits) {
+    return guard([&] {
+        auto cfg = field_from(mod, mod_len);
+        auto res = distinct::bitchange_experiment(count, cfg);
+        *bits = res.probabilities.size();
+        for (std::size_t k = 0; k < res.probabilities.size(); ++k)
+            set_counts[k] = static_cast<std::uint64_t>(res.probabilities[k] * static_cast<double>(count) + 0.5);
+        return OK;
     });
 }
 

@@ -226,3 +226,33 @@ def distpc(fld, rows, r, q=32, k=0):
 
 def traffic_json_equal(a: str, b: str) -> bool:
     return json.loads(a) == json.loads(b) and a == b
+
+
+# --- distinct.hpp (config C4) ------------------------------------------------
+def distinct_ah(fld, items) -> int:
+    out = C.create_string_buffer(fld.width)
+    b = fld.elems_to_bytes(items) if not isinstance(items, (bytes, bytearray)) else bytes(items)
+    n = len(b) // fld.width
+    _check(lib().ref_distinct_ah(*_mod(fld), _u8(b), C.c_size_t(n), out))
+    return fld.from_bytes(out.raw)
+
+
+def distinct_check(fld, a, a_sorted) -> bool:
+    ok = C.c_int()
+    _check(lib().ref_distinct_check(*_mod(fld), _u8(fld.elems_to_bytes(a)), C.c_size_t(len(a)),
+                                    _u8(fld.elems_to_bytes(a_sorted)), C.c_size_t(len(a_sorted)), C.byref(ok)))
+    return bool(ok.value)
+
+
+def distinct_chain_update(fld, h: int, n_max: int, items) -> int:
+    out = C.create_string_buffer(fld.width)
+    _check(lib().ref_distinct_chain_update(*_mod(fld), _u8(fld.to_bytes(h)), C.c_uint64(n_max),
+                                           _u8(fld.elems_to_bytes(items)), C.c_size_t(len(items)), out))
+    return fld.from_bytes(out.raw)
+
+
+def distinct_bitchange(fld, count: int):
+    counts = (C.c_uint64 * 512)()
+    bits = C.c_size_t()
+    _check(lib().ref_distinct_bitchange(*_mod(fld), C.c_size_t(count), counts, C.byref(bits)))
+    return list(counts[: bits.value])

@@ -893,6 +893,101 @@ void ensure_pad_table() {
     g_pad_uploaded = true;
 }
 
+
+// ---------------------------------------------------------------------------
+// distinct.hpp (config C4): associative array hash AH = sum_i F(e_i),
+// F(e) = 3 rounds of r <- (r + e + 2^32 - 1)^3 from r = 0 (distinct.hpp:17-27).
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ Fe f_hash_dev(const Fe& e, const Fe& off) {
+    const Fe eo = fe_add<F>(e, off);
+    Fe r = fe_zero();
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const Fe t = fe_add<F>(r, eo);
+        r = fe_mul<F>(fe_mul<F>(t, t), t);
+    }
+    return r;
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_ah(const Fe* __restrict__ items, std::uint64_t n, Fe off,
+                                                 Fe* partials, unsigned* counter, Fe* result) {
+    Fe s[1] = {fe_zero()};
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        s[0] = fe_add<F>(s[0], f_hash_dev<F>(fe_load_nc(items + i), off));
+    }
+    grid_finish<F, 1>(s, partials, counter, result);
+}
+
+/// little-endian canonical compare of two width-byte records: -1, 0, 1
+__device__ __forceinline__ int canon_cmp(const std::uint8_t* a, const std::uint8_t* b, int width) {
+    for (int k = width - 1; k >= 0; --k) {
+        if (a[k] != b[k]) return a[k] < b[k] ? -1 : 1;
+    }
+    return 0;
+}
+
+/// *bad = 1 unless canon[i-1] < canon[i] for every i (distinct.hpp:60-65)
+__global__ void k_strict_ascent(const std::uint8_t* __restrict__ canon, int width, std::uint64_t n, int* bad) {
+    for (std::uint64_t i = 1 + blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        if (canon_cmp(canon + (i - 1) * width, canon + i * width, width) >= 0) *bad = 1;
+    }
+}
+
+/// *bad = 1 if some canonical value exceeds n_max (distinct.hpp:84-89)
+__global__ void k_bound_check(const std::uint8_t* __restrict__ canon, int width, std::uint64_t n, std::uint64_t n_max,
+                              int* bad) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint8_t* q = canon + i * width;
+        std::uint64_t lo = 0;
+        bool high = false;
+        for (int k = 0; k < width; ++k) {
+            if (k < 8) lo |= static_cast<std::uint64_t>(q[k]) << (8 * k);
+            else if (q[k]) high = true;
+        }
+        if (high || lo > n_max) *bad = 1;
+    }
+}
+
+/// per-bit set counts of canonical F(x+1) - F(x), x = first .. first+n-1
+/// (distinct.hpp:112-145); warp ballots into shared counters, one global
+/// atomic per bit per CTA.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bitchange(std::uint64_t first, std::uint64_t n, int bits, Fe off,
+                                                        unsigned long long* counts) {
+    __shared__ unsigned int sc[256];
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) sc[k] = 0;
+    __syncthreads();
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    const std::uint64_t base = blockIdx.x * static_cast<std::uint64_t>(blockDim.x);
+    for (std::uint64_t i0 = base; i0 < n; i0 += stride) {  // warp-uniform trip count
+        const std::uint64_t i = i0 + threadIdx.x;
+        Fe d = fe_zero();
+        if (i < n) {
+            const std::uint64_t x = first + i;
+            Fe cx = fe_zero(), cy = fe_zero();
+            cx.v[0] = static_cast<uint32_t>(x);
+            cx.v[1] = static_cast<uint32_t>(x >> 32);
+            cy.v[0] = static_cast<uint32_t>(x + 1);
+            cy.v[1] = static_cast<uint32_t>((x + 1) >> 32);
+            const Fe hx = f_hash_dev<F>(fe_to_mont<F>(cx), off);
+            const Fe hy = f_hash_dev<F>(fe_to_mont<F>(cy), off);
+            d = fe_from_mont<F>(fe_sub<F>(hy, hx));
+        }
+        for (int k = 0; k < bits; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, (d.v[k >> 5] >> (k & 31)) & 1u);
+            if ((threadIdx.x & 31) == 0 && m) atomicAdd(&sc[k], __popc(m));
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < bits; k += blockDim.x)
+        if (sc[k]) atomicAdd(counts + k, static_cast<unsigned long long>(sc[k]));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1137,6 +1232,39 @@ void launch_beta_combine(FieldKind k, const Fe* rows, std::uint64_t cols, int M,
     const int g = grid_for(cols, kThreads, 148 * 16);
     DISPATCH_FIELD(k, F, (k_beta_combine<F><<<g, kThreads, 0, st>>>(rows, cols, M, beta, out)));
     check_launch("beta_combine");
+}
+
+void launch_ah(FieldKind k, const Fe* items, std::uint64_t n, const void* off, const ReduceWs& ws, cudaStream_t st) {
+    Fe o;
+    std::memcpy(&o, off, sizeof(Fe));
+    const int g = grid_for(std::max<std::uint64_t>(n, 1), kThreads, ws.max_blocks);
+    DISPATCH_FIELD(k, F, (k_ah<F><<<g, kThreads, 0, st>>>(items, n, o, ws.partials, ws.counter, ws.result)));
+    check_launch("ah");
+}
+
+void launch_strict_ascent(const std::uint8_t* canon, int width, std::uint64_t n, int* bad, cudaStream_t st) {
+    if (n < 2) return;
+    const int g = grid_for(n, kThreads, 148 * 16);
+    k_strict_ascent<<<g, kThreads, 0, st>>>(canon, width, n, bad);
+    check_launch("strict_ascent");
+}
+
+void launch_bound_check(const std::uint8_t* canon, int width, std::uint64_t n, std::uint64_t n_max, int* bad,
+                        cudaStream_t st) {
+    if (n == 0) return;
+    const int g = grid_for(n, kThreads, 148 * 16);
+    k_bound_check<<<g, kThreads, 0, st>>>(canon, width, n, n_max, bad);
+    check_launch("bound_check");
+}
+
+void launch_bitchange(FieldKind k, std::uint64_t first, std::uint64_t n, int bits, const void* off,
+                      unsigned long long* counts, cudaStream_t st) {
+    if (n == 0) return;
+    Fe o;
+    std::memcpy(&o, off, sizeof(Fe));
+    const int g = grid_for(n, kThreads, 148 * 8);
+    DISPATCH_FIELD(k, F, (k_bitchange<F><<<g, kThreads, 0, st>>>(first, n, bits, o, counts)));
+    check_launch("bitchange");
 }
 
 }  // namespace dgkr_b200

@@ -180,4 +180,16 @@ void launch_merkle(std::uint8_t* nodes, std::uint64_t n_leaves, cudaStream_t st)
 void launch_beta_combine(FieldKind k, const Fe* rows, std::uint64_t cols, int M, const Fe* beta, Fe* out,
                          cudaStream_t st);
 
+// ---- distinct.hpp (config C4) --------------------------------------------
+/// ws.result[0] = sum_i F(items[i]) (Montgomery), F = distinct.hpp:17-27; off = Montgomery(2^32 - 1) (32 bytes)
+void launch_ah(FieldKind k, const Fe* items, std::uint64_t n, const void* off, const ReduceWs& ws, cudaStream_t st);
+/// *bad = 1 unless the canonical records strictly ascend
+void launch_strict_ascent(const std::uint8_t* canon, int width, std::uint64_t n, int* bad, cudaStream_t st);
+/// *bad = 1 if a canonical record exceeds n_max
+void launch_bound_check(const std::uint8_t* canon, int width, std::uint64_t n, std::uint64_t n_max, int* bad,
+                        cudaStream_t st);
+/// counts[k] += #{x in [first, first+n): bit k of canonical F(x+1) - F(x) is set}, k < bits <= 256
+void launch_bitchange(FieldKind k, std::uint64_t first, std::uint64_t n, int bits, const void* off,
+                      unsigned long long* counts, cudaStream_t st);
+
 }  // namespace dgkr_b200

@@ -178,6 +178,7 @@ struct Lane {
     DBuf<unsigned> counter;
     DBuf<Fe> d_small;      // challenges, points, seeds, finals
     DBuf<int> d_err;
+    DBuf<int> d_flag;       // kernel-raised predicate flags (distinct checks)
     Fe* h_small = nullptr;  // pinned mirror of d_small
     // pinned staging layout (Fe units): [0] challenge, [1..4) reduction
     // results, [16, 8192) eq-table points/seeds, [8192, 12288) slot values,
@@ -221,6 +222,7 @@ struct Lane {
         d_small.ensure(kSmall);
         d_err.ensure(1);
         CK(cudaMemset(d_err.p, 0, sizeof(int)));
+        d_flag.ensure(2);
         CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
         CK(cudaEventCreate(&ev0));
         CK(cudaEventCreate(&ev1));
@@ -2350,6 +2352,135 @@ int dgkr_field_ntt_info(const dgkr_field* f, unsigned* two_adicity, std::uint8_t
         *two_adicity = f->two_adicity;
         if (root) f->f.to_bytes(f->root, root);
         if (coset) f->f.to_bytes(f->coset, coset);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// distinct.hpp (config C4): AH, pairwise-distinct check, chain update,
+// bit-change experiment. One host sync per call: the encoding error flag, the
+// predicate flags and the sums come back in one pinned read.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct AhPass {
+    std::uint64_t n = 0;
+    Fe* x = nullptr;
+    const std::uint8_t* canon = nullptr;  // device canonical bytes
+};
+
+/// upload + validate + AH of one list; the sum lands in h_small[slot] after sync
+AhPass ah_enqueue(Lane* ctx, const dgkr_field* f, const std::uint8_t* items, std::uint64_t n, DBuf<std::uint8_t>& stage,
+                  DBuf<Fe>& x, int slot) {
+    const FieldKind kind = ctx->use(f);
+    const std::size_t w = f->f.width();
+    AhPass a;
+    a.n = n;
+    x.ensure(std::max<std::uint64_t>(n, 1));
+    stage.ensure(std::max<std::size_t>(n * w, 1));
+    if (n) {
+        ctx->h2d(stage.p, items, n * w);
+        launch_from_canonical(kind, stage.p, static_cast<int>(w), x.p, n, ctx->d_err.p, ctx->st);
+        ctx->launched();
+    }
+    const U256 off = f->f.from_u64(4294967295ull);  // distinct.hpp:20
+    Fe offe = to_fe(off);
+    launch_ah(kind, x.p, n, &offe, ctx->ws, ctx->st);
+    ctx->launched();
+    ctx->d2h(ctx->h_small + slot, ctx->ws.result, sizeof(Fe));
+    a.x = x.p;
+    a.canon = stage.p;
+    return a;
+}
+
+/// read back error + flags (ints at h_small[kGatherOff]) with one sync
+void distinct_finish(Lane* ctx, int* flags_out) {
+    int* hf = reinterpret_cast<int*>(ctx->h_small + Lane::kGatherOff);
+    ctx->d2h(hf, ctx->d_err.p, sizeof(int));
+    ctx->d2h(hf + 1, ctx->d_flag.p, 2 * sizeof(int));
+    ctx->sync();
+    if (hf[0]) {
+        CK(cudaMemsetAsync(ctx->d_err.p, 0, sizeof(int), ctx->st));
+        fail(DGKR_INVALID_ARGUMENT, "non-canonical field element encoding (index list)");
+    }
+    if (flags_out) {
+        flags_out[0] = hf[1];
+        flags_out[1] = hf[2];
+    }
+}
+
+}  // namespace
+
+int dgkr_distinct_ah(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* items, std::size_t n,
+                     std::uint8_t* out) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        NttWs& ws = ctx->nttws();
+        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
+        ah_enqueue(ctx, f, items, n, ws.stage, ws.x, 1);
+        distinct_finish(ctx, nullptr);
+        f->f.to_bytes(to_u256(ctx->h_small[1]), out);
+        ctx->end_call();
+    });
+}
+
+int dgkr_distinct_check(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* a, std::size_t n_a,
+                        const std::uint8_t* a_sorted, std::size_t n_sorted, int* ok) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        NttWs& ws = ctx->nttws();
+        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
+        ah_enqueue(ctx, f, a, n_a, ws.stage, ws.x, 1);
+        AhPass s = ah_enqueue(ctx, f, a_sorted, n_sorted, ws.dbuf, ws.a, 2);
+        launch_strict_ascent(s.canon, static_cast<int>(f->f.width()), n_sorted, ctx->d_flag.p, ctx->st);
+        ctx->launched();
+        int flags[2];
+        distinct_finish(ctx, flags);
+        const bool same = std::memcmp(&ctx->h_small[1], &ctx->h_small[2], sizeof(Fe)) == 0;  // distinct.hpp:57-59
+        *ok = (same && !flags[0]) ? 1 : 0;
+        ctx->end_call();
+    });
+}
+
+int dgkr_distinct_chain_update(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* h, std::uint64_t n_max,
+                               const std::uint8_t* items, std::size_t n, std::uint8_t* h_out) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const HostField& F = f->f;
+        const U256 hv = F.from_bytes(h);  // throws DGKR_INVALID_ARGUMENT on >= p
+        NttWs& ws = ctx->nttws();
+        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
+        AhPass p = ah_enqueue(ctx, f, items, n, ws.stage, ws.x, 1);
+        launch_bound_check(p.canon, static_cast<int>(F.width()), n, n_max, ctx->d_flag.p, ctx->st);
+        ctx->launched();
+        int flags[2];
+        distinct_finish(ctx, flags);
+        if (flags[0]) fail(DGKR_OUT_OF_RANGE, "validator index above bound");  // distinct.hpp:86-88
+        F.to_bytes(F.add(hv, to_u256(ctx->h_small[1])), h_out);
+        ctx->end_call();
+    });
+}
+
+int dgkr_distinct_bitchange(dgkr_ctx* ctx, const dgkr_field* f, std::size_t count, std::uint64_t* set_counts) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (count < 10000) fail(DGKR_INVALID_ARGUMENT, "bit-change experiment needs count >= 10^4");  // :116-118
+        const int bits = static_cast<int>(f->f.bits());
+        if (bits > 256) fail(DGKR_UNSUPPORTED, "field too wide");
+        DBuf<unsigned long long> d;
+        d.ensure(bits);
+        CK(cudaMemsetAsync(d.p, 0, bits * sizeof(unsigned long long), ctx->st));
+        Fe offe = to_fe(f->f.from_u64(4294967295ull));
+        launch_bitchange(ctx->use(f), 1, count, bits, &offe, d.p, ctx->st);
+        ctx->launched();
+        std::vector<unsigned long long> h(bits);
+        ctx->d2h(h.data(), d.p, bits * sizeof(unsigned long long));
+        ctx->sync();
+        for (int k = 0; k < bits; ++k) set_counts[k] = h[k];
+        ctx->end_call();
     });
 }
 

@@ -501,3 +501,47 @@ def distpc(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], 
         pos += 4 + n
     return ([roots.raw[32 * i:32 * (i + 1)] for i in range(nr.value)], ops, int.from_bytes(comb.raw, "little"),
             js.value.decode())
+
+
+# ---------------------------------------------------------------------------
+# distinct.hpp (config C4): associative array hash over validator indexes
+# ---------------------------------------------------------------------------
+def distinct_ah(ctx: Context, field: Field, items: Elems) -> int:
+    """distinct::ah (distinct.hpp:37-44): sum_i F(e_i), F = 3 rounds of (r + e + 2^32-1)^3"""
+    b = field.encode(items)
+    out = C.create_string_buffer(field.width)
+    check(lib().dgkr_distinct_ah(ctx.handle, field.handle, C.c_char_p(b), C.c_size_t(len(b) // field.width), out))
+    return int.from_bytes(out.raw, "little")
+
+
+def pairwise_distinct_check(ctx: Context, field: Field, a: Elems, a_sorted: Elems) -> bool:
+    """distinct::pairwise_distinct_check (distinct.hpp:53-68)"""
+    ba, bs = field.encode(a), field.encode(a_sorted)
+    ok = C.c_int()
+    check(lib().dgkr_distinct_check(ctx.handle, field.handle, C.c_char_p(ba), C.c_size_t(len(ba) // field.width),
+                                    C.c_char_p(bs), C.c_size_t(len(bs) // field.width), C.byref(ok)))
+    return bool(ok.value)
+
+
+def chain_update(ctx: Context, field: Field, h: int, n_max: int, items: Elems) -> int:
+    """distinct::chain_update (distinct.hpp:82-92): h + AH(items); OutOfRange if an item > n_max"""
+    b = field.encode(items)
+    out = C.create_string_buffer(field.width)
+    check(lib().dgkr_distinct_chain_update(ctx.handle, field.handle, C.c_char_p(field.encode([h])),
+                                           C.c_uint64(n_max), C.c_char_p(b), C.c_size_t(len(b) // field.width), out))
+    return int.from_bytes(out.raw, "little")
+
+
+def bitchange_experiment(ctx: Context, field: Field, count: int) -> Tuple[List[int], List[float]]:
+    """distinct::bitchange_experiment (distinct.hpp:112-145): per-bit set counts
+    and probabilities of canonical F(x+1) - F(x), x = 1..count"""
+    bits = field.bits
+    counts = (C.c_uint64 * max(bits, 1))()
+    check(lib().dgkr_distinct_bitchange(ctx.handle, field.handle, C.c_size_t(count), counts))
+    cs = list(counts[:bits])
+    return cs, [c / count for c in cs]
+
+
+def bitchange_csv(probabilities: Sequence[float]) -> str:
+    """BitChangeResult::to_csv (distinct.hpp:98-106)"""
+    return "index,bit_change\n" + "".join(f"{i},{p:g}\n" for i, p in enumerate(probabilities))

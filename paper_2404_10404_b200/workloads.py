@@ -88,3 +88,71 @@ def random_inputs(p: int, n: int, seed: int) -> np.ndarray:
         out[filled:filled + len(ok)] = ok
         filled += len(ok)
     return out.reshape(-1)
+
+
+def _flat(input_size: int, layers) -> Tuple[int, Flat]:
+    """layers: per gate layer, a list of gates; a gate is a list of nested
+    (is_mul, left_layer, left_gate, right_layer, right_gate)."""
+    lgs, gns, rows = [0], [0], []
+    for gates in layers:
+        for g in gates:
+            rows.extend(g)
+            gns.append(gns[-1] + len(g))
+        lgs.append(lgs[-1] + len(gates))
+    return input_size, (np.array(lgs, np.uint64), np.array(gns, np.uint64), np.array(rows, np.uint32).reshape(-1, 5),
+                        np.ones(len(layers) + 1, np.uint64))
+
+
+F_HASH_OFFSET = 4294967295  # distinct.hpp:20
+
+
+def ah_circuit(k: int) -> Tuple[int, Flat]:
+    """Associative-hash sub-circuit over k
+    validator indexes: output = sum_i s_i * F(e_i), F(e) = three rounds of
+    r <- (r + e + 2^32-1)^3 from r = 0 (distinct.hpp:17-27), s_i in {0,1}
+    masking padding slots. Input layer (4k): [e_0..e_{k-1}, s_0..s_{k-1},
+    2^32-1, 0, ...] (see ah_inputs). Layers: eo = e + c; then per round
+    sq = t*t, r = sq*t, t' = r + eo; mask; then a log2(k) add tree to one
+    output per copy. Replicate with n_copies for the data-parallel proof; the
+    AH of the whole list is the sum of the copies' outputs."""
+    if k < 1 or k & (k - 1):
+        raise ValueError("k must be a power of two")
+    c_gate = 2 * k
+    L = []
+    L.append([[(0, 0, i, 0, c_gate)] for i in range(k)])            # 1: eo = e + c
+    t_layer = 1                                                       # t1 = eo (r = 0)
+    for rnd in range(3):
+        L.append([[(1, t_layer, i, t_layer, i)] for i in range(k)])   # sq = t*t
+        sq = len(L)
+        L.append([[(1, sq, i, t_layer, i)] for i in range(k)])        # r = sq*t
+        r_layer = len(L)
+        if rnd < 2:
+            L.append([[(0, r_layer, i, 1, i)] for i in range(k)])     # t' = r + eo
+            t_layer = len(L)
+    L.append([[(1, len(L), i, 0, k + i)] for i in range(k)])          # s_i * F(e_i)
+    w = k
+    while w > 1:                                                      # in-copy sum tree
+        prev = len(L)
+        w //= 2
+        L.append([[(0, prev, 2 * i, prev, 2 * i + 1)] for i in range(w)])
+    return _flat(4 * k, L)
+
+
+def ah_inputs(p: int, items, k: int) -> np.ndarray:
+    """canonical input layer of the replicated ah_circuit(k) for `items`
+    (padded with masked zero slots to a power-of-two number of copies) as
+    (uint8[n*w], copies)"""
+    w = (p.bit_length() + 7) // 8
+    n = len(items)
+    copies = 1
+    while copies * k < n:  # power-of-two copy count (copy index = high variables)
+        copies *= 2
+    vals = np.zeros((copies, 4 * k), dtype=object)
+    vals[:] = 0
+    for j, e in enumerate(items):
+        c, i = divmod(j, k)
+        vals[c, i] = int(e)
+        vals[c, k + i] = 1
+    vals[:, 2 * k] = F_HASH_OFFSET % p
+    flat = vals.reshape(-1)
+    return np.frombuffer(b"".join(int(v).to_bytes(w, "little") for v in flat), dtype=np.uint8).copy(), copies

@@ -36,7 +36,7 @@ def main():
     rng = np.random.default_rng(20240410)
     out = {"source": "oracle/_ref/libdgkr_ref.so (unmodified /root/reference/proj/include via oracle/shim)",
            "transcript": [], "product_sum": [], "layer_sum": [], "gkr": [], "pcs": [], "dist_sumcheck": [],
-           "distpc": []}
+           "distpc": [], "distinct": []}
     for name, p in FIELDS.items():
         fld = O.Field(p)
         el = O.random_elements(fld, 6, rng)
@@ -95,6 +95,21 @@ def main():
         roots, ops, comb, js = R.distpc(fld, rows, r, 4)
         out["distpc"].append({"field": "bn254", "rows": rows, "r": r, "q": 4, "roots": [x.hex() for x in roots],
                               "openings": [x.hex() for x in ops], "combined": comb, "traffic": js})
+    # distinct.hpp (C4): AH, pairwise check (true / false cases), chain update, bit-change counts
+    drng = np.random.default_rng(2404104)
+    for name, p in FIELDS.items():
+        fld = O.Field(p)
+        bound = min(p - 1, 100000)
+        items = [int(x) for x in drng.integers(0, bound + 1, 33)]
+        uniq = sorted(set(items))
+        perm = [uniq[i] for i in drng.permutation(len(uniq))]
+        case = {"field": name, "items": items, "ah": R.distinct_ah(fld, items), "ah_empty": R.distinct_ah(fld, []),
+                "perm": perm, "sorted": uniq, "check_true": R.distinct_check(fld, perm, uniq),
+                "check_dup": R.distinct_check(fld, items, sorted(items)),
+                "h0": 12345 % p, "n_max": bound, "chain": R.distinct_chain_update(fld, 12345 % p, bound, items)}
+        if p > 1 << 20:
+            case["bitchange_10000"] = R.distinct_bitchange(fld, 10000)
+        out["distinct"].append(case)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
