@@ -181,6 +181,27 @@ int dgkr_circuit_load_inputs_lane(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_fie
                                   const uint8_t* inputs);
 int dgkr_ctx_get_profile_lane(dgkr_ctx* ctx, int lane, dgkr_profile* out);
 
+/* Binary CSR circuit interchange (the reference's
+ * JSON, circuit.hpp:227-277, is impractical at ~10^8 gates). Layout (LE):
+ * "DGKRCSR1" | u32 input_size | u32 depth | u32 n_copies | u32 has_min_padded |
+ * u64 n_gates | u64 n_nested | u64 layer_gate_start[depth+1] |
+ * u64 gate_nested_start[n_gates+1] | u32 nested[n_nested][5] | u64 min_padded[depth+1]?
+ * dgkr_circuit_load validates like dgkr_circuit_create; n_copies = 0 keeps the
+ * file's copy count. */
+int dgkr_circuit_save(const dgkr_circuit* c, const char* path);
+int dgkr_circuit_load(dgkr_ctx* ctx, const char* path, uint32_t n_copies, dgkr_circuit** out);
+
+/* gkr_verify + check_input_claims (gkr.hpp:253-325) on the host, for proofs in
+ * the GkrProof layout above (single- or multi-GPU: the bytes are the same).
+ * outputs (nullable): the claimed output statement, n_outputs canonical
+ * elements, compared with the proof's padded outputs (padding must be zero);
+ * inputs (nullable): the full input layer (n_copies x input_size canonical
+ * elements); when given, the input-layer claims are discharged against it.
+ * *accept = 1 iff everything verifies. Malformed proof bytes reject (no
+ * error); the transcript is advanced like the reference verifier's. */
+int dgkr_gkr_verify(const dgkr_circuit* c, const dgkr_field* f, const uint8_t* outputs, size_t n_outputs,
+                    const uint8_t* inputs, const uint8_t* proof, size_t len, dgkr_transcript* t, int* accept);
+
 /* ---- multi-GPU data-parallel GKR (Sisu; cluster.hpp:182-320 generalised) ----
  * One process per GPU. Rank r proves copies [r*n, (r+1)*n) of a uniform-width
  * data-parallel circuit created with n_copies = n (the rank index is the top

@@ -524,6 +524,26 @@ int ref_distpc(const std::uint8_t* mod, std::size_t mod_len, std::size_t n_worke
     });
 }
 
+/// GeneralCircuit::to_json (circuit.hpp:227-248) of a flat circuit, dumped
+/// compactly; from_json (:250-277) round trip checked by re-dumping.
+int ref_circuit_json(std::uint32_t input_size, std::uint32_t depth, const std::uint64_t* layer_gate_start,
+                     const std::uint64_t* gate_nested_start, const std::uint32_t* nested, char* out, std::size_t cap,
+                     std::size_t* len) {
+    return guard([&] {
+        auto c = build_circuit(input_size, depth, layer_gate_start, gate_nested_start, nested, nullptr);
+        const std::string js = c.to_json().dump();
+        auto c2 = circuit::GeneralCircuit::from_json(nlohmann::json::parse(js));
+        if (c2.to_json().dump() != js) throw std::logic_error("from_json/to_json round trip differs");
+        *len = js.size();
+        if (js.size() + 1 > cap) {
+            g_err = "output buffer too small";
+            return static_cast<int>(CAPACITY);
+        }
+        std::memcpy(out, js.c_str(), js.size() + 1);
+        return static_cast<int>(OK);
+    });
+}
+
 /// distinct::ah (distinct.hpp:37-44)
 int ref_distinct_ah(const std::uint8_t* mod, std::size_t mod_len, const std::uint8_t* items, std::size_t n,
                     std::uint8_t* out) {

@@ -256,3 +256,16 @@ def distinct_bitchange(fld, count: int):
     bits = C.c_size_t()
     _check(lib().ref_distinct_bitchange(*_mod(fld), C.c_size_t(count), counts, C.byref(bits)))
     return list(counts[: bits.value])
+
+
+def circuit_json(circuit: O.Circuit, flat=None) -> str:
+    """the reference's GeneralCircuit::to_json().dump() of a circuit"""
+    flat = flat if flat is not None else circuit.to_flat()
+    keep, ptrs = _flat_args(flat)
+    depth = len(keep[0]) - 1
+    cap = 256 + 128 * int(keep[1][-1] if len(keep[1]) else 0) + 64 * int(keep[0][-1])
+    out = C.create_string_buffer(cap)
+    ln = C.c_size_t()
+    _check(lib().ref_circuit_json(C.c_uint32(circuit.input_size), C.c_uint32(depth), *ptrs[:3], out, C.c_size_t(cap),
+                                  C.byref(ln)))
+    return out.raw[: ln.value].decode()

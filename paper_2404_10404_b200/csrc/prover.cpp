@@ -904,6 +904,9 @@ struct dgkr_circuit {
     std::vector<std::unique_ptr<CircuitWs>> ws;  // per lane
 
     std::uint32_t padded_log2_full(std::uint32_t l) const { return sub_log[l] + log_copies; }
+    // host copy of the sub-circuit wiring (the verifier's sparse wire list)
+    std::vector<std::uint64_t> h_lgs, h_gns, h_min_padded;
+    std::vector<std::uint32_t> h_nested;
 };
 
 namespace {
@@ -2188,6 +2191,212 @@ int dgkr_prove_layer_sum(dgkr_ctx* ctx, const dgkr_field* f, std::size_t side_va
     });
 }
 
+// ===========================================================================
+// GKR verifier (host): gkr_verify + check_input_claims (gkr.hpp:253-325),
+// verify_layer_sum (sumcheck.hpp:461-505), run_round_checks (:249-270).
+// The wiring predicate is evaluated through eq tables (O(T + W) per layer
+// instead of the reference's O(W * s) chi_eval per wire; same values).
+// Rejection is a result: malformed bytes reject, they do not throw.
+// ===========================================================================
+namespace {
+
+struct ProofReader {
+    const std::uint8_t* p;
+    std::size_t n, pos = 0;
+    const HostField& F;
+    bool ok = true;
+    std::uint32_t u32() {
+        if (pos + 4 > n) {
+            ok = false;
+            return 0;
+        }
+        std::uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(p[pos + i]) << (8 * i);
+        pos += 4;
+        return v;
+    }
+    U256 elem() {
+        const std::size_t w = F.width();
+        if (pos + w > n || !F.canonical_lt_p(p + pos, w)) {
+            ok = false;
+            pos = n;
+            return U256{};
+        }
+        const U256 v = F.from_bytes(p + pos);
+        pos += w;
+        return v;
+    }
+};
+
+/// eq table: out[b] = seed * prod_k (b_k ? x_k : 1 - x_k), x_1 = LSB (mle.hpp:95-120)
+std::vector<U256> eq_table_host(const HostField& F, const std::vector<U256>& x, const U256& seed) {
+    std::vector<U256> t(std::size_t{1} << x.size());
+    t[0] = seed;
+    for (std::size_t k = 0; k < x.size(); ++k) {
+        const std::size_t half = std::size_t{1} << k;
+        for (std::size_t b = 0; b < half; ++b) {
+            const U256 hi = F.mul(t[b], x[k]);
+            t[b + half] = hi;
+            t[b] = F.sub(t[b], hi);
+        }
+    }
+    return t;
+}
+
+/// MLE of a table (entries beyond `vals` are zero) at `point`
+U256 mle_host(const HostField& F, const std::vector<U256>& vals, const std::vector<U256>& point) {
+    const std::vector<U256> eq = eq_table_host(F, point, F.one());
+    U256 acc{};
+    for (std::size_t i = 0; i < vals.size() && i < eq.size(); ++i) acc = F.add(acc, F.mul(vals[i], eq[i]));
+    return acc;
+}
+
+/// returns accept; input_claims = registry[0] on acceptance
+bool gkr_verify_host(const dgkr_circuit& c, const HostField& F, const std::uint8_t* proof, std::size_t len,
+                     const std::uint8_t* outputs, std::size_t n_outputs, Transcript& tr,
+                     std::vector<LayerClaim>& input_claims) {
+    ProofReader rd{proof, len, 0, F};
+    const std::uint32_t D = c.depth;
+    const std::uint64_t n_out = c.full_padded[D];
+    if (rd.u32() != n_out || !rd.ok) return false;
+    std::vector<U256> outs(n_out);
+    for (auto& o : outs) o = rd.elem();
+    if (!rd.ok) return false;
+    if (outputs) {  // the statement must match the proof's outputs, padding zero (gkr.hpp:260-268)
+        for (std::uint64_t i = 0; i < n_out; ++i) {
+            const U256 want = i < n_outputs ? F.from_bytes(outputs + i * F.width()) : U256{};
+            if (!(outs[i] == want)) return false;
+        }
+    }
+    if (rd.u32() != D || !rd.ok) return false;
+    for (const auto& o : outs) tr.absorb(o);
+    std::vector<U256> q;
+    for (std::uint32_t k = 0; k < c.padded_log2_full(D); ++k) q.push_back(tr.challenge());
+    std::vector<std::vector<LayerClaim>> registry(D + 1);
+    {
+        LayerClaim lc;
+        lc.layer = D;
+        lc.terms.push_back(ClaimTerm{q, F.one()});
+        lc.value = mle_host(F, outs, q);
+        registry[D].push_back(std::move(lc));
+    }
+    const U256 zero{};
+    for (std::uint32_t layer = D; layer >= 1; --layer) {
+        const auto& C = *c.cons[layer];
+        const std::uint32_t na = rd.u32();
+        std::vector<U256> pa(na);
+        for (auto& a : pa) a = rd.elem();
+        const std::uint32_t sb_len = rd.u32();
+        if (!rd.ok) return false;
+        const std::size_t sb_end = rd.pos + sb_len;
+        if (sb_end > len) return false;
+        std::vector<U256> alphas;
+        LayerClaim combined = combine_claims(std::move(registry[layer]), tr, F, &alphas);
+        registry[layer].clear();
+        if (alphas.size() != pa.size()) return false;
+        for (std::size_t i = 0; i < pa.size(); ++i)
+            if (!(alphas[i] == pa[i])) return false;
+        // SumcheckProof bytes (sumcheck.hpp:51-61)
+        const U256 claimed = rd.elem();
+        const std::uint32_t nr = rd.u32();
+        const std::uint32_t side = C.side;
+        const std::size_t ns = C.slots.size();
+        if (!rd.ok || !(claimed == combined.value) || nr != 2 * side) return false;
+        std::vector<std::array<U256, 4>> rounds(nr);
+        for (auto& r : rounds)
+            for (auto& x : r) x = rd.elem();
+        const std::uint32_t nf = rd.u32();
+        if (!rd.ok || nf != 2 * ns) return false;
+        std::vector<U256> finals(nf);
+        for (auto& x : finals) x = rd.elem();
+        if (!rd.ok || rd.pos != sb_end) return false;
+        // run_round_checks
+        tr.absorb(claimed);
+        U256 claim = claimed;
+        std::vector<U256> point;
+        for (const auto& r : rounds) {
+            if (!(r[3] == zero)) return false;
+            const U256 sum01 = F.add(F.add(r[0], r[0]), F.add(F.add(r[1], r[2]), r[3]));
+            if (!(sum01 == claim)) return false;
+            for (const auto& x : r) tr.absorb(x);
+            const U256 ch = tr.challenge();
+            claim = F.add(r[0], F.mul(ch, F.add(r[1], F.mul(ch, F.add(r[2], F.mul(ch, r[3]))))));
+            point.push_back(ch);
+        }
+        const std::vector<U256> xp(point.begin(), point.begin() + side), yp(point.begin() + side, point.end());
+        // wiring predicate at (combined claim, x, y): gate weights via eq tables of the claim points
+        const std::uint64_t sub_g = c.sub_size[layer], pad_g = c.sub_padded[layer];
+        const std::uint64_t n_gates_full = c.n_copies * pad_g;
+        std::vector<U256> wg(n_gates_full);
+        for (const auto& t : combined.terms) {
+            const std::vector<U256> eq = eq_table_host(F, t.point, t.weight);
+            for (std::uint64_t g = 0; g < n_gates_full && g < eq.size(); ++g) wg[g] = F.add(wg[g], eq[g]);
+        }
+        const std::vector<U256> ex = eq_table_host(F, xp, F.one()), ey = eq_table_host(F, yp, F.one());
+        auto slot_of = [&](std::uint32_t l) {
+            for (std::size_t s2 = 0; s2 < ns; ++s2)
+                if (C.slots[s2] == l) return s2;
+            return ns;
+        };
+        U256 expected{};
+        const std::uint64_t g0 = c.h_lgs[layer - 1];
+        for (std::uint32_t cp = 0; cp < c.n_copies; ++cp) {
+            for (std::uint64_t g = 0; g < sub_g; ++g) {
+                const U256 w = wg[cp * pad_g + g];
+                for (std::uint64_t e = c.h_gns[g0 + g]; e < c.h_gns[g0 + g + 1]; ++e) {
+                    const std::uint32_t* ng = &c.h_nested[5 * e];
+                    const std::size_t sx = slot_of(ng[1]), sy = slot_of(ng[3]);
+                    if (sx >= ns || sy >= ns) return false;
+                    const std::uint64_t xi = static_cast<std::uint64_t>(cp) * c.sub_padded[ng[1]] + ng[2];
+                    const std::uint64_t yi = static_cast<std::uint64_t>(cp) * c.sub_padded[ng[3]] + ng[4];
+                    const U256 t = F.mul(w, F.mul(ex[xi], ey[yi]));
+                    const U256 vx = finals[sx], vy = finals[ns + sy];
+                    expected = F.add(expected, F.mul(t, ng[0] ? F.mul(vx, vy) : F.add(vx, vy)));
+                }
+            }
+        }
+        if (!(expected == claim)) return false;
+        for (std::size_t s2 = 0; s2 < ns; ++s2) {
+            const std::uint32_t src = C.slots[s2];
+            const std::uint32_t native = c.padded_log2_full(src);
+            registry[src].push_back(shrink_claim(src, native, xp, finals[s2], F));
+            registry[src].push_back(shrink_claim(src, native, yp, finals[ns + s2], F));
+        }
+    }
+    if (rd.pos != len) return false;
+    input_claims = std::move(registry[0]);
+    return true;
+}
+
+}  // namespace
+
+int dgkr_gkr_verify(const dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* outputs, std::size_t n_outputs,
+                    const std::uint8_t* inputs, const std::uint8_t* proof, std::size_t len, dgkr_transcript* t,
+                    int* accept) {
+    return guard([&] {
+        const HostField& F = f->f;
+        Transcript tr(&F, t->state, t->draws);
+        std::vector<LayerClaim> claims;
+        bool ok = gkr_verify_host(*c, F, proof, len, outputs, n_outputs, tr, claims);
+        if (ok && inputs) {  // check_input_claims (gkr.hpp:314-325) against the padded input table
+            const std::uint64_t n_in = static_cast<std::uint64_t>(c->n_copies) * c->sub_padded[0];
+            std::vector<U256> tab(n_in);
+            for (std::uint32_t cp = 0; cp < c->n_copies; ++cp)
+                for (std::uint64_t i = 0; i < c->sub_size[0]; ++i)
+                    tab[cp * c->sub_padded[0] + i] =
+                        F.from_bytes(inputs + (static_cast<std::uint64_t>(cp) * c->sub_size[0] + i) * F.width());
+            for (const auto& cl : claims) {
+                U256 acc{};
+                for (const auto& term : cl.terms) acc = F.add(acc, F.mul(term.weight, mle_host(F, tab, term.point)));
+                if (!(acc == cl.value)) ok = false;
+            }
+        }
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        *accept = ok ? 1 : 0;
+    });
+}
+
 int dgkr_circuit_create(dgkr_ctx* ctx, std::uint32_t input_size, std::uint32_t depth, const std::uint64_t* lgs,
                         const std::uint64_t* gns, const std::uint32_t* nested, const std::uint64_t* min_padded,
                         std::uint32_t n_copies, dgkr_circuit** out) {
@@ -2201,10 +2410,79 @@ int dgkr_circuit_create(dgkr_ctx* ctx, std::uint32_t input_size, std::uint32_t d
         c->n_copies = n_copies;
         c->log_copies = log2_exact(n_copies);
         build_circuit(ctx, *c, lgs, gns, nested, min_padded);
+        c->h_lgs.assign(lgs, lgs + depth + 1);
+        c->h_gns.assign(gns, gns + lgs[depth] + 1);
+        c->h_nested.assign(nested, nested + 5 * gns[lgs[depth]]);
+        if (min_padded) c->h_min_padded.assign(min_padded, min_padded + depth + 1);
         *out = c.release();
     });
 }
 void dgkr_circuit_destroy(dgkr_circuit* c) { delete c; }
+
+// Binary CSR circuit file (little-endian):
+//   "DGKRCSR1" | u32 input_size | u32 depth | u32 n_copies | u32 has_min_padded
+//   | u64 n_gates | u64 n_nested | u64 layer_gate_start[depth+1]
+//   | u64 gate_nested_start[n_gates+1] | u32 nested[n_nested][5] | u64 min_padded[depth+1] (if flagged)
+namespace {
+constexpr char kCsrMagic[8] = {'D', 'G', 'K', 'R', 'C', 'S', 'R', '1'};
+}
+
+int dgkr_circuit_save(const dgkr_circuit* c, const char* path) {
+    return guard([&] {
+        std::FILE* fp = std::fopen(path, "wb");
+        if (!fp) fail(DGKR_INVALID_ARGUMENT, std::string("cannot open ") + path);
+        const std::uint32_t hdr[4] = {c->input_size, c->depth, c->n_copies, c->h_min_padded.empty() ? 0u : 1u};
+        const std::uint64_t n_gates = c->h_lgs.back(), n_nested = c->h_gns.back();
+        bool ok = std::fwrite(kCsrMagic, 1, 8, fp) == 8 && std::fwrite(hdr, 4, 4, fp) == 4 &&
+                  std::fwrite(&n_gates, 8, 1, fp) == 1 && std::fwrite(&n_nested, 8, 1, fp) == 1 &&
+                  std::fwrite(c->h_lgs.data(), 8, c->h_lgs.size(), fp) == c->h_lgs.size() &&
+                  std::fwrite(c->h_gns.data(), 8, c->h_gns.size(), fp) == c->h_gns.size() &&
+                  std::fwrite(c->h_nested.data(), 4, c->h_nested.size(), fp) == c->h_nested.size();
+        if (ok && !c->h_min_padded.empty())
+            ok = std::fwrite(c->h_min_padded.data(), 8, c->h_min_padded.size(), fp) == c->h_min_padded.size();
+        ok = (std::fclose(fp) == 0) && ok;
+        if (!ok) fail(DGKR_INVALID_ARGUMENT, std::string("short write to ") + path);
+    });
+}
+
+int dgkr_circuit_load(dgkr_ctx* ctx, const char* path, std::uint32_t n_copies, dgkr_circuit** out) {
+    return guard([&] {
+        std::FILE* fp = std::fopen(path, "rb");
+        if (!fp) fail(DGKR_INVALID_ARGUMENT, std::string("cannot open ") + path);
+        struct Closer {
+            std::FILE* f;
+            ~Closer() { std::fclose(f); }
+        } closer{fp};
+        char magic[8];
+        std::uint32_t hdr[4];
+        std::uint64_t n_gates = 0, n_nested = 0;
+        if (std::fread(magic, 1, 8, fp) != 8 || std::memcmp(magic, kCsrMagic, 8) != 0)
+            fail(DGKR_INVALID_ARGUMENT, "not a DGKRCSR1 circuit file");
+        if (std::fread(hdr, 4, 4, fp) != 4 || std::fread(&n_gates, 8, 1, fp) != 1 || std::fread(&n_nested, 8, 1, fp) != 1)
+            fail(DGKR_INVALID_ARGUMENT, "truncated circuit header");
+        const std::uint32_t depth = hdr[1];
+        if (depth == 0 || depth > (1u << 20) || n_gates > (1ull << 40) || n_nested > (1ull << 40))
+            fail(DGKR_INVALID_ARGUMENT, "implausible circuit header");
+        std::vector<std::uint64_t> lgs(depth + 1), gns(n_gates + 1), minp;
+        std::vector<std::uint32_t> nested(5 * n_nested);
+        if (std::fread(lgs.data(), 8, lgs.size(), fp) != lgs.size() || std::fread(gns.data(), 8, gns.size(), fp) != gns.size() ||
+            std::fread(nested.data(), 4, nested.size(), fp) != nested.size())
+            fail(DGKR_INVALID_ARGUMENT, "truncated circuit body");
+        if (hdr[3]) {
+            minp.resize(depth + 1);
+            if (std::fread(minp.data(), 8, minp.size(), fp) != minp.size()) fail(DGKR_INVALID_ARGUMENT, "truncated min_padded");
+        }
+        if (lgs[0] != 0 || lgs[depth] != n_gates || gns[0] != 0 || gns[n_gates] != n_nested)
+            fail(DGKR_INVALID_ARGUMENT, "inconsistent CSR offsets");
+        for (std::uint32_t l = 0; l < depth; ++l)
+            if (lgs[l + 1] < lgs[l]) fail(DGKR_INVALID_ARGUMENT, "inconsistent CSR offsets");
+        for (std::uint64_t g = 0; g < n_gates; ++g)
+            if (gns[g + 1] < gns[g]) fail(DGKR_INVALID_ARGUMENT, "inconsistent CSR offsets");
+        const int rc = dgkr_circuit_create(ctx, hdr[0], depth, lgs.data(), gns.data(), nested.data(),
+                                           minp.empty() ? nullptr : minp.data(), n_copies ? n_copies : hdr[2], out);
+        if (rc != DGKR_OK) fail(rc, g_err);  // g_err: the create call's message
+    });
+}
 std::size_t dgkr_circuit_output_size(const dgkr_circuit* c) { return c ? c->full_padded[c->depth] : 0; }
 
 int dgkr_circuit_evaluate(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* inputs,

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence, Tuple, Union
 
 import numpy as np
 
-from ._lib import Profile_t, Transcript_t, check, lib
+from ._lib import InvalidArgument, Profile_t, Transcript_t, check, lib
 
 BN254_P = 21888242871839275222246405745257275088548364400416034343698204186575808495617
 GOLDILOCKS_P = 18446744069414584321
@@ -231,6 +231,30 @@ class Circuit:
         self.n_gates = int(lgs[-1]) * self.n_copies
         self.output_size = int(lib().dgkr_circuit_output_size(h))
 
+    def save(self, path: str) -> None:
+        """binary CSR circuit file (dgkr_circuit_save; layout in include/dgkr_b200.h)"""
+        check(lib().dgkr_circuit_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(ctx: Context, path: str, n_copies: int = 0) -> "Circuit":
+        """dgkr_circuit_load: a binary CSR circuit file (n_copies = 0: the file's)"""
+        import struct
+        with open(path, "rb") as fh:
+            head = fh.read(40)
+        if len(head) < 40 or head[:8] != b"DGKRCSR1":
+            raise InvalidArgument(1, f"{path}: not a DGKRCSR1 circuit file")
+        insz, depth, ncp, _, n_gates, _ = struct.unpack("<4I2Q", head[8:40])
+        self = Circuit.__new__(Circuit)
+        self.ctx = ctx
+        self.input_size, self.depth = int(insz), int(depth)
+        self.n_copies = int(n_copies or ncp)
+        h = C.c_void_p()
+        check(lib().dgkr_circuit_load(ctx.handle, str(path).encode(), C.c_uint32(n_copies), C.byref(h)))
+        self._h = h
+        self.n_gates = int(n_gates) * self.n_copies
+        self.output_size = int(lib().dgkr_circuit_output_size(h))
+        return self
+
     @staticmethod
     def from_oracle(ctx: Context, c, n_copies: int = 1) -> "Circuit":
         lgs, gns, nested, minp = c.to_flat()
@@ -271,6 +295,23 @@ def gkr_prove(ctx: Context, circuit: Circuit, inputs: Elems, tr: Transcript, out
     check(lib().dgkr_gkr_prove(ctx.handle, circuit.handle, f.handle, _buf(data), C.byref(tr.t), out_buf,
                                C.c_size_t(cap), C.byref(ln)))
     return out_buf.raw[: ln.value]
+
+
+def gkr_verify(circuit: Circuit, proof: bytes, tr: Transcript, outputs: Optional[Elems] = None,
+               inputs: Optional[Elems] = None) -> bool:
+    """gkr_verify (gkr.hpp:253-311) on the host; with `inputs`, also
+    check_input_claims (:314-325). `outputs`: the claimed output statement."""
+    f = tr.field
+    ob = f.encode(outputs) if outputs is not None else None
+    ib = None
+    if inputs is not None:
+        ib = inputs.tobytes() if isinstance(inputs, np.ndarray) else f.encode(inputs)
+    acc = C.c_int()
+    check(lib().dgkr_gkr_verify(circuit.handle, f.handle, C.c_char_p(ob) if ob is not None else None,
+                                C.c_size_t(len(ob) // f.width if ob is not None else 0),
+                                C.c_char_p(ib) if ib is not None else None, C.c_char_p(bytes(proof)),
+                                C.c_size_t(len(proof)), C.byref(tr.t), C.byref(acc)))
+    return bool(acc.value)
 
 
 def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[Elems]], trs: Sequence[Transcript],
