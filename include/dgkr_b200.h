@@ -302,6 +302,26 @@ int dgkr_distinct_chain_update(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t
                                const uint8_t* items, size_t n, uint8_t* h_out);
 int dgkr_distinct_bitchange(dgkr_ctx* ctx, const dgkr_field* f, size_t count, uint64_t* set_counts);
 
+/* ---- beacon validator tree (beacon.hpp; config C3) ----------------------------------
+ * records: n x 64 bytes, each ValidatorRecord::encode() (pubkey | LE64 index |
+ * active flag | zero pad, beacon.hpp:27-37). SSZ-style tree of `depth` over a
+ * left-aligned active subtree of 2^a leaves (a = ceil log2 n), zero-cache
+ * digests above it (beacon.hpp:96-132).
+ *   dgkr_beacon_root    BeaconTree(validators, depth).root()
+ *                       (DGKR_INVALID_ARGUMENT if a > depth)
+ *   dgkr_beacon_prove   prove_membership(indices[i]) for m indices: leaves m x 32,
+ *                       siblings m x a x 32 (leaf to root), *active_log2 = a
+ *                       (DGKR_OUT_OF_RANGE for an index >= n, beacon.hpp:136-149)
+ *   dgkr_beacon_verify  verify_membership (beacon.hpp:151-174) per path, batched:
+ *                       ok[i] = 1 iff SHA256(record i) = leaf i, the index lies in
+ *                       the active region and the recomputed root equals root */
+int dgkr_beacon_root(dgkr_ctx* ctx, const uint8_t* records, size_t n, unsigned depth, uint8_t* root);
+int dgkr_beacon_prove(dgkr_ctx* ctx, const uint8_t* records, size_t n, unsigned depth, const uint64_t* indices,
+                      size_t m, uint8_t* leaves, uint8_t* siblings, unsigned* active_log2);
+int dgkr_beacon_verify(dgkr_ctx* ctx, const uint8_t* root, const uint8_t* records, const uint8_t* leaves,
+                       const uint8_t* siblings, const uint64_t* indices, size_t m, unsigned depth,
+                       unsigned active_log2, uint8_t* ok);
+
 /* ---- distributed runtime (cluster.hpp), N workers in one call -------------------
  * shard_pairs + dist_sumcheck (cluster.hpp:190-320) on full tables; proof
  * bytes equal the reference's, TrafficStats::to_json().dump() written to

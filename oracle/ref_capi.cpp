@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "dgkr/circuit.hpp"
+#include "dgkr/beacon.hpp"
 #include "dgkr/cluster.hpp"
 #include "dgkr/distinct.hpp"
 #include "dgkr/field.hpp"
@@ -540,6 +541,77 @@ int ref_circuit_json(std::uint32_t input_size, std::uint32_t depth, const std::u
             return static_cast<int>(CAPACITY);
         }
         std::memcpy(out, js.c_str(), js.size() + 1);
+        return static_cast<int>(OK);
+    });
+}
+
+// --- beacon.hpp (config C3); records cross as ValidatorRecord::encode() ---
+namespace {
+std::vector<beacon::ValidatorRecord> decode_records(const std::uint8_t* recs, std::size_t n) {
+    std::vector<beacon::ValidatorRecord> out(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const std::uint8_t* q = recs + 64 * i;
+        std::copy(q, q + 48, out[i].pubkey.begin());
+        std::uint64_t idx = 0;
+        for (int b = 0; b < 8; ++b) idx |= static_cast<std::uint64_t>(q[48 + b]) << (8 * b);
+        out[i].index = idx;
+        out[i].active = q[56] != 0;
+    }
+    return out;
+}
+}  // namespace
+
+int ref_beacon_gen(std::size_t n, std::uint64_t seed, std::uint8_t* recs) {
+    return guard([&] {
+        auto v = beacon::gen_validators(n, seed);
+        for (std::size_t i = 0; i < n; ++i) {
+            auto e = v[i].encode();
+            std::memcpy(recs + 64 * i, e.data(), 64);
+        }
+        return static_cast<int>(OK);
+    });
+}
+
+int ref_beacon_root(const std::uint8_t* recs, std::size_t n, std::size_t depth, std::uint8_t* root) {
+    return guard([&] {
+        auto v = decode_records(recs, n);
+        beacon::BeaconTree t(v, depth);
+        std::memcpy(root, t.root().data(), 32);
+        return static_cast<int>(OK);
+    });
+}
+
+int ref_beacon_prove(const std::uint8_t* recs, std::size_t n, std::size_t depth, std::uint64_t index,
+                     std::uint8_t* leaf, std::uint8_t* siblings, std::size_t* active_log2) {
+    return guard([&] {
+        auto v = decode_records(recs, n);
+        beacon::BeaconTree t(v, depth);
+        auto p = t.prove_membership(index);
+        std::memcpy(leaf, p.leaf.data(), 32);
+        for (std::size_t k = 0; k < p.siblings.size(); ++k) std::memcpy(siblings + 32 * k, p.siblings[k].data(), 32);
+        *active_log2 = p.active_log2;
+        return static_cast<int>(OK);
+    });
+}
+
+int ref_beacon_verify(const std::uint8_t* root, const std::uint8_t* rec, const std::uint8_t* leaf,
+                      const std::uint8_t* siblings, std::size_t active_log2, std::uint64_t index, std::size_t depth,
+                      int* ok) {
+    return guard([&] {
+        auto r = decode_records(rec, 1)[0];
+        beacon::MembershipPath p;
+        std::memcpy(p.leaf.data(), leaf, 32);
+        for (std::size_t k = 0; k < active_log2; ++k) {
+            Digest d;
+            std::memcpy(d.data(), siblings + 32 * k, 32);
+            p.siblings.push_back(d);
+        }
+        p.index = index;
+        p.depth = depth;
+        p.active_log2 = active_log2;
+        Digest rt;
+        std::memcpy(rt.data(), root, 32);
+        *ok = beacon::BeaconTree::verify_membership(rt, r, p) ? 1 : 0;
         return static_cast<int>(OK);
     });
 }

@@ -269,3 +269,33 @@ def circuit_json(circuit: O.Circuit, flat=None) -> str:
     _check(lib().ref_circuit_json(C.c_uint32(circuit.input_size), C.c_uint32(depth), *ptrs[:3], out, C.c_size_t(cap),
                                   C.byref(ln)))
     return out.raw[: ln.value].decode()
+
+
+# --- beacon.hpp (config C3) --------------------------------------------------
+def beacon_gen(n: int, seed: int) -> bytes:
+    out = C.create_string_buffer(64 * n)
+    _check(lib().ref_beacon_gen(C.c_size_t(n), C.c_uint64(seed), out))
+    return out.raw
+
+
+def beacon_root(records: bytes, depth: int) -> bytes:
+    out = C.create_string_buffer(32)
+    _check(lib().ref_beacon_root(_u8(records), C.c_size_t(len(records) // 64), C.c_size_t(depth), out))
+    return out.raw
+
+
+def beacon_prove(records: bytes, depth: int, index: int):
+    leaf = C.create_string_buffer(32)
+    sib = C.create_string_buffer(32 * 64)
+    a = C.c_size_t()
+    _check(lib().ref_beacon_prove(_u8(records), C.c_size_t(len(records) // 64), C.c_size_t(depth), C.c_uint64(index),
+                                  leaf, sib, C.byref(a)))
+    return leaf.raw, sib.raw[: 32 * a.value], a.value
+
+
+def beacon_verify(root: bytes, record: bytes, leaf: bytes, siblings: bytes, active_log2: int, index: int,
+                  depth: int) -> bool:
+    ok = C.c_int()
+    _check(lib().ref_beacon_verify(_u8(root), _u8(record), _u8(leaf), _u8(siblings), C.c_size_t(active_log2),
+                                   C.c_uint64(index), C.c_size_t(depth), C.byref(ok)))
+    return bool(ok.value)

@@ -678,6 +678,129 @@ __global__ void k_merkle_top(std::uint8_t* nodes, std::uint64_t lo) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Beacon validator tree (beacon.hpp, config C3): digests chain as SHA state
+// words (big-endian message words = state words), no byte swaps in between.
+// ---------------------------------------------------------------------------
+/// out = SHA256(l || r) for two digests held as state words (sha256_concat, sha256.hpp:153-158)
+__device__ __forceinline__ void hash_pair_words(const uint32_t l[8], const uint32_t r[8], uint32_t out[8]) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w[i] = l[i];
+        w[8 + i] = r[i];
+    }
+    sha_init(out);
+    sha_rounds(out, nullptr, false, w);
+    sha_rounds(out, c_pad64_wk, true, w);
+}
+
+__device__ __forceinline__ void load_digest_words(const std::uint8_t* src, uint32_t h[8]) {
+    const uint4* q = reinterpret_cast<const uint4*>(src);
+    const uint4 a = q[0], b = q[1];
+    h[0] = bswap32(a.x); h[1] = bswap32(a.y); h[2] = bswap32(a.z); h[3] = bswap32(a.w);
+    h[4] = bswap32(b.x); h[5] = bswap32(b.y); h[6] = bswap32(b.z); h[7] = bswap32(b.w);
+}
+
+/// leaf digest of a 64-byte ValidatorRecord encoding (beacon.hpp:27-42)
+__device__ __forceinline__ void record_digest(const std::uint8_t* rec, uint32_t h[8]) {
+    uint32_t w[16];
+    const uint4* q = reinterpret_cast<const uint4*>(rec);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint4 v = q[i];
+        w[4 * i] = bswap32(v.x);
+        w[4 * i + 1] = bswap32(v.y);
+        w[4 * i + 2] = bswap32(v.z);
+        w[4 * i + 3] = bswap32(v.w);
+    }
+    sha_init(h);
+    sha_rounds(h, nullptr, false, w);
+    sha_rounds(h, c_pad64_wk, true, w);
+}
+
+/// leaves[i] = SHA256(record_i) for i < n, zero-record digest zc0 for n <= i < cap
+__global__ void __launch_bounds__(kThreads) k_beacon_leaves(const std::uint8_t* __restrict__ recs, std::uint64_t n,
+                                                            std::uint64_t cap, const std::uint8_t* __restrict__ zc0,
+                                                            std::uint8_t* __restrict__ leaves) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < cap;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t h[8];
+        if (i < n) record_digest(recs + 64 * i, h);
+        else load_digest_words(zc0, h);
+        store_digest(leaves + 32 * i, h);
+    }
+}
+
+/// BeaconTree::verify_membership (beacon.hpp:151-174) for a batch of paths:
+/// ok[i] = leaf digest matches the record, the index is inside the active
+/// region, and the recomputed root (a siblings, then depth - a zero-cache
+/// digests) equals root.
+__global__ void __launch_bounds__(kThreads) k_beacon_verify(const std::uint8_t* __restrict__ root,
+                                                            const std::uint8_t* __restrict__ recs,
+                                                            const std::uint8_t* __restrict__ leaves,
+                                                            const std::uint8_t* __restrict__ sib,
+                                                            const std::uint64_t* __restrict__ idx, std::uint64_t m,
+                                                            int a, int depth, const std::uint8_t* __restrict__ zc,
+                                                            std::uint8_t* __restrict__ ok) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t h[8], leaf[8];
+        record_digest(recs + 64 * i, h);
+        load_digest_words(leaves + 32 * i, leaf);
+        bool good = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) good &= (h[k] == leaf[k]);
+        std::uint64_t node = idx[i];
+        if (a < 64 && (node >> a) != 0) good = false;
+        if (good) {
+            for (int k = 0; k < a; ++k) {
+                uint32_t s[8], t[8];
+                load_digest_words(sib + (i * a + k) * 32, s);
+                if (node & 1) hash_pair_words(s, h, t);
+                else hash_pair_words(h, s, t);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[j] = t[j];
+                node >>= 1;
+            }
+            for (int k = a; k < depth; ++k) {
+                uint32_t z[8], t[8];
+                load_digest_words(zc + 32 * k, z);
+                hash_pair_words(h, z, t);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[j] = t[j];
+            }
+            uint32_t rt[8];
+            load_digest_words(root, rt);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) good &= (h[k] == rt[k]);
+        }
+        ok[i] = good ? 1 : 0;
+    }
+}
+
+/// siblings of a batch of paths from the active-subtree heap (nodes[2^a + leaf] = leaf)
+__global__ void __launch_bounds__(kThreads) k_beacon_paths(const std::uint8_t* __restrict__ nodes, int a,
+                                                           const std::uint64_t* __restrict__ idx, std::uint64_t m,
+                                                           std::uint8_t* __restrict__ leaves,
+                                                           std::uint8_t* __restrict__ sib) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        std::uint64_t node = (std::uint64_t{1} << a) + idx[i];
+        const uint4* src = reinterpret_cast<const uint4*>(nodes + 32 * node);
+        uint4* dl = reinterpret_cast<uint4*>(leaves + 32 * i);
+        dl[0] = src[0];
+        dl[1] = src[1];
+        for (int k = 0; k < a; ++k) {
+            const uint4* s = reinterpret_cast<const uint4*>(nodes + 32 * (node ^ 1));
+            uint4* d = reinterpret_cast<uint4*>(sib + (i * a + k) * 32);
+            d[0] = s[0];
+            d[1] = s[1];
+            node >>= 1;
+        }
+    }
+}
+
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_beta_combine(const Fe* __restrict__ rows, std::uint64_t cols, int M,
                                                            const Fe* __restrict__ beta, Fe* __restrict__ out) {
@@ -1265,6 +1388,35 @@ void launch_bitchange(FieldKind k, std::uint64_t first, std::uint64_t n, int bit
     const int g = grid_for(n, kThreads, 148 * 8);
     DISPATCH_FIELD(k, F, (k_bitchange<F><<<g, kThreads, 0, st>>>(first, n, bits, o, counts)));
     check_launch("bitchange");
+}
+
+void launch_beacon_leaves(const std::uint8_t* recs, std::uint64_t n, std::uint64_t cap, const std::uint8_t* zc0,
+                          std::uint8_t* leaves, cudaStream_t st) {
+    if (cap == 0) return;
+    ensure_pad_table();
+    const int g = grid_for(cap, kThreads, 148 * 16);
+    k_beacon_leaves<<<g, kThreads, 0, st>>>(recs, n, cap, zc0, leaves);
+    check_launch("beacon_leaves");
+}
+
+void launch_beacon_verify(const std::uint8_t* root, const std::uint8_t* recs, const std::uint8_t* leaves,
+                          const std::uint8_t* sib, const std::uint64_t* idx, std::uint64_t m, int a, int depth,
+                          const std::uint8_t* zc, std::uint8_t* ok, cudaStream_t st) {
+    if (m == 0) return;
+    ensure_pad_table();
+    // one path per thread; small CTAs so short batches still spread over the SMs
+    const int threads = 64;
+    const int g = static_cast<int>(std::min<std::uint64_t>((m + threads - 1) / threads, 148 * 32));
+    k_beacon_verify<<<g, threads, 0, st>>>(root, recs, leaves, sib, idx, m, a, depth, zc, ok);
+    check_launch("beacon_verify");
+}
+
+void launch_beacon_paths(const std::uint8_t* nodes, int a, const std::uint64_t* idx, std::uint64_t m,
+                         std::uint8_t* leaves, std::uint8_t* sib, cudaStream_t st) {
+    if (m == 0) return;
+    const int g = grid_for(m, kThreads, 148 * 16);
+    k_beacon_paths<<<g, kThreads, 0, st>>>(nodes, a, idx, m, leaves, sib);
+    check_launch("beacon_paths");
 }
 
 }  // namespace dgkr_b200

@@ -192,4 +192,16 @@ void launch_bound_check(const std::uint8_t* canon, int width, std::uint64_t n, s
 void launch_bitchange(FieldKind k, std::uint64_t first, std::uint64_t n, int bits, const void* off,
                       unsigned long long* counts, cudaStream_t st);
 
+// ---- beacon validator tree (beacon.hpp, config C3) -------------------------
+/// leaves[i] = SHA256(64-byte record i) for i < n, the zero-leaf digest zc0 up to cap
+void launch_beacon_leaves(const std::uint8_t* recs, std::uint64_t n, std::uint64_t cap, const std::uint8_t* zc0,
+                          std::uint8_t* leaves, cudaStream_t st);
+/// batched BeaconTree::verify_membership; siblings m x a x 32, zc = zero cache (depth+1 digests)
+void launch_beacon_verify(const std::uint8_t* root, const std::uint8_t* recs, const std::uint8_t* leaves,
+                          const std::uint8_t* sib, const std::uint64_t* idx, std::uint64_t m, int a, int depth,
+                          const std::uint8_t* zc, std::uint8_t* ok, cudaStream_t st);
+/// membership paths (leaf + a siblings) out of the active-subtree heap
+void launch_beacon_paths(const std::uint8_t* nodes, int a, const std::uint64_t* idx, std::uint64_t m,
+                         std::uint8_t* leaves, std::uint8_t* sib, cudaStream_t st);
+
 }  // namespace dgkr_b200

@@ -165,6 +165,8 @@ struct NttWs {
     std::vector<std::unique_ptr<DBuf<Fe>>> layer;
     std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree;
     DBuf<std::uint64_t> didx;
+    // beacon tree (config C3)
+    DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
 };
 
 struct Lane {
@@ -2758,6 +2760,142 @@ int dgkr_distinct_bitchange(dgkr_ctx* ctx, const dgkr_field* f, std::size_t coun
         ctx->d2h(h.data(), d.p, bits * sizeof(unsigned long long));
         ctx->sync();
         for (int k = 0; k < bits; ++k) set_counts[k] = h[k];
+        ctx->end_call();
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Beacon validator tree (beacon.hpp; config C3): root, membership paths and
+// batched verify_membership on the device. Records cross as their 64-byte
+// ValidatorRecord::encode() (beacon.hpp:27-37).
+// ---------------------------------------------------------------------------
+namespace {
+
+/// zero_cache (beacon.hpp:66-83): z_0 = H(64 zero bytes), z_k = H(z_{k-1} || z_{k-1})
+std::vector<Digest> zero_cache_host(unsigned depth) {
+    std::vector<Digest> z;
+    std::uint8_t zero[64] = {};
+    z.push_back(sha256(zero, 64));
+    for (unsigned k = 1; k <= depth; ++k) {
+        std::uint8_t buf[64];
+        std::memcpy(buf, z.back().data(), 32);
+        std::memcpy(buf + 32, z.back().data(), 32);
+        z.push_back(sha256(buf, 64));
+    }
+    return z;
+}
+
+unsigned active_log2_of(std::uint64_t n) {
+    unsigned a = 0;
+    while ((std::uint64_t{1} << a) < n) ++a;
+    return a;
+}
+
+/// builds the active-subtree heap in ws.b_nodes (leaves at [2^a, 2^(a+1))); returns a
+unsigned beacon_build(Lane* ctx, NttWs& ws, const std::uint8_t* records, std::uint64_t n, unsigned depth,
+                      const std::vector<Digest>& zc) {
+    const unsigned a = active_log2_of(n);
+    if (a > depth) fail(DGKR_INVALID_ARGUMENT, "validator set exceeds tree capacity");  // beacon.hpp:113-115
+    const std::uint64_t cap = std::uint64_t{1} << a;
+    ws.b_recs.ensure(std::max<std::uint64_t>(n, 1) * 64);
+    if (n) ctx->h2d(ws.b_recs.p, records, n * 64);
+    ws.b_zc.ensure((depth + 1) * 32);
+    ctx->h2d(ws.b_zc.p, zc.data(), (depth + 1) * 32);
+    ws.b_nodes.ensure(2 * cap * 32);
+    ctx->tbeg();
+    launch_beacon_leaves(ws.b_recs.p, n, cap, ws.b_zc.p, ws.b_nodes.p + cap * 32, ctx->st);
+    launch_merkle(ws.b_nodes.p, cap, ctx->st);
+    ctx->tend(ctx->prof.merkle_ms);
+    ctx->launched(2);
+    return a;
+}
+
+}  // namespace
+
+int dgkr_beacon_root(dgkr_ctx* ctx, const std::uint8_t* records, std::size_t n, unsigned depth, std::uint8_t* root) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        const auto zc = zero_cache_host(depth);
+        NttWs& ws = ctx->nttws();
+        const unsigned a = beacon_build(ctx, ws, records, n, depth, zc);
+        Digest h;
+        ctx->d2h(h.data(), ws.b_nodes.p + 32, 32);
+        ctx->sync();
+        for (unsigned k = a; k < depth; ++k) {  // left spine (beacon.hpp:128-131)
+            std::uint8_t buf[64];
+            std::memcpy(buf, h.data(), 32);
+            std::memcpy(buf + 32, zc[k].data(), 32);
+            h = sha256(buf, 64);
+        }
+        std::memcpy(root, h.data(), 32);
+        ctx->end_call();
+    });
+}
+
+int dgkr_beacon_prove(dgkr_ctx* ctx, const std::uint8_t* records, std::size_t n, unsigned depth,
+                      const std::uint64_t* indices, std::size_t m, std::uint8_t* leaves, std::uint8_t* siblings,
+                      unsigned* active_log2) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        for (std::size_t i = 0; i < m; ++i)
+            if (indices[i] >= n) fail(DGKR_OUT_OF_RANGE, "inactive validator index");  // beacon.hpp:138-140
+        const auto zc = zero_cache_host(depth);
+        NttWs& ws = ctx->nttws();
+        const unsigned a = beacon_build(ctx, ws, records, n, depth, zc);
+        ws.didx.ensure(std::max<std::size_t>(m, 1));
+        ws.b_leaves.ensure(std::max<std::size_t>(m, 1) * 32);
+        ws.b_sib.ensure(std::max<std::size_t>(m * a, 1) * 32);
+        if (m) {
+            ctx->h2d(ws.didx.p, indices, m * 8);
+            launch_beacon_paths(ws.b_nodes.p, static_cast<int>(a), ws.didx.p, m, ws.b_leaves.p, ws.b_sib.p, ctx->st);
+            ctx->launched();
+            ctx->d2h(leaves, ws.b_leaves.p, m * 32);
+            if (a) ctx->d2h(siblings, ws.b_sib.p, m * a * 32);
+        }
+        ctx->sync();
+        *active_log2 = a;
+        ctx->end_call();
+    });
+}
+
+int dgkr_beacon_verify(dgkr_ctx* ctx, const std::uint8_t* root, const std::uint8_t* records, const std::uint8_t* leaves,
+                       const std::uint8_t* siblings, const std::uint64_t* indices, std::size_t m, unsigned depth,
+                       unsigned active_log2, std::uint8_t* ok) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (active_log2 > 64) fail(DGKR_INVALID_ARGUMENT, "active_log2 out of range");
+        if (m == 0) {
+            ctx->end_call();
+            return;
+        }
+        NttWs& ws = ctx->nttws();
+        const unsigned a = active_log2;
+        // paths claiming a > depth have no zero-cache tail; verify_membership walks a siblings then none
+        const unsigned zdepth = std::max(depth, a);
+        const auto zc = zero_cache_host(zdepth);
+        ws.b_root.ensure(32);
+        ws.b_recs.ensure(m * 64);
+        ws.b_leaves.ensure(m * 32);
+        ws.b_sib.ensure(std::max<std::size_t>(m * a, 1) * 32);
+        ws.didx.ensure(m);
+        ws.b_zc.ensure((zdepth + 1) * 32);
+        ws.b_ok.ensure(m);
+        ctx->h2d(ws.b_root.p, root, 32);
+        ctx->h2d(ws.b_recs.p, records, m * 64);
+        ctx->h2d(ws.b_leaves.p, leaves, m * 32);
+        if (a) ctx->h2d(ws.b_sib.p, siblings, m * a * 32);
+        ctx->h2d(ws.didx.p, indices, m * 8);
+        ctx->h2d(ws.b_zc.p, zc.data(), (zdepth + 1) * 32);
+        ctx->tbeg();
+        launch_beacon_verify(ws.b_root.p, ws.b_recs.p, ws.b_leaves.p, ws.b_sib.p, ws.didx.p, m, static_cast<int>(a),
+                             static_cast<int>(depth), ws.b_zc.p, ws.b_ok.p, ctx->st);
+        ctx->tend(ctx->prof.merkle_ms);
+        ctx->launched();
+        ctx->d2h(ok, ws.b_ok.p, m);
+        ctx->sync();
         ctx->end_call();
     });
 }

@@ -586,3 +586,47 @@ def bitchange_experiment(ctx: Context, field: Field, count: int) -> Tuple[List[i
 def bitchange_csv(probabilities: Sequence[float]) -> str:
     """BitChangeResult::to_csv (distinct.hpp:98-106)"""
     return "index,bit_change\n" + "".join(f"{i},{p:g}\n" for i, p in enumerate(probabilities))
+
+
+# ---------------------------------------------------------------------------
+# beacon.hpp (config C3): validator tree root, membership paths, batched verify
+# ---------------------------------------------------------------------------
+def _u64_arr(vals) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(vals, dtype=np.uint64))
+
+
+def beacon_root(ctx: Context, records: bytes, depth: int) -> bytes:
+    """BeaconTree(validators, depth).root() (beacon.hpp:102-132); records =
+    n x 64-byte ValidatorRecord::encode()"""
+    out = C.create_string_buffer(32)
+    check(lib().dgkr_beacon_root(ctx.handle, C.c_char_p(bytes(records)), C.c_size_t(len(records) // 64),
+                                 C.c_uint(depth), out))
+    return out.raw
+
+
+def beacon_prove(ctx: Context, records: bytes, depth: int, indices) -> Tuple[bytes, bytes, int]:
+    """prove_membership for each index (beacon.hpp:136-149) -> (leaves m x 32,
+    siblings m x a x 32, a)"""
+    idx = _u64_arr(indices)
+    m = len(idx)
+    n = len(records) // 64
+    a_max = max(1, (max(n, 1) - 1).bit_length())
+    leaves = C.create_string_buffer(32 * max(m, 1))
+    sib = C.create_string_buffer(32 * max(m * a_max, 1))
+    a = C.c_uint()
+    check(lib().dgkr_beacon_prove(ctx.handle, C.c_char_p(bytes(records)), C.c_size_t(n), C.c_uint(depth),
+                                  idx.ctypes.data_as(C.c_void_p), C.c_size_t(m), leaves, sib, C.byref(a)))
+    return leaves.raw[: 32 * m], sib.raw[: 32 * m * a.value], a.value
+
+
+def beacon_verify(ctx: Context, root: bytes, records: bytes, leaves: bytes, siblings: bytes, indices, depth: int,
+                  active_log2: int) -> np.ndarray:
+    """batched BeaconTree::verify_membership (beacon.hpp:151-174) -> uint8 ok per path"""
+    idx = _u64_arr(indices)
+    m = len(idx)
+    ok = np.zeros(max(m, 1), dtype=np.uint8)
+    check(lib().dgkr_beacon_verify(ctx.handle, C.c_char_p(bytes(root)), C.c_char_p(bytes(records)),
+                                   C.c_char_p(bytes(leaves)), C.c_char_p(bytes(siblings)),
+                                   idx.ctypes.data_as(C.c_void_p), C.c_size_t(m), C.c_uint(depth),
+                                   C.c_uint(active_log2), ok.ctypes.data_as(C.c_void_p)))
+    return ok[:m]

@@ -36,7 +36,7 @@ def main():
     rng = np.random.default_rng(20240410)
     out = {"source": "oracle/_ref/libdgkr_ref.so (unmodified /root/reference/proj/include via oracle/shim)",
            "transcript": [], "product_sum": [], "layer_sum": [], "gkr": [], "pcs": [], "dist_sumcheck": [],
-           "distpc": [], "distinct": []}
+           "distpc": [], "distinct": [], "beacon": []}
     for name, p in FIELDS.items():
         fld = O.Field(p)
         el = O.random_elements(fld, 6, rng)
@@ -110,6 +110,23 @@ def main():
         if p > 1 << 20:
             case["bitchange_10000"] = R.distinct_bitchange(fld, 10000)
         out["distinct"].append(case)
+    # beacon.hpp (C3): roots, membership paths and verdicts of the reference tree
+    here = os.path.dirname(os.path.abspath(__file__))
+    for n, depth, seed in ((1, 4, 1), (10, 8, 2), (37, 12, 3), (4096, 56, 4)):
+        recs = R.beacon_gen(n, seed)
+        idx = sorted({0, n - 1, n // 2, (7 * n) // 9})
+        paths = []
+        for i in idx:
+            leaf, sib, a = R.beacon_prove(recs, depth, i)
+            paths.append({"index": i, "leaf": leaf.hex(), "siblings": sib.hex(), "active_log2": a})
+        case = {"n": n, "depth": depth, "seed": seed, "root": R.beacon_root(recs, depth).hex(), "paths": paths}
+        if n <= 64:
+            case["records"] = recs.hex()
+        else:
+            case["records_file"] = f"beacon_{n}.bin"
+            with open(os.path.join(here, case["records_file"]), "wb") as fh:
+                fh.write(recs)
+        out["beacon"].append(case)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as fh:
         json.dump(out, fh, separators=(",", ":"))
