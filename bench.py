@@ -349,7 +349,7 @@ def run_b200(args, cfg_name):
     round_s = prof["round_ms"] * 1e-3
     achieved_gbs = prof["round_bytes"] / round_s / 1e9 if round_s > 0 else None
     achieved_mps = prof["round_mults"] / round_s if round_s > 0 else None
-    traffic = load_ncu_traffic()
+    traffic, traffic_ratio = load_ncu_traffic()
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -383,7 +383,7 @@ def run_b200(args, cfg_name):
             "note": "kernel times from one profiled single proof (per-launch CUDA events)"},
         "roofline": {"bound": "hbm", "kernel": "k_round (fused fold+round)", "achieved": achieved_gbs,
                      "peak": peak_gbs, "unit": "GB/s", "frac": (achieved_gbs / peak_gbs) if achieved_gbs else None,
-                     "traffic": traffic, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_over_algorithmic": traffic_ratio, "peak_source": peak_src,
                      "note": "algorithmic bytes: fold reads 4 + writes 2 elements (32 B) per table per output pair"},
         "roofline_int": {"bound": "imad", "kernel": "k_round (fused fold+round)",
                          "achieved": achieved_mps, "peak": mp.value, "unit": "BN254 mont-mul/s",
@@ -400,12 +400,14 @@ def run_b200(args, cfg_name):
 
 
 def load_ncu_traffic():
-    """dram bytes per launch of k_round from the committed ncu capture, if any."""
+    """(dram bytes per launch, dram / algorithmic bytes of the same launches)
+    of k_round from the committed ncu capture (profiles/ncu_round_traffic.json)"""
     path = os.path.join(ROOT, "profiles", "ncu_round_traffic.json")
     try:
-        return json.load(open(path)).get("dram_bytes_per_launch")
+        t = json.load(open(path))
+        return t.get("dram_bytes_per_launch"), t.get("dram_over_algorithmic")
     except Exception:
-        return None
+        return None, None
 
 
 def main():
