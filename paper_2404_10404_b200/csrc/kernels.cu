@@ -360,8 +360,9 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep1_sorted(BookkeepLaunch a)
         const std::uint32_t j = static_cast<std::uint32_t>(t & smask);
         const std::uint64_t x = (c << sd.log_stride) | a.perm[j];
         const uint2 sg = a.seg[j];
+        const std::uint32_t n_e = sg.y > a.heavy_min ? 0u : sg.y;
         Fe h = fe_zero(), gacc = fe_zero();
-        for (std::uint32_t e = sg.x; e < sg.x + sg.y; ++e) {
+        for (std::uint32_t e = sg.x; e < sg.x + n_e; ++e) {
             const uint4 en = sd.ent[e];
             const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
             const Fe vy = fe_load_nc(sd.V + ((c << sd.log_stride) | en.y));
@@ -387,8 +388,9 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(const __grid_cons
         const std::uint32_t j = static_cast<std::uint32_t>(t & smask);
         const std::uint64_t y = (c << sd.log_stride) | a.perm[j];
         const uint2 sg = a.seg[j];
+        const std::uint32_t n_e = sg.y > a.heavy_min ? 0u : sg.y;
         Fe ma = fe_zero(), cacc = fe_zero();
-        for (std::uint32_t e = sg.x; e < sg.x + sg.y; ++e) {
+        for (std::uint32_t e = sg.x; e < sg.x + n_e; ++e) {
             const uint4 en = sd.ent[e];
             const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
             const Fe eu = fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y));
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) 
             const std::uint32_t xl = static_cast<std::uint32_t>(x & ((std::uint64_t{1} << sd.log_stride) - 1));
             Fe h = fe_zero();
             if (c < a.n_copies) {
-                const std::uint32_t e0 = sd.off[xl], e1 = sd.off[xl + 1];
+                const std::uint32_t e0 = sd.off[xl], e1 = (sd.off[xl + 1] - sd.off[xl] > a.heavy_min) ? e0 : sd.off[xl + 1];
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
             const std::uint32_t yl = static_cast<std::uint32_t>(y & ((std::uint64_t{1} << sd.log_stride) - 1));
             Fe ma = fe_zero();
             if (c < a.n_copies) {
-                const std::uint32_t e0 = sd.off[yl], e1 = sd.off[yl + 1];
+                const std::uint32_t e0 = sd.off[yl], e1 = (sd.off[yl + 1] - sd.off[yl] > a.heavy_min) ? e0 : sd.off[yl + 1];
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
@@ -468,6 +470,70 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
         }
         fe_store(a.G + y, cacc);
     }
+}
+
+// Heavy rows: one CTA per item {slot, copy, local row}; the CTA's threads
+// stride over the row's entries and block-reduce (H_m, G) / (MA_m, C) into
+// per-item partials; k_bookkeep_merge then adds them to the tables.
+constexpr int kHeavyThreads = 128;
+
+template <class F>
+__device__ __forceinline__ Fe bk_weight(const BookkeepLaunch& a, std::uint64_t c, const uint4& en) {
+    const std::uint64_t g = (c << a.log_gcons) | en.x;
+    return a.wire_w ? fe_load_nc(a.wire_w + en.w) : a.gate_w ? fe_load_nc(a.gate_w + g) : split_eq<F>(a.w, g);
+}
+
+template <class F, int PHASE>
+__global__ void __launch_bounds__(kHeavyThreads) k_bookkeep_heavy(const __grid_constant__ BookkeepLaunch a) {
+    __shared__ Fe sh[32][2];
+    const uint4 it = a.heavy[blockIdx.x];
+    const SlotDesc sd = a.slots[it.x];
+    const std::uint64_t c = it.y;
+    const std::uint32_t e0 = sd.off[it.z], e1 = sd.off[it.z + 1];
+    Fe s[2] = {fe_zero(), fe_zero()};
+    for (std::uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const uint4 en = sd.ent[e];
+        const Fe w = bk_weight<F>(a, c, en);
+        const std::uint32_t os = en.z & 0x7fffffffu;
+        const bool mul = en.z >> 31;
+        if (PHASE == 1) {  // sumcheck.hpp:368-391: mul H += w V[y]; add H += w, G += w V[y]
+            const SlotDesc sy = a.slots[os];
+            const Fe prod = fe_mul<F>(w, fe_load_nc(sy.V + ((c << sy.log_stride) | en.y)));
+            s[0] = fe_add<F>(s[0], fe_select<F>(mul, prod, w));
+            s[1] = fe_select<F>(mul, s[1], fe_add<F>(s[1], prod));
+        } else {  // sumcheck.hpp:407-431: cx = w chi_x(u); mul MA += cx V(u); add MA += cx, C += cx V(u)
+            const std::uint64_t x = (c << a.slots[os].log_stride) | en.y;
+            const Fe cx = fe_mul<F>(w, a.eq_u ? fe_load_nc(a.eq_u + x) : split_eq<F>(a.u, x));
+            const Fe prod = fe_mul<F>(cx, fe_load(a.vx + os));
+            s[0] = fe_add<F>(s[0], fe_select<F>(mul, prod, cx));
+            s[1] = fe_select<F>(mul, s[1], fe_add<F>(s[1], prod));
+        }
+    }
+    block_sum<F, 2>(s, sh);
+    if (threadIdx.x == 0) {
+        fe_store(a.heavy_h + blockIdx.x, s[0]);
+        fe_store(a.heavy_g + blockIdx.x, s[1]);
+    }
+}
+
+__device__ __forceinline__ std::uint64_t heavy_row(const BookkeepLaunch& a, const uint4& it) {
+    return (static_cast<std::uint64_t>(it.y) << a.slots[it.x].log_stride) | it.z;
+}
+
+/// out_m[row] += H partial (unique per item); G[row] += sum of the partials of
+/// every item on that row (items are sorted by row: the first of a run sums it)
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_bookkeep_merge(const __grid_constant__ BookkeepLaunch a) {
+    const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_heavy) return;
+    const uint4 it = a.heavy[i];
+    const std::uint64_t r = heavy_row(a, it);
+    Fe* o = a.slots[it.x].out + r;
+    fe_store(o, fe_add<F>(fe_load(o), fe_load(a.heavy_h + i)));
+    if (i > 0 && heavy_row(a, a.heavy[i - 1]) == r) return;
+    Fe acc = fe_load(a.G + r);
+    for (std::uint32_t j = i; j < a.n_heavy && heavy_row(a, a.heavy[j]) == r; ++j) acc = fe_add<F>(acc, fe_load(a.heavy_g + j));
+    fe_store(a.G + r, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -1222,6 +1288,14 @@ void launch_eq_build(FieldKind k, const EqJob* jobs, int n_jobs, cudaStream_t st
     check_launch("eq_build");
 }
 
+void launch_bookkeep_heavy(FieldKind k, const BookkeepLaunch& a, int phase, cudaStream_t st) {
+    if (a.n_heavy == 0) return;
+    if (phase == 1) DISPATCH_FIELD(k, F, (k_bookkeep_heavy<F, 1><<<a.n_heavy, kHeavyThreads, 0, st>>>(a)));
+    else DISPATCH_FIELD(k, F, (k_bookkeep_heavy<F, 2><<<a.n_heavy, kHeavyThreads, 0, st>>>(a)));
+    DISPATCH_FIELD(k, F, (k_bookkeep_merge<F><<<(a.n_heavy + kThreads - 1) / kThreads, kThreads, 0, st>>>(a)));
+    check_launch("bookkeep_heavy");
+}
+
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
     if (a.perm && a.n_slots == 1 && a.gate_w) {
@@ -1230,6 +1304,7 @@ void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t s
         DISPATCH_FIELD(k, F, (k_bookkeep_phase1<F><<<g, kThreads, 0, st>>>(a)));
     }
     check_launch("bookkeep_phase1");
+    launch_bookkeep_heavy(k, a, 1, st);
 }
 
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
@@ -1242,6 +1317,7 @@ void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t s
         DISPATCH_FIELD(k, F, (k_bookkeep_phase2<F><<<g, kThreads, 0, st>>>(a)));
     }
     check_launch("bookkeep_phase2");
+    launch_bookkeep_heavy(k, a, 2, st);
 }
 
 void launch_evaluate(FieldKind k, const EvalLaunch& a, cudaStream_t st) {

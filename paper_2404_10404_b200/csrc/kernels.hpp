@@ -126,6 +126,16 @@ struct BookkeepLaunch {
     // degree-sorted order so the 32 rows of a warp have equal length.
     const std::uint32_t* perm = nullptr;  // [2^log_stride] row (x or y local index) per position
     const uint2* seg = nullptr;           // [2^log_stride] (entry start, entry count) per position
+    // Heavy rows (power-law degrees: constant wires, padding gates): CSR rows
+    // with more than heavy_min entries are skipped by the one-thread-per-row
+    // kernels and reduced by one CTA per (slot, copy, row) item instead;
+    // items {slot, copy, local row, 0} sorted by the global row index, so the
+    // merge adds partials to G without races.
+    const uint4* heavy = nullptr;
+    std::uint32_t n_heavy = 0;
+    std::uint32_t heavy_min = 0xffffffffu;
+    Fe* heavy_h = nullptr;  // scratch [n_heavy] per-item H_m / MA_m partials
+    Fe* heavy_g = nullptr;  // scratch [n_heavy] per-item G / C partials
 };
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);

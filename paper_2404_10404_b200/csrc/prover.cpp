@@ -863,6 +863,7 @@ struct CircuitWs {
     DBuf<const Fe*> d_layer_vals;
     DBuf<Fe> H, G;      // bookkeeping outputs, max_slots x Tmax and Tmax
     DBuf<Fe> Wg, EqU;   // dense per-gate weights and chi(u) tables
+    DBuf<Fe> heavy_scr; // heavy-row partials: 2 x max_heavy
     RoundBuffers rb;
     DBuf<std::uint8_t> stage;
     DBuf<Fe> eq_tabs;   // split-eq tables for weights and u
@@ -896,10 +897,13 @@ struct dgkr_circuit {
         DBuf<uint4> nested;
         DBuf<std::uint32_t> xperm, yperm;  // single-slot: degree-sorted rows
         DBuf<uint2> xseg, yseg;
+        DBuf<uint4> xheavy, yheavy;        // heavy-row items {slot, copy, row, 0}, sorted by table row
+        std::uint32_t n_xheavy = 0, n_yheavy = 0;
     };
     std::vector<std::unique_ptr<Consumer>> cons;  // index li (0 unused)
     DBuf<std::uint32_t> d_layer_log;
     std::uint32_t max_slots = 0;
+    std::uint32_t max_heavy = 0;  // largest heavy-row item list of any consumer / phase
     std::uint64_t Tmax = 1;
     std::uint64_t total_gates = 0;  // full circuit gate count
     std::mutex ws_mu;
@@ -912,6 +916,9 @@ struct dgkr_circuit {
 };
 
 namespace {
+
+/// CSR rows with more entries than this are reduced by a CTA, not a thread
+constexpr std::uint32_t kHeavyMin = 64;
 
 /// GeneralCircuit::validate (circuit.hpp:103-152) on the sub-circuit plus
 /// the data-parallel preconditions; builds all device-side structures.
@@ -1044,6 +1051,33 @@ void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const s
                 yent[yfill[ybase[ys] + e[4]]++] = make_uint4(gl, e[2], static_cast<std::uint32_t>(xs) | mul, wid);
             }
         }
+        // heavy rows (degree > kHeavyMin, e.g. constant wires and padding
+        // gates): one CTA per (slot, copy, row) instead of one thread
+        auto heavy_items = [&](const std::vector<std::uint32_t>& off, DBuf<uint4>& dst) -> std::uint32_t {
+            std::vector<std::pair<std::uint64_t, uint4>> items;
+            for (std::size_t s2 = 0; s2 < ns; ++s2) {
+                const std::uint32_t src = C.slots[s2];
+                for (std::uint64_t xl = 0; xl < c.sub_padded[src]; ++xl) {
+                    if (off[xbase[s2] + xl + 1] - off[xbase[s2] + xl] <= kHeavyMin) continue;
+                    for (std::uint32_t cp = 0; cp < c.n_copies; ++cp)
+                        items.push_back({(static_cast<std::uint64_t>(cp) << c.sub_log[src]) | xl,
+                                         make_uint4(static_cast<std::uint32_t>(s2), cp, static_cast<std::uint32_t>(xl), 0)});
+                }
+            }
+            std::stable_sort(items.begin(), items.end(),
+                             [](const auto& a, const auto& b) { return a.first < b.first; });
+            if (items.size() > 0x7fffffffu) fail(DGKR_UNSUPPORTED, "too many heavy rows");
+            std::vector<uint4> v(items.size());
+            for (std::size_t i = 0; i < items.size(); ++i) v[i] = items[i].second;
+            if (!v.empty()) {
+                dst.ensure(v.size());
+                CK(cudaMemcpy(dst.p, v.data(), v.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+            }
+            c.max_heavy = std::max<std::uint32_t>(c.max_heavy, static_cast<std::uint32_t>(v.size()));
+            return static_cast<std::uint32_t>(v.size());
+        };
+        C.n_xheavy = heavy_items(xoff, C.xheavy);
+        C.n_yheavy = heavy_items(yoff, C.yheavy);
         if (ns == 1) {
             // degree-sorted row order for the single-slot bookkeeping kernels
             const std::uint64_t S = c.sub_padded[C.slots[0]];
@@ -1126,6 +1160,7 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
         W.Wg.ensure(gmax);
         W.EqU.ensure(c.Tmax);
         W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
+        W.heavy_scr.ensure(2 * static_cast<std::size_t>(std::max<std::uint32_t>(c.max_heavy, 1)));
     }
     W.cons.resize(D + 1);
     for (std::uint32_t li = 1; li <= D; ++li) {
@@ -1435,6 +1470,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.gate_w = W.Wg.p;
         bk.perm = C.xperm.p;
         bk.seg = C.xseg.p;
+        bk.heavy_min = kHeavyMin;
+        bk.heavy_h = W.heavy_scr.p;
+        bk.heavy_g = W.heavy_scr.p + std::max<std::uint32_t>(c.max_heavy, 1);
+        bk.heavy = C.xheavy.p;
+        bk.n_heavy = C.n_xheavy;
         launch_bookkeep_phase1(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -1471,6 +1511,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.eq_u = W.EqU.p;
         bk.perm = C.yperm.p;
         bk.seg = C.yseg.p;
+        bk.heavy = C.yheavy.p;
+        bk.n_heavy = C.n_yheavy;
         launch_bookkeep_phase2(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {

@@ -277,3 +277,47 @@ def test_distpc_matches_oracle(ctx, N):
     roots2, ops2, comb2 = O.distpc(of, rows, r, 4, ts)
     assert roots == roots2 and ops == ops2 and comb == comb2
     assert js == ts.to_json()
+
+
+@pytest.mark.parametrize("n_copies", [1, 4])
+@pytest.mark.parametrize("multi_slot", [False, True])
+def test_gkr_heavy_rows(ctx, n_copies, multi_slot):
+    """CSR rows with more than 64 entries (constant wires / padding gates)
+    take the CTA-per-row bookkeeping path; proofs must not change."""
+    p = O.BN254_P
+    f, of = P.Field(p), O.Field(p)
+    rng = np.random.default_rng(31 + n_copies + 2 * multi_slot)
+    w, insz = 256, 256
+    layers = []
+    for li in range(1, 4):
+        gates = []
+        for g in range(w):
+            src = li - 1
+            if g < 192:      # heavy x row: input 0 of the previous layer
+                ng = [(int(rng.integers(0, 2)), src, 0, src, int(rng.integers(0, w)))]
+            elif g < 224:    # heavy y row: gate 7 of the previous layer
+                ng = [(int(rng.integers(0, 2)), src, int(rng.integers(0, w)), src, 7)]
+            else:
+                ng = [(int(rng.integers(0, 2)), src, int(rng.integers(0, w)), src, int(rng.integers(0, w)))]
+            if multi_slot and li >= 2:  # second slot: the input layer, also heavy on x
+                ng.append((int(rng.integers(0, 2)), 0, 3, li - 1, int(rng.integers(0, w))))
+            gates.append(ng)
+        layers.append(gates)
+    lgs, gns, rows = [0], [0], []
+    for gl in layers:
+        for g in gl:
+            rows.extend(g)
+            gns.append(gns[-1] + len(g))
+        lgs.append(lgs[-1] + len(gl))
+    flat = (np.array(lgs, np.uint64), np.array(gns, np.uint64), np.array(rows, np.uint32).reshape(-1, 5),
+            np.ones(len(layers) + 1, np.uint64))
+    dc = P.Circuit(ctx, insz, *flat, n_copies=n_copies)
+    full_in, full_flat = W.replicate(insz, flat, n_copies)
+    inputs = W.random_inputs(p, full_in, 77)
+    tr = P.Transcript(f, "heavy", [n_copies])
+    got = P.gkr_prove(ctx, dc, inputs, tr)
+    circ = O.Circuit.from_flat(full_in, *full_flat)
+    otr = O.Transcript("heavy", of, [n_copies])
+    outs, lay = O.gkr_prove(circ, of.elems_from_bytes(inputs.tobytes()), otr)
+    assert got == O.gkr_proof_bytes(of, outs, lay)
+    assert tr.state == otr.state
