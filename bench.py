@@ -280,7 +280,7 @@ def run_b200(args, cfg_name):
     # lane takes the next proof when it finishes one, so the serial host
     # transcript of one proof overlaps the GPU work of the others). Inputs
     # are resident in HBM on every lane.
-    lanes = args.lanes
+    lanes = args.lanes or 24
     for i in range(lanes):
         P.load_inputs_lane(ctx, circ, field, i, in_pinned)
     from paper_2404_10404_b200._lib import Profile_t, Transcript_t
@@ -418,8 +418,9 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=24,
-                    help="concurrent proofs per step (lanes); the single-proof latency is reported separately")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="concurrent proofs per step (lanes; default 24 on one GPU, min(64, 24 N) on N GPUs); "
+                         "the single-proof latency is reported separately")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args, args.config)

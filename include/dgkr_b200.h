@@ -223,11 +223,16 @@ int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, s
 /* host-only all-gather through a shared-memory communicator (transport test hook) */
 int dgkr_comm_allgather_host(dgkr_comm* comm, const void* in, size_t bytes, void* out);
 /* n distributed proofs over n_lanes lanes, lane l using comms[l] and proving
- * l, l+n_lanes, ... in order on every rank (inputs NULL = lane-resident). */
+ * l, l+n_lanes, ... in order on every rank (inputs NULL = lane-resident).
+ * absorb_policy: which rank gathers proof i's claimed outputs and runs their
+ * serial absorb (gkr.hpp:189-190) — 0: rank 0 for every proof; 1: rank
+ * i mod world, so the host hash chains of concurrent proofs spread over all
+ * ranks' cores. Every rank returns identical proof bytes except the claimed
+ * output section, which only the absorbing rank fills (zeros elsewhere). */
 int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, size_t n_lanes, dgkr_circuit* c,
                                const dgkr_field* f, size_t n, const uint8_t* const* inputs, dgkr_transcript* ts,
                                uint8_t* const* proofs, const size_t* caps, size_t* lens,
-                               dgkr_profile* lane_profiles);
+                               dgkr_profile* lane_profiles, int absorb_policy);
 /* inputs: this rank's n*input_size elements, or NULL for inputs already loaded
  * with dgkr_circuit_load_inputs */
 int dgkr_gkr_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, dgkr_circuit* c, const dgkr_field* f,

@@ -360,10 +360,10 @@ struct dgkr_comm {
         L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
         L->sync();
     }
-    /// rank 0: h_recv (host) = concatenation over ranks of d_send; others: untouched
-    virtual void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) = 0;
-    /// every rank's h (host, `bytes`) = rank 0's h
-    virtual void broadcast_host(void* h, std::size_t bytes, Lane* L) = 0;
+    /// rank `root`: h_recv (host) = concatenation over ranks of d_send; others: untouched
+    virtual void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) = 0;
+    /// every rank's h (host, `bytes`) = rank `root`'s h
+    virtual void broadcast_host(void* h, std::size_t bytes, Lane* L, int root) = 0;
 };
 
 namespace {
@@ -418,18 +418,18 @@ struct ThreadComm : dgkr_comm {
         g->barrier();
         std::memcpy(h_recv, g->buf.data(), world * bytes);
     }
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
         stage(bytes);
         CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
         L->sync();
         g->barrier();
-        if (rank == 0) std::memcpy(h_recv, g->buf.data(), world * bytes);
+        if (rank == root) std::memcpy(h_recv, g->buf.data(), world * bytes);
     }
-    void broadcast_host(void* h, std::size_t bytes, Lane*) override {
+    void broadcast_host(void* h, std::size_t bytes, Lane*, int root) override {
         stage(bytes);
-        if (rank == 0) std::memcpy(g->buf.data(), h, bytes);
+        if (rank == root) std::memcpy(g->buf.data(), h, bytes);
         g->barrier();
-        if (rank != 0) std::memcpy(h, g->buf.data(), bytes);
+        if (rank != root) std::memcpy(h, g->buf.data(), bytes);
     }
 };
 
@@ -491,21 +491,21 @@ struct ShmComm : dgkr_comm {
         barrier();
         for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
     }
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
         need(bytes);
         barrier();
         CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
         L->sync();
         barrier();
-        if (rank == 0)
+        if (rank == root)
             for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
     }
-    void broadcast_host(void* h, std::size_t bytes, Lane*) override {
+    void broadcast_host(void* h, std::size_t bytes, Lane*, int root) override {
         need(bytes);
         barrier();
-        if (rank == 0) std::memcpy(slot(0), h, bytes);
+        if (rank == root) std::memcpy(slot(root), h, bytes);
         barrier();
-        if (rank != 0) std::memcpy(h, slot(0), bytes);
+        if (rank != root) std::memcpy(h, slot(root), bytes);
     }
     /// host-only exchange (tests the transport without a GPU)
     void allgather_host(const void* in, std::size_t bytes, void* out) {
@@ -568,26 +568,28 @@ struct NcclComm : dgkr_comm {
     void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
         NCK(g_nccl.allGather(d_send, d_recv, bytes, ncclUint8, comm, L->st));
     }
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
-        if (rank == 0) scratch.ensure(static_cast<std::size_t>(world) * bytes);
+    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
+        if (rank == root) scratch.ensure(static_cast<std::size_t>(world) * bytes);
         NCK(g_nccl.groupStart());
-        if (rank == 0) {
-            for (int r = 1; r < world; ++r) NCK(g_nccl.recv(scratch.p + r * bytes, bytes, ncclUint8, r, comm, L->st));
+        if (rank == root) {
+            for (int r = 0; r < world; ++r)
+                if (r != root) NCK(g_nccl.recv(scratch.p + r * bytes, bytes, ncclUint8, r, comm, L->st));
         } else {
-            NCK(g_nccl.send(d_send, bytes, ncclUint8, 0, comm, L->st));
+            NCK(g_nccl.send(d_send, bytes, ncclUint8, root, comm, L->st));
         }
         NCK(g_nccl.groupEnd());
-        if (rank == 0) {
-            CK(cudaMemcpyAsync(scratch.p, d_send, bytes, cudaMemcpyDeviceToDevice, L->st));
+        if (rank == root) {
+            CK(cudaMemcpyAsync(scratch.p + static_cast<std::size_t>(root) * bytes, d_send, bytes,
+                               cudaMemcpyDeviceToDevice, L->st));
             L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
         }
         L->sync();
     }
-    void broadcast_host(void* h, std::size_t bytes, Lane* L) override {
+    void broadcast_host(void* h, std::size_t bytes, Lane* L, int root) override {
         bc.ensure(bytes);
-        if (rank == 0) L->h2d(bc.p, h, bytes);
-        NCK(g_nccl.bcast(bc.p, bc.p, bytes, ncclUint8, 0, comm, L->st));
-        if (rank != 0) L->d2h(h, bc.p, bytes);
+        if (rank == root) L->h2d(bc.p, h, bytes);
+        NCK(g_nccl.bcast(bc.p, bc.p, bytes, ncclUint8, root, comm, L->st));
+        if (rank != root) L->d2h(h, bc.p, bytes);
         L->sync();
     }
     DBuf<std::uint8_t> bc;
@@ -1333,8 +1335,11 @@ void evaluate_circuit(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
 /// gkr_prove (gkr.hpp:182-244) on the device-resident circuit. The proof is
 /// written straight into the caller's buffer (the claimed outputs, by far
 /// its largest part, land there by D2H); returns the proof length.
+/// comm != nullptr: this rank's share of a distributed proof; `root` is the
+/// rank that gathers the claimed outputs and runs their serial absorb (the
+/// other ranks' proof bytes carry zeros in the output section).
 std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs,
-                      Transcript& tr, std::uint8_t* out, std::size_t cap, dgkr_comm* comm = nullptr) {
+                      Transcript& tr, std::uint8_t* out, std::size_t cap, dgkr_comm* comm = nullptr, int root = 0) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
@@ -1365,13 +1370,13 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         launch_to_canonical(kind, W.values[out_layer]->p, W.stage.p, static_cast<int>(w), n_out_local, ctx->st);
         ctx->launched();
         if (comm) {
-            // outputs in global order on rank 0 only: it alone runs the serial absorb
-            comm->gather_to_root_host(W.stage.p, out + 4, n_out_local * w, ctx);
+            // outputs in global order on the root only: it alone runs the serial absorb
+            comm->gather_to_root_host(W.stage.p, out + 4, n_out_local * w, ctx, root);
         } else {
             ctx->d2h(out + 4, W.stage.p, n_out * w);
             ctx->sync();
         }
-        if (!comm || comm->rank == 0) {
+        if (!comm || comm->rank == root) {
             const double t0 = now_ms();
             const std::uint8_t* o = out + 4;
             for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(o + i * w, w);
@@ -1385,11 +1390,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             std::memcpy(st, tr.state().data(), 32);
             const std::uint64_t draws = tr.draws();
             std::memcpy(st + 32, &draws, 8);
-            comm->broadcast_host(st, 40, ctx);
+            comm->broadcast_host(st, 40, ctx, root);
             std::uint64_t d2;
             std::memcpy(&d2, st + 32, 8);
             tr = Transcript(&F, st, d2);
-            if (comm->rank != 0) std::memset(out + 4, 0, n_out * w);  // only rank 0 holds the outputs
+            if (comm->rank != root) std::memset(out + 4, 0, n_out * w);  // only the root holds the outputs
         }
     }
     // q and the output claim (gkr.hpp:192-202)
@@ -3090,10 +3095,11 @@ int dgkr_comm_allgather_host(dgkr_comm* comm, const void* in, std::size_t bytes,
 int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size_t n_lanes, dgkr_circuit* c,
                                const dgkr_field* f, std::size_t n, const std::uint8_t* const* inputs,
                                dgkr_transcript* ts, std::uint8_t* const* proofs, const std::size_t* caps,
-                               std::size_t* lens, dgkr_profile* lane_profiles) {
+                               std::size_t* lens, dgkr_profile* lane_profiles, int absorb_policy) {
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
         if (n == 0 || n_lanes == 0 || n_lanes > 64) fail(DGKR_OUT_OF_RANGE, "bad proof / lane count");
+        if (absorb_policy != 0 && absorb_policy != 1) fail(DGKR_INVALID_ARGUMENT, "unknown absorb policy");
         const std::size_t L = std::min(n, n_lanes);
         std::vector<Lane*> lanes(L);
         for (std::size_t i = 0; i < L; ++i) {
@@ -3113,8 +3119,9 @@ int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size
                 try {
                     Ln->begin_call();
                     Transcript tr(&f->f, ts[i].state, ts[i].draws);
+                    const int root = absorb_policy == 1 ? static_cast<int>(i % static_cast<std::size_t>(comms[li]->world)) : 0;
                     lens[i] = gkr_prove(Ln, *c, workspace(*c, static_cast<int>(li)), f, inputs ? inputs[i] : nullptr,
-                                        tr, proofs[i], caps[i], comms[li]);
+                                        tr, proofs[i], caps[i], comms[li], root);
                     std::memcpy(ts[i].state, tr.state().data(), 32);
                     ts[i].draws = tr.draws();
                     Ln->end_call();

@@ -63,8 +63,11 @@ def slot_bytes_for(circuit: P.Circuit, field: P.Field) -> int:
 
 
 def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field: P.Field, n: int, label: str,
-                      inputs=None, out_bufs=None):
-    """n distributed proofs over len(comms) lanes (lane l: proofs l, l+L, ...)."""
+                      inputs=None, out_bufs=None, spread_absorb: bool = False):
+    """n distributed proofs over len(comms) lanes (lane l: proofs l, l+L, ...).
+    spread_absorb: proof i's claimed outputs are gathered to and absorbed on
+    rank i mod world (else rank 0); only that rank's copy of proof i carries
+    the output section."""
     L = len(comms)
     cap = circuit.proof_bound(field) + (comms[0].world - 1) * circuit.output_size * field.width + 4096
     if out_bufs is None:
@@ -81,7 +84,8 @@ def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field
         in_ptrs = (C.c_void_p * n)(*([inputs.ctypes.data] * n))
     profs = (Profile_t * L)()
     check(lib().dgkr_gkr_prove_dist_stream(ctx.handle, carr, C.c_size_t(L), circuit.handle, field.handle,
-                                           C.c_size_t(n), in_ptrs, tarr, outs, caps, lens, profs))
+                                           C.c_size_t(n), in_ptrs, tarr, outs, caps, lens, profs,
+                                           C.c_int(1 if spread_absorb else 0)))
     return ([out_bufs[i][: lens[i]] for i in range(n)], [bytes(tarr[i].state) for i in range(n)],
             [profs[i].as_dict() for i in range(L)])
 
@@ -100,6 +104,15 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
     # (ranks exchange only through host shared memory; no kernel waits on another)
     device = int(os.environ.get("DGKR_DEVICE", local_rank))
     backend = os.environ.get("DGKR_DIST_BACKEND", "nccl")
+    # proofs in flight: the serial output absorb (~0.5 s of host time per C2
+    # proof, spread over the ranks) caps throughput at lanes / 0.5 s, so lanes
+    # grow with N; per-lane device memory shrinks as 1/N
+    lanes = args.lanes or min(64, 24 * world)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    if lanes * local_world > (os.cpu_count() or 1) and "DGKR_SPIN_US" not in os.environ:
+        # more lane threads than host cores: spin briefly, then block, so
+        # waiting lanes leave the cores to the lanes hashing their outputs
+        os.environ["DGKR_SPIN_US"] = "200"
     torch.cuda.set_device(device)
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", device))
@@ -116,7 +129,6 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
     all_inputs = W.random_inputs(field.p, insz * n_copies, input_seed)
     per = insz * n_local * field.width
     mine = np.ascontiguousarray(all_inputs[rank * per:(rank + 1) * per])
-    lanes = args.lanes
     token = [secrets.token_hex(6) if rank == 0 else None]
     dist.broadcast_object_list(token, src=0)
     comms = [ShmComm(ctx, f"/dgkr_{token[0]}_{l}", rank, world, slot_bytes_for(circ, field)) for l in range(lanes)]
@@ -128,7 +140,7 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2")
+        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2", spread_absorb=True)
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)  # max over ranks
@@ -149,6 +161,7 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
             "config": {"workload": desc, "field": "bn254", "n_copies": n_copies, "copies_per_gpu": n_local,
                        "gates_per_layer_per_copy": 1 << lw, "depth": depth, "gates": gates,
                        "parallelism": f"dp{world} (rank = top log2(N) variables)", "transport": "shm per lane",
+                       "output_absorb": "proof i on rank i mod N",
                        "l2": "no flush: layer tables exceed L2"},
             "lanes": lanes, "proof_latency_ms": 1e3 * lat,
             "e2e": {"value": lanes * gates / (ms_per_step * 1e-3), "unit": "gates/s",

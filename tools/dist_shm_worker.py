@@ -14,6 +14,7 @@ from paper_2404_10404_b200.dist import ShmComm, prove_dist_stream, slot_bytes_fo
 
 rank, world, token, lanes, n, out = (int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], int(sys.argv[4]),
                                      int(sys.argv[5]), sys.argv[6])
+spread = len(sys.argv) > 7 and sys.argv[7] == "spread"
 n_total = 8
 ctx = P.Context(0)
 f = P.Field.bn254()
@@ -25,9 +26,9 @@ mine = np.ascontiguousarray(inputs[rank * per:(rank + 1) * per])
 comms = [ShmComm(ctx, f"/dgkr_{token}_{l}", rank, world, slot_bytes_for(circ, f)) for l in range(lanes)]
 for l in range(lanes):
     P.load_inputs_lane(ctx, circ, f, l, mine)
-proofs, states, _ = prove_dist_stream(ctx, comms, circ, f, n, "shm")
-if rank == 0:
-    with open(out, "wb") as fh:
+proofs, states, _ = prove_dist_stream(ctx, comms, circ, f, n, "shm", spread_absorb=spread)
+if rank == 0 or spread:
+    with open(out + (f".{rank}" if spread else ""), "wb") as fh:
         for p_, s in zip(proofs, states):
             fh.write(len(p_).to_bytes(8, "little") + bytes(p_) + s)
 print("rank", rank, "ok")
