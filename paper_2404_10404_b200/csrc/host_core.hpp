@@ -299,6 +299,8 @@ inline Digest sha256(const std::uint8_t* d, std::size_t n) {
 
 /// SHA256(a(32) || b(32)): one data block + the constant padding block.
 Digest sha256_64(const std::uint8_t* a32, const std::uint8_t* b32);
+/// state <- SHA256(state || e_i) for n consecutive 32-byte elements
+void absorb_chain32(std::uint8_t* state, const std::uint8_t* elems, std::size_t n);
 
 // ---------------------------------------------------------------------------
 // Transcript (transcript.hpp:17-130)
@@ -320,6 +322,14 @@ public:
     const Digest& state() const { return state_; }
     std::uint64_t draws() const { return draws_; }
 
+    /// absorb_bytes of n consecutive elements of `width` bytes (already canonical)
+    void absorb_many(const std::uint8_t* d, std::size_t n, std::size_t width) {
+        if (width == 32) {
+            absorb_chain32(state_.data(), d, n);
+            return;
+        }
+        for (std::size_t i = 0; i < n; ++i) absorb_bytes(d + i * width, width);
+    }
     void absorb_bytes(const std::uint8_t* d, std::size_t n) {
         if (n == 32) {
             state_ = sha256_64(state_.data(), d);

@@ -96,6 +96,78 @@ __attribute__((target("sha,sse4.1,ssse3"))) void compress_shani(std::uint32_t st
     _mm_storeu_si128(reinterpret_cast<__m128i*>(&st[4]), s1);
 }
 
+// W+K of the constant padding block of a 64-byte message (0x80, zeros, bit
+// length 512): its message schedule never changes, so chained absorbs skip it.
+struct PadWK {
+    alignas(16) std::uint32_t wk[64];
+    PadWK() {
+        std::uint32_t w[64] = {0};
+        w[0] = 0x80000000u;
+        w[15] = 512;
+        for (int t = 16; t < 64; ++t) {
+            const std::uint32_t s0 = rotr(w[t - 15], 7) ^ rotr(w[t - 15], 18) ^ (w[t - 15] >> 3);
+            const std::uint32_t s1 = rotr(w[t - 2], 17) ^ rotr(w[t - 2], 19) ^ (w[t - 2] >> 10);
+            w[t] = w[t - 16] + s0 + w[t - 7] + s1;
+        }
+        for (int t = 0; t < 64; ++t) wk[t] = w[t] + kK[t];
+    }
+};
+const PadWK kPadWK;
+
+/// state <- SHA256(state || e_i) for i < n, 32-byte elements (the transcript's
+/// absorb of a field element, transcript.hpp:32-42, chained). The state stays
+/// in SHA-NI's ABEF/CDGH registers; each digest's words are the next block's
+/// first 8 message words as they are.
+__attribute__((target("sha,sse4.1,ssse3"))) void absorb_chain32_shani(std::uint8_t* state, const std::uint8_t* e,
+                                                                       std::size_t n) {
+    const __m128i bswap = _mm_set_epi64x(0x0c0d0e0f08090a0bULL, 0x0405060700010203ULL);
+    static const std::uint32_t iv[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                                        0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    __m128i tmp = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&iv[0]));
+    __m128i ivh = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&iv[4]));
+    tmp = _mm_shuffle_epi32(tmp, 0xB1);
+    ivh = _mm_shuffle_epi32(ivh, 0x1B);
+    const __m128i iv0 = _mm_alignr_epi8(tmp, ivh, 8);   // ABEF
+    const __m128i iv1 = _mm_blend_epi16(ivh, tmp, 0xF0);  // CDGH
+    // digest words h0..h3 / h4..h7 (lane 0 = first word)
+    __m128i wa = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(state)), bswap);
+    __m128i wb = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(state + 16)), bswap);
+    for (std::size_t i = 0; i < n; ++i, e += 32) {
+        __m128i w[16];
+        w[0] = wa;
+        w[1] = wb;
+        w[2] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(e)), bswap);
+        w[3] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(e + 16)), bswap);
+        for (int g = 4; g < 16; ++g) {
+            __m128i x = _mm_sha256msg1_epu32(w[g - 4], w[g - 3]);
+            x = _mm_add_epi32(x, _mm_alignr_epi8(w[g - 1], w[g - 2], 4));
+            w[g] = _mm_sha256msg2_epu32(x, w[g - 1]);
+        }
+        __m128i s0 = iv0, s1 = iv1;
+        for (int g = 0; g < 16; ++g) {
+            __m128i m = _mm_add_epi32(w[g], _mm_loadu_si128(reinterpret_cast<const __m128i*>(&kK[4 * g])));
+            s1 = _mm_sha256rnds2_epu32(s1, s0, m);
+            m = _mm_shuffle_epi32(m, 0x0E);
+            s0 = _mm_sha256rnds2_epu32(s0, s1, m);
+        }
+        s0 = _mm_add_epi32(s0, iv0);
+        s1 = _mm_add_epi32(s1, iv1);
+        const __m128i a0 = s0, a1 = s1;
+        for (int g = 0; g < 16; ++g) {  // padding block: precomputed W+K
+            __m128i m = _mm_load_si128(reinterpret_cast<const __m128i*>(&kPadWK.wk[4 * g]));
+            s1 = _mm_sha256rnds2_epu32(s1, s0, m);
+            m = _mm_shuffle_epi32(m, 0x0E);
+            s0 = _mm_sha256rnds2_epu32(s0, s1, m);
+        }
+        s0 = _mm_add_epi32(s0, a0);
+        s1 = _mm_add_epi32(s1, a1);
+        wa = _mm_shuffle_epi32(_mm_unpackhi_epi64(s1, s0), 0x1B);  // h0 h1 h2 h3
+        wb = _mm_shuffle_epi32(_mm_unpacklo_epi64(s1, s0), 0x1B);  // h4 h5 h6 h7
+    }
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(state), _mm_shuffle_epi8(wa, bswap));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(state + 16), _mm_shuffle_epi8(wb, bswap));
+}
+
 bool detect_shani() {
     unsigned a, b, c, d;
     if (!__get_cpuid_count(7, 0, &a, &b, &c, &d)) return false;
@@ -119,6 +191,17 @@ bool sha256_has_shani() { return g_shani; }
 void sha256_compress(std::uint32_t state[8], const std::uint8_t* blocks, std::size_t nblocks) {
     if (g_shani) compress_shani(state, blocks, nblocks);
     else compress_portable(state, blocks, nblocks);
+}
+
+void absorb_chain32(std::uint8_t* state, const std::uint8_t* elems, std::size_t n) {
+    if (g_shani) {
+        absorb_chain32_shani(state, elems, n);
+        return;
+    }
+    for (std::size_t i = 0; i < n; ++i) {
+        const Digest d = sha256_64(state, elems + 32 * i);
+        std::memcpy(state, d.data(), 32);
+    }
 }
 
 Digest sha256_64(const std::uint8_t* a32, const std::uint8_t* b32) {

@@ -1378,8 +1378,7 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         if (!comm || comm->rank == root) {
             const double t0 = now_ms();
-            const std::uint8_t* o = out + 4;
-            for (std::uint64_t i = 0; i < n_out; ++i) tr.absorb_bytes(o + i * w, w);
+            tr.absorb_many(out + 4, n_out, w);
             const double dt = now_ms() - t0;
             ctx->prof.output_absorb_ms += dt;
             ctx->prof.host_transcript_ms += dt;
@@ -1655,7 +1654,7 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
     for (const auto& x : r) tr.absorb(x);
     tr.absorb(value);
     for (const auto& x : row_evals) tr.absorb(x);
-    for (std::size_t j = 0; j < cols; ++j) tr.absorb_bytes(combined_bytes.data() + j * w, w);
+    tr.absorb_many(combined_bytes.data(), cols, w);
     std::vector<std::uint64_t> idx;
     if (q >= cols) {
         for (std::uint64_t j = 0; j < cols; ++j) idx.push_back(j);
@@ -1801,7 +1800,7 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     launch_to_canonical(kind, layer[L]->p, stage.p, static_cast<int>(w), NL, ctx->st);
     ctx->d2h(fin.data(), stage.p, NL * w);
     ctx->sync();
-    for (std::uint64_t i = 0; i < NL; ++i) tr.absorb_bytes(fin.data() + i * w, w);
+    tr.absorb_many(fin.data(), NL, w);
     // queries on the first layer's half domain (distinct, like pcs.hpp:199-206)
     const std::uint64_t H = N0 / 2;
     std::vector<std::uint64_t> qi;
@@ -2036,10 +2035,8 @@ int dgkr_transcript_absorb_elems(const dgkr_field* f, dgkr_transcript* t, const 
     return guard([&] {
         Transcript tr(&f->f, t->state, t->draws);
         const std::size_t w = f->f.width();
-        for (std::size_t i = 0; i < n; ++i) {
-            f->f.from_bytes(e + i * w);  // canonical check (field.hpp:183-185)
-            tr.absorb_bytes(e + i * w, w);
-        }
+        for (std::size_t i = 0; i < n; ++i) f->f.from_bytes(e + i * w);  // canonical check (field.hpp:183-185)
+        tr.absorb_many(e, n, w);
         std::memcpy(t->state, tr.state().data(), 32);
     });
 }
