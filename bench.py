@@ -280,7 +280,7 @@ def run_b200(args, cfg_name):
     # lane takes the next proof when it finishes one, so the serial host
     # transcript of one proof overlaps the GPU work of the others). Inputs
     # are resident in HBM on every lane.
-    lanes = args.lanes or 24
+    lanes = args.lanes or 32
     for i in range(lanes):
         P.load_inputs_lane(ctx, circ, field, i, in_pinned)
     from paper_2404_10404_b200._lib import Profile_t, Transcript_t
@@ -419,7 +419,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=None,
-                    help="concurrent proofs per step (lanes; default 24 on one GPU, min(64, 24 N) on N GPUs); "
+                    help="concurrent proofs per step (lanes; default 32 on one GPU, min(64, 32 N) on N GPUs); "
                          "the single-proof latency is reported separately")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -107,7 +107,7 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
     # proofs in flight: the serial output absorb (~0.5 s of host time per C2
     # proof, spread over the ranks) caps throughput at lanes / 0.5 s, so lanes
     # grow with N; per-lane device memory shrinks as 1/N
-    lanes = args.lanes or min(64, 24 * world)
+    lanes = args.lanes or min(64, 32 * world)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     if lanes * local_world > (os.cpu_count() or 1) and "DGKR_SPIN_US" not in os.environ:
         # more lane threads than host cores: spin briefly, then block, so
