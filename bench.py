@@ -389,6 +389,7 @@ def run_b200(args, cfg_name):
                          "achieved": achieved_mps, "peak": mp.value, "unit": "BN254 mont-mul/s",
                          "frac": (achieved_mps / mp.value) if achieved_mps else None,
                          "peak_source": "measured: dgkr_bench_mul_peak (4 independent CIOS chains/thread)"},
+        "roofline_proof": proof_roofline(n_copies, lw, depth, ms_per_step / lanes, mp.value),
         "cpu_baseline": cpu,
         "clocks": clk,
         "proof_bytes": proof_len,
@@ -397,6 +398,19 @@ def run_b200(args, cfg_name):
     check(lib().dgkr_host_unregister(in_pinned.ctypes.data_as(C.c_void_p)))
     check(lib().dgkr_host_unregister(out_buf.ctypes.data_as(C.c_void_p)))
     return 0
+
+
+def proof_roofline(n_copies, lw, depth, ms_per_proof, mul_peak):
+    """Whole-proof integer roofline with SURVEY.md §8(d)'s algorithmic count:
+    sum over layers of (K_l + 13) T_l + 3 W_l, plus the evaluate mul wires and
+    T_out, K_l = 1 at the output layer and 2 below (layered circuit, W = T,
+    half the gates mul); achieved = that count / the stream's time per proof."""
+    T = n_copies << lw
+    mults = sum((1 if l == depth else 2) * T + 13 * T + 3 * T for l in range(1, depth + 1)) + depth * T // 2 + T
+    achieved = mults / (ms_per_proof * 1e-3)
+    return {"bound": "imad", "unit": "BN254 mont-mul/s", "algorithmic_mults_per_proof": mults,
+            "ms_per_proof": ms_per_proof, "achieved": achieved, "peak": mul_peak, "frac": achieved / mul_peak,
+            "note": "survey count treats every fold as a full Montgomery multiplication"}
 
 
 def load_ncu_traffic():
