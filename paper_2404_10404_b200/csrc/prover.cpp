@@ -491,14 +491,23 @@ struct ShmComm : dgkr_comm {
         barrier();
         for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
     }
+    /// chunked through the slots (the claimed outputs exceed a slot): the
+    /// segment stays small however large a rank's share of the outputs is
     void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
-        need(bytes);
-        barrier();
-        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        barrier();
-        if (rank == root)
-            for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
+        const std::size_t chunk = hdr->slot_bytes;
+        std::size_t off = 0;
+        do {
+            const std::size_t nb = std::min(chunk, bytes - off);
+            barrier();
+            CK(cudaMemcpyAsync(slot(rank), static_cast<const std::uint8_t*>(d_send) + off, nb, cudaMemcpyDeviceToHost,
+                               L->st));
+            L->sync();
+            barrier();
+            if (rank == root)
+                for (int r = 0; r < world; ++r)
+                    std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes + off, slot(r), nb);
+            off += nb;
+        } while (off < bytes);
     }
     void broadcast_host(void* h, std::size_t bytes, Lane*, int root) override {
         need(bytes);
@@ -3054,7 +3063,6 @@ void dgkr_comm_destroy(dgkr_comm* c) { delete c; }
 int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, std::size_t slot_bytes,
                          dgkr_comm** out) {
     return guard([&] {
-        (void)ctx;
         if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
         if (!name || name[0] != '/') fail(DGKR_INVALID_ARGUMENT, "shm name must start with '/'");
         auto c = std::make_unique<ShmComm>();
@@ -3077,6 +3085,9 @@ int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, s
         c->hdr->world = static_cast<std::uint32_t>(world);
         c->hdr->slot_bytes = slot_bytes;
         c->data = static_cast<std::uint8_t*>(p) + hb;
+        // not cudaHostRegister'ed: ranks sharing one GPU would register the same
+        // physical pages twice, which corrupted device state (measured with 8 lanes x 2 ranks)
+        (void)ctx;
         *out = c.release();
     });
 }

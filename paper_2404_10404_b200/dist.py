@@ -57,9 +57,10 @@ class ShmComm:
             pass
 
 
-def slot_bytes_for(circuit: P.Circuit, field: P.Field) -> int:
-    """largest single exchange: one rank's claimed outputs"""
-    return max(circuit.output_size * field.width, 4096)
+def slot_bytes_for(circuit: P.Circuit, field: P.Field, cap: int = 8 << 20) -> int:
+    """per-rank slot: one rank's claimed outputs, capped (larger exchanges are
+    chunked through the slot), at least 4 KiB for the per-round sums"""
+    return max(min(circuit.output_size * field.width, cap), 4096)
 
 
 def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field: P.Field, n: int, label: str,
@@ -72,6 +73,10 @@ def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field
     cap = circuit.proof_bound(field) + (comms[0].world - 1) * circuit.output_size * field.width + 4096
     if out_bufs is None:
         out_bufs = [np.empty(cap, dtype=np.uint8) for _ in range(n)]
+    # fewer buffers than proofs: proof i uses buffer i mod len (proofs i and
+    # i + L run one after the other on lane i mod L, so reuse is safe when
+    # len(out_bufs) is a multiple of L); the returned proofs then alias
+    out_bufs = [out_bufs[i % len(out_bufs)] for i in range(n)]
     tarr = (Transcript_t * n)()
     for i in range(n):
         tarr[i] = P.Transcript(field, label).t
@@ -134,13 +139,16 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
     comms = [ShmComm(ctx, f"/dgkr_{token[0]}_{l}", rank, world, slot_bytes_for(circ, field)) for l in range(lanes)]
     for l in range(lanes):
         P.load_inputs_lane(ctx, circ, field, l, mine)
+    cap = circ.proof_bound(field) + (world - 1) * circ.output_size * field.width + 4096
+    bufs = [np.empty(cap, dtype=np.uint8) for _ in range(lanes)]  # one per lane, reused
     gates = n_copies * (1 << lw) * depth
 
     def timed(n):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2", spread_absorb=True)
+        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2", spread_absorb=True,
+                                                  out_bufs=bufs)
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)  # max over ranks

@@ -23,7 +23,8 @@ circ = P.Circuit(ctx, insz, *flat, n_copies=n_total // world)
 inputs = W.random_inputs(f.p, insz * n_total, 52)
 per = insz * (n_total // world) * f.width
 mine = np.ascontiguousarray(inputs[rank * per:(rank + 1) * per])
-comms = [ShmComm(ctx, f"/dgkr_{token}_{l}", rank, world, slot_bytes_for(circ, f)) for l in range(lanes)]
+# 4 KiB slots: the claimed-output gather (32 KiB per rank) runs chunked
+comms = [ShmComm(ctx, f"/dgkr_{token}_{l}", rank, world, slot_bytes_for(circ, f, cap=4096)) for l in range(lanes)]
 for l in range(lanes):
     P.load_inputs_lane(ctx, circ, f, l, mine)
 proofs, states, _ = prove_dist_stream(ctx, comms, circ, f, n, "shm", spread_absorb=spread)
