@@ -1048,6 +1048,13 @@ __global__ void k_gather32(const uint4* __restrict__ src, const std::uint64_t* _
 }
 
 void check_launch(const char* what) {
+    // DGKR_DEBUG_SYNC=1: synchronise after every launch so a device fault is
+    // reported against the kernel that raised it (debug builds of a run only)
+    static const bool dbg = std::getenv("DGKR_DEBUG_SYNC") != nullptr;
+    if (dbg) {
+        const cudaError_t s = cudaDeviceSynchronize();
+        if (s != cudaSuccess) std::fprintf(stderr, "dgkr_b200: device fault after %s: %s\n", what, cudaGetErrorString(s));
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         std::fprintf(stderr, "dgkr_b200: launch of %s failed: %s\n", what, cudaGetErrorString(e));

@@ -618,7 +618,11 @@ struct RoundBuffers {
     std::uint64_t cap = 0;  // max table size handled
     DBuf<Fe> bufA, bufB, finals;
     DBuf<const Fe*> ptrs;   // [A ptrs | B ptrs | finals ptrs] each ntab
-    void ensure(int nt, std::uint64_t size0) {
+    /// st: the stream that will use the buffers. The pointer table is
+    /// uploaded on it: a synchronous cudaMemcpy from pageable memory may
+    /// return before its NULL-stream DMA lands, and non-blocking lane streams
+    /// do not wait for the NULL stream.
+    void ensure(int nt, std::uint64_t size0, cudaStream_t st) {
         if (nt <= ntab && size0 <= cap) return;
         ntab = std::max(nt, ntab);
         cap = std::max(size0, cap);
@@ -633,11 +637,21 @@ struct RoundBuffers {
             h[2 * ntab + t] = finals.p + t;
         }
         ptrs.ensure(3 * ntab);
-        CK(cudaMemcpy(ptrs.p, h.data(), h.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ptrs.p, h.data(), h.size() * sizeof(const Fe*), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // h is pageable and local
     }
     const Fe* const* A() const { return ptrs.p; }
     const Fe* const* B() const { return ptrs.p + ntab; }
     const Fe* const* F() const { return ptrs.p + 2 * ntab; }
+};
+
+/// per-lane buffers of a distributed sum-check's phase boundary: this rank's
+/// finals, the world-sized tables, their pointer array and the tail round
+/// buffers (persistent: no device allocation inside a proof)
+struct DistTail {
+    DBuf<Fe> mine, tabs;
+    DBuf<const Fe*> ptrs;
+    RoundBuffers rb;
 };
 
 struct RoundPoly {
@@ -667,34 +681,31 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
 /// rebuilt world-sized tables — identical on all ranks, so the transcript
 /// equals the single-GPU one byte for byte.
 SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                            RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim = nullptr) {
+                            RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, DistTail& dt,
+                            const U256* claim = nullptr) {
     const int ntab = 2 * np + (has_g ? 1 : 0);
     const int world = comm->world;
     SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim);
     // boundary: gather every rank's final table values
     std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
     for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
-    DBuf<Fe> dmine;
-    dmine.ensure(ntab);
-    ctx->h2d(dmine.p, mine.data(), ntab * sizeof(Fe));
-    comm->allgather_to_host(dmine.p, all.data(), ntab * sizeof(Fe), ctx);
+    dt.mine.ensure(ntab);
+    ctx->h2d(dt.mine.p, mine.data(), ntab * sizeof(Fe));
+    comm->allgather_to_host(dt.mine.p, all.data(), ntab * sizeof(Fe), ctx);
     // world-sized tables, rank index = position (natural order)
-    DBuf<Fe> tabs;
-    tabs.ensure(static_cast<std::size_t>(ntab) * world);
+    dt.tabs.ensure(static_cast<std::size_t>(ntab) * world);
     std::vector<Fe> h(static_cast<std::size_t>(ntab) * world);
     for (int t = 0; t < ntab; ++t)
         for (int r = 0; r < world; ++r) h[static_cast<std::size_t>(t) * world + r] = all[static_cast<std::size_t>(r) * ntab + t];
-    ctx->h2d(tabs.p, h.data(), h.size() * sizeof(Fe));
+    ctx->h2d(dt.tabs.p, h.data(), h.size() * sizeof(Fe));
     std::vector<const Fe*> hp(ntab);
-    for (int t = 0; t < ntab; ++t) hp[t] = tabs.p + static_cast<std::size_t>(t) * world;
-    DBuf<const Fe*> dp;
-    dp.ensure(ntab);
-    ctx->h2d(dp.p, hp.data(), ntab * sizeof(const Fe*));
+    for (int t = 0; t < ntab; ++t) hp[t] = dt.tabs.p + static_cast<std::size_t>(t) * world;
+    dt.ptrs.ensure(ntab);
+    ctx->h2d(dt.ptrs.p, hp.data(), ntab * sizeof(const Fe*));
     int lw = 0;
     while ((1 << lw) < world) ++lw;
-    RoundBuffers tail_rb;
     const U256 mid = (nv > 0 || !claim) ? loc.claim_end : *claim;
-    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dp.p, tail_rb, tr, nullptr, claim ? &mid : nullptr);
+    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dt.ptrs.p, dt.rb, tr, nullptr, claim ? &mid : nullptr);
     loc.rounds.insert(loc.rounds.end(), tail.rounds.begin(), tail.rounds.end());
     loc.challenges.insert(loc.challenges.end(), tail.challenges.begin(), tail.challenges.end());
     loc.finals = tail.finals;
@@ -712,7 +723,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     const int ntab = 2 * np + (has_g ? 1 : 0);
     SumcheckRun out;
     const std::uint64_t size0 = std::uint64_t{1} << nv;
-    rb.ensure(ntab, size0);
+    rb.ensure(ntab, size0, ctx->st);
     Fe* d_r = ctx->d_small.p;
     const Fe* const* cur = base;
     const U256 zero{};
@@ -875,6 +886,7 @@ struct CircuitWs {
     DBuf<Fe> H, G;      // bookkeeping outputs, max_slots x Tmax and Tmax
     DBuf<Fe> Wg, EqU;   // dense per-gate weights and chi(u) tables
     DBuf<Fe> heavy_scr; // heavy-row partials: 2 x max_heavy
+    DistTail dist;      // distributed phase-boundary buffers (run_rounds_dist)
     RoundBuffers rb;
     DBuf<std::uint8_t> stage;
     DBuf<Fe> eq_tabs;   // split-eq tables for weights and u
@@ -1140,6 +1152,7 @@ void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const s
     for (std::uint32_t l = 0; l <= D; ++l) ll[l] = c.sub_log[l];
     c.d_layer_log.ensure(D + 1);
     CK(cudaMemcpy(c.d_layer_log.p, ll.data(), ll.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());  // see workspace(): setup DMA must land before lane streams run
     (void)ctx;
 }
 
@@ -1170,7 +1183,7 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
         for (std::uint32_t l = 1; l <= D; ++l) gmax = std::max(gmax, c.full_padded[l]);
         W.Wg.ensure(gmax);
         W.EqU.ensure(c.Tmax);
-        W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax);
+        W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax, cudaStreamLegacy);
         W.heavy_scr.ensure(2 * static_cast<std::size_t>(std::max<std::uint32_t>(c.max_heavy, 1)));
     }
     W.cons.resize(D + 1);
@@ -1202,6 +1215,9 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
         CK(cudaMemcpy(wc->base_ptrs.p, bp.data(), bp.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
         W.cons[li] = std::move(wc);
     }
+    // the setup copies above are synchronous cudaMemcpy from pageable memory:
+    // wait for their DMA before any lane stream (non-blocking) reads the tables
+    CK(cudaDeviceSynchronize());
     c.ws[lane] = std::move(wp);
     return *c.ws[lane];
 }
@@ -1498,7 +1514,7 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             ctx->prof.bookkeep_ms += ms;
         }
         SumcheckRun p1 =
-            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm,
+            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
                                    &combined.value)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
                               &combined.value);
@@ -1536,7 +1552,7 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             ctx->prof.bookkeep_ms += ms;
         }
         SumcheckRun p2 =
-            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm,
+            comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
                                    &p1.claim_end)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
                               &p1.claim_end);

@@ -14,11 +14,12 @@ from paper_2404_10404_b200.dist import ShmComm, prove_dist_stream, slot_bytes_fo
 
 rank, world, token, lanes, n, out = (int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], int(sys.argv[4]),
                                      int(sys.argv[5]), sys.argv[6])
-spread = len(sys.argv) > 7 and sys.argv[7] == "spread"
-n_total = 8
+spread = (len(sys.argv) > 7 and sys.argv[7] == "spread") or os.environ.get("DGKR_STRESS_SPREAD") == "1"
+n_total = int(os.environ.get("DGKR_STRESS_COPIES", "8"))
 ctx = P.Context(0)
 f = P.Field.bn254()
-insz, flat = W.layered_circuit(seed=51, log_width=8, depth=5)
+insz, flat = W.layered_circuit(seed=51, log_width=int(os.environ.get("DGKR_STRESS_LW", "8")),
+                               depth=int(os.environ.get("DGKR_STRESS_DEPTH", "5")))
 circ = P.Circuit(ctx, insz, *flat, n_copies=n_total // world)
 inputs = W.random_inputs(f.p, insz * n_total, 52)
 per = insz * (n_total // world) * f.width
@@ -28,6 +29,9 @@ comms = [ShmComm(ctx, f"/dgkr_{token}_{l}", rank, world, slot_bytes_for(circ, f,
 for l in range(lanes):
     P.load_inputs_lane(ctx, circ, f, l, mine)
 proofs, states, _ = prove_dist_stream(ctx, comms, circ, f, n, "shm", spread_absorb=spread)
+if os.environ.get("DGKR_STRESS_LW"):
+    print("rank", rank, "ok", len(set(states)) == 1)
+    sys.exit(0)
 if rank == 0 or spread:
     with open(out + (f".{rank}" if spread else ""), "wb") as fh:
         for p_, s in zip(proofs, states):
