@@ -453,7 +453,11 @@ struct ShmComm : dgkr_comm {
     std::size_t map_bytes = 0;
     std::string name;
     bool owner = false;
+    // pinned bounce buffer (slot_bytes): device <-> slot copies go through it
+    // as DMA + memcpy instead of the driver's pageable staging
+    std::uint8_t* bounce = nullptr;
     ~ShmComm() override {
+        if (bounce) cudaFreeHost(bounce);
         if (hdr) munmap(hdr, map_bytes);
         if (owner) shm_unlink(name.c_str());
     }
@@ -473,22 +477,27 @@ struct ShmComm : dgkr_comm {
     void need(std::size_t bytes) const {
         if (bytes > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small for this exchange");
     }
+    /// device -> own slot through the pinned bounce buffer (the copy runs
+    /// before the barrier that releases the slot)
+    void stage_send(const void* d_send, std::size_t bytes, Lane* L) {
+        if (!bounce) fail(DGKR_INVALID_ARGUMENT, "shared-memory communicator created without a context");
+        CK(cudaMemcpyAsync(bounce, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->sync();
+        barrier();  // previous contents consumed
+        std::memcpy(slot(rank), bounce, bytes);
+        barrier();
+    }
     void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
         need(bytes);
-        barrier();  // previous contents consumed
-        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        barrier();
-        for (int r = 0; r < world; ++r)
-            CK(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_recv) + r * bytes, slot(r), bytes, cudaMemcpyHostToDevice, L->st));
+        if (bytes * static_cast<std::size_t>(world) > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small");
+        stage_send(d_send, bytes, L);
+        for (int r = 0; r < world; ++r) std::memcpy(bounce + r * bytes, slot(r), bytes);
+        CK(cudaMemcpyAsync(d_recv, bounce, static_cast<std::size_t>(world) * bytes, cudaMemcpyHostToDevice, L->st));
         L->sync();
     }
     void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
         need(bytes);
-        barrier();
-        CK(cudaMemcpyAsync(slot(rank), d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        barrier();
+        stage_send(d_send, bytes, L);
         for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
     }
     /// chunked through the slots (the claimed outputs exceed a slot): the
@@ -498,11 +507,7 @@ struct ShmComm : dgkr_comm {
         std::size_t off = 0;
         do {
             const std::size_t nb = std::min(chunk, bytes - off);
-            barrier();
-            CK(cudaMemcpyAsync(slot(rank), static_cast<const std::uint8_t*>(d_send) + off, nb, cudaMemcpyDeviceToHost,
-                               L->st));
-            L->sync();
-            barrier();
+            stage_send(static_cast<const std::uint8_t*>(d_send) + off, nb, L);
             if (rank == root)
                 for (int r = 0; r < world; ++r)
                     std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes + off, slot(r), nb);
@@ -1371,6 +1376,7 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
     // distributed: this rank holds copies [rank*n, (rank+1)*n) of a
     // uniform-width data-parallel circuit; the rank index is the top log2(world)
     // variables of every layer (cluster.hpp:182-189).
+    if (comm && comm->world == 1) comm = nullptr;  // a 1-rank communicator exchanges nothing
     const std::uint64_t world = comm ? static_cast<std::uint64_t>(comm->world) : 1;
     const std::uint64_t rank = comm ? static_cast<std::uint64_t>(comm->rank) : 0;
     const std::uint32_t lw = log2_exact(world);
@@ -3101,6 +3107,10 @@ int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, s
         c->hdr->world = static_cast<std::uint32_t>(world);
         c->hdr->slot_bytes = slot_bytes;
         c->data = static_cast<std::uint8_t*>(p) + hb;
+        if (ctx) {  // device exchanges need the pinned bounce buffer; host-only test comms do not
+            CK(cudaSetDevice(ctx->device));
+            CK(cudaMallocHost(reinterpret_cast<void**>(&c->bounce), std::max<std::size_t>(slot_bytes, 64)));
+        }
         // not cudaHostRegister'ed: ranks sharing one GPU would register the same
         // physical pages twice, which corrupted device state (measured with 8 lanes x 2 ranks)
         (void)ctx;
