@@ -1086,6 +1086,9 @@ void ensure_pad_table() {
     uint32_t wk[64];
     for (int i = 0; i < 64; ++i) wk[i] = w[i] + K[i];
     cudaMemcpyToSymbol(c_pad64_wk, wk, sizeof(wk));
+    // the copy is from pageable memory on the NULL stream: let it land before
+    // kernels on non-blocking lane streams read the constant bank
+    cudaDeviceSynchronize();
     g_pad_uploaded = true;
 }
 
