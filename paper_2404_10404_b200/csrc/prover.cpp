@@ -2,614 +2,25 @@
 // (include/dgkr_b200.h). The protocol logic that must stay serial and
 // bit-exact — transcript order, claim registry, claim combination — runs here
 // on the host, following the reference line by line (citations inline); all
-// O(table) work runs in the sm_100a kernels of kernels.cu.
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <fcntl.h>
-#include <sys/mman.h>
-#include <unistd.h>
-#include <nccl.h>
-
-#include <atomic>
-#include <condition_variable>
-
+// O(table) work runs in the sm_100a kernels of kernels.cu. The runtime types
+// live in runtime.hpp, the transports in comm.hpp; distinct / beacon / NTT /
+// FRI entry points in ext.cpp.
 #include <algorithm>
 #include <array>
-#include <chrono>
-#include <cstdio>
 #include <cstring>
 #include <memory>
-#include <mutex>
-#include <thread>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "comm.hpp"
 #include "dgkr_b200.h"
-#include "fe.hpp"
 #include "host_core.hpp"
 #include "kernels.hpp"
+#include "runtime.hpp"
 
-using namespace dgkr_b200;
 
-namespace {
-
-thread_local std::string g_err;
-
-template <class Fn>
-int guard(Fn&& fn) {
-    try {
-        fn();
-        return DGKR_OK;
-    } catch (const Error& e) {
-        g_err = e.what();
-        return e.code;
-    } catch (const std::bad_alloc& e) {
-        g_err = std::string("host allocation failed: ") + e.what();
-        return DGKR_CUDA_ERROR;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return DGKR_LOGIC_ERROR;
-    }
-}
-
-#define CK(x)                                                                                   \
-    do {                                                                                        \
-        cudaError_t e_ = (x);                                                                   \
-        if (e_ != cudaSuccess) fail(DGKR_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
-    } while (0)
-
-double now_ms() {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-
-template <class T>
-struct DBuf {
-    T* p = nullptr;
-    std::size_t n = 0;
-    DBuf() = default;
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    void ensure(std::size_t count) {
-        if (count <= n && p) return;
-        release();
-        CK(cudaMalloc(reinterpret_cast<void**>(&p), std::max<std::size_t>(count, 1) * sizeof(T)));
-        n = std::max<std::size_t>(count, 1);
-    }
-};
-
-inline Fe to_fe(const U256& x) {
-    Fe f;
-    std::memcpy(f.v, x.w, 32);
-    return f;
-}
-inline U256 to_u256(const Fe& f) {
-    U256 x;
-    std::memcpy(x.w, f.v, 32);
-    return x;
-}
-
-std::uint32_t log2_exact(std::uint64_t n) {  // circuit.hpp:57-61
-    std::uint32_t l = 0;
-    while ((std::uint64_t{1} << l) < n) ++l;
-    return l;
-}
-std::uint64_t next_pow2(std::uint64_t n) {  // circuit.hpp:43-47
-    std::uint64_t p = 1;
-    while (p < n) p <<= 1;
-    return p;
-}
-
-void put32(std::vector<std::uint8_t>& out, std::uint32_t v) {
-    for (int i = 0; i < 4; ++i) out.push_back(static_cast<std::uint8_t>(v >> (8 * i)));
-}
-
-void emit(const std::vector<std::uint8_t>& bytes, std::uint8_t* out, std::size_t cap, std::size_t* len) {
-    *len = bytes.size();
-    if (bytes.size() > cap) fail(DGKR_CAPACITY, "output buffer too small");
-    if (!bytes.empty()) std::memcpy(out, bytes.data(), bytes.size());
-}
-
-}  // namespace
-
-// ===========================================================================
-// Opaque handles
-// ===========================================================================
-struct dgkr_field {
-    HostField f;
-    FieldKind kind = FieldKind::Runtime;
-    RtFieldHost rt{};
-    U256 fold_pow[8];  // canonical 2^(32k+64) mod p, for the fold constants
-    // NTT data (Montgomery): two-adicity s, w of order 2^s, coset shift g =
-    // smallest quadratic non-residue (not in any 2-power subgroup), g^-1
-    unsigned two_adicity = 0;
-    U256 root{}, coset{}, coset_inv{};
-
-    /// w_N for N = 2^log_n (log_n <= two_adicity)
-    U256 root_of_unity(unsigned log_n) const {
-        if (log_n > two_adicity) fail(DGKR_UNSUPPORTED, "domain larger than the field's 2-adic subgroup");
-        U256 w = root;
-        for (unsigned i = log_n; i < two_adicity; ++i) w = f.mul(w, w);
-        return w;
-    }
-
-    /// {c_0..c_7, r} with c_k = mont(r, 2^(32k+64)) (field.cuh FoldConst)
-    void fold_const(const U256& r, U256 out[9]) const {
-        for (int k = 0; k < 8; ++k) out[k] = f.mul(r, fold_pow[k]);
-        out[8] = r;
-    }
-};
-
-/// Runtime-modulus constants live in one __constant__ block per device;
-/// lanes share it (concurrent lanes must use the same runtime field).
-struct RtState {
-    std::mutex mu;
-    bool valid = false;
-    RtFieldHost cur{};
-};
-
-/// One in-flight proof: a CUDA stream, its reduction workspace, pinned
-/// staging and profile counters. A context owns one lane per concurrent
-/// proof (lane 0 serves the single-call API).
-/// device buffers of the NTT / RS / FRI entry points, kept across calls
-/// (multi-GiB at C5 sizes: cudaMalloc/cudaFree per call would dominate)
-struct NttWs {
-    DBuf<std::uint8_t> stage, dbuf;
-    DBuf<Fe> x, a, tw, cpow, scratch, twinv;
-    std::vector<std::unique_ptr<DBuf<Fe>>> layer;
-    std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree;
-    DBuf<std::uint64_t> didx;
-    // beacon tree (config C3)
-    DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
-};
-
-struct Lane {
-    int device = 0;
-    int sms = 0;
-    int index = 0;
-    RtState* rt = nullptr;
-    cudaStream_t st = nullptr;
-    ReduceWs ws;
-    DBuf<Fe> partials, result;
-    DBuf<unsigned> counter;
-    DBuf<Fe> d_small;      // challenges, points, seeds, finals
-    DBuf<int> d_err;
-    DBuf<int> d_flag;       // kernel-raised predicate flags (distinct checks)
-    Fe* h_small = nullptr;  // pinned mirror of d_small
-    // pinned staging layout (Fe units): [0] challenge, [1..4) reduction
-    // results, [16, 8192) eq-table points/seeds, [8192, 12288) slot values,
-    // [12288, 16384) round finals.
-    static constexpr std::size_t kSmall = 1 << 14;
-    static constexpr std::size_t kEqOff = 16, kEqOff2 = 4112, kVxOff = 8192, kFinalsOff = 12288;
-    static constexpr std::size_t kGatherOff = 14336;  // [14336, 16384): all-gathered round sums (<= 682 ranks)
-    bool profile_on = false;
-    dgkr_profile prof{};
-    /// profile-only CUDA-event bracket around a kernel group: tbeg(); ...; tend(prof.x_ms)
-    void tbeg() {
-        if (profile_on) CK(cudaEventRecord(ev0, st));
-    }
-    void tend(double& acc) {
-        if (!profile_on) return;
-        CK(cudaEventRecord(ev1, st));
-        CK(cudaEventSynchronize(ev1));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev0, ev1));
-        acc += ms;
-    }
-    std::unique_ptr<NttWs> ntt_ws;
-    NttWs& nttws() {
-        if (!ntt_ws) ntt_ws = std::make_unique<NttWs>();
-        return *ntt_ws;
-    }
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-
-    Lane(int dev, int sm_count, int idx, RtState* rts) : device(dev), sms(sm_count), index(idx), rt(rts) {
-        CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        ws.num_sms = sms;
-        ws.max_blocks = sms * 8;
-        partials.ensure(static_cast<std::size_t>(ws.max_blocks) * 3);
-        result.ensure(4);
-        counter.ensure(1);
-        CK(cudaMemset(counter.p, 0, sizeof(unsigned)));
-        ws.partials = partials.p;
-        ws.result = result.p;
-        ws.counter = counter.p;
-        d_small.ensure(kSmall);
-        d_err.ensure(1);
-        CK(cudaMemset(d_err.p, 0, sizeof(int)));
-        d_flag.ensure(2);
-        CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
-        CK(cudaEventCreate(&ev0));
-        CK(cudaEventCreate(&ev1));
-        CK(cudaEventCreateWithFlags(&ev_sync, cudaEventBlockingSync | cudaEventDisableTiming));
-        if (const char* e = std::getenv("DGKR_SPIN_US")) spin_ms = std::atof(e) * 1e-3;
-    }
-    Lane(const Lane&) = delete;
-    Lane& operator=(const Lane&) = delete;
-
-    ~Lane() {
-        if (ev_sync) cudaEventDestroy(ev_sync);
-        if (h_small) cudaFreeHost(h_small);
-        if (ev0) cudaEventDestroy(ev0);
-        if (ev1) cudaEventDestroy(ev1);
-        if (st) cudaStreamDestroy(st);
-    }
-
-    FieldKind use(const dgkr_field* f) {
-        if (f->kind == FieldKind::Runtime) {
-            std::lock_guard<std::mutex> lk(rt->mu);
-            if (!rt->valid || std::memcmp(&rt->cur, &f->rt, sizeof(RtFieldHost)) != 0) {
-                upload_rt_field(f->rt, st);
-                CK(cudaStreamSynchronize(st));
-                rt->cur = f->rt;
-                rt->valid = true;
-            }
-        }
-        return f->kind;
-    }
-
-    /// Wait for the stream: poll briefly (round kernels on small tables finish
-    /// in microseconds), then block on an event so that waiting lanes leave
-    /// the host cores to the lanes running their serial SHA-256 chains.
-    void sync() {
-        CK(cudaEventRecord(ev_sync, st));
-        const double t0 = now_ms();
-        for (;;) {
-            const cudaError_t q = cudaEventQuery(ev_sync);
-            if (q == cudaSuccess) return;
-            if (q != cudaErrorNotReady) CK(q);
-            if (now_ms() - t0 > spin_ms) break;
-        }
-        CK(cudaEventSynchronize(ev_sync));
-    }
-    cudaEvent_t ev_sync = nullptr;
-    double spin_ms = 1e12;  // measured: polling beats blocking even with 16 lanes (DGKR_SPIN_US to change)
-
-    void begin_call() {
-        std::memset(&prof, 0, sizeof(prof));
-        prof.total_ms = now_ms();
-    }
-    void end_call() { prof.total_ms = now_ms() - prof.total_ms; }
-
-    void h2d(void* dst, const void* src, std::size_t n) {
-        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
-        prof.h2d_bytes += n;
-    }
-    void d2h(void* dst, const void* src, std::size_t n) {
-        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
-        prof.d2h_bytes += n;
-    }
-    void launched(std::uint64_t n = 1) { prof.launches += n; }
-
-    void check_err_flag(const char* what) {
-        int h = 0;
-        CK(cudaMemcpyAsync(&h, d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-        sync();
-        if (h) {
-            CK(cudaMemsetAsync(d_err.p, 0, sizeof(int), st));
-            fail(DGKR_INVALID_ARGUMENT, std::string("non-canonical field element encoding (") + what + ")");
-        }
-    }
-
-    /// canonical bytes (host) -> Montgomery Fe (device)
-    void upload_elems(const dgkr_field* f, const std::uint8_t* host, std::uint64_t n, Fe* dst, DBuf<std::uint8_t>& stage) {
-        if (n == 0) return;
-        const std::size_t bytes = n * f->f.width();
-        stage.ensure(bytes);
-        h2d(stage.p, host, bytes);
-        launch_from_canonical(use(f), stage.p, static_cast<int>(f->f.width()), dst, n, d_err.p, st);
-        launched();
-        check_err_flag("input tables");
-    }
-};
-
-/// The context is lane 0 itself; extra lanes (concurrent proofs) are
-/// created on demand and share the runtime-field state.
-struct dgkr_ctx : Lane {
-    std::unique_ptr<RtState> rt_owner;
-    std::mutex lanes_mu;
-    std::vector<std::unique_ptr<Lane>> extra;  // lanes 1..
-    cudaEvent_t user_ev[8] = {};
-
-    dgkr_ctx(int dev, int sm_count, std::unique_ptr<RtState> rts)
-        : Lane(dev, sm_count, 0, rts.get()), rt_owner(std::move(rts)) {}
-
-    Lane* lane(int i) {
-        if (i == 0) return this;
-        std::lock_guard<std::mutex> lk(lanes_mu);
-        while (static_cast<int>(extra.size()) < i)
-            extra.push_back(std::make_unique<Lane>(device, sms, static_cast<int>(extra.size()) + 1, rt_owner.get()));
-        return extra[i - 1].get();
-    }
-
-    ~dgkr_ctx() {
-        for (auto& e : user_ev)
-            if (e) cudaEventDestroy(e);
-    }
-};
-
-// ===========================================================================
-// Communicators for the data-parallel (multi-GPU) prover. The protocol code
-// is shared; only the transport differs:
-//   NcclComm    one process per GPU, NCCL over NVLink/NVSwitch (production)
-//   ThreadComm  ranks as host threads driving lanes of ONE GPU, exchanging
-//               through host memory at barriers (tests the distributed
-//               protocol on a single device; no kernel ever waits on another)
-// Per sum-check round the only traffic is an all-gather of 3 field elements
-// per rank (cluster.hpp:272-286); at each phase boundary an all-gather of the
-// final table values (cluster.hpp:295-309).
-// ===========================================================================
-struct dgkr_comm {
-    int rank = 0;
-    int world = 1;
-    DBuf<std::uint8_t> scratch;
-    virtual ~dgkr_comm() = default;
-    /// d_recv (device) = concatenation over ranks of each rank's d_send
-    virtual void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) = 0;
-    /// h_recv (host) = concatenation over ranks of each rank's d_send
-    virtual void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) {
-        scratch.ensure(static_cast<std::size_t>(world) * bytes);
-        allgather(d_send, scratch.p, bytes, L);
-        L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
-        L->sync();
-    }
-    /// rank `root`: h_recv (host) = concatenation over ranks of d_send; others: untouched
-    virtual void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) = 0;
-    /// every rank's h (host, `bytes`) = rank `root`'s h
-    virtual void broadcast_host(void* h, std::size_t bytes, Lane* L, int root) = 0;
-};
-
-namespace {
-
-struct ThreadGroup {
-    int world = 1;
-    std::mutex mu;
-    std::condition_variable cv;
-    int arrived = 0;
-    std::uint64_t gen = 0;
-    std::vector<std::uint8_t> buf;
-    bool aborted = false;
-    void barrier() {
-        std::unique_lock<std::mutex> lk(mu);
-        if (aborted) fail(DGKR_COMM_ERROR, "thread group aborted");
-        const std::uint64_t g = gen;
-        if (++arrived == world) {
-            arrived = 0;
-            ++gen;
-            cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return gen != g || aborted; });
-            if (aborted) fail(DGKR_COMM_ERROR, "thread group aborted");
-        }
-    }
-    void abort() {
-        std::lock_guard<std::mutex> lk(mu);
-        aborted = true;
-        cv.notify_all();
-    }
-};
-
-struct ThreadComm : dgkr_comm {
-    ThreadGroup* g = nullptr;
-    void stage(std::size_t bytes) {
-        g->barrier();  // everyone is done with the previous contents
-        if (rank == 0 && g->buf.size() < static_cast<std::size_t>(world) * bytes) g->buf.resize(world * bytes);
-        g->barrier();
-    }
-    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
-        stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        g->barrier();
-        CK(cudaMemcpyAsync(d_recv, g->buf.data(), world * bytes, cudaMemcpyHostToDevice, L->st));
-        L->sync();
-    }
-    void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
-        stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        g->barrier();
-        std::memcpy(h_recv, g->buf.data(), world * bytes);
-    }
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
-        stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        g->barrier();
-        if (rank == root) std::memcpy(h_recv, g->buf.data(), world * bytes);
-    }
-    void broadcast_host(void* h, std::size_t bytes, Lane*, int root) override {
-        stage(bytes);
-        if (rank == root) std::memcpy(g->buf.data(), h, bytes);
-        g->barrier();
-        if (rank != root) std::memcpy(h, g->buf.data(), bytes);
-    }
-};
-
-// One-node multi-process transport: a POSIX shared-memory segment per lane
-// (ranks = processes, one per GPU). The per-round payloads are already on the
-// host (the transcript needs them there), so a host exchange is the
-// lowest-latency path; every lane has its own segment and barrier, so lanes
-// never order-depend on one another (no cross-lane deadlock, unlike sharing
-// NCCL communicators between concurrently progressing lanes).
-struct ShmHeader {
-    std::atomic<std::uint64_t> arrived;
-    std::atomic<std::uint64_t> gen;
-    std::atomic<std::uint32_t> aborted;
-    std::uint32_t world;
-    std::uint64_t slot_bytes;
-};
-
-struct ShmComm : dgkr_comm {
-    ShmHeader* hdr = nullptr;
-    std::uint8_t* data = nullptr;  // world * slot_bytes
-    std::size_t map_bytes = 0;
-    std::string name;
-    bool owner = false;
-    // pinned bounce buffer (slot_bytes): device <-> slot copies go through it
-    // as DMA + memcpy instead of the driver's pageable staging
-    std::uint8_t* bounce = nullptr;
-    ~ShmComm() override {
-        if (bounce) cudaFreeHost(bounce);
-        if (hdr) munmap(hdr, map_bytes);
-        if (owner) shm_unlink(name.c_str());
-    }
-    void barrier() {
-        const std::uint64_t g = hdr->gen.load(std::memory_order_acquire);
-        if (hdr->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<std::uint64_t>(world)) {
-            hdr->arrived.store(0, std::memory_order_relaxed);
-            hdr->gen.fetch_add(1, std::memory_order_acq_rel);
-            return;
-        }
-        for (std::uint64_t spins = 0; hdr->gen.load(std::memory_order_acquire) == g; ++spins) {
-            if (hdr->aborted.load(std::memory_order_relaxed)) fail(DGKR_COMM_ERROR, "peer rank aborted");
-            if (spins > 2000) std::this_thread::yield();
-        }
-    }
-    std::uint8_t* slot(int r) { return data + static_cast<std::size_t>(r) * hdr->slot_bytes; }
-    void need(std::size_t bytes) const {
-        if (bytes > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small for this exchange");
-    }
-    /// device -> own slot through the pinned bounce buffer (the copy runs
-    /// before the barrier that releases the slot)
-    void stage_send(const void* d_send, std::size_t bytes, Lane* L) {
-        if (!bounce) fail(DGKR_INVALID_ARGUMENT, "shared-memory communicator created without a context");
-        CK(cudaMemcpyAsync(bounce, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
-        L->sync();
-        barrier();  // previous contents consumed
-        std::memcpy(slot(rank), bounce, bytes);
-        barrier();
-    }
-    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
-        need(bytes);
-        if (bytes * static_cast<std::size_t>(world) > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small");
-        stage_send(d_send, bytes, L);
-        for (int r = 0; r < world; ++r) std::memcpy(bounce + r * bytes, slot(r), bytes);
-        CK(cudaMemcpyAsync(d_recv, bounce, static_cast<std::size_t>(world) * bytes, cudaMemcpyHostToDevice, L->st));
-        L->sync();
-    }
-    void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
-        need(bytes);
-        stage_send(d_send, bytes, L);
-        for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
-    }
-    /// chunked through the slots (the claimed outputs exceed a slot): the
-    /// segment stays small however large a rank's share of the outputs is
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
-        const std::size_t chunk = hdr->slot_bytes;
-        std::size_t off = 0;
-        do {
-            const std::size_t nb = std::min(chunk, bytes - off);
-            stage_send(static_cast<const std::uint8_t*>(d_send) + off, nb, L);
-            if (rank == root)
-                for (int r = 0; r < world; ++r)
-                    std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes + off, slot(r), nb);
-            off += nb;
-        } while (off < bytes);
-    }
-    void broadcast_host(void* h, std::size_t bytes, Lane*, int root) override {
-        need(bytes);
-        barrier();
-        if (rank == root) std::memcpy(slot(root), h, bytes);
-        barrier();
-        if (rank != root) std::memcpy(h, slot(root), bytes);
-    }
-    /// host-only exchange (tests the transport without a GPU)
-    void allgather_host(const void* in, std::size_t bytes, void* out) {
-        need(bytes);
-        barrier();
-        std::memcpy(slot(rank), in, bytes);
-        barrier();
-        for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(out) + r * bytes, slot(r), bytes);
-    }
-};
-
-// NCCL is resolved at run time (dlopen) so the library loads without it;
-// torch's bundled libnccl.so.2 is picked up when already loaded.
-struct NcclApi {
-    void* h = nullptr;
-    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-    const char* (*errStr)(ncclResult_t) = nullptr;
-    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*groupStart)() = nullptr;
-    ncclResult_t (*groupEnd)() = nullptr;
-    bool load() {
-        if (h) return true;
-        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
-        if (!h) return false;
-        getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
-        commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(h, "ncclCommInitRank"));
-        allGather = reinterpret_cast<decltype(allGather)>(dlsym(h, "ncclAllGather"));
-        commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
-        errStr = reinterpret_cast<decltype(errStr)>(dlsym(h, "ncclGetErrorString"));
-        send = reinterpret_cast<decltype(send)>(dlsym(h, "ncclSend"));
-        recv = reinterpret_cast<decltype(recv)>(dlsym(h, "ncclRecv"));
-        bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
-        groupStart = reinterpret_cast<decltype(groupStart)>(dlsym(h, "ncclGroupStart"));
-        groupEnd = reinterpret_cast<decltype(groupEnd)>(dlsym(h, "ncclGroupEnd"));
-        return getUniqueId && commInitRank && allGather && commDestroy && errStr && send && recv && bcast &&
-               groupStart && groupEnd;
-    }
-};
-NcclApi g_nccl;
-
-#define NCK(x)                                                                                         \
-    do {                                                                                               \
-        ncclResult_t r_ = (x);                                                                         \
-        if (r_ != ncclSuccess) fail(DGKR_COMM_ERROR, std::string(#x) + ": " + g_nccl.errStr(r_));     \
-    } while (0)
-
-struct NcclComm : dgkr_comm {
-    ncclComm_t comm = nullptr;
-    ~NcclComm() override {
-        if (comm) g_nccl.commDestroy(comm);
-    }
-    void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
-        NCK(g_nccl.allGather(d_send, d_recv, bytes, ncclUint8, comm, L->st));
-    }
-    void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
-        if (rank == root) scratch.ensure(static_cast<std::size_t>(world) * bytes);
-        NCK(g_nccl.groupStart());
-        if (rank == root) {
-            for (int r = 0; r < world; ++r)
-                if (r != root) NCK(g_nccl.recv(scratch.p + r * bytes, bytes, ncclUint8, r, comm, L->st));
-        } else {
-            NCK(g_nccl.send(d_send, bytes, ncclUint8, root, comm, L->st));
-        }
-        NCK(g_nccl.groupEnd());
-        if (rank == root) {
-            CK(cudaMemcpyAsync(scratch.p + static_cast<std::size_t>(root) * bytes, d_send, bytes,
-                               cudaMemcpyDeviceToDevice, L->st));
-            L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
-        }
-        L->sync();
-    }
-    void broadcast_host(void* h, std::size_t bytes, Lane* L, int root) override {
-        bc.ensure(bytes);
-        if (rank == root) L->h2d(bc.p, h, bytes);
-        NCK(g_nccl.bcast(bc.p, bc.p, bytes, ncclUint8, root, comm, L->st));
-        if (rank != root) L->d2h(h, bc.p, bytes);
-        L->sync();
-    }
-    DBuf<std::uint8_t> bc;
-};
-
-}  // namespace
 
 namespace {
 
@@ -1731,180 +1142,6 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
 }
 
 // ---------------------------------------------------------------------------
-// Reed-Solomon / NTT / FRI (north-star "Virgo/FRI"; no reference exists, see
-// pinned by the Python restatement oracle/fri_oracle.py).
-// ---------------------------------------------------------------------------
-void pow_table(Lane* ctx, const dgkr_field* f, const U256& base, std::uint64_t n, Fe* out, DBuf<Fe>& scratch) {
-    std::uint64_t na = 1;
-    while (na * na < n) na <<= 1;
-    scratch.ensure(na + n / na + 2);
-    Fe* db = ctx->d_small.p + Lane::kEqOff;  // one staged element
-    ctx->h_small[Lane::kEqOff] = to_fe(base);
-    ctx->h2d(db, ctx->h_small + Lane::kEqOff, sizeof(Fe));
-    launch_pow_table(ctx->use(f), db, n, out, scratch.p, ctx->st);
-    ctx->launched(2);
-}
-
-/// evaluations (natural order) on c * <w_N> of the polynomial with
-/// coefficients `coeff` (n_in <= N entries, rest zero): a := NTT(coset-scaled, bit-reversed coeff)
-void coset_ntt(Lane* ctx, const dgkr_field* f, const Fe* coeff, std::uint64_t n_in, unsigned log_n, const U256& c,
-               bool apply_coset, Fe* a, DBuf<Fe>& tw, DBuf<Fe>& cpow, DBuf<Fe>& scratch) {
-    const FieldKind kind = ctx->use(f);
-    const std::uint64_t N = std::uint64_t{1} << log_n;
-    const U256 w = f->root_of_unity(log_n);
-    tw.ensure(std::max<std::uint64_t>(N / 2, 1));
-    if (N >= 2) pow_table(ctx, f, w, N / 2, tw.p, scratch);
-    const Fe* scale = nullptr;
-    if (apply_coset) {
-        cpow.ensure(n_in);
-        pow_table(ctx, f, c, n_in, cpow.p, scratch);
-        scale = cpow.p;
-    }
-    ctx->tbeg();
-    launch_bitrev_scale(kind, coeff, scale, a, static_cast<int>(log_n), n_in, ctx->st);
-    launch_ntt(kind, a, static_cast<int>(log_n), tw.p, ctx->st);
-    ctx->tend(ctx->prof.ntt_ms);
-    ctx->launched(2 + log_n);
-}
-
-/// FRI over the RS codeword of `coeffs` (protocol in include/dgkr_b200.h)
-std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::uint64_t n,
-                                    unsigned blowup_log, unsigned final_log, std::size_t q, Transcript& tr) {
-    const HostField& F = f->f;
-    const FieldKind kind = ctx->use(f);
-    const std::size_t w = F.width();
-    if (n == 0 || (n & (n - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "coefficient count must be a power of two");
-    const unsigned log_n0 = log2_exact(n) + blowup_log;
-    if (final_log > log_n0) fail(DGKR_INVALID_ARGUMENT, "final layer larger than the codeword");
-    const unsigned L = log_n0 - final_log;
-    const std::uint64_t N0 = std::uint64_t{1} << log_n0;
-    NttWs& ws = ctx->nttws();
-    auto& stage = ws.stage;
-    auto& cf = ws.x;
-    auto& tw = ws.tw;
-    auto& cpow = ws.cpow;
-    auto& scratch = ws.scratch;
-    auto& twinv = ws.twinv;
-    cf.ensure(n);
-    ctx->upload_elems(f, coeffs, n, cf.p, stage);
-    // layer 0: RS encoding on the coset g<w_N0>
-    auto& layer = ws.layer;
-    auto& tree = ws.tree;
-    if (layer.size() < L + 1) layer.resize(L + 1);
-    if (tree.size() < L) tree.resize(L);
-    for (unsigned l = 0; l <= L; ++l) {
-        if (!layer[l]) layer[l] = std::make_unique<DBuf<Fe>>();
-        layer[l]->ensure(N0 >> l);
-    }
-    coset_ntt(ctx, f, cf.p, n, log_n0, f->coset, true, layer[0]->p, tw, cpow, scratch);
-    // inverse twiddles w^-i for the fold's 1/x
-    twinv.ensure(std::max<std::uint64_t>(N0 / 2, 1));
-    if (N0 >= 2) pow_table(ctx, f, F.inv(f->root_of_unity(log_n0)), N0 / 2, twinv.p, scratch);
-    std::vector<Digest> roots(L);
-    U256 ginv = f->coset_inv;  // (g^(2^l))^-1
-    for (unsigned l = 0; l < L; ++l) {
-        const std::uint64_t Nl = N0 >> l;
-        if (!tree[l]) tree[l] = std::make_unique<DBuf<std::uint8_t>>();
-        tree[l]->ensure(2 * Nl * 32);
-        ctx->tbeg();
-        launch_column_digests(kind, layer[l]->p, Nl, 1, static_cast<int>(w), tree[l]->p + Nl * 32, ctx->st);
-        launch_merkle(tree[l]->p, Nl, ctx->st);
-        ctx->tend(ctx->prof.merkle_ms);
-        ctx->launched(2);
-        ctx->d2h(roots[l].data(), tree[l]->p + 32, 32);
-        ctx->sync();
-        tr.absorb_bytes(roots[l].data(), 32);
-        const U256 beta = tr.challenge();
-        U256 bk[9];
-        f->fold_const(beta, bk);
-        Fe gi = to_fe(ginv);
-        ctx->tbeg();
-        launch_fri_fold(kind, layer[l]->p, Nl, twinv.p, std::uint64_t{1} << l, &gi, bk, layer[l + 1]->p, ctx->st);
-        ctx->tend(ctx->prof.fold_ms);
-        ctx->launched();
-        ginv = F.mul(ginv, ginv);
-    }
-    // final layer, absorbed element by element
-    const std::uint64_t NL = N0 >> L;
-    std::vector<std::uint8_t> fin(NL * w);
-    stage.ensure(NL * w);
-    launch_to_canonical(kind, layer[L]->p, stage.p, static_cast<int>(w), NL, ctx->st);
-    ctx->d2h(fin.data(), stage.p, NL * w);
-    ctx->sync();
-    tr.absorb_many(fin.data(), NL, w);
-    // queries on the first layer's half domain (distinct, like pcs.hpp:199-206)
-    const std::uint64_t H = N0 / 2;
-    std::vector<std::uint64_t> qi;
-    if (L > 0) {
-        if (q >= H) {
-            for (std::uint64_t i = 0; i < H; ++i) qi.push_back(i);
-        } else {
-            std::vector<bool> seen(H, false);
-            while (qi.size() < q) {
-                const std::uint64_t j = tr.challenge_index(H);
-                if (!seen[j]) {
-                    seen[j] = true;
-                    qi.push_back(j);
-                }
-            }
-        }
-    }
-    // gather opened values and Merkle paths on the device, one D2H per layer
-    std::vector<std::uint8_t> out;
-    put32(out, L);
-    for (const auto& r : roots) out.insert(out.end(), r.begin(), r.end());
-    put32(out, static_cast<std::uint32_t>(NL));
-    out.insert(out.end(), fin.begin(), fin.end());
-    put32(out, static_cast<std::uint32_t>(qi.size()));
-    std::vector<std::vector<std::uint8_t>> vals(L), paths(L);
-    std::vector<unsigned> depth(L);
-    auto& didx = ws.didx;
-    auto& dbuf = ws.dbuf;
-    for (unsigned l = 0; l < L; ++l) {
-        const std::uint64_t Nl = N0 >> l, hl = Nl / 2;
-        depth[l] = log2_exact(Nl);
-        std::vector<std::uint64_t> vidx, pidx;
-        for (std::uint64_t i : qi) {
-            const std::uint64_t il = i % hl;
-            vidx.push_back(il);
-            vidx.push_back(il + hl);
-            for (std::uint64_t leaf : {il, il + hl}) {
-                std::uint64_t node = Nl + leaf;
-                while (node > 1) {
-                    pidx.push_back(node ^ 1);
-                    node >>= 1;
-                }
-            }
-        }
-        const std::size_t nv = vidx.size(), np = pidx.size();
-        didx.ensure(nv + np);
-        dbuf.ensure((nv + np) * 32 + nv * w + 32);
-        ctx->h2d(didx.p, vidx.data(), nv * 8);
-        if (np) ctx->h2d(didx.p + nv, pidx.data(), np * 8);
-        launch_gather32(layer[l]->p, didx.p, nv, dbuf.p, ctx->st);
-        launch_to_canonical(kind, reinterpret_cast<const Fe*>(dbuf.p), dbuf.p + (nv + np) * 32, static_cast<int>(w), nv,
-                            ctx->st);
-        launch_gather32(tree[l]->p, didx.p + nv, np, dbuf.p + nv * 32, ctx->st);
-        ctx->launched(3);
-        vals[l].resize(nv * w);
-        paths[l].resize(np * 32);
-        ctx->d2h(vals[l].data(), dbuf.p + (nv + np) * 32, nv * w);
-        if (np) ctx->d2h(paths[l].data(), dbuf.p + nv * 32, np * 32);
-    }
-    ctx->sync();
-    for (std::size_t k = 0; k < qi.size(); ++k) {
-        put32(out, static_cast<std::uint32_t>(qi[k]));
-        for (unsigned l = 0; l < L; ++l) {
-            const std::uint8_t* v = vals[l].data() + 2 * k * w;
-            out.insert(out.end(), v, v + 2 * w);
-            const std::uint8_t* pth = paths[l].data() + 2 * k * depth[l] * 32;
-            out.insert(out.end(), pth, pth + 2 * depth[l] * 32);
-        }
-    }
-    return out;
-}
-
-// ---------------------------------------------------------------------------
 // TrafficStats (cluster.hpp:69-115), byte-accurate logical metering.
 // ---------------------------------------------------------------------------
 struct Traffic {
@@ -2699,430 +1936,6 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
         for (auto& t : th) t.join();
         for (std::size_t i = 0; i < n; ++i)
             if (codes[i] != DGKR_OK) fail(codes[i], "proof " + std::to_string(i) + ": " + errs[i]);
-    });
-}
-
-int dgkr_field_ntt_info(const dgkr_field* f, unsigned* two_adicity, std::uint8_t* root, std::uint8_t* coset) {
-    return guard([&] {
-        *two_adicity = f->two_adicity;
-        if (root) f->f.to_bytes(f->root, root);
-        if (coset) f->f.to_bytes(f->coset, coset);
-    });
-}
-
-// ---------------------------------------------------------------------------
-// distinct.hpp (config C4): AH, pairwise-distinct check, chain update,
-// bit-change experiment. One host sync per call: the encoding error flag, the
-// predicate flags and the sums come back in one pinned read.
-// ---------------------------------------------------------------------------
-namespace {
-
-struct AhPass {
-    std::uint64_t n = 0;
-    Fe* x = nullptr;
-    const std::uint8_t* canon = nullptr;  // device canonical bytes
-};
-
-/// upload + validate + AH of one list; the sum lands in h_small[slot] after sync
-AhPass ah_enqueue(Lane* ctx, const dgkr_field* f, const std::uint8_t* items, std::uint64_t n, DBuf<std::uint8_t>& stage,
-                  DBuf<Fe>& x, int slot) {
-    const FieldKind kind = ctx->use(f);
-    const std::size_t w = f->f.width();
-    AhPass a;
-    a.n = n;
-    x.ensure(std::max<std::uint64_t>(n, 1));
-    stage.ensure(std::max<std::size_t>(n * w, 1));
-    if (n) {
-        ctx->h2d(stage.p, items, n * w);
-        launch_from_canonical(kind, stage.p, static_cast<int>(w), x.p, n, ctx->d_err.p, ctx->st);
-        ctx->launched();
-    }
-    const U256 off = f->f.from_u64(4294967295ull);  // distinct.hpp:20
-    Fe offe = to_fe(off);
-    launch_ah(kind, x.p, n, &offe, ctx->ws, ctx->st);
-    ctx->launched();
-    ctx->d2h(ctx->h_small + slot, ctx->ws.result, sizeof(Fe));
-    a.x = x.p;
-    a.canon = stage.p;
-    return a;
-}
-
-/// read back error + flags (ints at h_small[kGatherOff]) with one sync
-void distinct_finish(Lane* ctx, int* flags_out) {
-    int* hf = reinterpret_cast<int*>(ctx->h_small + Lane::kGatherOff);
-    ctx->d2h(hf, ctx->d_err.p, sizeof(int));
-    ctx->d2h(hf + 1, ctx->d_flag.p, 2 * sizeof(int));
-    ctx->sync();
-    if (hf[0]) {
-        CK(cudaMemsetAsync(ctx->d_err.p, 0, sizeof(int), ctx->st));
-        fail(DGKR_INVALID_ARGUMENT, "non-canonical field element encoding (index list)");
-    }
-    if (flags_out) {
-        flags_out[0] = hf[1];
-        flags_out[1] = hf[2];
-    }
-}
-
-}  // namespace
-
-int dgkr_distinct_ah(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* items, std::size_t n,
-                     std::uint8_t* out) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        NttWs& ws = ctx->nttws();
-        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
-        ah_enqueue(ctx, f, items, n, ws.stage, ws.x, 1);
-        distinct_finish(ctx, nullptr);
-        f->f.to_bytes(to_u256(ctx->h_small[1]), out);
-        ctx->end_call();
-    });
-}
-
-int dgkr_distinct_check(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* a, std::size_t n_a,
-                        const std::uint8_t* a_sorted, std::size_t n_sorted, int* ok) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        NttWs& ws = ctx->nttws();
-        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
-        ah_enqueue(ctx, f, a, n_a, ws.stage, ws.x, 1);
-        AhPass s = ah_enqueue(ctx, f, a_sorted, n_sorted, ws.dbuf, ws.a, 2);
-        launch_strict_ascent(s.canon, static_cast<int>(f->f.width()), n_sorted, ctx->d_flag.p, ctx->st);
-        ctx->launched();
-        int flags[2];
-        distinct_finish(ctx, flags);
-        const bool same = std::memcmp(&ctx->h_small[1], &ctx->h_small[2], sizeof(Fe)) == 0;  // distinct.hpp:57-59
-        *ok = (same && !flags[0]) ? 1 : 0;
-        ctx->end_call();
-    });
-}
-
-int dgkr_distinct_chain_update(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* h, std::uint64_t n_max,
-                               const std::uint8_t* items, std::size_t n, std::uint8_t* h_out) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        const HostField& F = f->f;
-        const U256 hv = F.from_bytes(h);  // throws DGKR_INVALID_ARGUMENT on >= p
-        NttWs& ws = ctx->nttws();
-        CK(cudaMemsetAsync(ctx->d_flag.p, 0, 2 * sizeof(int), ctx->st));
-        AhPass p = ah_enqueue(ctx, f, items, n, ws.stage, ws.x, 1);
-        launch_bound_check(p.canon, static_cast<int>(F.width()), n, n_max, ctx->d_flag.p, ctx->st);
-        ctx->launched();
-        int flags[2];
-        distinct_finish(ctx, flags);
-        if (flags[0]) fail(DGKR_OUT_OF_RANGE, "validator index above bound");  // distinct.hpp:86-88
-        F.to_bytes(F.add(hv, to_u256(ctx->h_small[1])), h_out);
-        ctx->end_call();
-    });
-}
-
-int dgkr_distinct_bitchange(dgkr_ctx* ctx, const dgkr_field* f, std::size_t count, std::uint64_t* set_counts) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        if (count < 10000) fail(DGKR_INVALID_ARGUMENT, "bit-change experiment needs count >= 10^4");  // :116-118
-        const int bits = static_cast<int>(f->f.bits());
-        if (bits > 256) fail(DGKR_UNSUPPORTED, "field too wide");
-        DBuf<unsigned long long> d;
-        d.ensure(bits);
-        CK(cudaMemsetAsync(d.p, 0, bits * sizeof(unsigned long long), ctx->st));
-        Fe offe = to_fe(f->f.from_u64(4294967295ull));
-        launch_bitchange(ctx->use(f), 1, count, bits, &offe, d.p, ctx->st);
-        ctx->launched();
-        std::vector<unsigned long long> h(bits);
-        ctx->d2h(h.data(), d.p, bits * sizeof(unsigned long long));
-        ctx->sync();
-        for (int k = 0; k < bits; ++k) set_counts[k] = h[k];
-        ctx->end_call();
-    });
-}
-
-// ---------------------------------------------------------------------------
-// Beacon validator tree (beacon.hpp; config C3): root, membership paths and
-// batched verify_membership on the device. Records cross as their 64-byte
-// ValidatorRecord::encode() (beacon.hpp:27-37).
-// ---------------------------------------------------------------------------
-namespace {
-
-/// zero_cache (beacon.hpp:66-83): z_0 = H(64 zero bytes), z_k = H(z_{k-1} || z_{k-1})
-std::vector<Digest> zero_cache_host(unsigned depth) {
-    std::vector<Digest> z;
-    std::uint8_t zero[64] = {};
-    z.push_back(sha256(zero, 64));
-    for (unsigned k = 1; k <= depth; ++k) {
-        std::uint8_t buf[64];
-        std::memcpy(buf, z.back().data(), 32);
-        std::memcpy(buf + 32, z.back().data(), 32);
-        z.push_back(sha256(buf, 64));
-    }
-    return z;
-}
-
-unsigned active_log2_of(std::uint64_t n) {
-    unsigned a = 0;
-    while ((std::uint64_t{1} << a) < n) ++a;
-    return a;
-}
-
-/// builds the active-subtree heap in ws.b_nodes (leaves at [2^a, 2^(a+1))); returns a
-unsigned beacon_build(Lane* ctx, NttWs& ws, const std::uint8_t* records, std::uint64_t n, unsigned depth,
-                      const std::vector<Digest>& zc) {
-    const unsigned a = active_log2_of(n);
-    if (a > depth) fail(DGKR_INVALID_ARGUMENT, "validator set exceeds tree capacity");  // beacon.hpp:113-115
-    const std::uint64_t cap = std::uint64_t{1} << a;
-    ws.b_recs.ensure(std::max<std::uint64_t>(n, 1) * 64);
-    if (n) ctx->h2d(ws.b_recs.p, records, n * 64);
-    ws.b_zc.ensure((depth + 1) * 32);
-    ctx->h2d(ws.b_zc.p, zc.data(), (depth + 1) * 32);
-    ws.b_nodes.ensure(2 * cap * 32);
-    ctx->tbeg();
-    launch_beacon_leaves(ws.b_recs.p, n, cap, ws.b_zc.p, ws.b_nodes.p + cap * 32, ctx->st);
-    launch_merkle(ws.b_nodes.p, cap, ctx->st);
-    ctx->tend(ctx->prof.merkle_ms);
-    ctx->launched(2);
-    return a;
-}
-
-}  // namespace
-
-int dgkr_beacon_root(dgkr_ctx* ctx, const std::uint8_t* records, std::size_t n, unsigned depth, std::uint8_t* root) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        const auto zc = zero_cache_host(depth);
-        NttWs& ws = ctx->nttws();
-        const unsigned a = beacon_build(ctx, ws, records, n, depth, zc);
-        Digest h;
-        ctx->d2h(h.data(), ws.b_nodes.p + 32, 32);
-        ctx->sync();
-        for (unsigned k = a; k < depth; ++k) {  // left spine (beacon.hpp:128-131)
-            std::uint8_t buf[64];
-            std::memcpy(buf, h.data(), 32);
-            std::memcpy(buf + 32, zc[k].data(), 32);
-            h = sha256(buf, 64);
-        }
-        std::memcpy(root, h.data(), 32);
-        ctx->end_call();
-    });
-}
-
-int dgkr_beacon_prove(dgkr_ctx* ctx, const std::uint8_t* records, std::size_t n, unsigned depth,
-                      const std::uint64_t* indices, std::size_t m, std::uint8_t* leaves, std::uint8_t* siblings,
-                      unsigned* active_log2) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        for (std::size_t i = 0; i < m; ++i)
-            if (indices[i] >= n) fail(DGKR_OUT_OF_RANGE, "inactive validator index");  // beacon.hpp:138-140
-        const auto zc = zero_cache_host(depth);
-        NttWs& ws = ctx->nttws();
-        const unsigned a = beacon_build(ctx, ws, records, n, depth, zc);
-        ws.didx.ensure(std::max<std::size_t>(m, 1));
-        ws.b_leaves.ensure(std::max<std::size_t>(m, 1) * 32);
-        ws.b_sib.ensure(std::max<std::size_t>(m * a, 1) * 32);
-        if (m) {
-            ctx->h2d(ws.didx.p, indices, m * 8);
-            launch_beacon_paths(ws.b_nodes.p, static_cast<int>(a), ws.didx.p, m, ws.b_leaves.p, ws.b_sib.p, ctx->st);
-            ctx->launched();
-            ctx->d2h(leaves, ws.b_leaves.p, m * 32);
-            if (a) ctx->d2h(siblings, ws.b_sib.p, m * a * 32);
-        }
-        ctx->sync();
-        *active_log2 = a;
-        ctx->end_call();
-    });
-}
-
-int dgkr_beacon_verify(dgkr_ctx* ctx, const std::uint8_t* root, const std::uint8_t* records, const std::uint8_t* leaves,
-                       const std::uint8_t* siblings, const std::uint64_t* indices, std::size_t m, unsigned depth,
-                       unsigned active_log2, std::uint8_t* ok) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        if (active_log2 > 64) fail(DGKR_INVALID_ARGUMENT, "active_log2 out of range");
-        if (m == 0) {
-            ctx->end_call();
-            return;
-        }
-        NttWs& ws = ctx->nttws();
-        const unsigned a = active_log2;
-        // paths claiming a > depth have no zero-cache tail; verify_membership walks a siblings then none
-        const unsigned zdepth = std::max(depth, a);
-        const auto zc = zero_cache_host(zdepth);
-        ws.b_root.ensure(32);
-        ws.b_recs.ensure(m * 64);
-        ws.b_leaves.ensure(m * 32);
-        ws.b_sib.ensure(std::max<std::size_t>(m * a, 1) * 32);
-        ws.didx.ensure(m);
-        ws.b_zc.ensure((zdepth + 1) * 32);
-        ws.b_ok.ensure(m);
-        ctx->h2d(ws.b_root.p, root, 32);
-        ctx->h2d(ws.b_recs.p, records, m * 64);
-        ctx->h2d(ws.b_leaves.p, leaves, m * 32);
-        if (a) ctx->h2d(ws.b_sib.p, siblings, m * a * 32);
-        ctx->h2d(ws.didx.p, indices, m * 8);
-        ctx->h2d(ws.b_zc.p, zc.data(), (zdepth + 1) * 32);
-        ctx->tbeg();
-        launch_beacon_verify(ws.b_root.p, ws.b_recs.p, ws.b_leaves.p, ws.b_sib.p, ws.didx.p, m, static_cast<int>(a),
-                             static_cast<int>(depth), ws.b_zc.p, ws.b_ok.p, ctx->st);
-        ctx->tend(ctx->prof.merkle_ms);
-        ctx->launched();
-        ctx->d2h(ok, ws.b_ok.p, m);
-        ctx->sync();
-        ctx->end_call();
-    });
-}
-
-int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* in, unsigned log_n, int inverse,
-             std::uint8_t* out) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        const HostField& F = f->f;
-        const FieldKind kind = ctx->use(f);
-        const std::uint64_t N = std::uint64_t{1} << log_n;
-        const std::size_t w = F.width();
-        NttWs& ws = ctx->nttws();
-        auto& stage = ws.stage;
-        auto& x = ws.x;
-        auto& a = ws.a;
-        auto& tw = ws.tw;
-        auto& scratch = ws.scratch;
-        x.ensure(N);
-        a.ensure(N);
-        ctx->upload_elems(f, in, N, x.p, stage);
-        const U256 root = f->root_of_unity(log_n);
-        tw.ensure(std::max<std::uint64_t>(N / 2, 1));
-        if (N >= 2) pow_table(ctx, f, inverse ? F.inv(root) : root, N / 2, tw.p, scratch);
-        ctx->tbeg();
-        launch_bitrev_scale(kind, x.p, nullptr, a.p, static_cast<int>(log_n), N, ctx->st);
-        launch_ntt(kind, a.p, static_cast<int>(log_n), tw.p, ctx->st);
-        ctx->tend(ctx->prof.ntt_ms);
-        if (inverse) {
-            U256 k[9];
-            f->fold_const(F.inv(F.from_u64(N)), k);
-            launch_scale(kind, a.p, N, k, ctx->st);
-        }
-        stage.ensure(N * w);
-        launch_to_canonical(kind, a.p, stage.p, static_cast<int>(w), N, ctx->st);
-        ctx->d2h(out, stage.p, N * w);
-        ctx->sync();
-        ctx->end_call();
-    });
-}
-
-int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::size_t n,
-                   unsigned blowup_log, std::uint8_t* out) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        if (n == 0 || (n & (n - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "coefficient count must be a power of two");
-        const unsigned log_n = log2_exact(n) + blowup_log;
-        const std::uint64_t N = std::uint64_t{1} << log_n;
-        const std::size_t w = f->f.width();
-        NttWs& ws = ctx->nttws();
-        auto& stage = ws.stage;
-        auto& cf = ws.x;
-        auto& a = ws.a;
-        auto& tw = ws.tw;
-        auto& cpow = ws.cpow;
-        auto& scratch = ws.scratch;
-        cf.ensure(n);
-        a.ensure(N);
-        ctx->upload_elems(f, coeffs, n, cf.p, stage);
-        coset_ntt(ctx, f, cf.p, n, log_n, f->coset, true, a.p, tw, cpow, scratch);
-        stage.ensure(N * w);
-        launch_to_canonical(ctx->use(f), a.p, stage.p, static_cast<int>(w), N, ctx->st);
-        ctx->d2h(out, stage.p, N * w);
-        ctx->sync();
-        ctx->end_call();
-    });
-}
-
-int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::size_t n,
-                   unsigned blowup_log, unsigned final_log, std::size_t queries, dgkr_transcript* t,
-                   std::uint8_t* proof, std::size_t cap, std::size_t* len) {
-    return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
-        Transcript tr(&f->f, t->state, t->draws);
-        auto bytes = fri_prove(ctx, f, coeffs, n, blowup_log, final_log, queries, tr);
-        std::memcpy(t->state, tr.state().data(), 32);
-        t->draws = tr.draws();
-        ctx->end_call();
-        emit(bytes, proof, cap, len);
-    });
-}
-
-int dgkr_comm_nccl_unique_id(std::uint8_t* out128) {
-    return guard([&] {
-        if (!g_nccl.load()) fail(DGKR_COMM_ERROR, "libnccl.so.2 not found");
-        ncclUniqueId id;
-        NCK(g_nccl.getUniqueId(&id));
-        std::memcpy(out128, &id, sizeof(id));
-    });
-}
-
-int dgkr_comm_create_nccl(dgkr_ctx* ctx, const std::uint8_t* uid128, int rank, int world, dgkr_comm** out) {
-    return guard([&] {
-        if (!g_nccl.load()) fail(DGKR_COMM_ERROR, "libnccl.so.2 not found");
-        if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
-        CK(cudaSetDevice(ctx->device));
-        auto c = std::make_unique<NcclComm>();
-        c->rank = rank;
-        c->world = world;
-        ncclUniqueId id;
-        std::memcpy(&id, uid128, sizeof(id));
-        NCK(g_nccl.commInitRank(&c->comm, world, id, rank));
-        *out = c.release();
-    });
-}
-
-void dgkr_comm_destroy(dgkr_comm* c) { delete c; }
-
-int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, std::size_t slot_bytes,
-                         dgkr_comm** out) {
-    return guard([&] {
-        if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
-        if (!name || name[0] != '/') fail(DGKR_INVALID_ARGUMENT, "shm name must start with '/'");
-        auto c = std::make_unique<ShmComm>();
-        c->rank = rank;
-        c->world = world;
-        c->name = name;
-        c->owner = rank == 0;
-        const std::size_t hb = 64;
-        c->map_bytes = hb + static_cast<std::size_t>(world) * slot_bytes;
-        const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
-        if (fd < 0) fail(DGKR_COMM_ERROR, std::string("shm_open failed: ") + name);
-        if (ftruncate(fd, static_cast<off_t>(c->map_bytes)) != 0) {
-            close(fd);
-            fail(DGKR_COMM_ERROR, "ftruncate failed");
-        }
-        void* p = mmap(nullptr, c->map_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-        close(fd);
-        if (p == MAP_FAILED) fail(DGKR_COMM_ERROR, "mmap failed");
-        c->hdr = static_cast<ShmHeader*>(p);
-        c->hdr->world = static_cast<std::uint32_t>(world);
-        c->hdr->slot_bytes = slot_bytes;
-        c->data = static_cast<std::uint8_t*>(p) + hb;
-        if (ctx) {  // device exchanges need the pinned bounce buffer; host-only test comms do not
-            CK(cudaSetDevice(ctx->device));
-            CK(cudaMallocHost(reinterpret_cast<void**>(&c->bounce), std::max<std::size_t>(slot_bytes, 64)));
-        }
-        // not cudaHostRegister'ed: ranks sharing one GPU would register the same
-        // physical pages twice, which corrupted device state (measured with 8 lanes x 2 ranks)
-        (void)ctx;
-        *out = c.release();
-    });
-}
-
-int dgkr_comm_allgather_host(dgkr_comm* comm, const void* in, std::size_t bytes, void* out) {
-    return guard([&] {
-        auto* s = dynamic_cast<ShmComm*>(comm);
-        if (!s) fail(DGKR_UNSUPPORTED, "host all-gather is a shared-memory communicator test hook");
-        s->allgather_host(in, bytes, out);
     });
 }
 

@@ -1,0 +1,368 @@
+// Host runtime shared by the C-ABI translation units (prover.cpp, comm.cpp,
+// ext.cpp): error guard, device buffers, field handle, lanes (stream +
+// workspace + pinned staging), the context, and the communicator interface.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <condition_variable>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "dgkr_b200.h"
+#include "fe.hpp"
+#include "host_core.hpp"
+#include "kernels.hpp"
+
+using namespace dgkr_b200;
+
+namespace dgkr_b200 {
+
+/// last error message of a C-ABI call on this thread (dgkr_last_error)
+inline thread_local std::string g_err;
+
+template <class Fn>
+int guard(Fn&& fn) {
+    try {
+        fn();
+        return DGKR_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("host allocation failed: ") + e.what();
+        return DGKR_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DGKR_LOGIC_ERROR;
+    }
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) fail(DGKR_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(std::size_t count) {
+        if (count <= n && p) return;
+        release();
+        CK(cudaMalloc(reinterpret_cast<void**>(&p), std::max<std::size_t>(count, 1) * sizeof(T)));
+        n = std::max<std::size_t>(count, 1);
+    }
+};
+
+inline Fe to_fe(const U256& x) {
+    Fe f;
+    std::memcpy(f.v, x.w, 32);
+    return f;
+}
+inline U256 to_u256(const Fe& f) {
+    U256 x;
+    std::memcpy(x.w, f.v, 32);
+    return x;
+}
+
+inline std::uint32_t log2_exact(std::uint64_t n) {  // circuit.hpp:57-61
+    std::uint32_t l = 0;
+    while ((std::uint64_t{1} << l) < n) ++l;
+    return l;
+}
+inline std::uint64_t next_pow2(std::uint64_t n) {  // circuit.hpp:43-47
+    std::uint64_t p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+inline void put32(std::vector<std::uint8_t>& out, std::uint32_t v) {
+    for (int i = 0; i < 4; ++i) out.push_back(static_cast<std::uint8_t>(v >> (8 * i)));
+}
+
+inline void emit(const std::vector<std::uint8_t>& bytes, std::uint8_t* out, std::size_t cap, std::size_t* len) {
+    *len = bytes.size();
+    if (bytes.size() > cap) fail(DGKR_CAPACITY, "output buffer too small");
+    if (!bytes.empty()) std::memcpy(out, bytes.data(), bytes.size());
+}
+
+}  // namespace dgkr_b200
+
+// ===========================================================================
+// Opaque handles
+// ===========================================================================
+struct dgkr_field {
+    HostField f;
+    FieldKind kind = FieldKind::Runtime;
+    RtFieldHost rt{};
+    U256 fold_pow[8];  // canonical 2^(32k+64) mod p, for the fold constants
+    // NTT data (Montgomery): two-adicity s, w of order 2^s, coset shift g =
+    // smallest quadratic non-residue (not in any 2-power subgroup), g^-1
+    unsigned two_adicity = 0;
+    U256 root{}, coset{}, coset_inv{};
+
+    /// w_N for N = 2^log_n (log_n <= two_adicity)
+    U256 root_of_unity(unsigned log_n) const {
+        if (log_n > two_adicity) fail(DGKR_UNSUPPORTED, "domain larger than the field's 2-adic subgroup");
+        U256 w = root;
+        for (unsigned i = log_n; i < two_adicity; ++i) w = f.mul(w, w);
+        return w;
+    }
+
+    /// {c_0..c_7, r} with c_k = mont(r, 2^(32k+64)) (field.cuh FoldConst)
+    void fold_const(const U256& r, U256 out[9]) const {
+        for (int k = 0; k < 8; ++k) out[k] = f.mul(r, fold_pow[k]);
+        out[8] = r;
+    }
+};
+
+/// Runtime-modulus constants live in one __constant__ block per device;
+/// lanes share it (concurrent lanes must use the same runtime field).
+struct RtState {
+    std::mutex mu;
+    bool valid = false;
+    RtFieldHost cur{};
+};
+
+/// device buffers of the NTT / RS / FRI entry points, kept across calls
+/// (multi-GiB at C5 sizes: cudaMalloc/cudaFree per call would dominate)
+struct NttWs {
+    DBuf<std::uint8_t> stage, dbuf;
+    DBuf<Fe> x, a, tw, cpow, scratch, twinv;
+    std::vector<std::unique_ptr<DBuf<Fe>>> layer;
+    std::vector<std::unique_ptr<DBuf<std::uint8_t>>> tree;
+    DBuf<std::uint64_t> didx;
+    // beacon tree (config C3)
+    DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
+};
+
+/// One in-flight proof: a CUDA stream, its reduction workspace, pinned
+/// staging and profile counters. A context owns one lane per concurrent
+/// proof (lane 0 serves the single-call API).
+struct Lane {
+    int device = 0;
+    int sms = 0;
+    int index = 0;
+    RtState* rt = nullptr;
+    cudaStream_t st = nullptr;
+    ReduceWs ws;
+    DBuf<Fe> partials, result;
+    DBuf<unsigned> counter;
+    DBuf<Fe> d_small;      // challenges, points, seeds, finals
+    DBuf<int> d_err;
+    DBuf<int> d_flag;       // kernel-raised predicate flags (distinct checks)
+    Fe* h_small = nullptr;  // pinned mirror of d_small
+    // pinned staging layout (Fe units): [0] challenge, [1..4) reduction
+    // results, [16, 8192) eq-table points/seeds, [8192, 12288) slot values,
+    // [12288, 16384) round finals.
+    static constexpr std::size_t kSmall = 1 << 14;
+    static constexpr std::size_t kEqOff = 16, kEqOff2 = 4112, kVxOff = 8192, kFinalsOff = 12288;
+    static constexpr std::size_t kGatherOff = 14336;  // [14336, 16384): all-gathered round sums (<= 682 ranks)
+    bool profile_on = false;
+    dgkr_profile prof{};
+    /// profile-only CUDA-event bracket around a kernel group: tbeg(); ...; tend(prof.x_ms)
+    void tbeg() {
+        if (profile_on) CK(cudaEventRecord(ev0, st));
+    }
+    void tend(double& acc) {
+        if (!profile_on) return;
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        acc += ms;
+    }
+    std::unique_ptr<NttWs> ntt_ws;
+    NttWs& nttws() {
+        if (!ntt_ws) ntt_ws = std::make_unique<NttWs>();
+        return *ntt_ws;
+    }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    Lane(int dev, int sm_count, int idx, RtState* rts) : device(dev), sms(sm_count), index(idx), rt(rts) {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ws.num_sms = sms;
+        ws.max_blocks = sms * 8;
+        partials.ensure(static_cast<std::size_t>(ws.max_blocks) * 3);
+        result.ensure(4);
+        counter.ensure(1);
+        CK(cudaMemset(counter.p, 0, sizeof(unsigned)));
+        ws.partials = partials.p;
+        ws.result = result.p;
+        ws.counter = counter.p;
+        d_small.ensure(kSmall);
+        d_err.ensure(1);
+        CK(cudaMemset(d_err.p, 0, sizeof(int)));
+        d_flag.ensure(2);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
+        CK(cudaEventCreate(&ev0));
+        CK(cudaEventCreate(&ev1));
+        CK(cudaEventCreateWithFlags(&ev_sync, cudaEventBlockingSync | cudaEventDisableTiming));
+        if (const char* e = std::getenv("DGKR_SPIN_US")) spin_ms = std::atof(e) * 1e-3;
+    }
+    Lane(const Lane&) = delete;
+    Lane& operator=(const Lane&) = delete;
+
+    ~Lane() {
+        if (ev_sync) cudaEventDestroy(ev_sync);
+        if (h_small) cudaFreeHost(h_small);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    FieldKind use(const dgkr_field* f) {
+        if (f->kind == FieldKind::Runtime) {
+            std::lock_guard<std::mutex> lk(rt->mu);
+            if (!rt->valid || std::memcmp(&rt->cur, &f->rt, sizeof(RtFieldHost)) != 0) {
+                upload_rt_field(f->rt, st);
+                CK(cudaStreamSynchronize(st));
+                rt->cur = f->rt;
+                rt->valid = true;
+            }
+        }
+        return f->kind;
+    }
+
+    /// Wait for the stream: poll briefly (round kernels on small tables finish
+    /// in microseconds), then block on an event so that waiting lanes leave
+    /// the host cores to the lanes running their serial SHA-256 chains.
+    void sync() {
+        CK(cudaEventRecord(ev_sync, st));
+        const double t0 = now_ms();
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(ev_sync);
+            if (q == cudaSuccess) return;
+            if (q != cudaErrorNotReady) CK(q);
+            if (now_ms() - t0 > spin_ms) break;
+        }
+        CK(cudaEventSynchronize(ev_sync));
+    }
+    cudaEvent_t ev_sync = nullptr;
+    double spin_ms = 1e12;  // measured: polling beats blocking even with 16 lanes (DGKR_SPIN_US to change)
+
+    void begin_call() {
+        std::memset(&prof, 0, sizeof(prof));
+        prof.total_ms = now_ms();
+    }
+    void end_call() { prof.total_ms = now_ms() - prof.total_ms; }
+
+    void h2d(void* dst, const void* src, std::size_t n) {
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+        prof.h2d_bytes += n;
+    }
+    void d2h(void* dst, const void* src, std::size_t n) {
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
+        prof.d2h_bytes += n;
+    }
+    void launched(std::uint64_t n = 1) { prof.launches += n; }
+
+    void check_err_flag(const char* what) {
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        sync();
+        if (h) {
+            CK(cudaMemsetAsync(d_err.p, 0, sizeof(int), st));
+            fail(DGKR_INVALID_ARGUMENT, std::string("non-canonical field element encoding (") + what + ")");
+        }
+    }
+
+    /// canonical bytes (host) -> Montgomery Fe (device)
+    void upload_elems(const dgkr_field* f, const std::uint8_t* host, std::uint64_t n, Fe* dst, DBuf<std::uint8_t>& stage) {
+        if (n == 0) return;
+        const std::size_t bytes = n * f->f.width();
+        stage.ensure(bytes);
+        h2d(stage.p, host, bytes);
+        launch_from_canonical(use(f), stage.p, static_cast<int>(f->f.width()), dst, n, d_err.p, st);
+        launched();
+        check_err_flag("input tables");
+    }
+};
+
+/// The context is lane 0 itself; extra lanes (concurrent proofs) are
+/// created on demand and share the runtime-field state.
+struct dgkr_ctx : Lane {
+    std::unique_ptr<RtState> rt_owner;
+    std::mutex lanes_mu;
+    std::vector<std::unique_ptr<Lane>> extra;  // lanes 1..
+    cudaEvent_t user_ev[8] = {};
+
+    dgkr_ctx(int dev, int sm_count, std::unique_ptr<RtState> rts)
+        : Lane(dev, sm_count, 0, rts.get()), rt_owner(std::move(rts)) {}
+
+    Lane* lane(int i) {
+        if (i == 0) return this;
+        std::lock_guard<std::mutex> lk(lanes_mu);
+        while (static_cast<int>(extra.size()) < i)
+            extra.push_back(std::make_unique<Lane>(device, sms, static_cast<int>(extra.size()) + 1, rt_owner.get()));
+        return extra[i - 1].get();
+    }
+
+    ~dgkr_ctx() {
+        for (auto& e : user_ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+// ===========================================================================
+// Device communication for the data-parallel (multi-GPU) prover. The protocol
+// code is shared; only the transport differs (comm.hpp):
+//   NcclComm    one process per GPU, NCCL over NVLink/NVSwitch
+//   ShmComm     one process per GPU on one node, POSIX shared memory per lane
+//   ThreadComm  ranks as host threads driving lanes of ONE GPU, exchanging
+//               through host memory at barriers (tests the distributed
+//               protocol on a single device; no kernel ever waits on another)
+// Per sum-check round the only traffic is an all-gather of 2-3 field elements
+// per rank (cluster.hpp:272-286); at each phase boundary an all-gather of the
+// final table values (cluster.hpp:295-309).
+// ===========================================================================
+struct dgkr_comm {
+    int rank = 0;
+    int world = 1;
+    DBuf<std::uint8_t> scratch;
+    virtual ~dgkr_comm() = default;
+    /// d_recv (device) = concatenation over ranks of each rank's d_send
+    virtual void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) = 0;
+    /// h_recv (host) = concatenation over ranks of each rank's d_send
+    virtual void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) {
+        scratch.ensure(static_cast<std::size_t>(world) * bytes);
+        allgather(d_send, scratch.p, bytes, L);
+        L->d2h(h_recv, scratch.p, static_cast<std::size_t>(world) * bytes);
+        L->sync();
+    }
+    /// rank `root`: h_recv (host) = concatenation over ranks of d_send; others: untouched
+    virtual void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) = 0;
+    /// every rank's h (host, `bytes`) = rank `root`'s h
+    virtual void broadcast_host(void* h, std::size_t bytes, Lane* L, int root) = 0;
+};
