@@ -27,7 +27,7 @@ proof (copy index = high variables, as the Sisu layout).
 """
 from __future__ import annotations
 
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
@@ -59,6 +59,7 @@ class _Layout:
         self.words: Dict[Tuple[str, int], List[int]] = {}  # (name, t) -> 32 bit wires (LSB first)
         self.qbits: Dict[Tuple[str, int], List[int]] = {}  # carry quotient bits
         self.bits: List[int] = []  # every wire that must be boolean
+        self.rlc: List[int] = []   # random-linear-combination coefficients (rlc circuits)
 
     def alloc(self, k: int) -> List[int]:
         r = list(range(self.n, self.n + k))
@@ -186,8 +187,16 @@ def _small_sigma(B: _Builder, w: List[int], r1: int, r2: int, s: int) -> List[Tu
     return out
 
 
-def build_compression_circuit() -> Tuple[int, Flat, _Layout]:
-    """-> (input_size (power of two), flat circuit, input layout) of one compression"""
+def build_compression_circuit(rlc: bool = False) -> Tuple[int, Flat, _Layout]:
+    """-> (input_size (power of two), flat circuit, input layout) of one compression.
+
+    rlc=False: the output layer is the constraint vector (8,192 padded outputs
+    per copy, every one absorbed by the reference transcript).
+    rlc=True: one more layer folds the constraints of a copy into ONE output
+    sum_i R_i c_i, with the coefficients R_i public inputs (layout.rlc). In the
+    committed-witness setting the caller draws them by Fiat-Shamir after
+    committing the witness (e.g. from a transcript over pcs_commit's root);
+    a non-zero constraint then survives with probability >= 1 - n/p."""
     L = _layout()
     B = _Builder(L)
     pw, npw, one = L.pow, L.npow, L.const["one"]
@@ -244,6 +253,10 @@ def build_compression_circuit() -> Tuple[int, Flat, _Layout]:
     for bw in L.bits:
         constraints.append([(1, 0, bw, 0, bw), (1, 0, bw, 0, m1)])
     B.layers[3] = constraints
+    L.rlc = []
+    if rlc:
+        L.rlc = L.alloc(len(constraints))
+        B.layers.append([[(1, 0, L.rlc[i], 4, i) for i in range(len(constraints))]])
     # pad every layer to a power of two with zero gates (data-parallel precondition)
     zero = L.const["zero"]
     input_size = 1
@@ -308,11 +321,19 @@ def compress_trace(h_in: np.ndarray, block: np.ndarray):
     return {"W": W, "qw": qw, "A": A, "E": E, "qa": qa, "qe": qe, "hout": hout, "qh": qh}
 
 
+def rlc_coefficients(p: int, seed: bytes, n: int) -> List[int]:
+    """n coefficients R_i = SHA256(seed || LE64 i) mod p (seed: e.g. a
+    transcript challenge drawn after the witness commitment)"""
+    import hashlib
+    return [int.from_bytes(hashlib.sha256(seed + i.to_bytes(8, "little")).digest(), "little") % p for i in range(n)]
+
+
 def sha256_witness(p: int, layout: _Layout, input_size: int, h_in: np.ndarray,
-                   block: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+                   block: np.ndarray, rlc: Optional[List[int]] = None) -> Tuple[np.ndarray, np.ndarray]:
     """input layers (N copies x input_size field elements, canonical bytes,
     copy-major, uint8[N * input_size * w]) for the compression circuit, and
-    the digests (N, 8)."""
+    the digests (N, 8). rlc: the R_i of an rlc=True circuit (shared by all
+    copies)."""
     tr = compress_trace(h_in, block)
     N = tr["W"].shape[0]
     w = (p.bit_length() + 7) // 8
@@ -327,6 +348,11 @@ def sha256_witness(p: int, layout: _Layout, input_size: int, h_in: np.ndarray,
     for i in range(NPOW):
         put_const(layout.pow[i], 1 << i)
         put_const(layout.npow[i], -(1 << i))
+    if layout.rlc:
+        if rlc is None or len(rlc) != len(layout.rlc):
+            raise ValueError("this circuit needs len(layout.rlc) coefficients")
+        for idx, v in zip(layout.rlc, rlc):
+            put_const(idx, v)
     out = np.broadcast_to(base, (N, input_size, w)).copy()
 
     def put_bits(idx, val, nb):

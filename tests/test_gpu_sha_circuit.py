@@ -75,3 +75,26 @@ def test_sha_merkle_path_circuit(ctx, sha):
     per = dc.output_size // copies
     nz = {i // per for i, v in enumerate(outs) if v}
     assert nz == {k}
+
+
+def test_sha_rlc_circuit_matches_reference(ctx):
+    """the rlc=True circuit (one output per compression) proved by the GPU,
+    byte-equal to the compiled reference; outputs all zero"""
+    R = pytest.importorskip("oracle.refbind")
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    insz, flat, L = S.build_compression_circuit(rlc=True)
+    p = O.BN254_P
+    f, of = P.Field(p), O.Field(p)
+    rng = np.random.default_rng(8)
+    n = 2
+    coeffs = S.rlc_coefficients(p, b"gpu", len(L.rlc))
+    inputs, _ = S.sha256_witness(p, L, insz, rng.integers(0, 1 << 32, (n, 8), dtype=np.uint64),
+                                 rng.integers(0, 1 << 32, (n, 16), dtype=np.uint64), rlc=coeffs)
+    dc = P.Circuit(ctx, insz, *flat, n_copies=n)
+    got = P.gkr_prove(ctx, dc, inputs, P.Transcript(f, "rlc"))
+    assert _outs(got, f.width) == [0, 0]
+    full_in, full_flat = W.replicate(insz, flat, n)
+    circ = O.Circuit.from_flat(full_in, *full_flat)
+    want, _ = R.gkr_prove(of, "rlc", [], circ, of.elems_from_bytes(inputs.tobytes()), flat=full_flat)
+    assert got == want

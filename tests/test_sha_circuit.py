@@ -61,3 +61,21 @@ def test_corrupted_witness_is_caught(circ, what):
     assert any(c.evaluate(vals, O.BN254_P)[-1])
     vals[idx] = 2  # not a bit
     assert any(c.evaluate(vals, O.BN254_P)[-1])
+
+
+def test_rlc_circuit_single_output():
+    """rlc=True folds a copy's constraints into one output sum_i R_i c_i"""
+    insz, flat, L = S.build_compression_circuit(rlc=True)
+    c = O.Circuit.from_flat(insz, *flat)
+    assert int(flat[0][-1] - flat[0][-2]) == 1 and len(L.rlc) > 7000
+    R = S.rlc_coefficients(O.BN254_P, b"test", len(L.rlc))
+    rng = np.random.default_rng(9)
+    inp, _ = S.sha256_witness(O.BN254_P, L, insz, rng.integers(0, 1 << 32, (1, 8), dtype=np.uint64),
+                              rng.integers(0, 1 << 32, (1, 16), dtype=np.uint64), rlc=R)
+    vals = O.BN254.elems_from_bytes(inp.tobytes())
+    assert c.evaluate(vals, O.BN254_P)[-1] == [0]
+    vals[L.words[("w", 20)][0]] ^= 1
+    assert c.evaluate(vals, O.BN254_P)[-1][0] != 0
+    with pytest.raises(ValueError):
+        S.sha256_witness(O.BN254_P, L, insz, rng.integers(0, 1 << 32, (1, 8), dtype=np.uint64),
+                         rng.integers(0, 1 << 32, (1, 16), dtype=np.uint64))

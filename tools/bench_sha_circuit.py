@@ -1,10 +1,20 @@
 """§8(f) rank 2 / config C3 in-circuit: SHA-256 compressions proved as a
-data-parallel GKR circuit (sha_circuit.py; one compression per copy, 73,728
-padded gates and 161,818 wires per copy, depth 4). For each batch: Merkle
-paths of depth 56 over 64-byte nodes (114 compressions per path incl. the
-leaf), padded to a power-of-two copy count; GPU proof time (median of 3,
-inputs resident), gates/s and compressions/s, and the compiled reference's
-gkr_prove on a 2-copy sample (extrapolated per compression)."""
+data-parallel GKR circuit (sha_circuit.py; one compression per copy, depth 4,
+or 5 with --rlc). Merkle paths of depth 56 over 64-byte nodes (114
+compressions per path incl. the leaf), padded to a power-of-two copy count.
+
+Per batch: GPU proof time (median of 3, inputs resident), gates/s and
+compressions/s, the kernel / transcript breakdown, and the compiled
+reference's gkr_prove on a 2-copy sample (per compression). --rlc folds each
+copy's constraints into one output (sum R_i c_i), so the reference
+transcript's serial absorb covers 1 output per compression instead of 8,192.
+--stream L: steady-state throughput of 2L proofs of the largest batch over L
+lanes. C3 (4,096 validators x depth 56 = 466,944 compressions) is reported as
+the time at the measured compressions/s.
+
+usage: python tools/bench_sha_circuit.py [--rlc] [--stream L] [paths ...]"""
+import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -18,17 +28,27 @@ sys.path.insert(0, ROOT)
 import paper_2404_10404_b200 as P  # noqa: E402
 from paper_2404_10404_b200 import sha_circuit as S  # noqa: E402
 from paper_2404_10404_b200 import workloads as W  # noqa: E402
+from paper_2404_10404_b200._lib import check, lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("paths", nargs="*", type=int, default=[1, 8, 32])
+ap.add_argument("--rlc", action="store_true")
+ap.add_argument("--stream", type=int, default=0)
+args = ap.parse_args()
 
 ctx = P.Context(0)
 f = P.Field.bn254()
-insz, flat, L = S.build_compression_circuit()
+insz, flat, L = S.build_compression_circuit(rlc=args.rlc)
+coeffs = S.rlc_coefficients(f.p, b"bench.sha", len(L.rlc)) if args.rlc else None
 gates_per_copy = int(flat[0][-1])
 depth = 56
+C3_COMPRESSIONS = 4096 * (2 + 2 * depth) // 2  # 4,096 paths x 114 compressions
 rng = np.random.default_rng(56)
 ref_per_comp = None
-for n_paths in [int(x) for x in (sys.argv[1:] or ["1", "8", "32"])]:
+last = None
+for n_paths in args.paths:
     hs, bs = [], []
-    for p in range(n_paths):
+    for _ in range(n_paths):
         leaf = bytes(rng.integers(0, 256, 64, dtype=np.uint8))
         sibs = [bytes(rng.integers(0, 256, 32, dtype=np.uint8)) for _ in range(depth)]
         h, b, _ = S.merkle_path_compressions(leaf, sibs, int(rng.integers(0, 1 << 40)))
@@ -42,11 +62,9 @@ for n_paths in [int(x) for x in (sys.argv[1:] or ["1", "8", "32"])]:
     h_in = np.concatenate([h_in, np.tile(S.IV, (copies - comps, 1))])
     blocks = np.concatenate([blocks, np.zeros((copies - comps, 16), np.uint64)])
     t0 = time.perf_counter()
-    inputs, _ = S.sha256_witness(f.p, L, insz, h_in, blocks)
+    inputs, _ = S.sha256_witness(f.p, L, insz, h_in, blocks, rlc=coeffs)
     t_wit = time.perf_counter() - t0
     circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
-    import ctypes as C
-    from paper_2404_10404_b200._lib import check, lib
     check(lib().dgkr_circuit_load_inputs(ctx.handle, circ.handle, f.handle, inputs.ctypes.data_as(C.c_void_p)))
     cap = circ.proof_bound(f)
     buf = C.create_string_buffer(cap)
@@ -69,9 +87,10 @@ for n_paths in [int(x) for x in (sys.argv[1:] or ["1", "8", "32"])]:
     prof = ctx.profile()
     ctx.set_profile(False)
     gates = copies * gates_per_copy
-    line = {"config": f"SHA-256 in circuit: {n_paths} Merkle path(s) x depth {depth} = {comps} compressions "
-                      f"({copies} copies)", "gates": gates, "gpu_prove_ms": 1e3 * dt,
-            "gates_per_s": gates / dt, "compressions_per_s": comps / dt, "witness_gen_s": t_wit,
+    line = {"config": f"SHA-256 in circuit{' (rlc)' if args.rlc else ''}: {n_paths} Merkle path(s) x depth {depth}"
+                      f" = {comps} compressions ({copies} copies)", "gates": gates, "outputs": n_out,
+            "gpu_prove_ms": 1e3 * dt, "gates_per_s": gates / dt, "compressions_per_s": comps / dt,
+            "c3_4096_validators_s_at_this_rate": C3_COMPRESSIONS / (comps / dt), "witness_gen_s": t_wit,
             "breakdown_ms": {k: prof[k] for k in ("round_ms", "bookkeep_ms", "evaluate_ms", "host_transcript_ms",
                                                   "output_absorb_ms")}}
     if ref_per_comp is None:
@@ -92,3 +111,19 @@ for n_paths in [int(x) for x in (sys.argv[1:] or ["1", "8", "32"])]:
         line["ref_compressions_per_s"] = 1 / ref_per_comp
         line["ref_note"] = "compiled reference gkr_prove on 2 copies, single thread"
     print(json.dumps(line), flush=True)
+    last = (circ, inputs, comps, copies, gates)
+
+if args.stream and last:
+    circ, inputs, comps, copies, gates = last
+    lanes = args.stream
+    for lane in range(lanes):
+        P.load_inputs_lane(ctx, circ, f, lane, inputs)
+    P.gkr_prove_stream(ctx, circ, lanes, lanes, f)  # warm-up
+    n = 2 * lanes
+    t0 = time.perf_counter()
+    P.gkr_prove_stream(ctx, circ, n, lanes, f)
+    dt = time.perf_counter() - t0
+    print(json.dumps({"config": f"SHA-256 in circuit{' (rlc)' if args.rlc else ''}: stream of {n} proofs x {comps} "
+                                f"compressions over {lanes} lanes", "compressions_per_s": n * comps / dt,
+                      "gates_per_s": n * gates / dt,
+                      "c3_4096_validators_s_at_this_rate": C3_COMPRESSIONS / (n * comps / dt)}), flush=True)
