@@ -202,6 +202,15 @@ int dgkr_circuit_load(dgkr_ctx* ctx, const char* path, uint32_t n_copies, dgkr_c
 int dgkr_gkr_verify(const dgkr_circuit* c, const dgkr_field* f, const uint8_t* outputs, size_t n_outputs,
                     const uint8_t* inputs, const uint8_t* proof, size_t len, dgkr_transcript* t, int* accept);
 
+/* The input-layer claims of a proof (registry[0] after gkr_verify, gkr.hpp:
+ * 309-310), replayed like dgkr_gkr_verify, for composing the proof with a
+ * commitment of the inputs (open the input table at each term's point and
+ * check sum_t weight_t * value_t = claim value). out: u32 n_claims, per claim
+ * u32 n_terms, per term (u32 n_vars, point, weight), then the value; canonical
+ * elements. *accept = 0 (and no claims) when the proof does not verify. */
+int dgkr_gkr_input_claims(const dgkr_circuit* c, const dgkr_field* f, const uint8_t* proof, size_t len,
+                          dgkr_transcript* t, int* accept, uint8_t* out, size_t cap, size_t* out_len);
+
 /* ---- multi-GPU data-parallel GKR (Sisu; cluster.hpp:182-320 generalised) ----
  * One process per GPU. Rank r proves copies [r*n, (r+1)*n) of a uniform-width
  * data-parallel circuit created with n_copies = n (the rank index is the top

@@ -1711,6 +1711,33 @@ int dgkr_gkr_verify(const dgkr_circuit* c, const dgkr_field* f, const std::uint8
     });
 }
 
+int dgkr_gkr_input_claims(const dgkr_circuit* c, const dgkr_field* f, const std::uint8_t* proof, std::size_t len,
+                          dgkr_transcript* t, int* accept, std::uint8_t* out, std::size_t cap, std::size_t* out_len) {
+    return guard([&] {
+        const HostField& F = f->f;
+        Transcript tr(&F, t->state, t->draws);
+        std::vector<LayerClaim> claims;
+        const bool ok = gkr_verify_host(*c, F, proof, len, nullptr, 0, tr, claims);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        *accept = ok ? 1 : 0;
+        std::vector<std::uint8_t> b;
+        put32(b, static_cast<std::uint32_t>(ok ? claims.size() : 0));
+        if (ok) {
+            for (const auto& cl : claims) {
+                put32(b, static_cast<std::uint32_t>(cl.terms.size()));
+                for (const auto& term : cl.terms) {
+                    put32(b, static_cast<std::uint32_t>(term.point.size()));
+                    for (const auto& x : term.point) append_elem(b, F, x);
+                    append_elem(b, F, term.weight);
+                }
+                append_elem(b, F, cl.value);
+            }
+        }
+        emit(b, out, cap, out_len);
+    });
+}
+
 int dgkr_circuit_create(dgkr_ctx* ctx, std::uint32_t input_size, std::uint32_t depth, const std::uint64_t* lgs,
                         const std::uint64_t* gns, const std::uint32_t* nested, const std::uint64_t* min_padded,
                         std::uint32_t n_copies, dgkr_circuit** out) {

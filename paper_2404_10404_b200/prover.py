@@ -314,6 +314,42 @@ def gkr_verify(circuit: Circuit, proof: bytes, tr: Transcript, outputs: Optional
     return bool(acc.value)
 
 
+def gkr_input_claims(circuit: Circuit, proof: bytes, tr: Transcript):
+    """(accept, claims) with claims = [([(point, weight), ...], value)] of the
+    input layer (dgkr_gkr_input_claims)"""
+    f = tr.field
+    w = f.width
+    cap = 4096 + 8 * len(proof)
+    out, ln = _out(cap)
+    acc = C.c_int()
+    check(lib().dgkr_gkr_input_claims(circuit.handle, f.handle, C.c_char_p(bytes(proof)), C.c_size_t(len(proof)),
+                                      C.byref(tr.t), C.byref(acc), out, C.c_size_t(cap), C.byref(ln)))
+    raw = out.raw[: ln.value]
+    pos = 0
+
+    def u32():
+        nonlocal pos
+        v = int.from_bytes(raw[pos:pos + 4], "little")
+        pos += 4
+        return v
+
+    def elem():
+        nonlocal pos
+        v = int.from_bytes(raw[pos:pos + w], "little")
+        pos += w
+        return v
+
+    claims = []
+    for _ in range(u32()):
+        terms = []
+        for _ in range(u32()):
+            nv = u32()
+            point = [elem() for _ in range(nv)]
+            terms.append((point, elem()))
+        claims.append((terms, elem()))
+    return bool(acc.value), claims
+
+
 def gkr_prove_batch(ctx: Context, circuit: Circuit, inputs: Optional[Sequence[Elems]], trs: Sequence[Transcript],
                     out_bufs=None) -> List[bytes]:
     """n independent gkr_prove calls run concurrently (one lane = stream +

@@ -144,3 +144,23 @@ def test_cli_bench(tmp_path):
     rows = out.read_text().splitlines()
     assert rows[0] == "numval,time" and [x.split(",")[0] for x in rows[1:]] == ["1", "2", "4"]
     assert _cli("bench", "--workers", "3", "--vars", "8", "--out", str(out)).returncode == 2
+
+
+def test_input_claims_match_the_inputs(ctx):
+    """dgkr_gkr_input_claims: the verifier's input-layer claims, each equal to
+    sum_t weight_t * MLE(inputs, point_t) (check_input_claims, gkr.hpp:314-325)"""
+    p = O.BN254_P
+    f, of = P.Field(p), O.Field(p)
+    circ = R.random_general_circuit(17, input_size=6, depth=4, max_gates=9, max_nested=3)
+    flat = circ.to_flat()
+    dc = P.Circuit(ctx, circ.input_size, *flat)
+    inputs = O.random_elements(of, circ.input_size, np.random.default_rng(17))
+    proof = P.gkr_prove(ctx, dc, inputs, P.Transcript(f, "claims"))
+    ok, claims = P.gkr_input_claims(dc, proof, P.Transcript(f, "claims"))
+    assert ok and claims
+    table = list(inputs) + [0] * (circ.padded_size(0) - len(inputs))
+    for terms, value in claims:
+        assert sum(w * O.mle_eval(table, pt, p) for pt, w in terms) % p == value
+    tam = bytearray(proof)
+    tam[-40] ^= 1
+    assert P.gkr_input_claims(dc, bytes(tam), P.Transcript(f, "claims")) == (False, [])
