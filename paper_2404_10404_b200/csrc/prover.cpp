@@ -1598,6 +1598,7 @@ bool gkr_verify_host(const dgkr_circuit& c, const HostField& F, const std::uint8
     for (std::uint32_t layer = D; layer >= 1; --layer) {
         const auto& C = *c.cons[layer];
         const std::uint32_t na = rd.u32();
+        if (!rd.ok || na > (len - rd.pos) / F.width()) return false;  // count exceeds the remaining bytes
         std::vector<U256> pa(na);
         for (auto& a : pa) a = rd.elem();
         const std::uint32_t sb_len = rd.u32();
@@ -1804,6 +1805,14 @@ int dgkr_circuit_load(dgkr_ctx* ctx, const char* path, std::uint32_t n_copies, d
         const std::uint32_t depth = hdr[1];
         if (depth == 0 || depth > (1u << 20) || n_gates > (1ull << 40) || n_nested > (1ull << 40))
             fail(DGKR_INVALID_ARGUMENT, "implausible circuit header");
+        // the header's counts must describe exactly this file (before any allocation)
+        if (std::fseek(fp, 0, SEEK_END) != 0) fail(DGKR_INVALID_ARGUMENT, "cannot size circuit file");
+        const long fsize = std::ftell(fp);
+        const std::uint64_t want = 40 + 8ull * (depth + 1) + 8ull * (n_gates + 1) + 20ull * n_nested +
+                                   (hdr[3] ? 8ull * (depth + 1) : 0);
+        if (fsize < 0 || static_cast<std::uint64_t>(fsize) != want)
+            fail(DGKR_INVALID_ARGUMENT, "circuit file size does not match its header");
+        if (std::fseek(fp, 40, SEEK_SET) != 0) fail(DGKR_INVALID_ARGUMENT, "cannot seek circuit file");
         std::vector<std::uint64_t> lgs(depth + 1), gns(n_gates + 1), minp;
         std::vector<std::uint32_t> nested(5 * n_nested);
         if (std::fread(lgs.data(), 8, lgs.size(), fp) != lgs.size() || std::fread(gns.data(), 8, gns.size(), fp) != gns.size() ||

@@ -164,3 +164,48 @@ def test_input_claims_match_the_inputs(ctx):
     tam = bytearray(proof)
     tam[-40] ^= 1
     assert P.gkr_input_claims(dc, bytes(tam), P.Transcript(f, "claims")) == (False, [])
+
+
+def test_fuzz_verifier_and_loader(ctx, tmp_path):
+    """malformed proofs reject (no exception, no crash); corrupted circuit files
+    raise InvalidArgument"""
+    p = O.BN254_P
+    f = P.Field(p)
+    insz, flat = W.layered_circuit(seed=3, log_width=4, depth=3)
+    dc = P.Circuit(ctx, insz, *flat, n_copies=2)
+    inputs = W.random_inputs(p, insz * 2, 5)
+    proof = P.gkr_prove(ctx, dc, inputs, P.Transcript(f, "fz"))
+    rng = np.random.default_rng(99)
+    for trial in range(200):
+        b = bytearray(proof)
+        kind = trial % 4
+        if kind == 0:
+            for _ in range(int(rng.integers(1, 8))):
+                b[int(rng.integers(0, len(b)))] ^= int(rng.integers(1, 256))
+        elif kind == 1:
+            b = b[: int(rng.integers(0, len(b)))]
+        elif kind == 2:
+            b = bytearray(rng.integers(0, 256, int(rng.integers(0, 2 * len(proof))), dtype=np.uint8).tobytes())
+        else:
+            b += bytes(int(rng.integers(1, 64)))
+        assert not P.gkr_verify(dc, bytes(b), P.Transcript(f, "fz"), inputs=inputs)
+        assert P.gkr_input_claims(dc, bytes(b), P.Transcript(f, "fz"))[0] is False
+    assert P.gkr_verify(dc, proof, P.Transcript(f, "fz"), inputs=inputs)
+    # binary circuit files: corrupt header fields and truncations
+    path = str(tmp_path / "c.dgkrc")
+    dc.save(path)
+    blob = open(path, "rb").read()
+    for trial in range(40):
+        b = bytearray(blob)
+        if trial % 2:
+            off = int(rng.integers(8, 40))  # header: sizes / counts
+            b[off] ^= int(rng.integers(1, 256))
+        else:
+            b = b[: int(rng.integers(0, len(b)))]
+        open(path, "wb").write(bytes(b))
+        try:
+            P.Circuit.load(ctx, path)
+        except P._lib.InvalidArgument:
+            pass
+        except P._lib.DgkrError as e:  # e.g. a header that asks for too much memory
+            assert "CAPACITY" in str(e) or "UNSUPPORTED" in str(e) or "CUDA" in str(e), str(e)
