@@ -231,7 +231,9 @@ def run_b200(args, cfg_name):
     if world > 1 or os.environ.get("DGKR_FORCE_DIST") == "1":
         from paper_2404_10404_b200 import dist
 
-        return dist.run_bench_rank(args, cfg_name, CONFIGS, CIRCUIT_SEED, INPUT_SEED)
+        return dist.run_bench_rank(args, cfg_name, CONFIGS, CIRCUIT_SEED, INPUT_SEED,
+                                   helpers={"clock_sampler": ClockSampler, "measured_peaks": measured_peaks,
+                                            "proof_roofline": proof_roofline})
     ctx = P.Context(local_rank)
     field = P.Field.bn254()
     insz, flat = W.layered_circuit(CIRCUIT_SEED, lw, depth)

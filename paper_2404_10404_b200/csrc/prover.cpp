@@ -2015,6 +2015,12 @@ int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size
                     acc.output_absorb_ms += Ln->prof.output_absorb_ms;
                     acc.host_transcript_ms += Ln->prof.host_transcript_ms;
                     acc.total_ms += Ln->prof.total_ms;
+                    acc.round_launches += Ln->prof.round_launches;
+                    acc.round_ms += Ln->prof.round_ms;
+                    acc.round_bytes += Ln->prof.round_bytes;
+                    acc.round_mults += Ln->prof.round_mults;
+                    acc.bookkeep_ms += Ln->prof.bookkeep_ms;
+                    acc.evaluate_ms += Ln->prof.evaluate_ms;
                 } catch (const Error& e) {
                     codes[i] = e.code;
                     errs[i] = e.what();

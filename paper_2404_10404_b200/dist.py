@@ -95,9 +95,11 @@ def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field
             [profs[i].as_dict() for i in range(L)])
 
 
-def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
+def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=None):
     """bench.py --gpus N under torchrun: every rank proves its share of each
-    proof of a stream; rank 0 prints the JSON line (max-over-ranks timing)."""
+    proof of a stream; rank 0 prints the JSON line (max-over-ranks timing).
+    helpers (from bench.py): clock_sampler, measured_peaks, proof_roofline."""
+    helpers = helpers or {}
     import torch
     import torch.distributed as dist
 
@@ -155,9 +157,20 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
         return float(dt.item()), proofs, states, profs
 
     timed(lanes * args.warmup)
+    sampler = helpers["clock_sampler"](device) if (rank == 0 and "clock_sampler" in helpers) else None
+    if sampler:
+        sampler.start()
     dt, proofs, states, profs = timed(lanes * args.steps)
+    clk = sampler.stop() if sampler else None
     # single-proof latency (one lane)
     lat, _, _, _ = timed(1)
+    # one profiled proof (lane 0 of every rank): per-launch CUDA events around the round kernels
+    ctx.set_profile(True)
+    dist.barrier()
+    _, _, pprof = prove_dist_stream(ctx, comms[:1], circ, field, 1, "dgkr.bench.c2", spread_absorb=True,
+                                    out_bufs=bufs[:1])
+    ctx.set_profile(False)
+    pp = pprof[0]
     if rank == 0:
         assert len(set(states)) == 1
         ms_per_step = 1e3 * dt / args.steps
@@ -177,6 +190,23 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed):
                     "note": "multi-GPU arm measures the resident-input stream only"},
             "gpu_launches": sum(p["launches"] for p in profs),
         }
+        if pp["round_ms"] > 0 and "measured_peaks" in helpers:
+            peak_gbs, peak_src = helpers["measured_peaks"]()
+            mp = C.c_double()
+            check(lib().dgkr_bench_mul_peak(ctx.handle, C.byref(mp)))
+            gbs = pp["round_bytes"] / (pp["round_ms"] * 1e-3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": "k_round (fused fold+round), rank 0",
+                                "achieved": gbs, "peak": peak_gbs, "unit": "GB/s", "frac": gbs / peak_gbs,
+                                "traffic": None, "peak_source": peak_src}
+            mps = pp["round_mults"] / (pp["round_ms"] * 1e-3)
+            line["roofline_int"] = {"bound": "imad", "kernel": "k_round, rank 0", "achieved": mps, "peak": mp.value,
+                                    "unit": "BN254 mont-mul/s", "frac": mps / mp.value}
+            if "proof_roofline" in helpers:  # per GPU: each rank proves 1/N of every proof
+                line["roofline_proof"] = helpers["proof_roofline"](n_copies, lw, depth,
+                                                                    ms_per_step / lanes * world, mp.value)
+        line["breakdown_ms_rank0_per_proof"] = {k: pp[k] for k in ("round_ms", "bookkeep_ms", "evaluate_ms",
+                                                                   "output_absorb_ms", "host_transcript_ms")}
+        line["clocks"] = clk
         print(json.dumps(line))
     dist.barrier()
     dist.destroy_process_group()
