@@ -544,9 +544,14 @@ __global__ void __launch_bounds__(kThreads) k_evaluate(EvalLaunch a) {
     for (std::uint64_t g = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; g < a.n_write;
          g += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         Fe acc = fe_zero();
+        std::uint64_t gw = g;  // the gate this thread computes and writes
         if (g < a.n_gates) {
             const std::uint64_t c = g >> a.log_g;
-            const std::uint32_t gl = static_cast<std::uint32_t>(g & ((std::uint64_t{1} << a.log_g) - 1));
+            std::uint32_t gl = static_cast<std::uint32_t>(g & ((std::uint64_t{1} << a.log_g) - 1));
+            if (a.perm) {
+                gl = a.perm[gl];
+                gw = (a.log_g >= 63) ? gl : ((c << a.log_g) | gl);
+            }
             const std::uint32_t k0 = a.gstart[gl], k1 = a.gstart[gl + 1];
             for (std::uint32_t k = k0; k < k1; ++k) {
                 const uint4 e = a.nested[k];
@@ -556,7 +561,7 @@ __global__ void __launch_bounds__(kThreads) k_evaluate(EvalLaunch a) {
                 acc = fe_add<F>(acc, (e.x & 1) ? fe_mul<F>(va, vb) : fe_add<F>(va, vb));
             }
         }
-        fe_store(a.out + g, acc);
+        fe_store(a.out + gw, acc);
     }
 }
 

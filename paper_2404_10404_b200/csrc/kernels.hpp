@@ -150,6 +150,9 @@ struct EvalLaunch {
     const uint4* nested = nullptr;  // {kind | left_layer<<1 | right_layer<<16, left_gate, right_gate, 0}
     const Fe* const* layer_vals = nullptr;   // device array [depth+1]
     const std::uint32_t* layer_log_stride = nullptr;  // device array [depth+1]
+    // optional [sub_gates] visit order: gates sorted by their mul-wire count so
+    // a warp's threads take the same (add or mul) path
+    const std::uint32_t* perm = nullptr;
 };
 void launch_evaluate(FieldKind k, const EvalLaunch& a, cudaStream_t st);
 

@@ -333,6 +333,7 @@ struct dgkr_circuit {
         DBuf<std::uint32_t> xoff, yoff;    // concatenated per slot
         DBuf<uint4> xent, yent;
         DBuf<std::uint32_t> gstart;        // evaluation CSR
+        DBuf<std::uint32_t> eperm;         // evaluation order (mul-heavy gates first)
         DBuf<uint4> nested;
         DBuf<std::uint32_t> xperm, yperm;  // single-slot: degree-sorted rows
         DBuf<uint2> xseg, yseg;
@@ -556,6 +557,19 @@ void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const s
             const std::uint32_t* e = nested + 5 * k;
             nest[i] = make_uint4((e[0] ? 1u : 0u) | (e[1] << 1) | (e[3] << 16), e[2], e[4], 0);
         }
+        // evaluation order: gates with more mul wires first (uniform warps)
+        {
+            std::vector<std::uint32_t> nmul(ng, 0), ep(ng);
+            for (std::uint64_t g = 0; g < ng; ++g) {
+                ep[g] = static_cast<std::uint32_t>(g);
+                for (std::uint32_t k = gstart[g]; k < gstart[g + 1]; ++k) nmul[g] += nest[k].x & 1u;
+            }
+            std::stable_sort(ep.begin(), ep.end(), [&](std::uint32_t x, std::uint32_t y) {
+                return nmul[x] != nmul[y] ? nmul[x] > nmul[y] : gstart[x + 1] - gstart[x] > gstart[y + 1] - gstart[y];
+            });
+            C.eperm.ensure(std::max<std::uint64_t>(ng, 1));
+            if (ng) CK(cudaMemcpy(C.eperm.p, ep.data(), ng * 4, cudaMemcpyHostToDevice));
+        }
         C.gstart.ensure(ng + 1);
         C.nested.ensure(nw);
         CK(cudaMemcpy(C.gstart.p, gstart.data(), (ng + 1) * 4, cudaMemcpyHostToDevice));
@@ -753,6 +767,7 @@ void evaluate_layers(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field*
         el.log_g = (c.n_copies > 1) ? c.sub_log[li] : 63;
         el.gstart = C.gstart.p;
         el.nested = C.nested.p;
+        el.perm = C.eperm.p;
         el.layer_vals = W.d_layer_vals.p;
         el.layer_log_stride = c.d_layer_log.p;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
