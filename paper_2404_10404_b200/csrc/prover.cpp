@@ -1015,12 +1015,6 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
 // ---------------------------------------------------------------------------
 // PCS (pcs.hpp) on device
 // ---------------------------------------------------------------------------
-struct PcsDevice {
-    DBuf<Fe> m;              // rows x cols Montgomery
-    DBuf<std::uint8_t> nodes;  // 2*cols digests
-    DBuf<std::uint8_t> stage;
-};
-
 void pcs_build_tree(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols) {
     d.nodes.ensure(2 * cols * 32);
     ctx->tbeg();
@@ -1057,15 +1051,26 @@ U256 chi_eval_host(std::uint64_t index, const std::vector<U256>& point, const Ho
 }
 
 /// pcs::open (pcs.hpp:212-254) -> Opening::to_bytes
-std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows,
-                                   std::size_t cols, const std::uint8_t* data, const std::vector<U256>& r,
-                                   std::size_t q, Transcript& tr, U256* value_out) {
+/// Opening::to_bytes size (pcs.hpp:135-156)
+std::size_t pcs_opening_size(std::size_t w, std::size_t r_len, std::size_t rows, std::size_t cols, std::size_t q) {
+    const std::size_t nq = std::min(q, cols);
+    return 4 + r_len * w + w + 4 + rows * w + 4 + cols * w + 4 + nq * (4 + rows * w + 32 * log2_exact(cols));
+}
+
+/// pcs::open (pcs.hpp:212-254), written straight into `out` (cap bytes):
+/// the combined row lands in place by one D2H and is absorbed from there.
+/// Returns the opening's length.
+std::size_t pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols,
+                     const std::uint8_t* data, const std::vector<U256>& r, std::size_t q, Transcript& tr,
+                     U256* value_out, std::uint8_t* out, std::size_t cap) {
     check_matrix(rows, cols);
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
     const std::uint32_t row_vars = log2_exact(cols), index_vars = log2_exact(rows);
     if (r.size() != row_vars + index_vars) fail(DGKR_INVALID_ARGUMENT, "opening point has wrong dimension");
+    const std::size_t total = pcs_opening_size(w, r.size(), rows, cols, q);
+    if (total > cap) fail(DGKR_CAPACITY, "output buffer too small");
     d.m.ensure(rows * cols);
     ctx->upload_elems(f, data, rows * cols, d.m.p, d.stage);
     std::vector<U256> r_low(r.begin(), r.begin() + row_vars), r_high(r.begin() + row_vars, r.end());
@@ -1097,11 +1102,27 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
     ctx->launched();
     // leaves + tree (pcs.hpp:241-244)
     pcs_build_tree(ctx, f, d, rows, cols);
-    std::vector<std::uint8_t> combined_bytes(cols * w);
+    // Opening::to_bytes head (pcs.hpp:135-156): |r|, r, value, M, row evals, cols, combined row
+    std::size_t pos = 0;
+    auto put_u32 = [&](std::uint32_t v) {
+        for (int i = 0; i < 4; ++i) out[pos++] = static_cast<std::uint8_t>(v >> (8 * i));
+    };
+    auto put_elem = [&](const U256& x) {
+        F.to_bytes(x, out + pos);
+        pos += w;
+    };
+    put_u32(static_cast<std::uint32_t>(r.size()));
+    for (const auto& x : r) put_elem(x);
+    put_elem(value);
+    put_u32(static_cast<std::uint32_t>(rows));
+    for (const auto& x : row_evals) put_elem(x);
+    put_u32(static_cast<std::uint32_t>(cols));
+    std::uint8_t* combined = out + pos;
     d.stage.ensure(cols * w);
     launch_to_canonical(kind, comb.p, d.stage.p, static_cast<int>(w), cols, ctx->st);
     ctx->launched();
-    ctx->d2h(combined_bytes.data(), d.stage.p, cols * w);
+    ctx->d2h(combined, d.stage.p, cols * w);
+    pos += cols * w;
     Digest root;
     ctx->d2h(root.data(), d.nodes.p + 32, 32);
     ctx->sync();
@@ -1111,7 +1132,7 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
     for (const auto& x : r) tr.absorb(x);
     tr.absorb(value);
     for (const auto& x : row_evals) tr.absorb(x);
-    tr.absorb_many(combined_bytes.data(), cols, w);
+    tr.absorb_many(combined, cols, w);
     std::vector<std::uint64_t> idx;
     if (q >= cols) {
         for (std::uint64_t j = 0; j < cols; ++j) idx.push_back(j);
@@ -1126,34 +1147,25 @@ std::vector<std::uint8_t> pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d,
         }
     }
     ctx->prof.host_transcript_ms += now_ms() - t0;
-    // Opening::to_bytes (pcs.hpp:135-156)
-    std::vector<std::uint8_t> out;
-    put32(out, static_cast<std::uint32_t>(r.size()));
-    for (const auto& x : r) append_elem(out, F, x);
-    append_elem(out, F, value);
-    put32(out, static_cast<std::uint32_t>(rows));
-    for (const auto& x : row_evals) append_elem(out, F, x);
-    put32(out, static_cast<std::uint32_t>(cols));
-    out.insert(out.end(), combined_bytes.begin(), combined_bytes.end());
-    put32(out, static_cast<std::uint32_t>(idx.size()));
+    // spot checks: column + Merkle path (merkle.hpp:34-45) each
+    put_u32(static_cast<std::uint32_t>(idx.size()));
     for (std::uint64_t j : idx) {
-        put32(out, static_cast<std::uint32_t>(j));
+        put_u32(static_cast<std::uint32_t>(j));
         for (std::size_t i = 0; i < rows; ++i) {
-            const std::uint8_t* src = data + (i * cols + j) * w;
-            out.insert(out.end(), src, src + w);
+            std::memcpy(out + pos, data + (i * cols + j) * w, w);
+            pos += w;
         }
-        // Merkle path (merkle.hpp:34-45): siblings leaf -> root
         std::size_t node = cols + j;
         while (node > 1) {
-            const std::size_t off = out.size();
-            out.resize(off + 32);
-            ctx->d2h(out.data() + off, d.nodes.p + (node ^ 1) * 32, 32);
+            ctx->d2h(out + pos, d.nodes.p + (node ^ 1) * 32, 32);
+            pos += 32;
             node >>= 1;
         }
     }
     ctx->sync();
+    if (pos != total) fail(DGKR_LOGIC_ERROR, "opening size mismatch");
     if (value_out) *value_out = value;
-    return out;
+    return pos;
 }
 
 // ---------------------------------------------------------------------------
@@ -2195,7 +2207,7 @@ int dgkr_pcs_commit(dgkr_ctx* ctx, const dgkr_field* f, std::size_t rows, std::s
     return guard([&] {
         ctx->begin_call();
         CK(cudaSetDevice(ctx->device));
-        PcsDevice d;
+        PcsDevice& d = ctx->nttws().pcs;  // persistent: multi-GiB buffers are not reallocated per call
         const Digest root = pcs_commit(ctx, f, d, rows, cols, data);
         std::memcpy(root32, root.data(), 32);
         ctx->end_call();
@@ -2212,12 +2224,14 @@ int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, std::size_t rows, std::siz
         std::vector<U256> pt(r_len);
         for (std::size_t i = 0; i < r_len; ++i) pt[i] = F.from_bytes(r + i * F.width());
         Transcript tr(&f->f, t->state, t->draws);
-        PcsDevice d;
-        auto bytes = pcs_open(ctx, f, d, rows, cols, data, pt, q, tr, nullptr);
+        PcsDevice& d = ctx->nttws().pcs;
+        const std::size_t need = pcs_opening_size(F.width(), r_len, rows, cols, q);
+        *len = need;
+        if (need > cap) fail(DGKR_CAPACITY, "output buffer too small");
+        pcs_open(ctx, f, d, rows, cols, data, pt, q, tr, nullptr, out, cap);
         std::memcpy(t->state, tr.state().data(), 32);
         t->draws = tr.draws();
         ctx->end_call();
-        emit(bytes, out, cap, len);
     });
 }
 
@@ -2277,9 +2291,10 @@ int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::
             for (std::size_t e = 0; e < cols; ++e) F.from_bytes(rows + i * row_bytes + e * w);
             ts.mempool(row_bytes);
         }
-        std::vector<PcsDevice> dev(K);
+        auto& dev = ctx->nttws().pcs_clusters;
+        while (dev.size() < K) dev.push_back(std::make_unique<PcsDevice>());
         for (std::size_t c = 0; c < K; ++c) {
-            const Digest root = pcs_commit(ctx, f, dev[c], M, cols, rows + c * M * row_bytes);
+            const Digest root = pcs_commit(ctx, f, *dev[c], M, cols, rows + c * M * row_bytes);
             std::memcpy(roots_out + 32 * c, root.data(), 32);
             ts.msg(c * M, 0, 0, 32);
         }
@@ -2297,11 +2312,14 @@ int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::
             Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
             tr.absorb_u64(c);
             U256 value;
-            auto op = pcs_open(ctx, f, dev[c], M, cols, rows + c * M * row_bytes, r_local, q, tr, &value);
-            ts.msg(c * M, 0, 0, op.size());
+            const std::size_t osz = pcs_opening_size(w, r_local.size(), M, cols, q);
+            const std::size_t at = all.size();
+            all.resize(at + 4 + osz);
+            const std::size_t n_op =
+                pcs_open(ctx, f, *dev[c], M, cols, rows + c * M * row_bytes, r_local, q, tr, &value, all.data() + at + 4, osz);
+            for (int i = 0; i < 4; ++i) all[at + i] = static_cast<std::uint8_t>(n_op >> (8 * i));
+            ts.msg(c * M, 0, 0, n_op);
             combined = F.add(combined, F.mul(chi_eval_host(c, r_top, F), value));
-            put32(all, static_cast<std::uint32_t>(op.size()));
-            all.insert(all.end(), op.begin(), op.end());
         }
         F.to_bytes(combined, combined_out);
         write_json(ts.json(), traffic_json, json_cap);

@@ -154,6 +154,13 @@ struct RtState {
     RtFieldHost cur{};
 };
 
+/// device buffers of one polynomial commitment (pcs.hpp), kept across calls
+struct PcsDevice {
+    DBuf<Fe> m;                // rows x cols Montgomery
+    DBuf<std::uint8_t> nodes;  // 2*cols digests
+    DBuf<std::uint8_t> stage;
+};
+
 /// device buffers of the NTT / RS / FRI entry points, kept across calls
 /// (multi-GiB at C5 sizes: cudaMalloc/cudaFree per call would dominate)
 struct NttWs {
@@ -164,6 +171,9 @@ struct NttWs {
     DBuf<std::uint64_t> didx;
     // beacon tree (config C3)
     DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
+    // polynomial commitment (pcs_commit / pcs_open) and DistPc's clusters
+    PcsDevice pcs;
+    std::vector<std::unique_ptr<PcsDevice>> pcs_clusters;
 };
 
 /// One in-flight proof: a CUDA stream, its reduction workspace, pinned

@@ -528,11 +528,12 @@ def pcs_open(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int]
     cols = len(field.encode(rows[0])) // field.width
     depth = max(0, (cols - 1).bit_length())
     cap = 64 + (len(r) + 2 + M + cols) * field.width + min(spot_checks, cols) * (4 + M * field.width + 32 * depth) + 64
-    out, ln = _out(cap)
+    out = np.empty(cap, dtype=np.uint8)  # not zero-filled: the opening overwrites what it returns
+    ln = C.c_size_t()
     check(lib().dgkr_pcs_open(ctx.handle, field.handle, C.c_size_t(M), C.c_size_t(cols), C.c_char_p(data),
                               C.c_char_p(field.encode(r)), C.c_size_t(len(r)), C.c_size_t(spot_checks),
-                              C.byref(tr.t), out, C.c_size_t(cap), C.byref(ln)))
-    return out.raw[: ln.value]
+                              C.byref(tr.t), out.ctypes.data_as(C.c_void_p), C.c_size_t(cap), C.byref(ln)))
+    return out[: ln.value].tobytes()
 
 
 def dist_sumcheck(ctx: Context, n_workers: int, pairs, tr: Transcript):
