@@ -7,6 +7,7 @@
 // FRI entry points in ext.cpp.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -164,7 +165,11 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         }
         rl.n_out_pairs = size0 >> j;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        if (rl.n_out_pairs <= kSmallRoundPairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
+        static const std::uint64_t small_pairs = [] {  // tuning override (DGKR_SMALL_PAIRS)
+            const char* e = std::getenv("DGKR_SMALL_PAIRS");
+            return e ? std::strtoull(e, nullptr, 10) : kSmallRoundPairs;
+        }();
+        if (rl.n_out_pairs <= small_pairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
         else launch_round(kind, rl, ctx->ws, ctx->st);
         ctx->launched();
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev1, ctx->st));
