@@ -1,0 +1,95 @@
+// Drop-in dgkr/sumcheck.hpp: the reference header with prove_product_sum
+// (sumcheck.hpp:226) and prove_layer_sum (:342) on the B200 prover. Same
+// names, signatures, proofs (bit-exact) and exception types.
+#pragma once
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <vector>
+
+#include "dgkr/counters.hpp"
+#include "dgkr/field.hpp"
+#include "dgkr/mle.hpp"
+#include "dgkr/transcript.hpp"
+
+#define prove_product_sum prove_product_sum_cpu_reference
+#define prove_layer_sum prove_layer_sum_cpu_reference
+#include_next <dgkr/sumcheck.hpp>
+#undef prove_product_sum
+#undef prove_layer_sum
+
+#include "dgkr/b200_dropin_core.hpp"
+
+namespace dgkr::sumcheck {
+
+inline SumcheckProof prove_product_sum(std::span<const ProductPair> pairs, Transcript& transcript) {
+    namespace B = dgkr::b200_dropin;
+    if (pairs.empty()) throw std::invalid_argument("product sum needs at least one pair");  // sumcheck.hpp:155-157
+    const FieldConfigPtr& cfg = pairs.front().f.config();
+    const std::size_t vars = pairs.front().f.num_vars();
+    std::vector<std::uint8_t> tabs;
+    for (const auto& pr : pairs) {
+        if (pr.f.num_vars() != vars || pr.g.num_vars() != vars)
+            throw std::invalid_argument("mixed table sizes in product sum");
+        auto a = B::canonical(pr.f.evals()), b = B::canonical(pr.g.evals());
+        tabs.insert(tabs.end(), a.begin(), a.end());
+        tabs.insert(tabs.end(), b.begin(), b.end());
+    }
+    B::Device& dev = B::device(cfg);
+    std::vector<std::uint8_t> out(64 + (vars + 2) * 4 * cfg->byte_width() + 2 * pairs.size() * cfg->byte_width());
+    std::size_t len = 0;
+    dgkr_transcript t = B::load(transcript);
+    B::check(dgkr_prove_product_sum(dev.ctx(), dev.field(), pairs.size(), vars, tabs.data(), &t, out.data(),
+                                    out.size(), &len));
+    B::store(transcript, t);
+    return SumcheckProof::from_bytes(std::span<const std::uint8_t>(out.data(), len), cfg);
+}
+
+inline LayerProveResult prove_layer_sum(const LayerInstance& inst, const FieldElement& claimed,
+                                        Transcript& transcript) {
+    namespace B = dgkr::b200_dropin;
+    const FieldConfigPtr& cfg = claimed.config();
+    const std::size_t w = cfg->byte_width(), ns = inst.slot_tables.size();
+    std::vector<std::uint8_t> tabs;
+    for (const auto& t : inst.slot_tables) {  // sumcheck.hpp:349-353
+        if (t.num_vars() != inst.side_vars) throw std::invalid_argument("slot table not padded to side_vars");
+        auto b = B::canonical(t.evals());
+        tabs.insert(tabs.end(), b.begin(), b.end());
+    }
+    const std::uint64_t table_size = std::uint64_t{1} << inst.side_vars;
+    for (const auto& wi : inst.wires)  // sumcheck.hpp:354-359
+        if (wi.x_slot >= ns || wi.y_slot >= ns || wi.x_index >= table_size || wi.y_index >= table_size)
+            throw std::invalid_argument("layer wire index out of range");
+    std::vector<std::uint32_t> meta;
+    std::vector<std::uint64_t> idx;
+    std::vector<std::uint8_t> weights;
+    for (const auto& wi : inst.wires) {
+        meta.insert(meta.end(), {wi.is_mul ? 1u : 0u, wi.x_slot, wi.y_slot});
+        idx.insert(idx.end(), {wi.x_index, wi.y_index});
+        wi.weight.append_bytes(weights);
+    }
+    std::vector<std::uint8_t> cl;
+    claimed.append_bytes(cl);
+    B::Device& dev = B::device(cfg);
+    const std::size_t side = inst.side_vars;
+    std::vector<std::uint8_t> out(64 + (2 * side + 2) * 4 * w + 2 * ns * w + w), xp(std::max<std::size_t>(side, 1) * w),
+        yp(std::max<std::size_t>(side, 1) * w);
+    std::size_t len = 0;
+    dgkr_transcript t = B::load(transcript);
+    B::check(dgkr_prove_layer_sum(dev.ctx(), dev.field(), side, ns, tabs.data(), inst.wires.size(),
+                                  meta.empty() ? nullptr : meta.data(), idx.empty() ? nullptr : idx.data(),
+                                  weights.empty() ? nullptr : weights.data(), cl.data(), &t, out.data(), out.size(),
+                                  &len, xp.data(), yp.data()));
+    B::store(transcript, t);
+    LayerProveResult res;
+    res.proof = SumcheckProof::from_bytes(std::span<const std::uint8_t>(out.data(), len), cfg);
+    const std::uint8_t* px = xp.data();
+    const std::uint8_t* py = yp.data();
+    for (std::size_t k = 0; k < side; ++k) {
+        res.x_point.push_back(B::take_elem(px, cfg));
+        res.y_point.push_back(B::take_elem(py, cfg));
+    }
+    return res;
+}
+
+}  // namespace dgkr::sumcheck
