@@ -20,3 +20,27 @@ def test_reference_suite_on_the_gpu_prover(name):
         pytest.skip("drop-in test binaries not built (make -C oracle, needs /root/reference)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+
+
+@pytest.mark.parametrize("args", [
+    [],
+    ["64", "3", "8", "7"],
+    ["32", "4", "4", "1", "perturb-round-poly:1"],
+    ["32", "4", "4", "1", "flip-sibling:2"],
+    ["32", "4", "4", "1", "dup-index:0"],
+    ["32", "4", "4", "1", "mempool-overwrite:3"],
+])
+def test_reference_epoch_pipeline_on_the_gpu_prover(args):
+    """the reference's pipeline::run_epoch (pipeline.hpp) with gkr_prove and
+    pcs::commit / open on the B200 prover reports exactly what the CPU
+    reference reports: acceptance flags, final chain state, traffic, proof
+    sizes - and rejects the same tampered blocks"""
+    cpu = os.path.join(ROOT, "oracle", "_ref", "epoch_cpu")
+    gpu = os.path.join(ROOT, "oracle", "_ref", "epoch_gpu")
+    if not (os.path.exists(cpu) and os.path.exists(gpu)):
+        pytest.skip("epoch drivers not built (make -C oracle, needs /root/reference)")
+    a = subprocess.run([cpu, *args], capture_output=True, text=True, timeout=900)
+    b = subprocess.run([gpu, *args], capture_output=True, text=True, timeout=900)
+    assert a.returncode == 0 and b.returncode == 0, (a.stderr + b.stderr)[-3000:]
+    assert a.stdout == b.stdout
+    assert ('"all_accepted":true' in a.stdout) == (len(args) <= 4)
