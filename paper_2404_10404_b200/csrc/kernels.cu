@@ -325,6 +325,16 @@ __device__ __forceinline__ Fe split_eq(const SplitEq& e, std::uint64_t g) {
     return w;
 }
 
+/// out[i] = dense[i] + split_eq(e, i): one claim term already dense in HBM
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_split_eq_expand_add(SplitEq e, std::uint64_t n,
+                                                                  const Fe* __restrict__ dense, Fe* __restrict__ out) {
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        fe_store(out + i, fe_add<F>(fe_load_nc(dense + i), split_eq<F>(e, i)));
+    }
+}
+
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_split_eq_expand(SplitEq e, std::uint64_t n, Fe* __restrict__ out) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -1276,6 +1286,13 @@ void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, c
 #undef LAUNCH_ROUND
 #undef BY_MODE
     check_launch("round_small");
+}
+
+void launch_split_eq_expand_add(FieldKind k, const SplitEq& e, std::uint64_t n, const Fe* dense, Fe* out,
+                                cudaStream_t st) {
+    const int g = grid_for(n, kThreads, 148 * 16);
+    DISPATCH_FIELD(k, F, (k_split_eq_expand_add<F><<<g, kThreads, 0, st>>>(e, n, dense, out)));
+    check_launch("split_eq_expand_add");
 }
 
 void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st) {

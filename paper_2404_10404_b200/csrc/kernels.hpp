@@ -96,6 +96,9 @@ struct SplitEq {
 /// Dense expansion of a split-eq: out[i] = sum_t A[t][i & m] * B[t][i >> klo], i < n
 /// (coalesced; turns the per-wire split-eq lookups into one 32-byte gather).
 void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st);
+/// out[i] = dense[i] + sum_t seed_t A_t[lo] B_t[hi]  (one term reused from a dense chi table)
+void launch_split_eq_expand_add(FieldKind k, const SplitEq& e, std::uint64_t n, const Fe* dense, Fe* out,
+                                cudaStream_t st);
 
 /// Per-slot description of a data-parallel layer: values are laid out as
 /// n_copies blocks of 2^log_stride (copy = high bits).

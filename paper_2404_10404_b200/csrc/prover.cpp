@@ -894,6 +894,10 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         registry[out_layer].push_back(std::move(lc));
     }
     put32(proof, out_layer);
+    // chi_x(u) of the previous (consumer) layer's phase 2 stays in W.EqU; it is
+    // the first claim term of the next layer in uniform layered circuits
+    std::vector<U256> equ_point;
+    std::uint64_t equ_n = 0;
     for (std::uint32_t layer = out_layer; layer >= 1; --layer) {
         auto& C = *c.cons[layer];
         auto& WC = *W.cons[layer];
@@ -916,8 +920,16 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         for (auto& p : pts)
             if (p.size() != lgc) fail(DGKR_LOGIC_ERROR, "claim point length mismatch");
         if (pts.size() > max_terms) fail(DGKR_UNSUPPORTED, "too many claim terms");
+        const std::uint64_t n_gates_local = c.sub_size[layer] * c.n_copies;
+        // w(g) = chi_g(u) + alpha chi_g(v): reuse the dense chi_x(u) table when
+        // term 0 is exactly (u, 1) over the same index range (one mult per gate saved)
+        const bool reuse_u = pts.size() == 2 && equ_n == n_gates_local && seeds[0] == F.one() && pts[0] == equ_point;
+        if (reuse_u) {
+            pts.erase(pts.begin());
+            seeds.erase(seeds.begin());
+        }
         SplitEq wq = build_split_eq(ctx, f, pts, seeds, W.eq_tabs.p, W.eq_jobs, Lane::kEqOff);
-        wq.offset = rank * (c.sub_size[layer] * c.n_copies);  // global gate index of local gate 0
+        wq.offset = rank * n_gates_local;  // global gate index of local gate 0
         const std::size_t wq_elems = pts.size() * ((std::size_t{1} << wq.klo) + (std::size_t{1} << wq.khi));
 
         // prove_layer_sum (sumcheck.hpp:342-448)
@@ -931,7 +943,10 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.G = W.G.p;
         bk.w = wq;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        launch_split_eq_expand(kind, wq, c.sub_size[layer] * c.n_copies, W.Wg.p, ctx->st);  // w(g), gkr.hpp:140-148
+        if (reuse_u)
+            launch_split_eq_expand_add(kind, wq, n_gates_local, W.EqU.p, W.Wg.p, ctx->st);  // w(g), gkr.hpp:140-148
+        else
+            launch_split_eq_expand(kind, wq, n_gates_local, W.Wg.p, ctx->st);
         ctx->launched();
         bk.gate_w = W.Wg.p;
         bk.perm = C.xperm.p;
@@ -973,6 +988,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.vx_const = vxk;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
         launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st);  // chi_x(u), sumcheck.hpp:415
+        equ_point = p1.challenges;
+        equ_n = T;
         ctx->launched();
         bk.eq_u = W.EqU.p;
         bk.perm = C.yperm.p;
