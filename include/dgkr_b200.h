@@ -289,12 +289,28 @@ int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, size_t rows, size_t cols, 
  *     Q = min(queries, N/2) distinct challenge_index(N/2) positions.
  *   proof = u32 L || L roots || u32 |f_L| || f_L || u32 Q || per query:
  *     u32 i || per layer l: f_l[i mod h_l] || f_l[i mod h_l + h_l] || their two Merkle paths */
+/*   dgkr_fri_prove_dist: distributed FRI (BASELINE config C5 at N GPUs), rank r
+ *     holding the r-th chunk of n coefficients (one polynomial per rank, shared
+ *     Fiat-Shamir): per layer every rank's root is all-gathered and absorbed in
+ *     rank order before beta_l is drawn; all ranks' final layers are absorbed
+ *     in rank order; the Q query positions (over this rank's half domain) are
+ *     shared. proof_r = u32 world || u32 rank || u32 L || L x world roots
+ *     (layer-major, rank order) || u32 |f_L| || world x |f_L| final elements ||
+ *     u32 Q || per query: u32 i || per layer this rank's two values + paths.
+ *   dgkr_fri_prove_dist_emulated: the same with `world` ranks as host threads
+ *     on lanes of one device (coeffs[r] = rank r's chunk); proofs[r], lens[r]. */
 int dgkr_field_ntt_info(const dgkr_field* f, unsigned* two_adicity, uint8_t* root, uint8_t* coset);
 int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* in, unsigned log_n, int inverse, uint8_t* out);
 int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, size_t n, unsigned blowup_log,
                    uint8_t* out);
 int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const uint8_t* coeffs, size_t n, unsigned blowup_log,
                    unsigned final_log, size_t queries, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+int dgkr_fri_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, const dgkr_field* f, const uint8_t* coeffs, size_t n,
+                        unsigned blowup_log, unsigned final_log, size_t queries, dgkr_transcript* t, uint8_t* proof,
+                        size_t cap, size_t* len);
+int dgkr_fri_prove_dist_emulated(dgkr_ctx* ctx, const dgkr_field* f, int world, const uint8_t* const* coeffs, size_t n,
+                                 unsigned blowup_log, unsigned final_log, size_t queries, dgkr_transcript* t,
+                                 uint8_t* const* proofs, const size_t* caps, size_t* lens);
 
 /* ---- distinct indexes: associative array hash (distinct.hpp; config C4) ------------
  * F(e) = three rounds of r <- (r + e + 2^32 - 1)^3 from r = 0; AH(list) = sum F(e_i),

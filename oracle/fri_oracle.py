@@ -240,3 +240,168 @@ def fri_verify(fld: Field, proof: bytes, n: int, blowup_log: int, final_log: int
         return pos == len(proof)
     except ValueError:
         return False
+
+
+# --- distributed FRI (dgkr_fri_prove_dist; include/dgkr_b200.h) ---
+
+def _draw_queries(tr: Transcript, H: int, queries: int, L: int) -> List[int]:
+    if L == 0:
+        return []
+    if queries >= H:
+        return list(range(H))
+    qi: List[int] = []
+    seen = set()
+    while len(qi) < queries:
+        j = tr.challenge_index(H)
+        if j not in seen:
+            seen.add(j)
+            qi.append(j)
+    return qi
+
+
+def fri_prove_dist(fld: Field, chunks: Sequence[Sequence[int]], blowup_log: int, final_log: int, queries: int,
+                   tr: Transcript) -> List[bytes]:
+    """Rank r folds chunks[r]; one shared transcript: per layer all ranks'
+    roots in rank order, then every rank's final layer in rank order, then the
+    shared query positions. Returns one proof per rank."""
+    world = len(chunks)
+    n = len(chunks[0])
+    log_n0 = n.bit_length() - 1 + blowup_log
+    L = log_n0 - final_log
+    layers = [[rs_encode(fld, c, blowup_log)] for c in chunks]
+    trees: List[List[MerkleTree]] = [[] for _ in range(world)]
+    roots: List[List[bytes]] = []
+    for l in range(L):
+        rl = []
+        for r in range(world):
+            t = MerkleTree(_leaves(fld, layers[r][l]))
+            trees[r].append(t)
+            rl.append(t.root)
+        roots.append(rl)
+        for x in rl:
+            tr.absorb_bytes(x)
+        beta = tr.challenge()
+        for r in range(world):
+            layers[r].append(fri_fold(fld, layers[r][l], beta, l, log_n0))
+    for r in range(world):
+        for x in layers[r][L]:
+            tr.absorb(x)
+    qi = _draw_queries(tr, (1 << log_n0) // 2, queries, L)
+    nf = len(layers[0][L])
+    head = L.to_bytes(4, "little") + b"".join(b"".join(rl) for rl in roots) + nf.to_bytes(4, "little")
+    head += b"".join(fld.elems_to_bytes(layers[r][L]) for r in range(world)) + len(qi).to_bytes(4, "little")
+    out = []
+    for r in range(world):
+        pr = world.to_bytes(4, "little") + r.to_bytes(4, "little") + head
+        for i in qi:
+            pr += i.to_bytes(4, "little")
+            for l in range(L):
+                hl = len(layers[r][l]) // 2
+                il = i % hl
+                pr += fld.to_bytes(layers[r][l][il]) + fld.to_bytes(layers[r][l][il + hl])
+                pr += b"".join(trees[r][l].path(il)) + b"".join(trees[r][l].path(il + hl))
+        out.append(pr)
+    return out
+
+
+def fri_verify_dist(fld: Field, proofs: Sequence[bytes], n: int, blowup_log: int, final_log: int, queries: int,
+                    tr: Transcript) -> bool:
+    """Accept iff the `world` per-rank proofs agree on every rank's roots and
+    final layer, each final layer has degree < n >> L, and each rank's query
+    openings verify against its own roots with the shared betas."""
+    p = fld.p
+    w_ = fld.width
+    world = len(proofs)
+    _, _, g = two_adic(fld)
+    log_n0 = n.bit_length() - 1 + blowup_log
+    L = log_n0 - final_log
+    w = root_of_unity(fld, log_n0)
+    nf = 1 << final_log
+    head_len = 4 + L * world * 32 + 4 + world * nf * w_ + 4
+    if world < 1 or any(len(pr) < 8 + head_len for pr in proofs):
+        return False
+    heads = [pr[8:8 + head_len] for pr in proofs]
+    if any(h != heads[0] for h in heads):
+        return False
+    for r, pr in enumerate(proofs):
+        if int.from_bytes(pr[0:4], "little") != world or int.from_bytes(pr[4:8], "little") != r:
+            return False
+    h = heads[0]
+    if int.from_bytes(h[0:4], "little") != L:
+        return False
+    pos = 4
+    roots = []
+    for _ in range(L):
+        roots.append([h[pos + 32 * r: pos + 32 * r + 32] for r in range(world)])
+        pos += 32 * world
+    if int.from_bytes(h[pos:pos + 4], "little") != nf:
+        return False
+    pos += 4
+    finals = []
+    for _ in range(world):
+        finals.append(fld.elems_from_bytes(h[pos:pos + nf * w_]))
+        pos += nf * w_
+    Q = int.from_bytes(h[pos:pos + 4], "little")
+    betas = []
+    for l in range(L):
+        for x in roots[l]:
+            tr.absorb_bytes(x)
+        betas.append(tr.challenge())
+    gL = pow(g, 1 << L, p)
+    deg_bound = max(n >> L, 1)
+    for fin in finals:
+        if any(x >= p for x in fin):
+            return False
+        coeffs = ntt_fast(fld, fin, inverse=True)
+        coeffs = [c * pow(gL, p - 1 - j, p) % p for j, c in enumerate(coeffs)]
+        if any(coeffs[deg_bound:]):
+            return False
+    for fin in finals:
+        for x in fin:
+            tr.absorb(x)
+    H = (1 << log_n0) // 2
+    expect = _draw_queries(tr, H, queries, L)
+    if Q != len(expect):
+        return False
+    inv2 = pow(2, p - 2, p)
+    for r, pr in enumerate(proofs):
+        pos = 8 + head_len
+
+        def take(k):
+            nonlocal pos
+            b = pr[pos:pos + k]
+            if len(b) != k:
+                raise ValueError("truncated")
+            pos += k
+            return b
+
+        try:
+            for k in range(Q):
+                if int.from_bytes(take(4), "little") != expect[k]:
+                    return False
+                i = expect[k]
+                carry = None
+                for l in range(L):
+                    Nl = (1 << log_n0) >> l
+                    hl = Nl // 2
+                    il = i % hl
+                    f0 = fld.from_bytes(take(w_))
+                    f1 = fld.from_bytes(take(w_))
+                    depth = Nl.bit_length() - 1
+                    p0 = [take(32) for _ in range(depth)]
+                    p1 = [take(32) for _ in range(depth)]
+                    if not MerkleTree.verify_path(roots[l][r], sha256(fld.to_bytes(f0)), il, p0):
+                        return False
+                    if not MerkleTree.verify_path(roots[l][r], sha256(fld.to_bytes(f1)), il + hl, p1):
+                        return False
+                    if carry is not None and (f0 if carry[0] == il else f1) != carry[1]:
+                        return False
+                    x = pow(g, 1 << l, p) * pow(w, (1 << l) * il, p) % p
+                    carry = (il, ((f0 + f1) + betas[l] * pow(x, p - 2, p) % p * (f0 - f1)) * inv2 % p)
+                if L > 0 and finals[r][carry[0]] != carry[1]:
+                    return False
+        except ValueError:
+            return False
+        if pos != len(pr):
+            return False
+    return True

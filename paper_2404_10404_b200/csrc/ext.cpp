@@ -6,6 +6,10 @@
 #include <memory>
 #include <vector>
 
+#include <string>
+#include <thread>
+
+#include "comm.hpp"
 #include "dgkr_b200.h"
 #include "host_core.hpp"
 #include "kernels.hpp"
@@ -51,8 +55,15 @@ void coset_ntt(Lane* ctx, const dgkr_field* f, const Fe* coeff, std::uint64_t n_
 }
 
 /// FRI over the RS codeword of `coeffs` (protocol in include/dgkr_b200.h)
+/// comm != nullptr: distributed FRI: this rank folds its own
+/// chunk; per layer every rank's root is all-gathered and absorbed in rank
+/// order (one shared beta), the final layers likewise, the query positions
+/// are shared, and the proof carries every rank's roots and final layer plus
+/// this rank's openings (format in include/dgkr_b200.h).
 std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::uint8_t* coeffs, std::uint64_t n,
-                                    unsigned blowup_log, unsigned final_log, std::size_t q, Transcript& tr) {
+                                    unsigned blowup_log, unsigned final_log, std::size_t q, Transcript& tr,
+                                    dgkr_comm* comm = nullptr) {
+    const std::size_t world = comm ? static_cast<std::size_t>(comm->world) : 1;
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
@@ -84,6 +95,7 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     twinv.ensure(std::max<std::uint64_t>(N0 / 2, 1));
     if (N0 >= 2) pow_table(ctx, f, F.inv(f->root_of_unity(log_n0)), N0 / 2, twinv.p, scratch);
     std::vector<Digest> roots(L);
+    std::vector<std::uint8_t> all_roots;  // distributed: L x world roots, layer-major, rank order
     U256 ginv = f->coset_inv;  // (g^(2^l))^-1
     for (unsigned l = 0; l < L; ++l) {
         const std::uint64_t Nl = N0 >> l;
@@ -96,7 +108,14 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
         ctx->launched(2);
         ctx->d2h(roots[l].data(), tree[l]->p + 32, 32);
         ctx->sync();
-        tr.absorb_bytes(roots[l].data(), 32);
+        if (comm) {
+            std::vector<std::uint8_t> rl(world * 32);
+            comm->allgather_to_host(tree[l]->p + 32, rl.data(), 32, ctx);
+            for (std::size_t r = 0; r < world; ++r) tr.absorb_bytes(rl.data() + 32 * r, 32);
+            all_roots.insert(all_roots.end(), rl.begin(), rl.end());
+        } else {
+            tr.absorb_bytes(roots[l].data(), 32);
+        }
         const U256 beta = tr.challenge();
         U256 bk[9];
         f->fold_const(beta, bk);
@@ -114,7 +133,14 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     launch_to_canonical(kind, layer[L]->p, stage.p, static_cast<int>(w), NL, ctx->st);
     ctx->d2h(fin.data(), stage.p, NL * w);
     ctx->sync();
-    tr.absorb_many(fin.data(), NL, w);
+    std::vector<std::uint8_t> all_fin;  // distributed: world final layers, rank order
+    if (comm) {
+        all_fin.resize(world * NL * w);
+        comm->allgather_to_host(stage.p, all_fin.data(), NL * w, ctx);
+        tr.absorb_many(all_fin.data(), world * NL, w);
+    } else {
+        tr.absorb_many(fin.data(), NL, w);
+    }
     // queries on the first layer's half domain (distinct, like pcs.hpp:199-206)
     const std::uint64_t H = N0 / 2;
     std::vector<std::uint64_t> qi;
@@ -134,10 +160,19 @@ std::vector<std::uint8_t> fri_prove(Lane* ctx, const dgkr_field* f, const std::u
     }
     // gather opened values and Merkle paths on the device, one D2H per layer
     std::vector<std::uint8_t> out;
-    put32(out, L);
-    for (const auto& r : roots) out.insert(out.end(), r.begin(), r.end());
-    put32(out, static_cast<std::uint32_t>(NL));
-    out.insert(out.end(), fin.begin(), fin.end());
+    if (comm) {
+        put32(out, static_cast<std::uint32_t>(world));
+        put32(out, static_cast<std::uint32_t>(comm->rank));
+        put32(out, L);
+        out.insert(out.end(), all_roots.begin(), all_roots.end());
+        put32(out, static_cast<std::uint32_t>(NL));
+        out.insert(out.end(), all_fin.begin(), all_fin.end());
+    } else {
+        put32(out, L);
+        for (const auto& r : roots) out.insert(out.end(), r.begin(), r.end());
+        put32(out, static_cast<std::uint32_t>(NL));
+        out.insert(out.end(), fin.begin(), fin.end());
+    }
     put32(out, static_cast<std::uint32_t>(qi.size()));
     std::vector<std::vector<std::uint8_t>> vals(L), paths(L);
     std::vector<unsigned> depth(L);
@@ -540,6 +575,80 @@ int dgkr_fri_prove(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeff
         t->draws = tr.draws();
         ctx->end_call();
         emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_fri_prove_dist(dgkr_ctx* ctx, dgkr_comm* comm, const dgkr_field* f, const std::uint8_t* coeffs, std::size_t n,
+                        unsigned blowup_log, unsigned final_log, std::size_t queries, dgkr_transcript* t,
+                        std::uint8_t* proof, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (!comm) fail(DGKR_INVALID_ARGUMENT, "communicator must not be NULL");
+        Transcript tr(&f->f, t->state, t->draws);
+        auto bytes = fri_prove(ctx, f, coeffs, n, blowup_log, final_log, queries, tr, comm);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_fri_prove_dist_emulated(dgkr_ctx* ctx, const dgkr_field* f, int world, const std::uint8_t* const* coeffs,
+                                 std::size_t n, unsigned blowup_log, unsigned final_log, std::size_t queries,
+                                 dgkr_transcript* t, std::uint8_t* const* proofs, const std::size_t* caps,
+                                 std::size_t* lens) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (world < 1 || world > 64) fail(DGKR_INVALID_ARGUMENT, "world must be 1..64");
+        std::vector<Lane*> lanes(world);
+        for (int r = 0; r < world; ++r) {
+            lanes[r] = ctx->lane(r);
+            lanes[r]->profile_on = ctx->profile_on;
+        }
+        ctx->use(f);
+        ThreadGroup group;
+        group.world = world;
+        std::vector<ThreadComm> comms(world);
+        std::vector<dgkr_transcript> ts(world, *t);
+        std::vector<int> codes(world, DGKR_OK);
+        std::vector<std::string> errs(world);
+        for (int r = 0; r < world; ++r) {
+            comms[r].rank = r;
+            comms[r].world = world;
+            comms[r].g = &group;
+        }
+        auto work = [&](int r) {
+            try {
+                CK(cudaSetDevice(ctx->device));
+                Lane* L = lanes[r];
+                L->begin_call();
+                Transcript tr(&f->f, ts[r].state, ts[r].draws);
+                auto bytes = fri_prove(L, f, coeffs[r], n, blowup_log, final_log, queries, tr, &comms[r]);
+                std::memcpy(ts[r].state, tr.state().data(), 32);
+                ts[r].draws = tr.draws();
+                L->end_call();
+                emit(bytes, proofs[r], caps[r], &lens[r]);
+            } catch (const Error& e) {
+                codes[r] = e.code;
+                errs[r] = e.what();
+                group.abort();
+            } catch (const std::exception& e) {
+                codes[r] = DGKR_LOGIC_ERROR;
+                errs[r] = e.what();
+                group.abort();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int r = 1; r < world; ++r) th.emplace_back(work, r);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int r = 0; r < world; ++r)
+            if (codes[r] != DGKR_OK) fail(codes[r], "rank " + std::to_string(r) + ": " + errs[r]);
+        for (int r = 1; r < world; ++r)
+            if (std::memcmp(ts[r].state, ts[0].state, 32) != 0 || ts[r].draws != ts[0].draws)
+                fail(DGKR_LOGIC_ERROR, "ranks disagree on the transcript");
+        *t = ts[0];
     });
 }
 

@@ -416,6 +416,51 @@ def fri_prove(ctx: Context, field: Field, coeffs: Elems, blowup_log: int, final_
     return out.raw[: ln.value]
 
 
+def _fri_cap(field: Field, n: int, blowup_log: int, final_log: int, queries: int, world: int) -> int:
+    log_n0 = n.bit_length() - 1 + blowup_log
+    L = max(log_n0 - final_log, 0)
+    H = (1 << log_n0) // 2
+    q = min(queries, H) if L else 0
+    return (64 + world * (L * 32 + (1 << final_log) * field.width)
+            + q * (4 + L * (2 * field.width + 2 * 32 * log_n0)))
+
+
+def fri_prove_dist(ctx: Context, comm: "Comm", field: Field, coeffs: Elems, blowup_log: int, final_log: int,
+                   queries: int, tr: Transcript) -> bytes:
+    """dgkr_fri_prove_dist: this rank's chunk of a distributed FRI (proof
+    layout in include/dgkr_b200.h); every rank calls it collectively."""
+    b = field.encode(coeffs)
+    n = len(b) // field.width
+    cap = _fri_cap(field, n, blowup_log, final_log, queries, comm.world)
+    out = C.create_string_buffer(cap)
+    ln = C.c_size_t()
+    check(lib().dgkr_fri_prove_dist(ctx.handle, comm.handle, field.handle, C.c_char_p(b), C.c_size_t(n),
+                                    C.c_uint(blowup_log), C.c_uint(final_log), C.c_size_t(queries), C.byref(tr.t),
+                                    out, C.c_size_t(cap), C.byref(ln)))
+    return out.raw[: ln.value]
+
+
+def fri_prove_dist_emulated(ctx: Context, field: Field, chunks: Sequence[Elems], blowup_log: int, final_log: int,
+                            queries: int, tr: Transcript) -> List[bytes]:
+    """dgkr_fri_prove_dist_emulated: len(chunks) ranks as threads on lanes of
+    one device; returns one proof per rank (tr ends in the shared state)."""
+    world = len(chunks)
+    bs = [field.encode(c) for c in chunks]
+    if len({len(x) for x in bs}) != 1:
+        raise ValueError("all ranks need chunks of the same size")
+    n = len(bs[0]) // field.width
+    cap = _fri_cap(field, n, blowup_log, final_log, queries, world)
+    outs = [C.create_string_buffer(cap) for _ in range(world)]
+    ptrs = (C.c_void_p * world)(*[C.cast(o, C.c_void_p) for o in outs])
+    caps = (C.c_size_t * world)(*([cap] * world))
+    lens = (C.c_size_t * world)()
+    ins = (C.c_char_p * world)(*bs)
+    check(lib().dgkr_fri_prove_dist_emulated(ctx.handle, field.handle, C.c_int(world), ins,
+                                             C.c_size_t(n), C.c_uint(blowup_log), C.c_uint(final_log),
+                                             C.c_size_t(queries), C.byref(tr.t), ptrs, caps, lens))
+    return [outs[r].raw[: lens[r]] for r in range(world)]
+
+
 def gkr_prove_stream(ctx: Context, circuit: Circuit, n: int, lanes: int, field: Field, label: str = "stream",
                      inputs: Optional[Sequence[Elems]] = None, out_bufs=None):
     """n proofs over `lanes` lanes as a work queue (dgkr_gkr_prove_stream).

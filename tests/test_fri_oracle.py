@@ -53,3 +53,42 @@ def test_fri_honest_accepts_tampered_rejects(n, blowup, final, q):
         bad = bytearray(pr)
         bad[k] ^= 1
         assert not FO.fri_verify(fld, bytes(bad), n, blowup, final, q, O.Transcript("fri", fld))
+
+
+def test_fri_dist_world1_is_single_proof_with_header():
+    fld = O.BN254
+    co = O.random_elements(fld, 16, np.random.default_rng(3))
+    one = FO.fri_prove(fld, co, 2, 1, 8, O.Transcript("fri", fld))
+    (d,) = FO.fri_prove_dist(fld, [co], 2, 1, 8, O.Transcript("fri", fld))
+    assert d == (1).to_bytes(4, "little") + (0).to_bytes(4, "little") + one
+
+
+@pytest.mark.parametrize("world,n,blowup,final,q", [(2, 8, 2, 1, 4), (3, 16, 1, 2, 100), (4, 4, 3, 0, 8)])
+def test_fri_dist_honest_accepts_tampered_rejects(world, n, blowup, final, q):
+    fld = O.BN254
+    rng = np.random.default_rng(world * 100 + n)
+    chunks = [O.random_elements(fld, n, rng) for _ in range(world)]
+    prs = FO.fri_prove_dist(fld, chunks, blowup, final, q, O.Transcript("fri.d", fld))
+    assert FO.fri_verify_dist(fld, prs, n, blowup, final, q, O.Transcript("fri.d", fld))
+    # ranks swapped, a rank's proof missing, a flipped byte in the shared head or in the openings
+    assert not FO.fri_verify_dist(fld, prs[::-1], n, blowup, final, q, O.Transcript("fri.d", fld))
+    assert not FO.fri_verify_dist(fld, prs[:-1], n, blowup, final, q, O.Transcript("fri.d", fld))
+    for r in range(world):
+        for k in (20, len(prs[r]) // 2, len(prs[r]) - 3):
+            bad = list(prs)
+            b = bytearray(bad[r])
+            b[k] ^= 1
+            bad[r] = bytes(b)
+            assert not FO.fri_verify_dist(fld, bad, n, blowup, final, q, O.Transcript("fri.d", fld))
+
+
+def test_fri_dist_rejects_high_degree_rank():
+    """a rank whose codeword is not low-degree (random word) is caught"""
+    fld = O.BN254
+    rng = np.random.default_rng(5)
+    good = O.random_elements(fld, 8, rng)
+    bad = O.random_elements(fld, 32, rng)  # 4x the degree bound on the same domain with blowup 0
+    prs_good = FO.fri_prove_dist(fld, [good, good], 2, 1, 100, O.Transcript("fri.d", fld))
+    assert FO.fri_verify_dist(fld, prs_good, 8, 2, 1, 100, O.Transcript("fri.d", fld))
+    prs = FO.fri_prove_dist(fld, [good[:8] * 4, bad], 0, 1, 100, O.Transcript("fri.d", fld))
+    assert not FO.fri_verify_dist(fld, prs, 8, 2, 1, 100, O.Transcript("fri.d", fld))

@@ -54,3 +54,81 @@ def test_fri_large_verifies(ctx):
     co = W.random_inputs(fld.p, n, 9)
     got = P.fri_prove(ctx, f, co, 2, 6, 16, P.Transcript(f, "fri.big"))
     assert FO.fri_verify(fld, got, n, 2, 6, 16, O.Transcript("fri.big", fld))
+
+
+@pytest.mark.parametrize("world,n,blowup,final,q", [(1, 16, 2, 1, 8), (2, 8, 2, 1, 4), (3, 16, 1, 2, 100),
+                                                    (4, 256, 2, 3, 16), (8, 64, 1, 2, 12)])
+def test_fri_dist_emulated_matches_oracle(ctx, world, n, blowup, final, q):
+    """distributed FRI, `world` ranks as threads on lanes of one GPU: every
+    rank's proof equals the oracle's, the transcript ends in the same state
+    and the distributed verifier accepts"""
+    fld = O.BN254
+    f = P.Field(fld.p)
+    rng = np.random.default_rng(world * 1000 + n)
+    chunks = [O.random_elements(fld, n, rng) for _ in range(world)]
+    tr = P.Transcript(f, "fri.d", [world])
+    got = P.fri_prove_dist_emulated(ctx, f, chunks, blowup, final, q, tr)
+    otr = O.Transcript("fri.d", fld, [world])
+    assert got == FO.fri_prove_dist(fld, chunks, blowup, final, q, otr)
+    assert tr.state == otr.state
+    assert FO.fri_verify_dist(fld, got, n, blowup, final, q, O.Transcript("fri.d", fld, [world]))
+    if world == 1:
+        single = P.fri_prove(ctx, f, chunks[0], blowup, final, q, P.Transcript(f, "fri.d", [world]))
+        assert got[0][8:] == single
+
+
+@pytest.mark.parametrize("p", [O.GOLDILOCKS_P, 97])
+def test_fri_dist_emulated_runtime_fields(ctx, p):
+    fld = O.Field(p)
+    f = P.Field(p)
+    rng = np.random.default_rng(p % 1000)
+    n = 4 if p == 97 else 64
+    chunks = [O.random_elements(fld, n, rng) for _ in range(2)]
+    got = P.fri_prove_dist_emulated(ctx, f, chunks, 1, 1, 6, P.Transcript(f, "fri.d"))
+    assert got == FO.fri_prove_dist(fld, chunks, 1, 1, 6, O.Transcript("fri.d", fld))
+
+
+def test_fri_dist_large_verifies(ctx):
+    """4 ranks x 2^14 coefficients, blowup 4: the distributed verifier accepts"""
+    from paper_2404_10404_b200 import workloads as W
+
+    fld = O.BN254
+    f = P.Field(fld.p)
+    n = 1 << 14
+    chunks = [W.random_inputs(fld.p, n, 20 + r) for r in range(4)]
+    got = P.fri_prove_dist_emulated(ctx, f, chunks, 2, 5, 12, P.Transcript(f, "fri.dbig"))
+    assert FO.fri_verify_dist(fld, got, n, 2, 5, 12, O.Transcript("fri.dbig", fld))
+
+
+def test_fri_dist_two_process_shm(ctx, tmp_path):
+    """two processes (one per rank) over the shared-memory transport: each
+    rank's proof equals the emulated run's and the verifier accepts"""
+    import os
+    import secrets
+    import subprocess
+    import sys
+
+    from paper_2404_10404_b200 import workloads as W
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    world, n, blowup, final, q = 2, 1 << 10, 2, 3, 16
+    token = secrets.token_hex(4)
+    out = str(tmp_path / "fri")
+    worker = os.path.join(root, "tools", "fri_shm_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), token, str(n), str(blowup), str(final),
+                               str(q), out], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(world)]
+    logs = [p.communicate(timeout=300)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(logs)
+    fld = O.BN254
+    f = P.Field(fld.p)
+    chunks = [W.random_inputs(fld.p, n, 100 + r) for r in range(world)]
+    tr = P.Transcript(f, "fri.shm", [world])
+    want = P.fri_prove_dist_emulated(ctx, f, chunks, blowup, final, q, tr)
+    got = []
+    for r in range(world):
+        raw = open(f"{out}.{r}", "rb").read()
+        got.append(raw[:-32])
+        assert raw[-32:] == tr.state
+    assert got == want
+    assert FO.fri_verify_dist(fld, got, n, blowup, final, q, O.Transcript("fri.shm", fld, [world]))
