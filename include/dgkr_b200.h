@@ -171,8 +171,8 @@ int dgkr_gkr_prove_batch(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, si
                          const size_t* caps, size_t* lens);
 /* n proofs over n_lanes lanes as a work queue (a lane takes the next proof
  * when it finishes one), so the host transcript phases of different proofs
- * stagger instead of coinciding. inputs == NULL: every proof uses the inputs
- * loaded on the lane that runs it. lane_profiles (n_lanes entries, or NULL)
+ * stagger instead of coinciding. inputs == NULL: proof i runs on lane
+ * i mod n_lanes and proves the inputs loaded there (static assignment). lane_profiles (n_lanes entries, or NULL)
  * receives each lane's accumulated counters. */
 int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, size_t n, size_t n_lanes,
                           const uint8_t* const* inputs, dgkr_transcript* ts, uint8_t* const* proofs,

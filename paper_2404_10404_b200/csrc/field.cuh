@@ -177,8 +177,41 @@ __device__ __forceinline__ Fe fe_sub(const Fe& a, const Fe& b) {
     return r;
 }
 
+/// b - a + p in [0, 2p) without the conditional correction: for operands
+/// that only feed a Montgomery product. CIOS keeps its < 2p output (and one
+/// final subtraction) for inputs < 2p since 4p < R = 2^256 (p < 2^254), and
+/// the constant-multiplier path accepts any 256-bit input.
+template <class F>
+__device__ __forceinline__ Fe fe_sub_lazy(const Fe& b, const Fe& a) {
+    Fe r;
+    asm("sub.cc.u32  %0, %8, %16;\n\t"
+        "subc.cc.u32 %1, %9, %17;\n\t"
+        "subc.cc.u32 %2, %10, %18;\n\t"
+        "subc.cc.u32 %3, %11, %19;\n\t"
+        "subc.cc.u32 %4, %12, %20;\n\t"
+        "subc.cc.u32 %5, %13, %21;\n\t"
+        "subc.cc.u32 %6, %14, %22;\n\t"
+        "subc.u32    %7, %15, %23;\n\t"
+        "add.cc.u32  %0, %0, %24;\n\t"
+        "addc.cc.u32 %1, %1, %25;\n\t"
+        "addc.cc.u32 %2, %2, %26;\n\t"
+        "addc.cc.u32 %3, %3, %27;\n\t"
+        "addc.cc.u32 %4, %4, %28;\n\t"
+        "addc.cc.u32 %5, %5, %29;\n\t"
+        "addc.cc.u32 %6, %6, %30;\n\t"
+        "addc.u32    %7, %7, %31;"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]),
+          "=r"(r.v[7])
+        : "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]),
+          "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(F::p(0)), "r"(F::p(1)), "r"(F::p(2)), "r"(F::p(3)), "r"(F::p(4)), "r"(F::p(5)), "r"(F::p(6)),
+          "r"(F::p(7)));
+    return r;
+}
+
 /// One CIOS step: t[0..8] += a * bi; m = t0*np0; t += m*p; t >>= 32.
-/// t[8] is 0 on entry and exit (values stay < 2p < 2^255).
+/// t[8] is 0 on entry and exit: for a < 2p (lazy differences, fe_sub_lazy) the
+/// running value stays < 4p < 2^256, and the result < 2p needs 4p < R.
 template <class F>
 __device__ __forceinline__ void cios_step(uint32_t t[9], const Fe& a, uint32_t bi) {
     asm("mad.lo.cc.u32  %0, %9, %17, %0;\n\t"
@@ -261,6 +294,10 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
 /// 64 32x32 products + 2 Montgomery steps instead of CIOS's 8 (~40% fewer
 /// IMADs). S = sum < 8 * 2^32 * p < 2^289, so after the two steps the value
 /// is < 2^225 + p < 2p (needs p > 2^253 + 2^224, true for BN254 Fr).
+/// The 64-bit C form lowers to IMAD.WIDE (a third of the IMAD rate, on the
+/// FMA pipe); a PTX mad.lo/madc.hi form uses full-rate IMADs but adds ALU
+/// carry adds, and k_round is bound by the ALU pipe, so the C form measured
+/// as fast or faster.
 struct FoldConst {
     Fe c[8];  // c_k above (fully reduced)
     Fe r;     // r itself (Montgomery form), for the generic path
@@ -297,17 +334,25 @@ __device__ __forceinline__ Fe fe_mul_const_bn254(const Fe& x, const FoldConst& K
         t[8] = static_cast<uint32_t>(s);
         t[9] = 0;
     }
+    Fe d;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9, %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(Bn254::p(0)),
+          "r"(Bn254::p(1)), "r"(Bn254::p(2)), "r"(Bn254::p(3)), "r"(Bn254::p(4)), "r"(Bn254::p(5)), "r"(Bn254::p(6)),
+          "r"(Bn254::p(7)));
     Fe r;
-    uint32_t d[8];
-    uint64_t br = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint64_t s = static_cast<uint64_t>(t[j]) - Bn254::p(j) - br;
-        d[j] = static_cast<uint32_t>(s);
-        br = s >> 63;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r.v[j] = br ? t[j] : d[j];
+    for (int j = 0; j < 8; ++j) r.v[j] = borrow ? t[j] : d.v[j];
     return r;
 }
 

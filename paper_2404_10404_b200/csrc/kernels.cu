@@ -182,7 +182,7 @@ enum RoundMode : int { kScan = 0, kFoldNat = 1, kFoldRev = 2 };
 
 template <class F>
 __device__ __forceinline__ Fe foldk(const Fe& a, const Fe& b, const FoldConst& K) {
-    return fe_add<F>(a, fe_mul_fold<F>(fe_sub<F>(b, a), K));
+    return fe_add<F>(a, fe_mul_fold<F>(fe_sub_lazy<F>(b, a), K));
 }
 
 template <class F, int MODE>
@@ -225,7 +225,7 @@ __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i
         load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
         s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
         if constexpr (S1) s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
-        s[NS - 1] = fe_add<F>(s[NS - 1], fe_mul<F>(fe_sub<F>(f1, f0), fe_sub<F>(g1, g0)));
+        s[NS - 1] = fe_add<F>(s[NS - 1], fe_mul<F>(fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0)));
     }
     if (HAS_G) {
         Fe g0, g1;

@@ -1981,13 +1981,15 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
         ctx->use(f);  // upload runtime-field constants once, before concurrency
         std::vector<std::string> errs(n);
         std::vector<int> codes(n, DGKR_OK);
+        // host inputs: a work queue (any lane may take any proof); resident
+        // inputs: proof i belongs to lane i mod L, whose loaded inputs it proves
         std::atomic<std::size_t> next{0};
         auto work = [&](std::size_t li) {
             CK(cudaSetDevice(ctx->device));
             Lane* Ln = lanes[li];
             dgkr_profile acc{};
-            for (;;) {
-                const std::size_t i = next.fetch_add(1);
+            for (std::size_t k = 0;; ++k) {
+                const std::size_t i = inputs ? next.fetch_add(1) : li + k * L;
                 if (i >= n) break;
                 try {
                     Ln->begin_call();
