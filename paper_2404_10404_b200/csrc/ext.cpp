@@ -25,10 +25,7 @@ void pow_table(Lane* ctx, const dgkr_field* f, const U256& base, std::uint64_t n
     std::uint64_t na = 1;
     while (na * na < n) na <<= 1;
     scratch.ensure(na + n / na + 2);
-    Fe* db = ctx->d_small.p + Lane::kEqOff;  // one staged element
-    ctx->h_small[Lane::kEqOff] = to_fe(base);
-    ctx->h2d(db, ctx->h_small + Lane::kEqOff, sizeof(Fe));
-    launch_pow_table(ctx->use(f), db, n, out, scratch.p, ctx->st);
+    launch_pow_table(ctx->use(f), to_fe(base), n, out, scratch.p, ctx->st);
     ctx->launched(2);
 }
 

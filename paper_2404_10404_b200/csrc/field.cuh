@@ -1,7 +1,7 @@
 // Device prime-field arithmetic for sm_100a: 256-bit Montgomery form
 // (R = 2^256, 8 x 32-bit little-endian limbs, the same bits as the host's
-// 4 x 64-bit HostField), multiplication by CIOS on the integer pipe with
-// PTX carry chains (mad.lo.cc / madc.hi.cc -> IMAD / IMAD.HI with CC).
+// 4 x 64-bit HostField), multiplication by CIOS with 64-bit partial products
+// (IMAD.WIDE on the integer pipe) and PTX carry chains for add/sub.
 //
 // Two modulus policies:
 //   Bn254  - BN254 Fr (field.hpp:44-49) with the modulus as immediates;
@@ -209,65 +209,40 @@ __device__ __forceinline__ Fe fe_sub_lazy(const Fe& b, const Fe& a) {
     return r;
 }
 
-/// One CIOS step: t[0..8] += a * bi; m = t0*np0; t += m*p; t >>= 32.
-/// t[8] is 0 on entry and exit: for a < 2p (lazy differences, fe_sub_lazy) the
-/// running value stays < 4p < 2^256, and the result < 2p needs 4p < R.
-template <class F>
-__device__ __forceinline__ void cios_step(uint32_t t[9], const Fe& a, uint32_t bi) {
-    asm("mad.lo.cc.u32  %0, %9, %17, %0;\n\t"
-        "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"
-        "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"
-        "madc.lo.cc.u32 %3, %12, %17, %3;\n\t"
-        "madc.lo.cc.u32 %4, %13, %17, %4;\n\t"
-        "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"
-        "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"
-        "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"
-        "addc.u32       %8, 0, 0;\n\t"
-        "mad.hi.cc.u32  %1, %9, %17, %1;\n\t"
-        "madc.hi.cc.u32 %2, %10, %17, %2;\n\t"
-        "madc.hi.cc.u32 %3, %11, %17, %3;\n\t"
-        "madc.hi.cc.u32 %4, %12, %17, %4;\n\t"
-        "madc.hi.cc.u32 %5, %13, %17, %5;\n\t"
-        "madc.hi.cc.u32 %6, %14, %17, %6;\n\t"
-        "madc.hi.cc.u32 %7, %15, %17, %7;\n\t"
-        "madc.hi.u32    %8, %16, %17, %8;"
-        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8])
-        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
-          "r"(bi));
-    const uint32_t m = t[0] * F::np0();
-    asm("mad.lo.cc.u32  %0, %9, %17, %0;\n\t"
-        "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"
-        "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"
-        "madc.lo.cc.u32 %3, %12, %17, %3;\n\t"
-        "madc.lo.cc.u32 %4, %13, %17, %4;\n\t"
-        "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"
-        "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"
-        "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"
-        "addc.u32       %8, %8, 0;\n\t"
-        "mad.hi.cc.u32  %1, %9, %17, %1;\n\t"
-        "madc.hi.cc.u32 %2, %10, %17, %2;\n\t"
-        "madc.hi.cc.u32 %3, %11, %17, %3;\n\t"
-        "madc.hi.cc.u32 %4, %12, %17, %4;\n\t"
-        "madc.hi.cc.u32 %5, %13, %17, %5;\n\t"
-        "madc.hi.cc.u32 %6, %14, %17, %6;\n\t"
-        "madc.hi.cc.u32 %7, %15, %17, %7;\n\t"
-        "madc.hi.u32    %8, %16, %17, %8;"
-        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8])
-        : "r"(F::p(0)), "r"(F::p(1)), "r"(F::p(2)), "r"(F::p(3)), "r"(F::p(4)), "r"(F::p(5)), "r"(F::p(6)),
-          "r"(F::p(7)), "r"(m));
-    // shift down one limb (t[0] is zero by construction)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = t[j + 1];
-    t[8] = 0;
-}
-
-/// Montgomery product a*b*R^{-1} mod p, fully reduced.
+/// Montgomery product a*b*R^{-1} mod p, fully reduced: CIOS with 64-bit C
+/// partial products. ptxas lowers a*b+t+c to IMAD.WIDE plus one add, which
+/// measured 7% faster than PTX mad.lo/madc.hi carry chains (IMAD + IADD3.X
+/// per product): 4.53 vs 4.23e10 mul/s on B200,
+/// profiles/mulbench_r1.jsonl. Inputs may be < 2p (lazy differences): the
+/// running value stays < 4p and the result < 2p since 4p < R.
 template <class F>
 __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
-    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cios_step<F>(t, a, b.v[i]);
-    Fe s;
+    for (int i = 0; i < 8; ++i) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = static_cast<uint32_t>(s >> 32);
+        const uint32_t m = t[0] * F::np0();
+        c = (static_cast<uint64_t>(m) * F::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s2 = static_cast<uint64_t>(m) * F::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s2);
+            c = s2 >> 32;
+        }
+        s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        t[8] = t[9] + static_cast<uint32_t>(s >> 32);
+    }
+    Fe d;
     uint32_t borrow;
     asm("sub.cc.u32  %0, %9, %17;\n\t"
         "subc.cc.u32 %1, %10, %18;\n\t"
@@ -278,13 +253,13 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
         "subc.cc.u32 %6, %15, %23;\n\t"
         "subc.cc.u32 %7, %16, %24;\n\t"
         "subc.u32    %8, 0, 0;"
-        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]),
-          "=r"(s.v[7]), "=r"(borrow)
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
         : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(F::p(0)),
           "r"(F::p(1)), "r"(F::p(2)), "r"(F::p(3)), "r"(F::p(4)), "r"(F::p(5)), "r"(F::p(6)), "r"(F::p(7)));
     Fe r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.v[i] = borrow ? t[i] : s.v[i];
+    for (int j = 0; j < 8; ++j) r.v[j] = borrow ? t[j] : d.v[j];
     return r;
 }
 

@@ -931,8 +931,7 @@ __device__ __forceinline__ Fe fe_pow_small(Fe b, std::uint64_t e) {
 
 // scratch: [0, 2^k) = base^j, [2^k, 2^k + ceil(n/2^k)) = base^(m 2^k)
 template <class F>
-__global__ void __launch_bounds__(kThreads) k_pow_parts(const Fe* base, int k, std::uint64_t nb, Fe* scratch) {
-    const Fe b = fe_load(base);
+__global__ void __launch_bounds__(kThreads) k_pow_parts(const Fe b, int k, std::uint64_t nb, Fe* scratch) {
     const std::uint64_t na = std::uint64_t{1} << k;
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < na + nb;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -1371,7 +1370,9 @@ void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st) {
     check_launch("mul_peak");
 }
 
-void launch_pow_table(FieldKind k, const Fe* base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st) {
+/// base travels by value in the launch parameters: no host staging buffer
+/// that a later call could overwrite before an async upload reads it
+void launch_pow_table(FieldKind k, const Fe& base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st) {
     int kk = 0;
     while ((std::uint64_t{1} << (2 * (kk + 1))) <= n) ++kk;  // 2^kk ~ sqrt(n)
     const std::uint64_t na = std::uint64_t{1} << kk, nb = (n + na - 1) >> kk;

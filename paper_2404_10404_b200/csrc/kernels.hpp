@@ -170,7 +170,7 @@ void launch_mul_peak(int n_blocks, int iters, Fe* sink, cudaStream_t st);
 // ---- Reed-Solomon encoding (NTT) and FRI folding ------------------------
 /// out[i] = A[i & (2^k - 1)] * B[i >> k] for i < n, where A[j] = base^j and
 /// B[m] = base^(m 2^k) are built per thread by square-and-multiply.
-void launch_pow_table(FieldKind k, const Fe* base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st);
+void launch_pow_table(FieldKind k, const Fe& base, std::uint64_t n, Fe* out, Fe* scratch, cudaStream_t st);
 /// out[brev(i)] = in[i] * (scale ? scale[i] : 1), i < 2^log_n  (scale: coset powers)
 void launch_bitrev_scale(FieldKind k, const Fe* in, const Fe* scale, Fe* out, int log_n, std::uint64_t n_in,
                          cudaStream_t st);

@@ -123,6 +123,90 @@ __device__ __forceinline__ Fe mul_r26(const Fe& a, const Fe& b) {
 
 constexpr int kThreads = 256;
 
+// CIOS with 64-bit C partial products (IMAD.WIDE)
+__device__ __forceinline__ Fe mul_wide(const Fe& a, const Fe& b) {
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = static_cast<uint32_t>(s >> 32);
+        const uint32_t m = t[0] * Bn254::np0();
+        c = (static_cast<uint64_t>(m) * Bn254::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s2 = static_cast<uint64_t>(m) * Bn254::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s2);
+            c = s2 >> 32;
+        }
+        s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        t[8] = t[9] + static_cast<uint32_t>(s >> 32);
+    }
+    Fe d;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9, %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(Bn254::p(0)),
+          "r"(Bn254::p(1)), "r"(Bn254::p(2)), "r"(Bn254::p(3)), "r"(Bn254::p(4)), "r"(Bn254::p(5)), "r"(Bn254::p(6)),
+          "r"(Bn254::p(7)));
+    Fe r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = borrow ? t[j] : d.v[j];
+    return r;
+}
+
+// constant-multiplier throughput: K in kernel-parameter space (as k_round) or
+// staged in shared memory (a per-block multiplier)
+__global__ void __launch_bounds__(kThreads) k_const_param(int iters, Fe* sink, unsigned never,
+                                                          const __grid_constant__ FoldConst K) {
+    Fe a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[k].v[i] = (threadIdx.x * 0x9e3779b9u + k * 0x85ebca6bu + i) & 0x0fffffffu;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = fe_mul_const_bn254(a[k], K);
+    }
+    Fe s = fe_add<Bn254>(fe_add<Bn254>(a[0], a[1]), fe_add<Bn254>(a[2], a[3]));
+    if (s.v[0] == never) fe_store(sink, s);
+}
+
+__global__ void __launch_bounds__(kThreads) k_const_smem(int iters, Fe* sink, unsigned never, const FoldConst* Kg) {
+    __shared__ FoldConst K;
+    if (threadIdx.x < sizeof(FoldConst) / 4)
+        reinterpret_cast<uint32_t*>(&K)[threadIdx.x] = reinterpret_cast<const uint32_t*>(Kg)[threadIdx.x];
+    __syncthreads();
+    Fe a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[k].v[i] = (threadIdx.x * 0x9e3779b9u + k * 0x85ebca6bu + i) & 0x0fffffffu;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = fe_mul_const_bn254(a[k], K);
+    }
+    Fe s = fe_add<Bn254>(fe_add<Bn254>(a[0], a[1]), fe_add<Bn254>(a[2], a[3]));
+    if (s.v[0] == never) fe_store(sink, s);
+}
+
 template <int V>
 __global__ void __launch_bounds__(kThreads) k_bench(int iters, Fe* sink, unsigned never) {
     Fe a[4], b;
@@ -134,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_bench(int iters, Fe* sink, unsigne
     for (int i = 0; i < 8; ++i) b.v[i] = (blockIdx.x * 0x27d4eb2fu + i) & 0x0fffffffu;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] = V == 0 ? fe_mul<Bn254>(a[k], b) : mul_r26(a[k], b);
+        for (int k = 0; k < 4; ++k) a[k] = V == 0 ? fe_mul<Bn254>(a[k], b) : V == 1 ? mul_r26(a[k], b) : mul_wide(a[k], b);
     }
     Fe s = fe_add<Bn254>(fe_add<Bn254>(a[0], a[1]), fe_add<Bn254>(a[2], a[3]));
     if (s.v[0] == never) fe_store(sink, s);
@@ -181,6 +265,9 @@ __global__ void k_check(const Fe* a, const Fe* b, Fe* out0, Fe* out1, int n) {
     if (i >= n) return;
     out0[i] = fe_mul<Bn254>(a[i], b[i]);
     out1[i] = mul_r26(a[i], b[i]);
+    const Fe w = mul_wide(a[i], b[i]);
+    for (int j = 0; j < 8; ++j)
+        if (w.v[j] != out0[i].v[j]) out1[i].v[0] ^= 0x80000000u;
 }
 
 static void set_consts() {
@@ -237,7 +324,7 @@ int main() {
     CK(cudaMemcpy(r1.data(), o1, n * sizeof(Fe), cudaMemcpyDeviceToHost));
     int bad = 0;
     for (int i = 0; i < n; ++i) bad += std::memcmp(&r0[i], &r1[i], sizeof(Fe)) != 0;
-    std::printf("{\"check\": \"r26 vs cios on %d random products\", \"mismatches\": %d}\n", n, bad);
+    std::printf("{\"check\": \"r26 and cios_wide vs cios on %d random products\", \"mismatches\": %d}\n", n, bad);
 
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
@@ -268,5 +355,18 @@ int main() {
     std::printf("{\"probe\": \"cios\", \"mul_per_s\": %.4g}\n", thr * miters * 4 / (ms * 1e-3));
     ms = timeit([&] { k_bench<1><<<blocks, kThreads>>>(miters, sink, 0xffffffffu); });
     std::printf("{\"probe\": \"r26\", \"mul_per_s\": %.4g}\n", thr * miters * 4 / (ms * 1e-3));
+    ms = timeit([&] { k_bench<2><<<blocks, kThreads>>>(miters, sink, 0xffffffffu); });
+    std::printf("{\"probe\": \"cios_wide\", \"mul_per_s\": %.4g}\n", thr * miters * 4 / (ms * 1e-3));
+    FoldConst hk;
+    for (int k = 0; k < 8; ++k)
+        for (int i = 0; i < 8; ++i) hk.c[k].v[i] = static_cast<uint32_t>(rng()) & (i == 7 ? 0x2fffffffu : ~0u);
+    hk.r = hk.c[0];
+    FoldConst* dk;
+    CK(cudaMalloc(&dk, sizeof(FoldConst)));
+    CK(cudaMemcpy(dk, &hk, sizeof(FoldConst), cudaMemcpyHostToDevice));
+    ms = timeit([&] { k_const_param<<<blocks, kThreads>>>(miters, sink, 0xffffffffu, hk); });
+    std::printf("{\"probe\": \"const_param\", \"mul_per_s\": %.4g}\n", thr * miters * 4 / (ms * 1e-3));
+    ms = timeit([&] { k_const_smem<<<blocks, kThreads>>>(miters, sink, 0xffffffffu, dk); });
+    std::printf("{\"probe\": \"const_smem\", \"mul_per_s\": %.4g}\n", thr * miters * 4 / (ms * 1e-3));
     return 0;
 }
