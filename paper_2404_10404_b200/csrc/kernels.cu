@@ -343,6 +343,54 @@ __global__ void __launch_bounds__(kThreads) k_split_eq_expand(SplitEq e, std::ui
     }
 }
 
+// BN254 single-term split-eq with the constant-multiplier product: B[h] is
+// constant over the 2^klo outputs of row h, so its FoldConst table
+// (c_k = mont(B[h], 2^(32k+64)), one per row) is built once and each block
+// multiplies its chunk by the row's constants staged in shared memory.
+struct FoldPow {
+    Fe c[8];
+};
+
+__global__ void __launch_bounds__(kThreads) k_eq_hi_const(const Fe* __restrict__ B, std::uint64_t nh,
+                                                          const __grid_constant__ FoldPow fp, Fe* __restrict__ hc) {
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < nh * 9;
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t h = t / 9;
+        const int k = static_cast<int>(t % 9);
+        const Fe b = fe_load_nc(B + h);
+        fe_store(hc + t, k < 8 ? fe_mul<Bn254>(b, fp.c[k]) : b);
+    }
+}
+
+/// chunks of 256 outputs, a contiguous run of chunks per block (the row
+/// constant changes every 2^klo / 256 chunks); dense != nullptr adds dense[i]
+__global__ void __launch_bounds__(kThreads) k_split_eq_expand_const(const Fe* __restrict__ A, int klo,
+                                                                    std::uint64_t offset, std::uint64_t n,
+                                                                    const Fe* __restrict__ hc,
+                                                                    const Fe* __restrict__ dense, Fe* __restrict__ out) {
+    __shared__ FoldConst K;
+    const std::uint64_t chunks = n >> 8;
+    const std::uint64_t per = (chunks + gridDim.x - 1) / gridDim.x;
+    const std::uint64_t q0 = blockIdx.x * per, q1 = q0 + per < chunks ? q0 + per : chunks;
+    const std::uint64_t mask = (std::uint64_t{1} << klo) - 1;
+    std::uint64_t cur = ~std::uint64_t{0};
+    for (std::uint64_t q = q0; q < q1; ++q) {
+        const std::uint64_t g0 = (q << 8) + offset;
+        const std::uint64_t h = g0 >> klo;  // block-uniform
+        if (h != cur) {
+            __syncthreads();  // the previous row's constants are no longer read
+            if (threadIdx.x < sizeof(FoldConst) / 16)
+                reinterpret_cast<uint4*>(&K)[threadIdx.x] = reinterpret_cast<const uint4*>(hc + h * 9)[threadIdx.x];
+            __syncthreads();
+            cur = h;
+        }
+        const std::uint64_t i = (q << 8) + threadIdx.x;
+        Fe w = fe_mul_const_bn254(fe_load_nc(A + ((g0 + threadIdx.x) & mask)), K);
+        if (dense) w = fe_add<Bn254>(fe_load_nc(dense + i), w);
+        fe_store(out + i, w);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // GKR layer bookkeeping (CSR gather-reduce; the wiring transpose is built once
 // per circuit, so there are no atomics on 256-bit values).
@@ -1287,14 +1335,41 @@ void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, c
     check_launch("round_small");
 }
 
+/// the constant-multiplier path applies: BN254, one term, rows of >= 256
+/// outputs aligned to the chunks
+static bool eq_const_path(FieldKind k, const SplitEq& e, std::uint64_t n, const std::uint8_t* fold_pow, Fe* hc) {
+    return fold_pow && hc && k == FieldKind::Bn254 && e.K == 1 && e.klo >= 8 && n % 256 == 0 && e.offset % 256 == 0;
+}
+
+static void launch_eq_const(const SplitEq& e, std::uint64_t n, const Fe* dense, Fe* out, cudaStream_t st,
+                            const std::uint8_t* fold_pow, Fe* hc) {
+    FoldPow fp;
+    std::memcpy(&fp, fold_pow, sizeof(fp));
+    const std::uint64_t nh = std::uint64_t{1} << e.khi;
+    k_eq_hi_const<<<grid_for(nh * 9, kThreads, 148 * 8), kThreads, 0, st>>>(e.B, nh, fp, hc);
+    const int g = static_cast<int>(std::min<std::uint64_t>(n >> 8, 148 * 8));
+    k_split_eq_expand_const<<<g, kThreads, 0, st>>>(e.A, e.klo, e.offset, n, hc, dense, out);
+}
+
 void launch_split_eq_expand_add(FieldKind k, const SplitEq& e, std::uint64_t n, const Fe* dense, Fe* out,
-                                cudaStream_t st) {
+                                cudaStream_t st, const std::uint8_t* fold_pow, Fe* hc) {
+    if (eq_const_path(k, e, n, fold_pow, hc)) {
+        launch_eq_const(e, n, dense, out, st, fold_pow, hc);
+        check_launch("split_eq_expand_add(const)");
+        return;
+    }
     const int g = grid_for(n, kThreads, 148 * 16);
     DISPATCH_FIELD(k, F, (k_split_eq_expand_add<F><<<g, kThreads, 0, st>>>(e, n, dense, out)));
     check_launch("split_eq_expand_add");
 }
 
-void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st) {
+void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st,
+                            const std::uint8_t* fold_pow, Fe* hc) {
+    if (eq_const_path(k, e, n, fold_pow, hc)) {
+        launch_eq_const(e, n, nullptr, out, st, fold_pow, hc);
+        check_launch("split_eq_expand(const)");
+        return;
+    }
     const int g = grid_for(n, kThreads, 148 * 16);
     DISPATCH_FIELD(k, F, (k_split_eq_expand<F><<<g, kThreads, 0, st>>>(e, n, out)));
     check_launch("split_eq_expand");

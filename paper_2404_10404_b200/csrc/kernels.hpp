@@ -95,10 +95,16 @@ struct SplitEq {
 
 /// Dense expansion of a split-eq: out[i] = sum_t A[t][i & m] * B[t][i >> klo], i < n
 /// (coalesced; turns the per-wire split-eq lookups into one 32-byte gather).
-void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st);
+/// fold_pow (8 canonical 2^(32k+64) mod p, 32 B each) and hc (>= 9 * 2^khi
+/// elements of scratch) enable the BN254 single-term path: the B factor is
+/// constant over 2^klo consecutive outputs, so each block multiplies by it
+/// with the constant-multiplier product (field.cuh FoldConst; 1.6-1.7x CIOS).
+/// Either may be null (generic CIOS path).
+void launch_split_eq_expand(FieldKind k, const SplitEq& e, std::uint64_t n, Fe* out, cudaStream_t st,
+                            const std::uint8_t* fold_pow = nullptr, Fe* hc = nullptr);
 /// out[i] = dense[i] + sum_t seed_t A_t[lo] B_t[hi]  (one term reused from a dense chi table)
 void launch_split_eq_expand_add(FieldKind k, const SplitEq& e, std::uint64_t n, const Fe* dense, Fe* out,
-                                cudaStream_t st);
+                                cudaStream_t st, const std::uint8_t* fold_pow = nullptr, Fe* hc = nullptr);
 
 /// Per-slot description of a data-parallel layer: values are laid out as
 /// n_copies blocks of 2^log_stride (copy = high bits).

@@ -306,6 +306,7 @@ struct CircuitWs {
     DBuf<const Fe*> d_layer_vals;
     DBuf<Fe> H, G;      // bookkeeping outputs, max_slots x Tmax and Tmax
     DBuf<Fe> Wg, EqU;   // dense per-gate weights and chi(u) tables
+    DBuf<Fe> eq_hc;     // split-eq row constants (9 per hi row) for the BN254 constant-multiplier expansion
     DBuf<Fe> heavy_scr; // heavy-row partials: 2 x max_heavy
     DistTail dist;      // distributed phase-boundary buffers (run_rounds_dist)
     RoundBuffers rb;
@@ -618,6 +619,11 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
         for (std::uint32_t l = 1; l <= D; ++l) gmax = std::max(gmax, c.full_padded[l]);
         W.Wg.ensure(gmax);
         W.EqU.ensure(c.Tmax);
+        {  // hi rows of a split eq: 2^(nv - ceil(nv/2)); headroom for the rank bits of up to 16 ranks
+            unsigned lg = 0;
+            while ((std::uint64_t{1} << lg) < std::max(gmax, c.Tmax)) ++lg;
+            W.eq_hc.ensure(std::size_t{9} << (lg / 2 + 2));
+        }
         W.rb.ensure(2 * static_cast<int>(c.max_slots) + 1, c.Tmax, cudaStreamLegacy);
         W.heavy_scr.ensure(2 * static_cast<std::size_t>(std::max<std::uint32_t>(c.max_heavy, 1)));
     }
@@ -750,6 +756,14 @@ SplitEq build_split_eq(Lane* ctx, const dgkr_field* f, const std::vector<std::ve
     launch_eq_build(ctx->use(f), jobs_buf.p, static_cast<int>(jobs.size()), ctx->st);
     ctx->launched();
     return e;
+}
+
+/// fold_pow for the constant-multiplier split-eq expansion, after sizing the
+/// row-constant scratch for this expansion (null: the generic path)
+const std::uint8_t* eq_fold_pow(const dgkr_field* f, CircuitWs& W, const SplitEq& e) {
+    if (f->kind != FieldKind::Bn254 || e.K != 1) return nullptr;
+    W.eq_hc.ensure(std::size_t{9} << e.khi);
+    return reinterpret_cast<const std::uint8_t*>(f->fold_pow);
 }
 
 void load_inputs(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs) {
@@ -943,10 +957,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.G = W.G.p;
         bk.w = wq;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
+        const std::uint8_t* fp_w = eq_fold_pow(f, W, wq);  // sizes W.eq_hc first
         if (reuse_u)
-            launch_split_eq_expand_add(kind, wq, n_gates_local, W.EqU.p, W.Wg.p, ctx->st);  // w(g), gkr.hpp:140-148
+            launch_split_eq_expand_add(kind, wq, n_gates_local, W.EqU.p, W.Wg.p, ctx->st, fp_w, W.eq_hc.p);
         else
-            launch_split_eq_expand(kind, wq, n_gates_local, W.Wg.p, ctx->st);
+            launch_split_eq_expand(kind, wq, n_gates_local, W.Wg.p, ctx->st, fp_w, W.eq_hc.p);  // w(g), gkr.hpp:140-148
         ctx->launched();
         bk.gate_w = W.Wg.p;
         bk.perm = C.xperm.p;
@@ -987,7 +1002,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         f->fold_const(vx[0], vxk);
         bk.vx_const = vxk;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st);  // chi_x(u), sumcheck.hpp:415
+        const std::uint8_t* fp_u = eq_fold_pow(f, W, uq);
+        launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st, fp_u, W.eq_hc.p);  // chi_x(u), sumcheck.hpp:415
         equ_point = p1.challenges;
         equ_n = T;
         ctx->launched();
