@@ -356,8 +356,9 @@ public:
         const std::size_t w = f_->width();
         const unsigned top = static_cast<unsigned>(f_->bits() - 8 * (w - 1));
         const std::uint8_t mask = top >= 8 ? 0xff : static_cast<std::uint8_t>((1u << top) - 1);
-        const std::uint64_t draw = draws_++;
         std::uint8_t buf[64];
+        if (w == 0 || w > sizeof(buf)) fail(DGKR_LOGIC_ERROR, "field width out of range");
+        const std::uint64_t draw = draws_++;
         for (std::uint64_t ctr = 0;; ++ctr) {
             squeeze("chal", draw, ctr, w, buf);
             buf[w - 1] &= mask;
