@@ -53,22 +53,22 @@ struct ThreadComm : dgkr_comm {
     }
     void allgather(const void* d_send, void* d_recv, std::size_t bytes, Lane* L) override {
         stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->d2h(g->buf.data() + rank * bytes, d_send, bytes);
         L->sync();
         g->barrier();
-        CK(cudaMemcpyAsync(d_recv, g->buf.data(), world * bytes, cudaMemcpyHostToDevice, L->st));
+        L->h2d(d_recv, g->buf.data(), world * bytes);
         L->sync();
     }
     void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
         stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->d2h(g->buf.data() + rank * bytes, d_send, bytes);
         L->sync();
         g->barrier();
         std::memcpy(h_recv, g->buf.data(), world * bytes);
     }
     void gather_to_root_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L, int root) override {
         stage(bytes);
-        CK(cudaMemcpyAsync(g->buf.data() + rank * bytes, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->d2h(g->buf.data() + rank * bytes, d_send, bytes);
         L->sync();
         g->barrier();
         if (rank == root) std::memcpy(h_recv, g->buf.data(), world * bytes);
@@ -129,7 +129,7 @@ struct ShmComm : dgkr_comm {
     /// before the barrier that releases the slot)
     void stage_send(const void* d_send, std::size_t bytes, Lane* L) {
         if (!bounce) fail(DGKR_INVALID_ARGUMENT, "shared-memory communicator created without a context");
-        CK(cudaMemcpyAsync(bounce, d_send, bytes, cudaMemcpyDeviceToHost, L->st));
+        L->d2h(bounce, d_send, bytes);  // counted in the lane profile
         L->sync();
         barrier();  // previous contents consumed
         std::memcpy(slot(rank), bounce, bytes);
@@ -140,7 +140,7 @@ struct ShmComm : dgkr_comm {
         if (bytes * static_cast<std::size_t>(world) > hdr->slot_bytes) fail(DGKR_CAPACITY, "shm slot too small");
         stage_send(d_send, bytes, L);
         for (int r = 0; r < world; ++r) std::memcpy(bounce + r * bytes, slot(r), bytes);
-        CK(cudaMemcpyAsync(d_recv, bounce, static_cast<std::size_t>(world) * bytes, cudaMemcpyHostToDevice, L->st));
+        L->h2d(d_recv, bounce, static_cast<std::size_t>(world) * bytes);
         L->sync();
     }
     void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {

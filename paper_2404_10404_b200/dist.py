@@ -145,14 +145,18 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
     bufs = [np.empty(cap, dtype=np.uint8) for _ in range(lanes)]  # one per lane, reused
     gates = n_copies * (1 << lw) * depth
 
-    def timed(n):
+    def timed(n, inputs=None):
+        """device time of n proofs (CUDA events on the context stream around
+        the call, which returns after every lane's work is done), max over ranks"""
         dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2", spread_absorb=True,
-                                                  out_bufs=bufs)
-        torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], device="cuda" if backend == "nccl" else "cpu")
+        check(lib().dgkr_ctx_event_record(ctx.handle, 4))
+        proofs, states, profs = prove_dist_stream(ctx, comms, circ, field, n, "dgkr.bench.c2", inputs=inputs,
+                                                  spread_absorb=True, out_bufs=bufs)
+        check(lib().dgkr_ctx_event_record(ctx.handle, 5))
+        ev_ms = C.c_float()
+        check(lib().dgkr_ctx_event_elapsed(ctx.handle, 4, 5, C.byref(ev_ms)))
+        dt = torch.tensor([ev_ms.value * 1e-3], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)  # max over ranks
         return float(dt.item()), proofs, states, profs
 
@@ -162,6 +166,20 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
         sampler.start()
     dt, proofs, states, profs = timed(lanes * args.steps)
     clk = sampler.stop() if sampler else None
+    # e2e: the same stream with this rank's inputs read from pinned host memory
+    # by every proof (H2D inside) and proof bytes written to pinned host buffers
+    mine_p = np.empty_like(mine)
+    mine_p[:] = mine
+    pinned = [mine_p] + bufs
+    for a_ in pinned:
+        check(lib().dgkr_host_register(a_.ctypes.data_as(C.c_void_p), C.c_size_t(a_.nbytes)))
+    timed(lanes, inputs=mine_p)
+    dt_e2e, _, states_e2e, profs_e2e = timed(lanes * args.steps, inputs=mine_p)
+    io = torch.tensor([sum(p_["h2d_bytes"] for p_ in profs_e2e), sum(p_["d2h_bytes"] for p_ in profs_e2e)],
+                      dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(io, op=dist.ReduceOp.SUM)  # whole-job bytes
+    for a_ in pinned:
+        check(lib().dgkr_host_unregister(a_.ctypes.data_as(C.c_void_p)))
     # single-proof latency (one lane)
     lat, _, _, _ = timed(1)
     # one profiled proof (lane 0 of every rank): per-launch CUDA events around the round kernels
@@ -172,8 +190,9 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
     ctx.set_profile(False)
     pp = pprof[0]
     if rank == 0:
-        assert len(set(states)) == 1
+        assert len(set(states)) == 1 and set(states_e2e) == set(states)
         ms_per_step = 1e3 * dt / args.steps
+        e2e_ms = 1e3 * dt_e2e / args.steps
         line = {
             "metric": "gkr_prover_gates_per_sec", "value": lanes * gates / (ms_per_step * 1e-3), "unit": "gates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -185,9 +204,11 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
                        "output_absorb": "proof i on rank i mod N",
                        "l2": "no flush: layer tables exceed L2"},
             "lanes": lanes, "proof_latency_ms": 1e3 * lat,
-            "e2e": {"value": lanes * gates / (ms_per_step * 1e-3), "unit": "gates/s",
-                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": sum(p["d2h_bytes"] for p in profs) // args.steps,
-                    "note": "multi-GPU arm measures the resident-input stream only"},
+            "e2e": {"value": lanes * gates / (e2e_ms * 1e-3), "unit": "gates/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(io[0].item()) // args.steps,
+                    "d2h_bytes_per_step": int(io[1].item()) // args.steps,
+                    "note": "every rank's inputs from pinned host memory per proof, proof bytes to pinned host; "
+                            "bytes summed over ranks"},
             "gpu_launches": sum(p["launches"] for p in profs),
         }
         if pp["round_ms"] > 0 and "measured_peaks" in helpers:
