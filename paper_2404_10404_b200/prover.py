@@ -464,7 +464,8 @@ def fri_prove_dist_emulated(ctx: Context, field: Field, chunks: Sequence[Elems],
 def gkr_prove_stream(ctx: Context, circuit: Circuit, n: int, lanes: int, field: Field, label: str = "stream",
                      inputs: Optional[Sequence[Elems]] = None, out_bufs=None):
     """n proofs over `lanes` lanes as a work queue (dgkr_gkr_prove_stream).
-    inputs=None: each proof uses the inputs loaded on its lane. Returns
+    inputs=None: proof i runs on lane i mod lanes and proves the inputs loaded
+    there (static assignment; host inputs use a work queue). Returns
     (proofs, transcripts, per-lane profile dicts)."""
     from ._lib import Profile_t
 
