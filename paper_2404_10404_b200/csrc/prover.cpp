@@ -12,6 +12,7 @@
 #include <memory>
 #include <set>
 #include <string>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -1608,7 +1609,24 @@ struct ProofReader {
 };
 
 /// eq table: out[b] = seed * prod_k (b_k ? x_k : 1 - x_k), x_1 = LSB (mle.hpp:95-120)
-std::vector<U256> eq_table_host(const HostField& F, const std::vector<U256>& x, const U256& seed) {
+/// fn(begin, end) over [0, n) on up to 16 host threads (serial below 2^15)
+void par_for(std::uint64_t n, const std::function<void(std::uint64_t, std::uint64_t)>& fn) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < (std::uint64_t{1} << 15) || hw == 1) {
+        fn(std::uint64_t{0}, n);
+        return;
+    }
+    const std::uint64_t chunk = (n + hw - 1) / hw;
+    std::vector<std::thread> th;
+    for (unsigned i = 1; i < hw; ++i) {
+        const std::uint64_t b = std::min<std::uint64_t>(n, i * chunk), e = std::min<std::uint64_t>(n, b + chunk);
+        if (b < e) th.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    fn(std::uint64_t{0}, std::min<std::uint64_t>(n, chunk));
+    for (auto& t : th) t.join();
+}
+
+std::vector<U256> eq_table_doubling(const HostField& F, const std::vector<U256>& x, const U256& seed) {
     std::vector<U256> t(std::size_t{1} << x.size());
     t[0] = seed;
     for (std::size_t k = 0; k < x.size(); ++k) {
@@ -1619,6 +1637,22 @@ std::vector<U256> eq_table_host(const HostField& F, const std::vector<U256>& x, 
             t[b] = F.sub(t[b], hi);
         }
     }
+    return t;
+}
+
+/// seed * eq(x, b) for every b (b_k = bit k, mle.hpp:95-120): large tables as
+/// eq(low half) x eq(high half), expanded on host threads; the same field
+/// elements as the doubling (products mod p commute)
+std::vector<U256> eq_table_host(const HostField& F, const std::vector<U256>& x, const U256& seed) {
+    if (x.size() < 16) return eq_table_doubling(F, x, seed);
+    const std::size_t klo = x.size() / 2;
+    const std::vector<U256> lo = eq_table_doubling(F, std::vector<U256>(x.begin(), x.begin() + klo), seed);
+    const std::vector<U256> hi = eq_table_doubling(F, std::vector<U256>(x.begin() + klo, x.end()), F.one());
+    std::vector<U256> t(std::size_t{1} << x.size());
+    const std::uint64_t m = (std::uint64_t{1} << klo) - 1;
+    par_for(t.size(), [&](std::uint64_t b0, std::uint64_t b1) {
+        for (std::uint64_t b = b0; b < b1; ++b) t[b] = F.mul(lo[b & m], hi[b >> klo]);
+    });
     return t;
 }
 
@@ -1710,7 +1744,9 @@ bool gkr_verify_host(const dgkr_circuit& c, const HostField& F, const std::uint8
         std::vector<U256> wg(n_gates_full);
         for (const auto& t : combined.terms) {
             const std::vector<U256> eq = eq_table_host(F, t.point, t.weight);
-            for (std::uint64_t g = 0; g < n_gates_full && g < eq.size(); ++g) wg[g] = F.add(wg[g], eq[g]);
+            par_for(std::min<std::uint64_t>(n_gates_full, eq.size()), [&](std::uint64_t b0, std::uint64_t b1) {
+                for (std::uint64_t g = b0; g < b1; ++g) wg[g] = F.add(wg[g], eq[g]);
+            });
         }
         const std::vector<U256> ex = eq_table_host(F, xp, F.one()), ey = eq_table_host(F, yp, F.one());
         auto slot_of = [&](std::uint32_t l) {
@@ -1718,23 +1754,46 @@ bool gkr_verify_host(const dgkr_circuit& c, const HostField& F, const std::uint8
                 if (C.slots[s2] == l) return s2;
             return ns;
         };
-        U256 expected{};
+        // sum_wires w(g) chi_x(u) chi_y(v) * (V_x V_y | V_x + V_y), bucketed by
+        // (x slot, y slot, mul/add) so each wire costs two products; copies
+        // (or gate ranges) are split over host threads with private buckets
         const std::uint64_t g0 = c.h_lgs[layer - 1];
-        for (std::uint32_t cp = 0; cp < c.n_copies; ++cp) {
-            for (std::uint64_t g = 0; g < sub_g; ++g) {
+        const std::size_t nb = 2 * ns * ns;
+        std::mutex bmu;
+        std::vector<U256> bucket(nb);
+        bool wiring_ok = true;
+        const std::uint64_t n_items = static_cast<std::uint64_t>(c.n_copies) * sub_g;
+        par_for(n_items, [&](std::uint64_t i0, std::uint64_t i1) {
+            std::vector<U256> acc(nb);
+            bool ok_local = true;
+            for (std::uint64_t it = i0; it < i1; ++it) {
+                const std::uint64_t cp = it / sub_g, g = it % sub_g;
                 const U256 w = wg[cp * pad_g + g];
                 for (std::uint64_t e = c.h_gns[g0 + g]; e < c.h_gns[g0 + g + 1]; ++e) {
                     const std::uint32_t* ng = &c.h_nested[5 * e];
                     const std::size_t sx = slot_of(ng[1]), sy = slot_of(ng[3]);
-                    if (sx >= ns || sy >= ns) return false;
-                    const std::uint64_t xi = static_cast<std::uint64_t>(cp) * c.sub_padded[ng[1]] + ng[2];
-                    const std::uint64_t yi = static_cast<std::uint64_t>(cp) * c.sub_padded[ng[3]] + ng[4];
-                    const U256 t = F.mul(w, F.mul(ex[xi], ey[yi]));
-                    const U256 vx = finals[sx], vy = finals[ns + sy];
-                    expected = F.add(expected, F.mul(t, ng[0] ? F.mul(vx, vy) : F.add(vx, vy)));
+                    if (sx >= ns || sy >= ns) {
+                        ok_local = false;
+                        continue;
+                    }
+                    const std::uint64_t xi = cp * c.sub_padded[ng[1]] + ng[2];
+                    const std::uint64_t yi = cp * c.sub_padded[ng[3]] + ng[4];
+                    U256& bk = acc[(sx * ns + sy) * 2 + (ng[0] ? 1 : 0)];
+                    bk = F.add(bk, F.mul(w, F.mul(ex[xi], ey[yi])));
                 }
             }
-        }
+            std::lock_guard<std::mutex> lk(bmu);
+            if (!ok_local) wiring_ok = false;
+            for (std::size_t k = 0; k < nb; ++k) bucket[k] = F.add(bucket[k], acc[k]);
+        });
+        if (!wiring_ok) return false;
+        U256 expected{};
+        for (std::size_t sx = 0; sx < ns; ++sx)
+            for (std::size_t sy = 0; sy < ns; ++sy) {
+                const U256 vx = finals[sx], vy = finals[ns + sy];
+                expected = F.add(expected, F.mul(bucket[(sx * ns + sy) * 2 + 1], F.mul(vx, vy)));
+                expected = F.add(expected, F.mul(bucket[(sx * ns + sy) * 2], F.add(vx, vy)));
+            }
         if (!(expected == claim)) return false;
         for (std::size_t s2 = 0; s2 < ns; ++s2) {
             const std::uint32_t src = C.slots[s2];
