@@ -252,7 +252,7 @@ AhPass ah_enqueue(Lane* ctx, const dgkr_field* f, const std::uint8_t* items, std
     x.ensure(std::max<std::uint64_t>(n, 1));
     stage.ensure(std::max<std::size_t>(n * w, 1));
     if (n) {
-        ctx->h2d(stage.p, items, n * w);
+        ctx->h2d_large(stage.p, items, n * w);
         launch_from_canonical(kind, stage.p, static_cast<int>(w), x.p, n, ctx->d_err.p, ctx->st);
         ctx->launched();
     }
@@ -392,7 +392,7 @@ unsigned beacon_build(Lane* ctx, NttWs& ws, const std::uint8_t* records, std::ui
     if (a > depth) fail(DGKR_INVALID_ARGUMENT, "validator set exceeds tree capacity");  // beacon.hpp:113-115
     const std::uint64_t cap = std::uint64_t{1} << a;
     ws.b_recs.ensure(std::max<std::uint64_t>(n, 1) * 64);
-    if (n) ctx->h2d(ws.b_recs.p, records, n * 64);
+    if (n) ctx->h2d_large(ws.b_recs.p, records, n * 64);
     ws.b_zc.ensure((depth + 1) * 32);
     ctx->h2d(ws.b_zc.p, zc.data(), (depth + 1) * 32);
     ws.b_nodes.ensure(2 * cap * 32);
@@ -478,9 +478,9 @@ int dgkr_beacon_verify(dgkr_ctx* ctx, const std::uint8_t* root, const std::uint8
         ws.b_zc.ensure((zdepth + 1) * 32);
         ws.b_ok.ensure(m);
         ctx->h2d(ws.b_root.p, root, 32);
-        ctx->h2d(ws.b_recs.p, records, m * 64);
-        ctx->h2d(ws.b_leaves.p, leaves, m * 32);
-        if (a) ctx->h2d(ws.b_sib.p, siblings, m * a * 32);
+        ctx->h2d_large(ws.b_recs.p, records, m * 64);
+        ctx->h2d_large(ws.b_leaves.p, leaves, m * 32);
+        if (a) ctx->h2d_large(ws.b_sib.p, siblings, m * a * 32);
         ctx->h2d(ws.didx.p, indices, m * 8);
         ctx->h2d(ws.b_zc.p, zc.data(), (zdepth + 1) * 32);
         ctx->tbeg();
