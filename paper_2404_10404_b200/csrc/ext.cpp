@@ -445,8 +445,8 @@ int dgkr_beacon_prove(dgkr_ctx* ctx, const std::uint8_t* records, std::size_t n,
             ctx->h2d(ws.didx.p, indices, m * 8);
             launch_beacon_paths(ws.b_nodes.p, static_cast<int>(a), ws.didx.p, m, ws.b_leaves.p, ws.b_sib.p, ctx->st);
             ctx->launched();
-            ctx->d2h(leaves, ws.b_leaves.p, m * 32);
-            if (a) ctx->d2h(siblings, ws.b_sib.p, m * a * 32);
+            ctx->d2h_large(leaves, ws.b_leaves.p, m * 32);
+            if (a) ctx->d2h_large(siblings, ws.b_sib.p, m * a * 32);
         }
         ctx->sync();
         *active_log2 = a;
@@ -526,8 +526,7 @@ int dgkr_ntt(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* in, unsigne
         }
         stage.ensure(N * w);
         launch_to_canonical(kind, a.p, stage.p, static_cast<int>(w), N, ctx->st);
-        ctx->d2h(out, stage.p, N * w);
-        ctx->sync();
+        ctx->d2h_large(out, stage.p, N * w);
         ctx->end_call();
     });
 }
@@ -554,8 +553,7 @@ int dgkr_rs_encode(dgkr_ctx* ctx, const dgkr_field* f, const std::uint8_t* coeff
         coset_ntt(ctx, f, cf.p, n, log_n, f->coset, true, a.p, tw, cpow, scratch);
         stage.ensure(N * w);
         launch_to_canonical(ctx->use(f), a.p, stage.p, static_cast<int>(w), N, ctx->st);
-        ctx->d2h(out, stage.p, N * w);
-        ctx->sync();
+        ctx->d2h_large(out, stage.p, N * w);
         ctx->end_call();
     });
 }

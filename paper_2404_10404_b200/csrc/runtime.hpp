@@ -302,7 +302,7 @@ struct Lane {
     /// host copies run in parallel and overlap the DMA. Stream order covers
     /// later kernels; a slot is rewritten only after its previous DMA's event.
     /// Pinned sources and small copies take the plain path.
-    static constexpr int kUpThreads = 4;
+    static constexpr int kUpThreads = 8;
     static constexpr std::size_t kUpChunk = std::size_t{8} << 20;
     std::uint8_t* up_ring = nullptr;  // kUpThreads * 2 * kUpChunk, pinned, lazily
     cudaEvent_t up_ev[kUpThreads * 2] = {};
@@ -353,6 +353,68 @@ struct Lane {
         for (int k = 0; k < kUpThreads; ++k)
             if (errs[k]) fail(DGKR_CUDA_ERROR, std::string("chunked upload: ") + cudaGetErrorString(cudaGetLastError()));
         prof.h2d_bytes += n;
+    }
+    /// Large downloads into pageable memory, the mirror of h2d_large: chunk
+    /// DMAs into per-thread pinned slots on the lane stream, host threads copy
+    /// each slot out once its event fires. Returns with the data in dst (the
+    /// lane stream has reached the last chunk). Pinned destinations and small
+    /// copies take the plain path plus a stream sync.
+    void d2h_large(void* dst, const void* src, std::size_t n) {
+        cudaPointerAttributes at{};
+        const bool pinned = cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        if (!pinned) (void)cudaGetLastError();
+        if (pinned || n < 4 * kUpChunk) {
+            d2h(dst, src, n);
+            sync();
+            return;
+        }
+        if (!up_ring) {
+            CK(cudaMallocHost(reinterpret_cast<void**>(&up_ring), kUpThreads * 2 * kUpChunk));
+            for (auto& e : up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const std::size_t part = (n + kUpThreads - 1) / kUpThreads;
+        std::vector<std::thread> th;
+        std::vector<int> errs(kUpThreads, 0);
+        auto work = [&](int k) {
+            if (cudaSetDevice(device) != cudaSuccess) {
+                errs[k] = 1;
+                return;
+            }
+            const std::size_t b = std::min(n, k * part), e = std::min(n, b + part);
+            auto enqueue = [&](std::size_t off, int slot) {
+                const int s = 2 * k + slot;
+                const std::size_t len = std::min(kUpChunk, e - off);
+                if (up_recorded[s] && cudaEventSynchronize(up_ev[s]) != cudaSuccess) return false;
+                if (cudaMemcpyAsync(up_ring + static_cast<std::size_t>(s) * kUpChunk,
+                                    static_cast<const std::uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                    st) != cudaSuccess ||
+                    cudaEventRecord(up_ev[s], st) != cudaSuccess)
+                    return false;
+                up_recorded[s] = true;
+                return true;
+            };
+            // two chunks in flight per thread: copy one out while the next lands
+            if (b < e && !enqueue(b, 0)) errs[k] = 1;
+            if (b + kUpChunk < e && !enqueue(b + kUpChunk, 1)) errs[k] = 1;
+            int slot = 0;
+            for (std::size_t off = b; off < e && !errs[k]; off += kUpChunk, slot ^= 1) {
+                const int s = 2 * k + slot;
+                const std::size_t len = std::min(kUpChunk, e - off);
+                if (cudaEventSynchronize(up_ev[s]) != cudaSuccess) {
+                    errs[k] = 1;
+                    break;
+                }
+                std::memcpy(static_cast<std::uint8_t*>(dst) + off, up_ring + static_cast<std::size_t>(s) * kUpChunk,
+                            len);
+                if (off + 2 * kUpChunk < e && !enqueue(off + 2 * kUpChunk, slot)) errs[k] = 1;
+            }
+        };
+        for (int k = 1; k < kUpThreads; ++k) th.emplace_back(work, k);
+        work(0);
+        for (auto& t : th) t.join();
+        for (int k = 0; k < kUpThreads; ++k)
+            if (errs[k]) fail(DGKR_CUDA_ERROR, std::string("chunked download: ") + cudaGetErrorString(cudaGetLastError()));
+        prof.d2h_bytes += n;
     }
     void d2h(void* dst, const void* src, std::size_t n) {
         CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));

@@ -31,6 +31,7 @@ for e in range(e_min, e_max + 1):
     root = P.pcs_commit(ctx, f, [data])
     t_commit = time.perf_counter() - t0
     r = [int.from_bytes(W.random_inputs(f.p, 1, 1000 + k).tobytes(), "little") for k in range(e)]
+    P.pcs_open(ctx, f, [data], r, P.Transcript(f, "dgkr.pc.cluster", [0]), 32)  # warm-up (workspace, pages)
     tr = P.Transcript(f, "dgkr.pc.cluster", [0])
     t0 = time.perf_counter()
     op = P.pcs_open(ctx, f, [data], r, tr, 32)
