@@ -132,3 +132,21 @@ def test_fri_dist_two_process_shm(ctx, tmp_path):
         assert raw[-32:] == tr.state
     assert got == want
     assert FO.fri_verify_dist(fld, got, n, blowup, final, q, O.Transcript("fri.shm", fld, [world]))
+
+
+def test_ntt_large_roundtrip_through_chunked_transfers(ctx):
+    """2^21 elements (64 MiB each way, pageable host buffers): the upload and
+    the download take the chunked pinned-staging path (Lane::h2d_large /
+    d2h_large); iNTT(NTT(a)) = a byte for byte, and entry 0 of the forward
+    transform is the sum of the inputs"""
+    from paper_2404_10404_b200 import workloads as W
+
+    f = P.Field.bn254()
+    n_log = 21
+    a = W.random_inputs(f.p, 1 << n_log, 77).tobytes()
+    fwd = P.ntt(ctx, f, a)
+    back = P.ntt(ctx, f, f.encode(fwd), inverse=True)
+    assert f.encode(back) == a
+    # the forward transform's first entry is the sum of the inputs
+    fld = O.BN254
+    assert fwd[0] == sum(fld.elems_from_bytes(a)) % fld.p
