@@ -4,7 +4,9 @@ byte for byte, over three families (a GPU box with oracle/_ref built):
   * data-parallel layered circuits of 2^13..2^17 gates per layer, so the BN254
     constant-multiplier chi expansion (k_split_eq_expand_const, klo >= 8) and
     the lazy-difference round kernels run at size;
-  * general circuits over the runtime-modulus path (p = 97, Goldilocks).
+  * general circuits over the runtime-modulus path (p = 97, Goldilocks);
+  * the distributed prover (emulated ranks 2/4/8) against the single proof;
+  * pcs commit roots and openings (M rows, random sizes, BN254/Goldilocks).
 usage: python tools/fuzz_parity.py [general_cases] [layered_cases] [seconds]
 Prints one line per family and exits 1 on any mismatch."""
 import os
@@ -78,9 +80,63 @@ def layered(cases):
     print(f"layered BN254 (2^13..2^17 gates/layer): {done} circuits, mismatches so far {bad}", flush=True)
 
 
+def distributed(cases):
+    """emulated ranks (threads on lanes of this GPU) vs the single-GPU proof"""
+    global bad
+    f = P.Field.bn254()
+    rng = np.random.default_rng(11)
+    done = 0
+    for k in range(cases):
+        if time.time() > t_end:
+            break
+        world = int(1 << rng.integers(1, 4))
+        lw = int(rng.integers(4, 12))
+        copies = world * int(1 << rng.integers(0, 3))
+        depth = int(rng.integers(2, 6))
+        insz, flat = W.layered_circuit(3000 + k, lw, depth)
+        inputs = W.random_inputs(f.p, insz * copies, 60 + k)
+        tr1, tr2 = P.Transcript(f, "fd", [k]), P.Transcript(f, "fd", [k])
+        want = P.gkr_prove(ctx, P.Circuit(ctx, insz, *flat, n_copies=copies), inputs, tr1)
+        got = P.gkr_prove_dist_emulated(ctx, P.Circuit(ctx, insz, *flat, n_copies=copies // world), world, inputs,
+                                        tr2)
+        if got != want or tr1.state != tr2.state:
+            bad += 1
+            print(f"MISMATCH dist k={k} world={world} lw={lw} copies={copies} depth={depth}", flush=True)
+        done += 1
+    print(f"distributed (emulated ranks 2/4/8) vs single: {done} circuits, mismatches so far {bad}", flush=True)
+
+
+def pcs(cases):
+    """pcs::commit root and pcs::open bytes vs the compiled reference"""
+    global bad
+    done = 0
+    rng = np.random.default_rng(13)
+    for k in range(cases):
+        if time.time() > t_end:
+            break
+        fld = O.BN254 if k % 3 else O.Field(O.GOLDILOCKS_P)
+        f = P.Field(fld.p)
+        lm = int(rng.integers(0, 3))  # M = 1, 2, 4 rows
+        M = 1 << lm
+        lc = int(rng.integers(0, 13))
+        rows = [O.random_elements(fld, 1 << lc, rng) for _ in range(M)]
+        point = O.random_elements(fld, lc + lm, rng)
+        q = int(rng.integers(1, 40))
+        ok = P.pcs_commit(ctx, f, rows) == R.pcs_commit(fld, rows)
+        got = P.pcs_open(ctx, f, rows, point, P.Transcript(f, "fp", [k]), q)
+        want = R.pcs_open(fld, "fp", [k], rows, point, q)[0]
+        if not ok or got != want:
+            bad += 1
+            print(f"MISMATCH pcs k={k} p={fld.p} M={M} cols=2^{lc} q={q}", flush=True)
+        done += 1
+    print(f"pcs commit/open: {done} instances, mismatches so far {bad}", flush=True)
+
+
 general(O.BN254, n_general, "gen")
 layered(n_layered)
 general(O.Field(O.GOLDILOCKS_P), n_general // 3, "gen")
 general(O.Field(97), n_general // 3, "gen")
+distributed(max(8, n_layered))
+pcs(max(20, n_layered * 2))
 print("total mismatches", bad)
 sys.exit(1 if bad else 0)
