@@ -48,7 +48,7 @@ void coset_ntt(Lane* ctx, const dgkr_field* f, const Fe* coeff, std::uint64_t n_
     launch_bitrev_scale(kind, coeff, scale, a, static_cast<int>(log_n), n_in, ctx->st);
     launch_ntt(kind, a, static_cast<int>(log_n), tw.p, ctx->st);
     ctx->tend(ctx->prof.ntt_ms);
-    ctx->launched(2 + log_n);
+    ctx->launched(1 + ntt_launches(static_cast<int>(log_n)));  // bit-reverse/scale + the transform
 }
 
 /// FRI over the RS codeword of `coeffs` (protocol in include/dgkr_b200.h)

@@ -1053,6 +1053,33 @@ __global__ void __launch_bounds__(kThreads) k_ntt_stage(Fe* a, int log_n, int s,
     }
 }
 
+/// Stages s and s+1 in one pass (radix-4 grouping of two radix-2 stages):
+/// group (i0, i0+h, i0+2h, i0+3h), h = 2^(s-1), i0 = (t / h) * 4h + t mod h.
+/// Stage s pairs (i0, i1) and (i2, i3) with w_s(j); stage s+1 pairs (i0, i2)
+/// with w_{s+1}(j) and (i1, i3) with w_{s+1}(j + h). The same butterflies as
+/// two k_ntt_stage passes, with half the HBM traffic.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_ntt_stage2(Fe* a, int log_n, int s, const Fe* __restrict__ tw) {
+    const std::uint64_t h = std::uint64_t{1} << (s - 1);
+    const std::uint64_t ng = std::uint64_t{1} << (log_n - 2);
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < ng;
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t j = t & (h - 1);
+        const std::uint64_t i0 = ((t >> (s - 1)) << (s + 1)) + j;
+        const Fe w1 = fe_load_nc(tw + (j << (log_n - s)));
+        const Fe x0 = fe_load(a + i0), x1 = fe_mul<F>(w1, fe_load(a + i0 + h));
+        const Fe x2 = fe_load(a + i0 + 2 * h), x3 = fe_mul<F>(w1, fe_load(a + i0 + 3 * h));
+        const Fe y0 = fe_add<F>(x0, x1), y1 = fe_sub<F>(x0, x1);
+        const Fe y2 = fe_add<F>(x2, x3), y3 = fe_sub<F>(x2, x3);
+        const Fe z2 = fe_mul<F>(fe_load_nc(tw + (j << (log_n - s - 1))), y2);
+        const Fe z3 = fe_mul<F>(fe_load_nc(tw + ((j + h) << (log_n - s - 1))), y3);
+        fe_store(a + i0, fe_add<F>(y0, z2));
+        fe_store(a + i0 + 2 * h, fe_sub<F>(y0, z2));
+        fe_store(a + i0 + h, fe_add<F>(y1, z3));
+        fe_store(a + i0 + 3 * h, fe_sub<F>(y1, z3));
+    }
+}
+
 // (a + b) / 2 without a multiplication: halve a + b (or a + b + p if odd)
 template <class F>
 __device__ __forceinline__ Fe fe_half(const Fe& x) {
@@ -1467,6 +1494,12 @@ void launch_bitrev_scale(FieldKind k, const Fe* in, const Fe* scale, Fe* out, in
     check_launch("bitrev_scale");
 }
 
+int ntt_launches(int log_n) {
+    if (log_n == 0) return 0;
+    const int global = log_n - std::min(log_n, kNttLocalLog);
+    return 1 + (global + 1) / 2;
+}
+
 void launch_ntt(FieldKind k, Fe* a, int log_n, const Fe* tw, cudaStream_t st) {
     if (log_n == 0) return;
     const int b = std::min(log_n, kNttLocalLog);
@@ -1480,7 +1513,12 @@ void launch_ntt(FieldKind k, Fe* a, int log_n, const Fe* tw, cudaStream_t st) {
             attr = true;
         }
         k_ntt_local<F><<<static_cast<unsigned>(chunks), 512, smem, st>>>(a, log_n, b, tw);
-        for (int s = b + 1; s <= log_n; ++s) {
+        int s = b + 1;
+        for (; s + 1 <= log_n; s += 2) {  // two stages per pass
+            const int g = grid_for(std::uint64_t{1} << (log_n - 2), kThreads, 148 * 16);
+            k_ntt_stage2<F><<<g, kThreads, 0, st>>>(a, log_n, s, tw);
+        }
+        if (s == log_n) {
             const int g = grid_for(std::uint64_t{1} << (log_n - 1), kThreads, 148 * 16);
             k_ntt_stage<F><<<g, kThreads, 0, st>>>(a, log_n, s, tw);
         }

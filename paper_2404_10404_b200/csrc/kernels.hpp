@@ -182,6 +182,8 @@ void launch_bitrev_scale(FieldKind k, const Fe* in, const Fe* scale, Fe* out, in
                          cudaStream_t st);
 /// in-place radix-2 DIT NTT stages on bit-reversed input; tw[i] = w_N^i, i < N/2
 void launch_ntt(FieldKind k, Fe* a, int log_n, const Fe* tw, cudaStream_t st);
+/// kernels launch_ntt issues for a 2^log_n transform (shared-memory stages + two-stage passes)
+int ntt_launches(int log_n);
 /// one FRI fold: out[i] = (f[i] + f[i+h] + beta * xinv_i * (f[i] - f[i+h])) / 2, h = n/2,
 /// xinv_i = ginv * twinv[i * step]  (beta_const: host FoldConst of beta; ginv: host Fe
 /// (32 bytes) of the layer's inverse coset shift)
