@@ -27,7 +27,7 @@ proof (copy index = high variables, as the Sisu layout).
 """
 from __future__ import annotations
 
-from typing import Dict, List, Optional, Tuple
+from typing import Dict, List, NamedTuple, Optional, Tuple
 
 import numpy as np
 
@@ -405,3 +405,96 @@ def merkle_path_compressions(leaf_msg: bytes, siblings, index: int):
 
 def digest_words(data: bytes) -> np.ndarray:
     return np.frombuffer(data, dtype=">u4").astype(np.uint64)
+
+
+class RlcProof(NamedTuple):
+    root: bytes          # witness commitment (input layer, R_i slots zero)
+    proof: bytes         # GkrProof bytes on the continued transcript
+    digests: np.ndarray  # (m, 8) output chaining values
+    inputs: np.ndarray   # the input layer with the R_i filled in
+
+
+def _witness_root(ctx, field, inputs: np.ndarray) -> bytes:
+    """pcs_commit (pcs.hpp:105-113) of the input layer as one row, zero-padded
+    to a power-of-two column count (merkle.hpp:16-19 needs one)"""
+    from . import prover as P
+    w = field.width
+    cols = len(inputs) // w
+    padded = 1 << max(0, (cols - 1).bit_length())
+    row = inputs if padded == cols else np.concatenate([inputs, np.zeros((padded - cols) * w, np.uint8)])
+    return P.pcs_commit(ctx, field, [row])
+
+
+def _rlc_seed(tr, root: bytes) -> bytes:
+    tr.absorb_bytes(root)
+    return tr.field.encode([tr.challenge()])
+
+
+def prove_compressions_rlc(ctx, field, h_in: np.ndarray, blocks: np.ndarray, label: str = "sha.rlc",
+                           built=None):
+    """Committed-witness proof of a batch of compressions with the rlc=True
+    circuit (one claimed output per compression):
+
+      1. the input layer with every R_i slot zero is committed (pcs_commit);
+      2. the transcript absorbs the root and draws one challenge c;
+      3. R_i = rlc_coefficients(p, bytes(c), n) fill the R_i slots;
+      4. gkr_prove on the same transcript.
+
+    The R_i are fixed only after the witness is, so a wrong witness leaves
+    sum_i R_i c_i non-zero except with probability ~n/p. The number of
+    compressions is padded to a power of two with compress(IV, 0) copies.
+    built: an optional (input_size, flat, layout, Circuit) from a previous
+    call with the same copy count. Returns (RlcProof, built); RlcProof.inputs
+    is the witness the verifier below checks against."""
+    from . import prover as P
+    m = len(h_in)
+    copies = 1 << max(0, (m - 1).bit_length())
+    if copies != m:
+        h_in = np.concatenate([h_in, np.tile(IV, (copies - m, 1))])
+        blocks = np.concatenate([blocks, np.zeros((copies - m, 16), np.uint64)])
+    if built is None:
+        insz, flat, L = build_compression_circuit(rlc=True)
+        built = (insz, flat, L, P.Circuit(ctx, insz, *flat, n_copies=copies))
+    insz, flat, L, dc = built
+    p = field.p
+    inputs, hout = sha256_witness(p, L, insz, h_in, blocks, rlc=[0] * len(L.rlc))
+    root = _witness_root(ctx, field, inputs)
+    tr = P.Transcript(field, label, [copies])
+    coeffs = rlc_coefficients(p, _rlc_seed(tr, root), len(L.rlc))
+    _put_rlc(field, L, insz, copies, inputs, coeffs)
+    proof = P.gkr_prove(ctx, dc, inputs, tr)
+    return RlcProof(root, proof, hout[:m], inputs), built
+
+
+def _put_rlc(field, L, insz, copies, inputs, coeffs) -> None:
+    w = field.width
+    view = inputs.reshape(copies, insz, w)
+    enc = np.frombuffer(field.encode(coeffs), np.uint8).reshape(len(coeffs), w)
+    view[:, L.rlc, :] = enc[None, :, :]
+
+
+def verify_compressions_rlc(ctx, field, built, inputs: np.ndarray, root: bytes, proof: bytes,
+                            label: str = "sha.rlc") -> bool:
+    """Verifier of prove_compressions_rlc given the witness (the setting of
+    gkr_verify with inputs, gkr.hpp:314-325): the root matches the input layer
+    with the R_i slots zeroed, the R_i in the input layer are the ones the
+    transcript draws after absorbing the root, every claimed output is zero,
+    and the GKR proof verifies on the continued transcript."""
+    from . import prover as P
+    insz, _, L, dc = built
+    w = field.width
+    copies = len(inputs) // (insz * w)
+    zeroed = inputs.copy()
+    _put_rlc(field, L, insz, copies, zeroed, [0] * len(L.rlc))
+    if _witness_root(ctx, field, zeroed) != root:
+        return False
+    tr = P.Transcript(field, label, [copies])
+    coeffs = rlc_coefficients(field.p, _rlc_seed(tr, root), len(L.rlc))
+    want = zeroed.copy()
+    _put_rlc(field, L, insz, copies, want, coeffs)
+    if not np.array_equal(want, inputs):
+        return False
+    n = int.from_bytes(proof[:4], "little")
+    if any(proof[4:4 + n * w]):
+        return False
+    return P.gkr_verify(dc, proof, tr, inputs=inputs)
