@@ -558,11 +558,17 @@ def load_inputs_lane(ctx: Context, circuit: Circuit, field: Field, lane: int, in
 
 def pcs_commit(ctx: Context, field: Field, rows: Sequence[Elems]) -> bytes:
     """pcs::commit (pcs.hpp:105-113) -> 32-byte root"""
-    data = b"".join(field.encode(r) for r in rows)
-    cols = len(field.encode(rows[0])) // field.width
+    r0 = rows[0]
+    if all(isinstance(r, np.ndarray) and r.dtype == np.uint8 for r in rows):
+        # byte rows: one contiguous buffer without the bytes round trip
+        data = np.ascontiguousarray(r0 if len(rows) == 1 else np.concatenate([r.reshape(-1) for r in rows]))
+        cols = r0.size // field.width
+    else:
+        data = np.frombuffer(b"".join(field.encode(r) for r in rows), np.uint8)
+        cols = len(field.encode(r0)) // field.width
     root = C.create_string_buffer(32)
     check(lib().dgkr_pcs_commit(ctx.handle, field.handle, C.c_size_t(len(rows)), C.c_size_t(cols),
-                                C.c_char_p(data), root))
+                                _buf(data), root))
     return root.raw
 
 

@@ -79,3 +79,26 @@ def test_rlc_circuit_single_output():
     with pytest.raises(ValueError):
         S.sha256_witness(O.BN254_P, L, insz, rng.integers(0, 1 << 32, (1, 8), dtype=np.uint64),
                          rng.integers(0, 1 << 32, (1, 16), dtype=np.uint64))
+
+
+def test_rlc_slots_filled_after_commit():
+    """prove_compressions_rlc's host steps: a witness built with zero R_i and
+    then filled by _put_rlc equals the witness built with the R_i directly,
+    and the R_i depend on the seed (the challenge drawn from the root)"""
+    class _F:
+        width, p = 32, O.BN254_P
+
+        def encode(self, v):
+            return b"".join(int(x).to_bytes(32, "little") for x in v)
+
+    f = _F()
+    insz, _, L = S.build_compression_circuit(rlc=True)
+    rng = np.random.default_rng(4)
+    h_in = rng.integers(0, 1 << 32, (2, 8), dtype=np.uint64)
+    blocks = rng.integers(0, 1 << 32, (2, 16), dtype=np.uint64)
+    co = S.rlc_coefficients(f.p, b"seed-a", len(L.rlc))
+    assert co != S.rlc_coefficients(f.p, b"seed-b", len(L.rlc))
+    want, _ = S.sha256_witness(f.p, L, insz, h_in, blocks, rlc=co)
+    got, _ = S.sha256_witness(f.p, L, insz, h_in, blocks, rlc=[0] * len(L.rlc))
+    S._put_rlc(f, L, insz, 2, got, co)
+    assert np.array_equal(got, want)
