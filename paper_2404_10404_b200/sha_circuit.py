@@ -354,10 +354,12 @@ def sha256_witness(p: int, layout: _Layout, input_size: int, h_in: np.ndarray,
         for idx, v in zip(layout.rlc, rlc):
             put_const(idx, v)
     out = np.broadcast_to(base, (N, input_size, w)).copy()
+    cols: List[np.ndarray] = []   # bit wire indices
+    bits: List[np.ndarray] = []   # (N, nb) bit values, LSB first
 
     def put_bits(idx, val, nb):
-        for j in range(nb):
-            out[:, idx[j], 0] = ((val >> j) & 1).astype(np.uint8)
+        cols.append(np.asarray(idx[:nb], np.int64))
+        bits.append(((val[:, None] >> np.arange(nb, dtype=np.uint64)) & 1).astype(np.uint8))
 
     h = _u32(h_in)
     for i in range(8):
@@ -373,6 +375,8 @@ def sha256_witness(p: int, layout: _Layout, input_size: int, h_in: np.ndarray,
         put_bits(layout.words[("e", t)], tr["E"][t], 32)
         put_bits(layout.qbits[("a", t)], tr["qa"][t], 3)
         put_bits(layout.qbits[("e", t)], tr["qe"][t], 3)
+    # one scatter of every bit wire (low byte; the other bytes stay zero)
+    out[:, np.concatenate(cols), 0] = np.concatenate(bits, axis=1)
     return out.reshape(-1), tr["hout"]
 
 
