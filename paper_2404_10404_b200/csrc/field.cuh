@@ -378,6 +378,148 @@ __device__ __forceinline__ bool fe_lt_p(const Fe& a) {
     return borrow != 0;
 }
 
+// ---------------------------------------------------------------------------
+// Wide (unreduced) accumulation of Montgomery products for round sums:
+// the 512-bit products a_i b_i (< 4p^2 < 2^510 for lazy inputs < 2p) are
+// added into a 17-limb accumulator T and REDC(T) = T R^-1 mod p is taken once
+// per CTA (acc_reduce), saving the reduction half of CIOS and the modular add
+// on every product. A Montgomery value g (= gR) joins the sum as g * 2^256
+// (acc_add_hi). Capacity 2^544 / 2^510 = 2^34 products.
+// ---------------------------------------------------------------------------
+struct Acc {
+    uint32_t v[17];
+};
+
+__device__ __forceinline__ void acc_zero(Acc& a) {
+#pragma unroll
+    for (int i = 0; i < 17; ++i) a.v[i] = 0;
+}
+
+/// acc += t (16 limbs)
+__device__ __forceinline__ void acc_add16(Acc& a, const uint32_t (&t)[16]) {
+    asm("add.cc.u32  %0, %0, %17;\n\t"
+        "addc.cc.u32 %1, %1, %18;\n\t"
+        "addc.cc.u32 %2, %2, %19;\n\t"
+        "addc.cc.u32 %3, %3, %20;\n\t"
+        "addc.cc.u32 %4, %4, %21;\n\t"
+        "addc.cc.u32 %5, %5, %22;\n\t"
+        "addc.cc.u32 %6, %6, %23;\n\t"
+        "addc.cc.u32 %7, %7, %24;\n\t"
+        "addc.cc.u32 %8, %8, %25;\n\t"
+        "addc.cc.u32 %9, %9, %26;\n\t"
+        "addc.cc.u32 %10, %10, %27;\n\t"
+        "addc.cc.u32 %11, %11, %28;\n\t"
+        "addc.cc.u32 %12, %12, %29;\n\t"
+        "addc.cc.u32 %13, %13, %30;\n\t"
+        "addc.cc.u32 %14, %14, %31;\n\t"
+        "addc.cc.u32 %15, %15, %32;\n\t"
+        "addc.u32    %16, %16, 0;"
+        : "+r"(a.v[0]), "+r"(a.v[1]), "+r"(a.v[2]), "+r"(a.v[3]), "+r"(a.v[4]), "+r"(a.v[5]), "+r"(a.v[6]),
+          "+r"(a.v[7]), "+r"(a.v[8]), "+r"(a.v[9]), "+r"(a.v[10]), "+r"(a.v[11]), "+r"(a.v[12]), "+r"(a.v[13]),
+          "+r"(a.v[14]), "+r"(a.v[15]), "+r"(a.v[16])
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(t[8]),
+          "r"(t[9]), "r"(t[10]), "r"(t[11]), "r"(t[12]), "r"(t[13]), "r"(t[14]), "r"(t[15]));
+}
+
+/// acc += a * b (512-bit schoolbook product, no reduction)
+__device__ __forceinline__ void acc_mad(Acc& acc, const Fe& a, const Fe& b) {
+    uint32_t t[16];
+    {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[0] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        t[8] = static_cast<uint32_t>(c);
+    }
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[i + j] + c;
+            t[i + j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        t[i + 8] = static_cast<uint32_t>(c);
+    }
+    acc_add16(acc, t);
+}
+
+/// acc += g * 2^256
+__device__ __forceinline__ void acc_add_hi(Acc& a, const Fe& g) {
+    asm("add.cc.u32  %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.cc.u32 %2, %2, %11;\n\t"
+        "addc.cc.u32 %3, %3, %12;\n\t"
+        "addc.cc.u32 %4, %4, %13;\n\t"
+        "addc.cc.u32 %5, %5, %14;\n\t"
+        "addc.cc.u32 %6, %6, %15;\n\t"
+        "addc.cc.u32 %7, %7, %16;\n\t"
+        "addc.u32    %8, %8, 0;"
+        : "+r"(a.v[8]), "+r"(a.v[9]), "+r"(a.v[10]), "+r"(a.v[11]), "+r"(a.v[12]), "+r"(a.v[13]), "+r"(a.v[14]),
+          "+r"(a.v[15]), "+r"(a.v[16])
+        : "r"(g.v[0]), "r"(g.v[1]), "r"(g.v[2]), "r"(g.v[3]), "r"(g.v[4]), "r"(g.v[5]), "r"(g.v[6]), "r"(g.v[7]));
+}
+
+/// a += b
+__device__ __forceinline__ void acc_add(Acc& a, const Acc& b) {
+    uint32_t t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = b.v[i];
+    acc_add16(a, t);
+    a.v[16] += b.v[16];
+}
+
+__device__ __forceinline__ Acc acc_shfl_down(const Acc& a, int off) {
+    Acc r;
+#pragma unroll
+    for (int i = 0; i < 17; ++i) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], off);
+    return r;
+}
+
+/// T R^-1 mod p, fully reduced (T < 2^544): 8 REDC steps leave the 9-limb
+/// X = (T + m p) / 2^256 = T R^-1 (mod p); then
+/// X mod p = ((X_lo R^2) R^-1) R^-1 ... = X_lo mod p + x_8 R mod p.
+template <class F>
+__device__ Fe acc_reduce(const Acc& acc) {
+    uint32_t t[17];
+#pragma unroll
+    for (int i = 0; i < 17; ++i) t[i] = acc.v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t m = t[i] * F::np0();
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(m) * F::p(j) + t[i + j] + c;
+            t[i + j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+#pragma unroll
+        for (int k = i + 8; k < 17; ++k) {
+            const uint64_t s = static_cast<uint64_t>(t[k]) + c;
+            t[k] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+    }
+    Fe lo, hi, r2, one_raw;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        lo.v[i] = t[8 + i];
+        hi.v[i] = 0;
+        r2.v[i] = F::r2(i);
+        one_raw.v[i] = 0;
+    }
+    hi.v[0] = t[16];
+    one_raw.v[0] = 1;
+    const Fe lo_red = fe_mul<F>(fe_mul<F>(lo, r2), one_raw);  // X_lo mod p
+    const Fe hi_r = fe_mul<F>(hi, r2);                        // x_8 R mod p
+    return fe_add<F>(lo_red, hi_r);
+}
+
 __device__ __forceinline__ Fe fe_shfl_down(const Fe& a, int off) {
     Fe r;
 #pragma unroll

@@ -85,11 +85,44 @@ __device__ __forceinline__ Fe fe_ldcg(const Fe* p) {
     return r;
 }
 
+// CTA sum of K wide accumulators, reduced once; result in thread 0.
 template <class F, int K>
-__device__ __forceinline__ void grid_finish(Fe (&s)[K], Fe* partials, unsigned* counter, Fe* result) {
+__device__ __forceinline__ void block_sum_wide(Acc (&s)[K], Fe (&out)[K]) {
+    __shared__ Acc sh[32][K];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc_add(s[k], acc_shfl_down(s[k], off));
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[warp][k] = s[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (lane < nw) s[k] = sh[lane][k];
+            else acc_zero(s[k]);
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc_add(s[k], acc_shfl_down(s[k], off));
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) out[k] = acc_reduce<F>(s[k]);
+        }
+    }
+    __syncthreads();
+}
+
+template <class F, int K>
+__device__ __forceinline__ void grid_finish(Fe (&s)[K], Fe* partials, unsigned* counter, Fe* result,
+                                            bool summed = false) {
     __shared__ Fe sh[32][K];
     __shared__ bool last;
-    block_sum<F, K>(s, sh);
+    if (!summed) block_sum<F, K>(s, sh);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) fe_store(&partials[blockIdx.x * K + k], s[k]);
@@ -214,8 +247,17 @@ __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __rest
 // from the sum-check invariant p(0) + p(1) = claim (only where the claim is
 // the prover's own, i.e. inside gkr_prove), saving one Montgomery product and
 // one accumulator per index. Accumulators: s[0] = S0, s[NS-1] = S2, s[1] = S1.
-template <class F, int NP, bool HAS_G, int MODE, bool S1>
-__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, Fe (&s)[S1 ? 3 : 2]) {
+template <class F>
+__device__ __forceinline__ void sum_prod(Fe& s, const Fe& x, const Fe& y) { s = fe_add<F>(s, fe_mul<F>(x, y)); }
+template <class F>
+__device__ __forceinline__ void sum_prod(Acc& s, const Fe& x, const Fe& y) { acc_mad(s, x, y); }
+template <class F>
+__device__ __forceinline__ void sum_val(Fe& s, const Fe& g) { s = fe_add<F>(s, g); }
+template <class F>
+__device__ __forceinline__ void sum_val(Acc& s, const Fe& g) { acc_add_hi(s, g); }
+
+template <class F, int NP, bool HAS_G, int MODE, bool S1, class A>
+__device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, A (&s)[S1 ? 3 : 2]) {
     constexpr int NS = S1 ? 3 : 2;
     const int np = NP > 0 ? NP : a.np;
     const std::uint64_t P = a.n_out_pairs;
@@ -223,29 +265,46 @@ __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i
         Fe f0, f1, g0, g1;
         load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, a.k, f0, f1);
         load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
-        s[0] = fe_add<F>(s[0], fe_mul<F>(f0, g0));
-        if constexpr (S1) s[1] = fe_add<F>(s[1], fe_mul<F>(f1, g1));
-        s[NS - 1] = fe_add<F>(s[NS - 1], fe_mul<F>(fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0)));
+        sum_prod<F>(s[0], f0, g0);
+        if constexpr (S1) sum_prod<F>(s[1], f1, g1);
+        sum_prod<F>(s[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0));
     }
     if (HAS_G) {
         Fe g0, g1;
         load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, a.k, g0, g1);
-        s[0] = fe_add<F>(s[0], g0);
-        if constexpr (S1) s[1] = fe_add<F>(s[1], g1);
+        sum_val<F>(s[0], g0);
+        if constexpr (S1) sum_val<F>(s[1], g1);
     }
 }
 
 template <class F, int NP, bool HAS_G, int MODE, bool S1, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant__ RoundParams a) {
     constexpr int NS = S1 ? 3 : 2;
-    Fe s[NS];
+    if constexpr (MODE == kScan && !S1) {
+        // Round 1 (no fold): the two general products per index are the
+        // whole cost, so the sums are kept unreduced (Acc) and reduced once
+        // per CTA. Fold rounds keep CIOS sums (wide sums there
+        // cost registers and spills).
+        Acc w[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) s[k] = fe_zero();
-    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < a.n_out_pairs;
-         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        round_body<F, NP, HAS_G, MODE, S1>(a, i, s);
+        for (int k = 0; k < NS; ++k) acc_zero(w[k]);
+        for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+             i < a.n_out_pairs; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+            round_body<F, NP, HAS_G, MODE, S1>(a, i, w);
+        }
+        Fe s[NS];
+        block_sum_wide<F, NS>(w, s);
+        grid_finish<F, NS>(s, a.partials, a.counter, a.result, true);
+    } else {
+        Fe s[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s[k] = fe_zero();
+        for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+             i < a.n_out_pairs; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+            round_body<F, NP, HAS_G, MODE, S1>(a, i, s);
+        }
+        grid_finish<F, NS>(s, a.partials, a.counter, a.result);
     }
-    grid_finish<F, NS>(s, a.partials, a.counter, a.result);
 }
 
 // Small-table variant: one CTA covers all pairs; the CTA sum is the result.
