@@ -20,6 +20,7 @@ int dgkr_comm_create_nccl(dgkr_ctx* ctx, const std::uint8_t* uid128, int rank, i
     return guard([&] {
         if (!g_nccl.load()) fail(DGKR_COMM_ERROR, "libnccl.so.2 not found");
         if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
+        if (world > kMaxCommWorld) fail(DGKR_INVALID_ARGUMENT, "world larger than the round-sum gather buffer");
         CK(cudaSetDevice(ctx->device));
         auto c = std::make_unique<NcclComm>();
         c->rank = rank;
@@ -37,6 +38,7 @@ int dgkr_comm_create_shm(dgkr_ctx* ctx, const char* name, int rank, int world, s
                          dgkr_comm** out) {
     return guard([&] {
         if (world < 1 || rank < 0 || rank >= world) fail(DGKR_INVALID_ARGUMENT, "bad rank / world");
+        if (world > kMaxCommWorld) fail(DGKR_INVALID_ARGUMENT, "world larger than the round-sum gather buffer");
         if (!name || name[0] != '/') fail(DGKR_INVALID_ARGUMENT, "shm name must start with '/'");
         auto c = std::make_unique<ShmComm>();
         c->rank = rank;

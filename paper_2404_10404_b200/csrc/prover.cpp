@@ -1405,7 +1405,7 @@ int dgkr_ctx_create(int device, dgkr_ctx** out) {
         cudaDeviceProp prop{};
         CK(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) fail(DGKR_UNSUPPORTED, "this build targets sm_100a (B200)");
-        auto c = std::make_unique<dgkr_ctx>(device, prop.multiProcessorCount, std::make_unique<RtState>());
+        auto c = std::make_unique<dgkr_ctx>(device, prop.multiProcessorCount);
         *out = c.release();
     });
 }
@@ -2060,12 +2060,19 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
         // inputs: proof i belongs to lane i mod L, whose loaded inputs it proves
         std::atomic<std::size_t> next{0};
         auto work = [&](std::size_t li) {
-            CK(cudaSetDevice(ctx->device));
+            // no exception may leave a std::thread: a failed cudaSetDevice
+            // fails every proof this lane takes
+            const cudaError_t se = cudaSetDevice(ctx->device);
             Lane* Ln = lanes[li];
             dgkr_profile acc{};
             for (std::size_t k = 0;; ++k) {
                 const std::size_t i = inputs ? next.fetch_add(1) : li + k * L;
                 if (i >= n) break;
+                if (se != cudaSuccess) {
+                    codes[i] = DGKR_CUDA_ERROR;
+                    errs[i] = std::string("cudaSetDevice: ") + cudaGetErrorString(se);
+                    continue;
+                }
                 try {
                     Ln->begin_call();
                     Transcript tr(&f->f, ts[i].state, ts[i].draws);
@@ -2121,10 +2128,16 @@ int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size
         // static assignment: lane l proves l, l+L, l+2L, ... in order on every
         // rank, so lane l's exchanges pair up across ranks
         auto work = [&](std::size_t li) {
-            CK(cudaSetDevice(ctx->device));
+            const cudaError_t se = cudaSetDevice(ctx->device);  // checked per proof: nothing may throw out of a thread
             Lane* Ln = lanes[li];
             dgkr_profile acc{};
             for (std::size_t i = li; i < n; i += L) {
+                if (se != cudaSuccess) {
+                    codes[i] = DGKR_CUDA_ERROR;
+                    errs[i] = std::string("cudaSetDevice: ") + cudaGetErrorString(se);
+                    if (auto* s = dynamic_cast<ShmComm*>(comms[li])) s->hdr->aborted.store(1);
+                    break;
+                }
                 try {
                     Ln->begin_call();
                     Transcript tr(&f->f, ts[i].state, ts[i].draws);

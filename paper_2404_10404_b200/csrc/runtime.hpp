@@ -146,13 +146,23 @@ struct dgkr_field {
     }
 };
 
-/// Runtime-modulus constants live in one __constant__ block per device;
-/// lanes share it (concurrent lanes must use the same runtime field).
+/// Runtime-modulus constants live in one __constant__ block per device,
+/// shared by every context and lane of the process on that device, so the
+/// upload-skip cache is per device too (device_rt_state): a context that
+/// switches moduli re-uploads no matter which context loaded the block last.
+/// Concurrent proofs over DIFFERENT runtime moduli on one device are not
+/// supported (they would share the constant block); BN254 has immediates.
 struct RtState {
     std::mutex mu;
     bool valid = false;
     RtFieldHost cur{};
 };
+
+inline RtState* device_rt_state(int device) {
+    static RtState states[64];
+    if (device < 0 || device >= 64) fail(DGKR_UNSUPPORTED, "device index out of range");
+    return &states[device];
+}
 
 /// device buffers of one polynomial commitment (pcs.hpp), kept across calls
 struct PcsDevice {
@@ -447,19 +457,17 @@ struct Lane {
 /// The context is lane 0 itself; extra lanes (concurrent proofs) are
 /// created on demand and share the runtime-field state.
 struct dgkr_ctx : Lane {
-    std::unique_ptr<RtState> rt_owner;
     std::mutex lanes_mu;
     std::vector<std::unique_ptr<Lane>> extra;  // lanes 1..
     cudaEvent_t user_ev[8] = {};
 
-    dgkr_ctx(int dev, int sm_count, std::unique_ptr<RtState> rts)
-        : Lane(dev, sm_count, 0, rts.get()), rt_owner(std::move(rts)) {}
+    dgkr_ctx(int dev, int sm_count) : Lane(dev, sm_count, 0, device_rt_state(dev)) {}
 
     Lane* lane(int i) {
         if (i == 0) return this;
         std::lock_guard<std::mutex> lk(lanes_mu);
         while (static_cast<int>(extra.size()) < i)
-            extra.push_back(std::make_unique<Lane>(device, sms, static_cast<int>(extra.size()) + 1, rt_owner.get()));
+            extra.push_back(std::make_unique<Lane>(device, sms, static_cast<int>(extra.size()) + 1, rt));
         return extra[i - 1].get();
     }
 
@@ -468,6 +476,10 @@ struct dgkr_ctx : Lane {
             if (e) cudaEventDestroy(e);
     }
 };
+
+/// largest communicator: the per-round all-gather of up to 3 round sums per
+/// rank lands in h_small[kGatherOff, kSmall)
+constexpr int kMaxCommWorld = static_cast<int>((Lane::kSmall - Lane::kGatherOff) / 3);
 
 // ===========================================================================
 // Device communication for the data-parallel (multi-GPU) prover. The protocol

@@ -558,14 +558,22 @@ def load_inputs_lane(ctx: Context, circuit: Circuit, field: Field, lane: int, in
 
 def pcs_commit(ctx: Context, field: Field, rows: Sequence[Elems]) -> bytes:
     """pcs::commit (pcs.hpp:105-113) -> 32-byte root"""
+    if not rows:
+        raise InvalidArgument(1, "matrix needs at least one row")  # pcs.hpp:35-37
     r0 = rows[0]
     if all(isinstance(r, np.ndarray) and r.dtype == np.uint8 for r in rows):
         # byte rows: one contiguous buffer without the bytes round trip
+        sizes = {r.size for r in rows}
+        if len(sizes) != 1 or r0.size % field.width:
+            raise InvalidArgument(1, "ragged evaluation matrix")  # pcs.hpp:38-43
         data = np.ascontiguousarray(r0 if len(rows) == 1 else np.concatenate([r.reshape(-1) for r in rows]))
         cols = r0.size // field.width
     else:
-        data = np.frombuffer(b"".join(field.encode(r) for r in rows), np.uint8)
-        cols = len(field.encode(r0)) // field.width
+        enc = [field.encode(r) for r in rows]
+        if len({len(e) for e in enc}) != 1 or len(enc[0]) % field.width:
+            raise InvalidArgument(1, "ragged evaluation matrix")
+        data = np.frombuffer(b"".join(enc), np.uint8)
+        cols = len(enc[0]) // field.width
     root = C.create_string_buffer(32)
     check(lib().dgkr_pcs_commit(ctx.handle, field.handle, C.c_size_t(len(rows)), C.c_size_t(cols),
                                 _buf(data), root))
@@ -575,9 +583,12 @@ def pcs_commit(ctx: Context, field: Field, rows: Sequence[Elems]) -> bytes:
 def pcs_open(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], tr: Transcript,
              spot_checks: int = 32) -> bytes:
     """pcs::open (pcs.hpp:212-254) -> Opening::to_bytes"""
-    data = b"".join(field.encode(x) for x in rows)
+    enc = [field.encode(x) for x in rows]
+    if not enc or len({len(e) for e in enc}) != 1 or len(enc[0]) % field.width:
+        raise InvalidArgument(1, "ragged evaluation matrix")
+    data = b"".join(enc)
     M = len(rows)
-    cols = len(field.encode(rows[0])) // field.width
+    cols = len(enc[0]) // field.width
     depth = max(0, (cols - 1).bit_length())
     cap = 64 + (len(r) + 2 + M + cols) * field.width + min(spot_checks, cols) * (4 + M * field.width + 32 * depth) + 64
     out = np.empty(cap, dtype=np.uint8)  # not zero-filled: the opening overwrites what it returns

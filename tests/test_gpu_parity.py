@@ -321,3 +321,33 @@ def test_gkr_heavy_rows(ctx, n_copies, multi_slot):
     outs, lay = O.gkr_prove(circ, of.elems_from_bytes(inputs.tobytes()), otr)
     assert got == O.gkr_proof_bytes(of, outs, lay)
     assert tr.state == otr.state
+
+
+def test_runtime_moduli_alternate_across_contexts():
+    """Two contexts on one device, each proving over its own runtime modulus,
+    interleaved: the device's constant block is shared, so the upload cache
+    must be per device (a per-context cache proved p=97 with
+    Goldilocks constants after the other context had loaded them)."""
+    ctx_a, ctx_b = P.Context(0), P.Context(0)
+    fa, fb = P.Field(97), P.Field(O.GOLDILOCKS_P)
+    oa, ob = O.Field(97), O.Field(O.GOLDILOCKS_P)
+    rng = np.random.default_rng(77)
+    pa, pb = _pairs(oa, 2, 6, rng), _pairs(ob, 2, 6, rng)
+    for _ in range(3):
+        for ctx, f, of, pairs in ((ctx_a, fa, oa, pa), (ctx_b, fb, ob, pb)):
+            tr = P.Transcript(f, "alt", [1])
+            otr = O.Transcript("alt", of, [1])
+            assert P.prove_product_sum(ctx, pairs, tr) == O.prove_product_sum(pairs, otr).to_bytes(of)
+            assert tr.state == otr.state
+
+
+def test_pcs_rejects_ragged_rows(ctx):
+    f = P.Field.bn254()
+    a = W.random_inputs(f.p, 8, 1)
+    b = W.random_inputs(f.p, 4, 2)
+    with pytest.raises(InvalidArgument):
+        P.pcs_commit(ctx, f, [a, b])
+    with pytest.raises(InvalidArgument):
+        P.pcs_commit(ctx, f, [a[:-1]])
+    with pytest.raises(InvalidArgument):
+        P.pcs_open(ctx, f, [a, b], [1, 2], P.Transcript(f, "x"))
