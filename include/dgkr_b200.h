@@ -263,6 +263,12 @@ int dgkr_host_unregister(void* ptr);
 /* Montgomery-multiplication throughput of the device (BN254), as the
  * measured integer-pipe roofline denominator: field mults per second. */
 int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
+/* Process-wide launch tuning (no reference counterpart; proofs never depend
+ * on it): "small_round_pairs" = largest round run on a single CTA (default
+ * 256), "tma_min_pairs" = smallest round taking the TMA-staged round kernel
+ * (default 16384; 0 = off). Unknown names -> DGKR_INVALID_ARGUMENT. */
+int dgkr_set_tuning(const char* name, uint64_t value);
+int dgkr_get_tuning(const char* name, uint64_t* value);
 
 /* ---- polynomial commitment (pcs.hpp) ------------------------------------------ */
 /* pcs::commit (pcs.hpp:105-113): rows x cols row-major matrix -> Merkle root */

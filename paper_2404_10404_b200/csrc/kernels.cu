@@ -22,8 +22,10 @@
 //   k_merkle_*         merkle.hpp:16-28
 //   k_beta_combine     pcs.hpp:233-239
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -328,6 +330,8 @@ __global__ void __launch_bounds__(kThreads) k_round_small(const __grid_constant_
         for (int k = 0; k < NS; ++k) fe_store(&a.result[k], s[k]);
     }
 }
+
+#include "round_tma.cuh"
 
 template <class F>
 __global__ void k_fold_final(const Fe* const* in, Fe* const* out, int n_tabs, const Fe* rp) {
@@ -1371,12 +1375,101 @@ void launch_to_canonical(FieldKind k, const Fe* in, std::uint8_t* out, int width
     check_launch("to_canonical");
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged round (round_tma.cuh): tensor maps built on the host per launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+/// a table of `elems` field elements as rows of 128 B (4 elements), boxes of
+/// box_rows rows, 128-byte swizzle
+static bool encode_table_map(CUtensorMap* m, const Fe* base, std::uint64_t elems, int box_rows) {
+    auto fn = tensor_map_encoder();
+    if (!fn || (elems & 3) != 0 || (reinterpret_cast<std::uintptr_t>(base) & 127) != 0) return false;
+    const cuuint64_t dims[2] = {32, elems / 4};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<Fe*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+Tuning& tuning() {
+    static Tuning t = [] {
+        Tuning v{kSmallRoundPairs, std::uint64_t{1} << 14};
+        if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
+        return v;
+    }();
+    return t;
+}
+
+template <class F, int MODE, bool S1>
+static void launch_round_tma_t(const RoundTmaParams& p, int grid, cudaStream_t st) {
+    static bool attr = false;
+    const int smem = kTmaRingBytes + 1024;
+    if (!attr) {
+        cudaFuncSetAttribute(k_round_tma<F, MODE, S1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_round_tma<F, MODE, S1><<<grid, kTmaThreads, smem, st>>>(p);
+}
+
+static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, int lp, cudaStream_t st) {
+    const std::uint64_t P = a.n_out_pairs;
+    const std::uint64_t lim = tuning().tma_min_pairs;
+    if (lim == 0 || P < lim || P % kTmaConsumers != 0 || a.np != 1 || !a.has_g || !a.in_host ||
+        (a.mode != kScan && !a.out_host))
+        return false;
+    RoundTmaParams p{};
+    p.n_out_pairs = P;
+    p.log_p = lp;
+    p.ntab = 3;
+    p.partials = ws.partials;
+    p.counter = ws.counter;
+    p.result = ws.result;
+    if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
+    const std::uint64_t elems = a.mode == kScan ? 2 * P : 4 * P;
+    const int box = a.mode == kScan ? kTmaConsumers / 2 : (a.mode == kFoldNat ? kTmaConsumers : kTmaConsumers / 4);
+    for (int t = 0; t < 3; ++t) {
+        if (!encode_table_map(&p.map[t], a.in_host[t], elems, box)) return false;
+        p.out[t] = a.mode == kScan ? nullptr : a.out_host[t];
+    }
+    const std::uint64_t tiles = P / kTmaConsumers;
+    const int grid = static_cast<int>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(2 * ws.num_sms)));
+    DISPATCH_FIELD(k, F, {
+        if (a.mode == kScan) {
+            if (a.need_s1) launch_round_tma_t<F, kScan, true>(p, grid, st);
+            else launch_round_tma_t<F, kScan, false>(p, grid, st);
+        } else if (a.mode == kFoldNat) {
+            if (a.need_s1) launch_round_tma_t<F, kFoldNat, true>(p, grid, st);
+            else launch_round_tma_t<F, kFoldNat, false>(p, grid, st);
+        } else {
+            if (a.need_s1) launch_round_tma_t<F, kFoldRev, true>(p, grid, st);
+            else launch_round_tma_t<F, kFoldRev, false>(p, grid, st);
+        }
+    });
+    check_launch("round_tma");
+    return true;
+}
+
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
     RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}};
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
+    if (launch_round_tma(k, a, ws, lp, st)) return;
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
     // 2 CTAs/SM (<= 128 registers); forcing 3 (80 registers, small spill) measured no faster
 #define LAUNCH_ROUND(NP, HG, MD)                                                   \

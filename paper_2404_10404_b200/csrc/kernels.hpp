@@ -57,6 +57,11 @@ struct RoundLaunch {
     const void* fold_const = nullptr;
     // false: compute only (S0, S2) into result[0..2) (S1 = claim - S0 on the host)
     bool need_s1 = true;
+    // host copies of the in/out pointer arrays: enable the TMA-staged round
+    // kernel (round_tma.cuh) for the layer tables (np = 1 with G) on large
+    // rounds; null keeps the register-fed k_round
+    const Fe* const* in_host = nullptr;
+    Fe* const* out_host = nullptr;
 };
 constexpr std::size_t kFoldConstBytes = 9 * 32;
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
@@ -65,6 +70,16 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
 /// (the tail rounds of every sum-check phase are latency-bound).
 void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
 constexpr std::uint64_t kSmallRoundPairs = 256;
+
+/// Process-wide launch tuning (dgkr_set_tuning; env DGKR_SMALL_PAIRS /
+/// DGKR_TMA_MIN_PAIRS give the start values): rounds of <= small_round_pairs
+/// output pairs run on one CTA; rounds of >= tma_min_pairs take the
+/// TMA-staged kernel where it applies (0 disables it).
+struct Tuning {
+    std::uint64_t small_round_pairs;
+    std::uint64_t tma_min_pairs;
+};
+Tuning& tuning();
 
 /// out[t][0] = in[t][0] + r (in[t][1] - in[t][0]) for each table t.
 void launch_fold_final(FieldKind k, const Fe* const* in, Fe* const* out, int n_tabs, const Fe* r, cudaStream_t st);

@@ -36,6 +36,7 @@ struct RoundBuffers {
     std::uint64_t cap = 0;  // max table size handled
     DBuf<Fe> bufA, bufB, finals;
     DBuf<const Fe*> ptrs;   // [A ptrs | B ptrs | finals ptrs] each ntab
+    std::vector<const Fe*> hptrs;  // host copy of ptrs (tensor maps of the TMA round kernel)
     /// st: the stream that will use the buffers. The pointer table is
     /// uploaded on it: a synchronous cudaMemcpy from pageable memory may
     /// return before its NULL-stream DMA lands, and non-blocking lane streams
@@ -57,7 +58,10 @@ struct RoundBuffers {
         ptrs.ensure(3 * ntab);
         CK(cudaMemcpyAsync(ptrs.p, h.data(), h.size() * sizeof(const Fe*), cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));  // h is pageable and local
+        hptrs = std::move(h);
     }
+    const Fe* const* hA() const { return hptrs.data(); }
+    const Fe* const* hB() const { return hptrs.data() + ntab; }
     const Fe* const* A() const { return ptrs.p; }
     const Fe* const* B() const { return ptrs.p + ntab; }
     const Fe* const* F() const { return ptrs.p + 2 * ntab; }
@@ -89,7 +93,8 @@ struct SumcheckRun {
 /// (then p(0) + p(1) = claim holds exactly and S1 = claim - S0 is not
 /// computed on the device); nullptr = derive every round from the tables.
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr, const U256* claim = nullptr);
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr, const U256* claim = nullptr,
+                       const Fe* const* base_host = nullptr);
 
 /// Distributed form (cluster.hpp:228-320 generalised to the layer
 /// sum-check): `nv` local variables per rank, rank = high variables. Local
@@ -100,10 +105,10 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
 /// equals the single-GPU one byte for byte.
 SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                             RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, DistTail& dt,
-                            const U256* claim = nullptr) {
+                            const U256* claim = nullptr, const Fe* const* base_host = nullptr) {
     const int ntab = 2 * np + (has_g ? 1 : 0);
     const int world = comm->world;
-    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim);
+    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim, base_host);
     // boundary: gather every rank's final table values
     std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
     for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
@@ -132,7 +137,8 @@ SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, 
 }
 
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
-                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim) {
+                       RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim,
+                       const Fe* const* base_host) {
     const HostField& F = f->f;
     const bool skip_s1 = claim != nullptr;
     const int nres = skip_s1 ? 2 : 3;  // device sums per round: (S0, S2) or (S0, S1, S2)
@@ -144,6 +150,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     rb.ensure(ntab, size0, ctx->st);
     Fe* d_r = ctx->d_small.p;
     const Fe* const* cur = base;
+    const Fe* const* cur_h = base_host;  // host mirror of cur (null: no TMA round kernel)
     const U256 zero{};
     U256 fk[9] = {};
     for (int j = 1; j <= nv; ++j) {
@@ -157,19 +164,21 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             rl.mode = 0;  // scan the natural-order base tables
             rl.in = base;
             rl.out = nullptr;
+            rl.in_host = base_host;
         } else {
             rl.mode = (j == 2) ? 1 : 2;  // fold natural -> bit-reversed, then bit-reversed -> bit-reversed
             rl.in = cur;
+            rl.in_host = cur_h;
             const Fe* const* nxt = (j % 2 == 0) ? rb.A() : rb.B();
+            const Fe* const* nxt_h = (j % 2 == 0) ? rb.hA() : rb.hB();
             rl.out = const_cast<Fe* const*>(nxt);
+            rl.out_host = cur_h ? const_cast<Fe* const*>(nxt_h) : nullptr;
             cur = nxt;
+            if (cur_h) cur_h = nxt_h;
         }
         rl.n_out_pairs = size0 >> j;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        static const std::uint64_t small_pairs = [] {  // tuning override (DGKR_SMALL_PAIRS)
-            const char* e = std::getenv("DGKR_SMALL_PAIRS");
-            return e ? std::strtoull(e, nullptr, 10) : kSmallRoundPairs;
-        }();
+        const std::uint64_t small_pairs = tuning().small_round_pairs;
         if (rl.n_out_pairs <= small_pairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
         else launch_round(kind, rl, ctx->ws, ctx->st);
         ctx->launched();
@@ -317,6 +326,7 @@ struct CircuitWs {
     struct Cons {
         DBuf<SlotDesc> d_slots1, d_slots2;
         DBuf<const Fe*> base_ptrs;  // V0,H0,V1,H1,...,G
+        std::vector<const Fe*> base_host;  // host copy of base_ptrs
     };
     std::vector<std::unique_ptr<Cons>> cons;
     bool inputs_loaded = false;
@@ -655,6 +665,7 @@ CircuitWs& workspace(dgkr_circuit& c, int lane) {
         bp.push_back(W.G.p);
         wc->base_ptrs.ensure(bp.size());
         CK(cudaMemcpy(wc->base_ptrs.p, bp.data(), bp.size() * sizeof(const Fe*), cudaMemcpyHostToDevice));
+        wc->base_host = bp;
         W.cons[li] = std::move(wc);
     }
     // the setup copies above are synchronous cudaMemcpy from pageable memory:
@@ -983,9 +994,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         SumcheckRun p1 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
-                                   &combined.value)
+                                   &combined.value, WC.base_host.data())
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
-                              &combined.value);
+                              &combined.value, WC.base_host.data());
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
@@ -1024,9 +1035,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         SumcheckRun p2 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
-                                   &p1.claim_end)
+                                   &p1.claim_end, WC.base_host.data())
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
-                              &p1.claim_end);
+                              &p1.claim_end, WC.base_host.data());
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;
@@ -2295,6 +2306,24 @@ int dgkr_host_register(void* ptr, std::size_t bytes) {
 }
 int dgkr_host_unregister(void* ptr) {
     return guard([&] { CK(cudaHostUnregister(ptr)); });
+}
+
+int dgkr_set_tuning(const char* name, std::uint64_t value) {
+    return guard([&] {
+        const std::string n = name ? name : "";
+        if (n == "small_round_pairs") tuning().small_round_pairs = value;
+        else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
+        else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
+    });
+}
+
+int dgkr_get_tuning(const char* name, std::uint64_t* value) {
+    return guard([&] {
+        const std::string n = name ? name : "";
+        if (n == "small_round_pairs") *value = tuning().small_round_pairs;
+        else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
+        else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
+    });
 }
 
 int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s) {

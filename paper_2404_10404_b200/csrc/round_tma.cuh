@@ -1,0 +1,218 @@
+// TMA-staged sum-check round (sm_100a): the large-table form of k_round
+// (sumcheck.hpp:118-144 round_poly_over + fold_over, mle.hpp:75-85) for the
+// GKR layer sum-check's pair (V, H) plus the G table (sumcheck.hpp:368-440).
+//
+// Why: the register-fed k_round runs at 2 CTAs/SM (112 registers) with one
+// output pair in flight per thread, so HBM latency is exposed (ncu r1: 24%
+// warps active, 35-53% issue active, long-scoreboard the top stall on the
+// fold rounds). Here a producer warp streams each tile's tables into a
+// shared-memory ring with cp.async.bulk.tensor (TMA) while 8 consumer warps
+// fold and sum the previous tiles from shared memory, so the loads are in
+// flight during the field arithmetic without costing registers. The producer
+// is thread 0 of the CTA (not a dedicated warp): a 9th warp would cap the
+// registers at 96 (5 warps on some SM sub-partitions) and spill; with 8 warps
+// x 2 CTAs per SM every thread keeps 128.
+//
+// Layout: every table is viewed as a 2-D tensor of 128-byte rows (4 field
+// elements) with the 128-byte swizzle, so each consumer's 16-byte shared
+// loads are bank-conflict free in all three access patterns:
+//   kScan     (round 1)   index i = elements (2i, 2i+1): tile = 128 rows
+//   kFoldNat  (round 2)   index i = elements 4i..4i+3:   tile = 256 rows
+//   kFoldRev  (rounds>=3) index i = elements i, i+P, i+2P, i+3P of the
+//                         bit-reversed table: 4 boxes of 64 rows per tile
+// One ring stage holds one table's part of one tile; a tile is ntab stages.
+#pragma once
+
+#include <cuda.h>  // CUtensorMap (the map is built on the host by cuTensorMapEncodeTiled)
+
+constexpr int kTmaConsumers = 256;                 // one output pair per thread per tile
+constexpr int kTmaThreads = kTmaConsumers;
+constexpr int kTmaRingBytes = 96 * 1024;           // 3 stages of a fold tile (6 of a scan tile)
+constexpr int kTmaMaxTabs = 3;
+
+struct RoundTmaParams {
+    CUtensorMap map[kTmaMaxTabs];  // input tables, 2-D {32 x u32, rows}, SWIZZLE_128B
+    Fe* out[kTmaMaxTabs];          // fold outputs (unused by kScan)
+    std::uint64_t n_out_pairs;     // P (a multiple of kTmaConsumers)
+    int log_p;
+    int ntab;
+    Fe* partials;
+    unsigned* counter;
+    Fe* result;
+    FoldConst k;  // fold challenge (kernel-parameter space: IMAD constant operands)
+};
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+/// TMA: box at (c0, c1) of *map -> dst (shared), completion on bar (tx bytes)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+/// element at (row, first 16-byte chunk c0) of a SWIZZLE_128B tile (1024-aligned):
+/// chunk c of row r sits at chunk c ^ (r & 7)
+__device__ __forceinline__ Fe lds_fe_swz(const std::uint8_t* tile, std::uint32_t row, std::uint32_t c0) {
+    const std::uint32_t sw = row & 7;
+    const std::uint8_t* r = tile + row * 128;
+    const uint4 lo = *reinterpret_cast<const uint4*>(r + ((c0 ^ sw) << 4));
+    const uint4 hi = *reinterpret_cast<const uint4*>(r + (((c0 + 1) ^ sw) << 4));
+    Fe x;
+    x.v[0] = lo.x; x.v[1] = lo.y; x.v[2] = lo.z; x.v[3] = lo.w;
+    x.v[4] = hi.x; x.v[5] = hi.y; x.v[6] = hi.z; x.v[7] = hi.w;
+    return x;
+}
+
+template <int MODE>
+struct TmaShape {
+    static constexpr int kStageBytes = MODE == kScan ? kTmaConsumers * 64 : kTmaConsumers * 128;
+    static constexpr int kStages = kTmaRingBytes / kStageBytes;
+    static constexpr int kBoxRows = MODE == kScan ? kTmaConsumers / 2 : (MODE == kFoldNat ? kTmaConsumers : kTmaConsumers / 4);
+};
+
+/// Consumer view of one table of one tile: the pair (x0, x1) of index
+/// i = tile * 256 + tid, folded with the challenge unless kScan; fold outputs
+/// are stored as in load_pair (kFoldNat writes bit-reversed).
+template <class F, int MODE>
+__device__ __forceinline__ void tma_pair(const std::uint8_t* st, int tid, std::uint64_t i, const RoundTmaParams& a,
+                                         Fe* dst, Fe& x0, Fe& x1) {
+    if (MODE == kScan) {
+        const std::uint32_t row = tid >> 1, cb = (tid & 1) * 4;
+        x0 = lds_fe_swz(st, row, cb);
+        x1 = lds_fe_swz(st, row, cb + 2);
+    } else if (MODE == kFoldNat) {
+        const Fe a0 = lds_fe_swz(st, tid, 0), a1 = lds_fe_swz(st, tid, 2);
+        const Fe b0 = lds_fe_swz(st, tid, 4), b1 = lds_fe_swz(st, tid, 6);
+        x0 = foldk<F>(a0, a1, a.k);
+        x1 = foldk<F>(b0, b1, a.k);
+        const std::uint64_t P = a.n_out_pairs;
+        const std::uint64_t s = a.log_p ? (__brevll(i) >> (64 - a.log_p)) : 0;
+        fe_store(dst + s, x0);
+        fe_store(dst + s + P, x1);
+    } else {
+        const std::uint32_t row = tid >> 2, cb = (tid & 3) * 2;
+        constexpr int seg = kTmaConsumers * 32;  // one box: 256 elements
+        const Fe a0 = lds_fe_swz(st, row, cb), b0 = lds_fe_swz(st + seg, row, cb);
+        const Fe a1 = lds_fe_swz(st + 2 * seg, row, cb), b1 = lds_fe_swz(st + 3 * seg, row, cb);
+        x0 = foldk<F>(a0, a1, a.k);
+        x1 = foldk<F>(b0, b1, a.k);
+        const std::uint64_t P = a.n_out_pairs;
+        fe_store(dst + i, x0);
+        fe_store(dst + i + P, x1);
+    }
+}
+
+/// One round over the layer tables (V, H, G): S0 = sum V0 H0 + G0,
+/// S2 = sum dV dH (and S1 = sum V1 H1 + G1 when S1). Grid: persistent CTAs
+/// (<= 2 per SM), each striding over tiles of 256 output pairs; a CTA's
+/// units (tile, table) stream through a ring of kStages shared-memory stages.
+template <class F, int MODE, bool S1>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_constant__ RoundTmaParams a) {
+    using Shape = TmaShape<MODE>;
+    constexpr int NS = S1 ? 3 : 2;
+    constexpr int kStages = Shape::kStages;
+    constexpr bool kWide = MODE == kScan && !S1;  // round 1: unreduced products, one REDC per CTA
+    extern __shared__ std::uint8_t smem_raw[];
+    __shared__ std::uint64_t full[kStages], empty[kStages];
+    std::uint8_t* ring = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    const std::uint64_t P = a.n_out_pairs;
+    const std::uint64_t n_tiles = P / kTmaConsumers;
+    const std::uint64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const std::uint64_t n_units = my_tiles * a.ntab;
+    // unit u = (tile blockIdx.x + (u / ntab) * gridDim.x, table u % ntab) -> ring stage s
+    auto issue = [&](std::uint64_t u, int s) {
+        const std::uint64_t tile = blockIdx.x + (u / a.ntab) * gridDim.x;
+        const int t = static_cast<int>(u % a.ntab);
+        std::uint8_t* dst = ring + s * Shape::kStageBytes;
+        mbar_expect_tx(&full[s], Shape::kStageBytes);
+        if (MODE == kScan) {
+            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(tile * (kTmaConsumers / 2)));
+        } else if (MODE == kFoldNat) {
+            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(tile * kTmaConsumers));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                tma_load_2d(dst + q * (kTmaConsumers * 32), &a.map[t], &full[s], 0,
+                            static_cast<int>((tile * kTmaConsumers + q * P) >> 2));
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTmaConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kStages && static_cast<std::uint64_t>(s) < n_units; ++s) issue(s, s);
+    }
+    __syncthreads();
+    std::conditional_t<kWide, Acc, Fe> w[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        if constexpr (kWide) acc_zero(w[k]);
+        else w[k] = fe_zero();
+    }
+    int s = 0;
+    std::uint32_t ph = 0;
+    std::uint64_t u = 0;
+    // consume unit u from stage s; thread 0 refills the stage with unit
+    // u + kStages once all 8 warps have released it
+    auto next = [&](Fe* dst, std::uint64_t i, Fe& x0, Fe& x1) {
+        mbar_wait(&full[s], ph);
+        tma_pair<F, MODE>(ring + s * Shape::kStageBytes, tid, i, a, dst, x0, x1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && u + kStages < n_units) {
+            mbar_wait(&empty[s], ph);
+            issue(u + kStages, s);
+        }
+        ++u;
+        if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+        }
+    };
+    for (std::uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const std::uint64_t i = tile * kTmaConsumers + tid;
+        Fe f0, f1, g0, g1;
+        next(a.out[0], i, f0, f1);
+        next(a.out[1], i, g0, g1);
+        sum_prod<F>(w[0], f0, g0);
+        if constexpr (S1) sum_prod<F>(w[1], f1, g1);
+        sum_prod<F>(w[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0));
+        next(a.out[2], i, g0, g1);
+        sum_val<F>(w[0], g0);
+        if constexpr (S1) sum_val<F>(w[1], g1);
+    }
+    Fe sums[NS];
+    if constexpr (kWide) {
+        block_sum_wide<F, NS>(w, sums);
+        grid_finish<F, NS>(sums, a.partials, a.counter, a.result, true);
+    } else {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) sums[k] = w[k];
+        grid_finish<F, NS>(sums, a.partials, a.counter, a.result);
+    }
+}

@@ -75,6 +75,19 @@ class Field:
         return [int.from_bytes(b[i:i + w], "little") for i in range(0, len(b), w)]
 
 
+def set_tuning(name: str, value: int) -> None:
+    """Process-wide launch tuning (dgkr_set_tuning): "small_round_pairs",
+    "tma_min_pairs" (0 disables the TMA-staged round kernel). Proof bytes never
+    depend on it."""
+    check(lib().dgkr_set_tuning(name.encode(), C.c_uint64(value)))
+
+
+def get_tuning(name: str) -> int:
+    v = C.c_uint64()
+    check(lib().dgkr_get_tuning(name.encode(), C.byref(v)))
+    return v.value
+
+
 class Transcript:
     """dgkr::Transcript (transcript.hpp:17-130); host-side SHA-256 chain."""
 

@@ -144,7 +144,7 @@ def test_c5_pcs_commit_open_equals_reference(ctx, log_n, M):
     rows_b = [raw[i * cols * 32:(i + 1) * cols * 32] for i in range(M)]
     rows = [FLD.elems_from_bytes(r.tobytes()) for r in rows_b]
     rng = np.random.default_rng(log_n)
-    r = O.random_elements(FLD, cols.bit_length() - 1, rng)
+    r = O.random_elements(FLD, log_n, rng)  # row_vars + index_vars (pcs.hpp:215)
     root = P.pcs_commit(ctx, f, rows_b)
     assert root == R.pcs_commit(FLD, rows)
     tr = P.Transcript(f, PCS_LABEL)
