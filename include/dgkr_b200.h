@@ -92,6 +92,12 @@ int dgkr_transcript_init(const dgkr_field* f, const char* label, dgkr_transcript
 int dgkr_transcript_absorb_bytes(const dgkr_field* f, dgkr_transcript* t, const uint8_t* data, size_t n); /* :32-37 */
 int dgkr_transcript_absorb_u64(const dgkr_field* f, dgkr_transcript* t, uint64_t v);      /* :44-48 */
 int dgkr_transcript_absorb_elems(const dgkr_field* f, dgkr_transcript* t, const uint8_t* elems, size_t n); /* :39-42 */
+/* k independent transcripts, each absorbing its own n elements: the same
+ * bytes as k calls of dgkr_transcript_absorb_elems. 32-byte fields run the
+ * chains interleaved (multi-buffer SHA-NI); threads > 1 runs one host thread
+ * per transcript through the proof stream's combining absorb scheduler. */
+int dgkr_transcript_absorb_elems_multi(const dgkr_field* f, dgkr_transcript* const* ts, size_t k,
+                                       const uint8_t* const* elems, size_t n, int threads);
 int dgkr_transcript_challenge(const dgkr_field* f, dgkr_transcript* t, uint8_t* out);     /* :52-68 */
 int dgkr_transcript_challenge_index(const dgkr_field* f, dgkr_transcript* t, uint64_t bound, uint64_t* out); /* :71-83 */
 /* raw SHA-256 (sha256.hpp:138-151), exposed for tests */
@@ -266,7 +272,7 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
 /* Process-wide launch tuning (no reference counterpart; proofs never depend
  * on it): "small_round_pairs" = largest round run on a single CTA (default
  * 256), "tma_min_pairs" = smallest round taking the TMA-staged round kernel
- * (default 16384; 0 = off). Unknown names -> DGKR_INVALID_ARGUMENT. */
+ * (default 0 = off: measured slower than the register-fed kernel on C2). Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);
 

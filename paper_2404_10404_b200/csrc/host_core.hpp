@@ -301,6 +301,11 @@ inline Digest sha256(const std::uint8_t* d, std::size_t n) {
 Digest sha256_64(const std::uint8_t* a32, const std::uint8_t* b32);
 /// state <- SHA256(state || e_i) for n consecutive 32-byte elements
 void absorb_chain32(std::uint8_t* state, const std::uint8_t* elems, std::size_t n);
+/// k independent chains of n absorbs each, interleaved (multi-buffer SHA-NI):
+/// states[j] <- chain of elems[j][0..n) (32-byte elements), byte-identical to
+/// k calls of absorb_chain32
+void absorb_chain32_multi(std::uint8_t* const* states, const std::uint8_t* const* elems, std::size_t k,
+                          std::size_t n);
 
 // ---------------------------------------------------------------------------
 // Transcript (transcript.hpp:17-130)
@@ -321,6 +326,8 @@ public:
 
     const Digest& state() const { return state_; }
     std::uint64_t draws() const { return draws_; }
+    /// the 32-byte chaining state, for absorbs run elsewhere (AbsorbPool)
+    std::uint8_t* state_bytes() { return state_.data(); }
 
     /// absorb_bytes of n consecutive elements of `width` bytes (already canonical)
     void absorb_many(const std::uint8_t* d, std::size_t n, std::size_t width) {

@@ -168,6 +168,89 @@ __attribute__((target("sha,sse4.1,ssse3"))) void absorb_chain32_shani(std::uint8
     _mm_storeu_si128(reinterpret_cast<__m128i*>(state + 16), _mm_shuffle_epi8(wb, bswap));
 }
 
+/// K independent absorb chains interleaved in one thread (multi-buffer
+/// SHA-NI): chain k does state_k <- SHA256(state_k || e_k[i]) for i < n.
+/// One chain is bound by SHA256RNDS2 latency (64 dependent rounds-pairs per
+/// absorb); K chains fill its pipeline, so K proofs' output absorbs cost
+/// about as much wall time as one (gkr.hpp:189-190 per proof, unchanged).
+template <int K>
+__attribute__((target("sha,sse4.1,ssse3"))) void absorb_chain32_shani_x(std::uint8_t* const* state,
+                                                                         const std::uint8_t* const* e, std::size_t n) {
+    const __m128i bswap = _mm_set_epi64x(0x0c0d0e0f08090a0bULL, 0x0405060700010203ULL);
+    static const std::uint32_t iv[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                                        0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    __m128i tmp = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&iv[0]));
+    __m128i ivh = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&iv[4]));
+    tmp = _mm_shuffle_epi32(tmp, 0xB1);
+    ivh = _mm_shuffle_epi32(ivh, 0x1B);
+    const __m128i iv0 = _mm_alignr_epi8(tmp, ivh, 8);
+    const __m128i iv1 = _mm_blend_epi16(ivh, tmp, 0xF0);
+    __m128i wa[K], wb[K];
+    const std::uint8_t* p[K];
+    for (int k = 0; k < K; ++k) {
+        wa[k] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(state[k])), bswap);
+        wb[k] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(state[k] + 16)), bswap);
+        p[k] = e[k];
+    }
+    for (std::size_t i = 0; i < n; ++i) {
+        __m128i w[K][16], s0[K], s1[K], a0[K], a1[K];
+#pragma GCC unroll 4
+        for (int k = 0; k < K; ++k) {
+            w[k][0] = wa[k];
+            w[k][1] = wb[k];
+            w[k][2] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(p[k])), bswap);
+            w[k][3] = _mm_shuffle_epi8(_mm_loadu_si128(reinterpret_cast<const __m128i*>(p[k] + 16)), bswap);
+            p[k] += 32;
+            s0[k] = iv0;
+            s1[k] = iv1;
+        }
+#pragma GCC unroll 16
+        for (int g = 0; g < 16; ++g) {
+            const __m128i kk = _mm_loadu_si128(reinterpret_cast<const __m128i*>(&kK[4 * g]));
+#pragma GCC unroll 4
+            for (int k = 0; k < K; ++k) {
+                if (g >= 4) {
+                    __m128i x = _mm_sha256msg1_epu32(w[k][g - 4], w[k][g - 3]);
+                    x = _mm_add_epi32(x, _mm_alignr_epi8(w[k][g - 1], w[k][g - 2], 4));
+                    w[k][g] = _mm_sha256msg2_epu32(x, w[k][g - 1]);
+                }
+                __m128i m = _mm_add_epi32(w[k][g], kk);
+                s1[k] = _mm_sha256rnds2_epu32(s1[k], s0[k], m);
+                m = _mm_shuffle_epi32(m, 0x0E);
+                s0[k] = _mm_sha256rnds2_epu32(s0[k], s1[k], m);
+            }
+        }
+#pragma GCC unroll 4
+        for (int k = 0; k < K; ++k) {
+            s0[k] = _mm_add_epi32(s0[k], iv0);
+            s1[k] = _mm_add_epi32(s1[k], iv1);
+            a0[k] = s0[k];
+            a1[k] = s1[k];
+        }
+#pragma GCC unroll 16
+        for (int g = 0; g < 16; ++g) {
+            const __m128i mm = _mm_load_si128(reinterpret_cast<const __m128i*>(&kPadWK.wk[4 * g]));
+            const __m128i mh = _mm_shuffle_epi32(mm, 0x0E);
+#pragma GCC unroll 4
+            for (int k = 0; k < K; ++k) {
+                s1[k] = _mm_sha256rnds2_epu32(s1[k], s0[k], mm);
+                s0[k] = _mm_sha256rnds2_epu32(s0[k], s1[k], mh);
+            }
+        }
+#pragma GCC unroll 4
+        for (int k = 0; k < K; ++k) {
+            s0[k] = _mm_add_epi32(s0[k], a0[k]);
+            s1[k] = _mm_add_epi32(s1[k], a1[k]);
+            wa[k] = _mm_shuffle_epi32(_mm_unpackhi_epi64(s1[k], s0[k]), 0x1B);
+            wb[k] = _mm_shuffle_epi32(_mm_unpacklo_epi64(s1[k], s0[k]), 0x1B);
+        }
+    }
+    for (int k = 0; k < K; ++k) {
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(state[k]), _mm_shuffle_epi8(wa[k], bswap));
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(state[k] + 16), _mm_shuffle_epi8(wb[k], bswap));
+    }
+}
+
 bool detect_shani() {
     unsigned a, b, c, d;
     if (!__get_cpuid_count(7, 0, &a, &b, &c, &d)) return false;
@@ -202,6 +285,19 @@ void absorb_chain32(std::uint8_t* state, const std::uint8_t* elems, std::size_t 
         const Digest d = sha256_64(state, elems + 32 * i);
         std::memcpy(state, d.data(), 32);
     }
+}
+
+void absorb_chain32_multi(std::uint8_t* const* states, const std::uint8_t* const* elems, std::size_t k,
+                          std::size_t n) {
+    if (!g_shani) {
+        for (std::size_t j = 0; j < k; ++j) absorb_chain32(states[j], elems[j], n);
+        return;
+    }
+    std::size_t j = 0;
+    for (; j + 4 <= k; j += 4) absorb_chain32_shani_x<4>(states + j, elems + j, n);
+    if (k - j == 3) absorb_chain32_shani_x<3>(states + j, elems + j, n);
+    else if (k - j == 2) absorb_chain32_shani_x<2>(states + j, elems + j, n);
+    else if (k - j == 1) absorb_chain32_shani(states[j], elems[j], n);
 }
 
 Digest sha256_64(const std::uint8_t* a32, const std::uint8_t* b32) {

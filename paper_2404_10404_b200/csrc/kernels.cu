@@ -1406,7 +1406,9 @@ static bool encode_table_map(CUtensorMap* m, const Fe* base, std::uint64_t elems
 
 Tuning& tuning() {
     static Tuning t = [] {
-        Tuning v{kSmallRoundPairs, std::uint64_t{1} << 14};
+        // the TMA-staged round kernel measured slower than k_round on C2
+        // (DESIGN.md §11), so it is off unless asked for
+        Tuning v{kSmallRoundPairs, 0};
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
         return v;
@@ -1444,7 +1446,26 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
     for (int t = 0; t < 3; ++t) {
         if (!encode_table_map(&p.map[t], a.in_host[t], elems, box)) return false;
         p.out[t] = a.mode == kScan ? nullptr : a.out_host[t];
+        p.in[t] = a.in_host[t];
     }
+    // DGKR_TMA_VERIFY=1: check after every launch (synchronous); =2: count
+    // asynchronously, report at exit (keeps the launch concurrency)
+    static const int verify = std::getenv("DGKR_TMA_VERIFY") ? std::atoi(std::getenv("DGKR_TMA_VERIFY")) : 0;
+    static unsigned* dbg = [] {
+        unsigned* d = nullptr;
+        if (verify) {
+            cudaMallocManaged(&d, 8 * sizeof(unsigned));
+            std::memset(d, 0, 8 * sizeof(unsigned));
+            static unsigned* keep = d;
+            std::atexit([] {
+                cudaDeviceSynchronize();
+                std::fprintf(stderr, "dgkr_b200: TMA verify at exit: %u mismatches; first table %u index %u mode %u block %u\n",
+                             keep[0], keep[1], keep[2], keep[3], keep[4]);
+            });
+        }
+        return d;
+    }();
+    p.dbg = dbg;
     const std::uint64_t tiles = P / kTmaConsumers;
     const int grid = static_cast<int>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(2 * ws.num_sms)));
     DISPATCH_FIELD(k, F, {
@@ -1460,6 +1481,14 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
         }
     });
     check_launch("round_tma");
+    if (dbg && verify == 1) {
+        cudaStreamSynchronize(st);
+        if (dbg[0]) {
+            std::fprintf(stderr, "dgkr_b200: TMA verify: %u mismatches (mode %d, P %llu): first table %u index %u block %u\n",
+                         dbg[0], a.mode, static_cast<unsigned long long>(P), dbg[1], dbg[2], dbg[4]);
+            dbg[0] = 0;
+        }
+    }
     return true;
 }
 

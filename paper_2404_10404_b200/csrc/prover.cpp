@@ -826,7 +826,8 @@ void evaluate_circuit(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
 /// rank that gathers the claimed outputs and runs their serial absorb (the
 /// other ranks' proof bytes carry zeros in the output section).
 std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field* f, const std::uint8_t* inputs,
-                      Transcript& tr, std::uint8_t* out, std::size_t cap, dgkr_comm* comm = nullptr, int root = 0) {
+                      Transcript& tr, std::uint8_t* out, std::size_t cap, dgkr_comm* comm = nullptr, int root = 0,
+                      AbsorbPool* pool = nullptr) {
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
     const std::size_t w = F.width();
@@ -866,7 +867,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         if (!comm || comm->rank == root) {
             const double t0 = now_ms();
-            tr.absorb_many(out + 4, n_out, w);
+            if (pool && w == 32) pool->run(tr.state_bytes(), out + 4, n_out);  // interleaved with other proofs' chains
+            else tr.absorb_many(out + 4, n_out, w);
             const double dt = now_ms() - t0;
             ctx->prof.output_absorb_ms += dt;
             ctx->prof.host_transcript_ms += dt;
@@ -1385,6 +1387,35 @@ int dgkr_transcript_absorb_elems(const dgkr_field* f, dgkr_transcript* t, const 
         std::memcpy(t->state, tr.state().data(), 32);
     });
 }
+int dgkr_transcript_absorb_elems_multi(const dgkr_field* f, dgkr_transcript* const* ts, std::size_t k,
+                                       const std::uint8_t* const* elems, std::size_t n, int threads) {
+    return guard([&] {
+        const std::size_t w = f->f.width();
+        for (std::size_t j = 0; j < k; ++j)
+            for (std::size_t i = 0; i < n; ++i) f->f.from_bytes(elems[j] + i * w);  // canonical check
+        if (w != 32 || threads <= 1) {  // one thread: the interleaved chains directly
+            std::vector<std::uint8_t*> st(k);
+            for (std::size_t j = 0; j < k; ++j) st[j] = ts[j]->state;
+            if (w == 32) {
+                absorb_chain32_multi(st.data(), elems, k, n);
+            } else {
+                for (std::size_t j = 0; j < k; ++j) {
+                    Transcript tr(&f->f, ts[j]->state, ts[j]->draws);
+                    tr.absorb_many(elems[j], n, w);
+                    std::memcpy(ts[j]->state, tr.state().data(), 32);
+                }
+            }
+            return;
+        }
+        // one host thread per transcript through the combining scheduler of
+        // the proof stream (AbsorbPool): the same bytes, whatever the grouping
+        AbsorbPool pool;
+        std::vector<std::thread> th;
+        for (std::size_t j = 0; j < k; ++j) th.emplace_back([&, j] { pool.run(ts[j]->state, elems[j], n); });
+        for (auto& x : th) x.join();
+    });
+}
+
 int dgkr_transcript_challenge(const dgkr_field* f, dgkr_transcript* t, std::uint8_t* out) {
     return guard([&] {
         Transcript tr(&f->f, t->state, t->draws);
@@ -2088,7 +2119,7 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
                     Ln->begin_call();
                     Transcript tr(&f->f, ts[i].state, ts[i].draws);
                     lens[i] = gkr_prove(Ln, *c, workspace(*c, static_cast<int>(li)), f, inputs ? inputs[i] : nullptr,
-                                        tr, proofs[i], caps[i]);
+                                        tr, proofs[i], caps[i], nullptr, 0, L > 1 ? &ctx->absorb_pool : nullptr);
                     std::memcpy(ts[i].state, tr.state().data(), 32);
                     ts[i].draws = tr.draws();
                     Ln->end_call();
@@ -2154,7 +2185,7 @@ int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size
                     Transcript tr(&f->f, ts[i].state, ts[i].draws);
                     const int root = absorb_policy == 1 ? static_cast<int>(i % static_cast<std::size_t>(comms[li]->world)) : 0;
                     lens[i] = gkr_prove(Ln, *c, workspace(*c, static_cast<int>(li)), f, inputs ? inputs[i] : nullptr,
-                                        tr, proofs[i], caps[i], comms[li], root);
+                                        tr, proofs[i], caps[i], comms[li], root, L > 1 ? &ctx->absorb_pool : nullptr);
                     std::memcpy(ts[i].state, tr.state().data(), 32);
                     ts[i].draws = tr.draws();
                     Ln->end_call();

@@ -40,6 +40,10 @@ struct RoundTmaParams {
     unsigned* counter;
     Fe* result;
     FoldConst k;  // fold challenge (kernel-parameter space: IMAD constant operands)
+    // debug (DGKR_TMA_VERIFY=1): every staged element is compared with a
+    // direct global load of in[t]; mismatches counted in dbg[0], first one in dbg[1..4]
+    const Fe* in[kTmaMaxTabs];
+    unsigned* dbg;
 };
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -63,22 +67,30 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
         "r"(parity)
         : "memory");
 }
-/// TMA: box at (c0, c1) of *map -> dst (shared), completion on bar (tx bytes)
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
+/// TMA: box at (c0, c1) of *map -> dst (shared-window address), completion on bar (tx bytes)
+__device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
+            dst),
         "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
 
-/// element at (row, first 16-byte chunk c0) of a SWIZZLE_128B tile (1024-aligned):
-/// chunk c of row r sits at chunk c ^ (r & 7)
-__device__ __forceinline__ Fe lds_fe_swz(const std::uint8_t* tile, std::uint32_t row, std::uint32_t c0) {
+/// 16 bytes from shared memory at a 32-bit shared-window address (LDS.128;
+/// a generic pointer here compiles to LD.E through the generic path)
+__device__ __forceinline__ uint4 lds128(std::uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
+
+/// element at (row, first 16-byte chunk c0) of a SWIZZLE_128B tile at shared
+/// address `tile` (1024-aligned): chunk c of row r sits at chunk c ^ (r & 7)
+__device__ __forceinline__ Fe lds_fe_swz(std::uint32_t tile, std::uint32_t row, std::uint32_t c0) {
     const std::uint32_t sw = row & 7;
-    const std::uint8_t* r = tile + row * 128;
-    const uint4 lo = *reinterpret_cast<const uint4*>(r + ((c0 ^ sw) << 4));
-    const uint4 hi = *reinterpret_cast<const uint4*>(r + (((c0 + 1) ^ sw) << 4));
+    const std::uint32_t r = tile + row * 128;
+    const uint4 lo = lds128(r + ((c0 ^ sw) << 4));
+    const uint4 hi = lds128(r + (((c0 + 1) ^ sw) << 4));
     Fe x;
     x.v[0] = lo.x; x.v[1] = lo.y; x.v[2] = lo.z; x.v[3] = lo.w;
     x.v[4] = hi.x; x.v[5] = hi.y; x.v[6] = hi.z; x.v[7] = hi.w;
@@ -95,19 +107,42 @@ struct TmaShape {
 /// Consumer view of one table of one tile: the pair (x0, x1) of index
 /// i = tile * 256 + tid, folded with the challenge unless kScan; fold outputs
 /// are stored as in load_pair (kFoldNat writes bit-reversed).
+__device__ __noinline__ void tma_verify(const RoundTmaParams& a, int t, std::uint64_t gi, const Fe& x, int mode) {
+    const Fe y = fe_load(a.in[t] + gi);
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ok &= x.v[k] == y.v[k];
+    if (!ok && atomicAdd(a.dbg, 1u) == 0) {
+        a.dbg[1] = static_cast<unsigned>(t);
+        a.dbg[2] = static_cast<unsigned>(gi);
+        a.dbg[3] = static_cast<unsigned>(mode);
+        a.dbg[4] = blockIdx.x;
+    }
+}
+
 template <class F, int MODE>
-__device__ __forceinline__ void tma_pair(const std::uint8_t* st, int tid, std::uint64_t i, const RoundTmaParams& a,
-                                         Fe* dst, Fe& x0, Fe& x1) {
+__device__ __forceinline__ void tma_pair(std::uint32_t st, int tid, std::uint64_t i, const RoundTmaParams& a,
+                                         Fe* dst, Fe& x0, Fe& x1, int t) {
+    const std::uint64_t P = a.n_out_pairs;
     if (MODE == kScan) {
         const std::uint32_t row = tid >> 1, cb = (tid & 1) * 4;
         x0 = lds_fe_swz(st, row, cb);
         x1 = lds_fe_swz(st, row, cb + 2);
+        if (a.dbg) {
+            tma_verify(a, t, 2 * i, x0, MODE);
+            tma_verify(a, t, 2 * i + 1, x1, MODE);
+        }
     } else if (MODE == kFoldNat) {
         const Fe a0 = lds_fe_swz(st, tid, 0), a1 = lds_fe_swz(st, tid, 2);
         const Fe b0 = lds_fe_swz(st, tid, 4), b1 = lds_fe_swz(st, tid, 6);
+        if (a.dbg) {
+            tma_verify(a, t, 4 * i, a0, MODE);
+            tma_verify(a, t, 4 * i + 1, a1, MODE);
+            tma_verify(a, t, 4 * i + 2, b0, MODE);
+            tma_verify(a, t, 4 * i + 3, b1, MODE);
+        }
         x0 = foldk<F>(a0, a1, a.k);
         x1 = foldk<F>(b0, b1, a.k);
-        const std::uint64_t P = a.n_out_pairs;
         const std::uint64_t s = a.log_p ? (__brevll(i) >> (64 - a.log_p)) : 0;
         fe_store(dst + s, x0);
         fe_store(dst + s + P, x1);
@@ -116,9 +151,14 @@ __device__ __forceinline__ void tma_pair(const std::uint8_t* st, int tid, std::u
         constexpr int seg = kTmaConsumers * 32;  // one box: 256 elements
         const Fe a0 = lds_fe_swz(st, row, cb), b0 = lds_fe_swz(st + seg, row, cb);
         const Fe a1 = lds_fe_swz(st + 2 * seg, row, cb), b1 = lds_fe_swz(st + 3 * seg, row, cb);
+        if (a.dbg) {
+            tma_verify(a, t, i, a0, MODE);
+            tma_verify(a, t, i + P, b0, MODE);
+            tma_verify(a, t, i + 2 * P, a1, MODE);
+            tma_verify(a, t, i + 3 * P, b1, MODE);
+        }
         x0 = foldk<F>(a0, a1, a.k);
         x1 = foldk<F>(b0, b1, a.k);
-        const std::uint64_t P = a.n_out_pairs;
         fe_store(dst + i, x0);
         fe_store(dst + i + P, x1);
     }
@@ -136,7 +176,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     constexpr bool kWide = MODE == kScan && !S1;  // round 1: unreduced products, one REDC per CTA
     extern __shared__ std::uint8_t smem_raw[];
     __shared__ std::uint64_t full[kStages], empty[kStages];
-    std::uint8_t* ring = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    // the ring as a 32-bit shared-window address, 1024-aligned for the swizzle
+    const std::uint32_t ring = (smem_u32(smem_raw) + 1023u) & ~1023u;
     const int lane = threadIdx.x & 31, tid = threadIdx.x;
     const std::uint64_t P = a.n_out_pairs;
     const std::uint64_t n_tiles = P / kTmaConsumers;
@@ -146,7 +187,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     auto issue = [&](std::uint64_t u, int s) {
         const std::uint64_t tile = blockIdx.x + (u / a.ntab) * gridDim.x;
         const int t = static_cast<int>(u % a.ntab);
-        std::uint8_t* dst = ring + s * Shape::kStageBytes;
+        const std::uint32_t dst = ring + s * Shape::kStageBytes;
         mbar_expect_tx(&full[s], Shape::kStageBytes);
         if (MODE == kScan) {
             tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(tile * (kTmaConsumers / 2)));
@@ -179,13 +220,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     std::uint64_t u = 0;
     // consume unit u from stage s; thread 0 refills the stage with unit
     // u + kStages once all 8 warps have released it
-    auto next = [&](Fe* dst, std::uint64_t i, Fe& x0, Fe& x1) {
+    auto next = [&](Fe* dst, std::uint64_t i, Fe& x0, Fe& x1, int t) {
         mbar_wait(&full[s], ph);
-        tma_pair<F, MODE>(ring + s * Shape::kStageBytes, tid, i, a, dst, x0, x1);
+        tma_pair<F, MODE>(ring + s * Shape::kStageBytes, tid, i, a, dst, x0, x1, t);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (tid == 0 && u + kStages < n_units) {
             mbar_wait(&empty[s], ph);
+            // the generic-proxy reads of this stage are ordered before the
+            // async-proxy (TMA) writes that refill it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(u + kStages, s);
         }
         ++u;
@@ -197,12 +241,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     for (std::uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const std::uint64_t i = tile * kTmaConsumers + tid;
         Fe f0, f1, g0, g1;
-        next(a.out[0], i, f0, f1);
-        next(a.out[1], i, g0, g1);
+        next(a.out[0], i, f0, f1, 0);
+        next(a.out[1], i, g0, g1, 1);
         sum_prod<F>(w[0], f0, g0);
         if constexpr (S1) sum_prod<F>(w[1], f1, g1);
         sum_prod<F>(w[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0));
-        next(a.out[2], i, g0, g1);
+        next(a.out[2], i, g0, g1, 2);
         sum_val<F>(w[0], g0);
         if constexpr (S1) sum_val<F>(w[1], g1);
     }

@@ -186,6 +186,94 @@ struct NttWs {
     std::vector<std::unique_ptr<PcsDevice>> pcs_clusters;
 };
 
+/// Combining scheduler for the serial output absorbs of concurrent proofs
+/// (gkr.hpp:189-190: state <- SHA256(state || out_i) for every padded
+/// output). One chain is bound by SHA-NI round latency; K chains interleaved
+/// in one thread (absorb_chain32_multi) run ~1.5x (one core) to ~2.3x (all
+/// cores busy) the absorbs per core (tools/absorb, profiles/absorb_r2.txt).
+/// A lane that reaches its absorb queues its job; if its job is not being
+/// processed it becomes a processor: it owns its job plus up to kMaxK - 1
+/// queued ones and advances them together chunk by chunk, topping up free
+/// slots at chunk boundaries. When its own job is done it hands the others
+/// back (their state and position travel with the job) and returns; a lane
+/// whose job is owned elsewhere sleeps until it is done or handed back. Every
+/// chain's bytes are exactly absorb_chain32's.
+struct AbsorbPool {
+    struct Job {
+        std::uint8_t* state;
+        const std::uint8_t* data;
+        std::size_t n;
+        std::size_t pos = 0;
+        bool owned = false;
+        bool done = false;
+    };
+    static constexpr std::size_t kChunk = std::size_t{1} << 15;
+    static constexpr int kMaxK = 4;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<Job*> pending;  // unowned and unfinished, FIFO
+
+    void run(std::uint8_t* state, const std::uint8_t* data, std::size_t n) {
+        Job me{state, data, n};
+        if (n == 0) return;
+        std::unique_lock<std::mutex> lk(mu);
+        pending.push_back(&me);
+        for (;;) {
+            if (me.done) return;
+            if (!me.owned) {
+                std::vector<Job*> mine;
+                take(&me, mine);
+                fill(mine);
+                lk.unlock();
+                process(mine, &me);
+                lk.lock();
+                continue;
+            }
+            cv.wait(lk);
+        }
+    }
+
+private:
+    void take(Job* j, std::vector<Job*>& mine) {  // mu held
+        pending.erase(std::find(pending.begin(), pending.end(), j));
+        j->owned = true;
+        mine.push_back(j);
+    }
+    void fill(std::vector<Job*>& mine) {  // mu held
+        while (static_cast<int>(mine.size()) < kMaxK && !pending.empty()) take(pending.front(), mine);
+    }
+    void process(std::vector<Job*> mine, Job* me) {
+        std::uint8_t* st[kMaxK];
+        const std::uint8_t* in[kMaxK];
+        for (;;) {
+            std::size_t m = kChunk;
+            for (Job* j : mine) m = std::min(m, j->n - j->pos);
+            for (std::size_t k = 0; k < mine.size(); ++k) {
+                st[k] = mine[k]->state;
+                in[k] = mine[k]->data + 32 * mine[k]->pos;
+            }
+            absorb_chain32_multi(st, in, mine.size(), m);
+            std::lock_guard<std::mutex> lk(mu);
+            bool any_done = false;
+            for (Job* j : mine) {
+                j->pos += m;
+                if (j->pos == j->n) j->done = any_done = true;
+            }
+            mine.erase(std::remove_if(mine.begin(), mine.end(), [](Job* j) { return j->done; }), mine.end());
+            if (me->done) {
+                for (Job* j : mine) {  // hand back, progress kept
+                    j->owned = false;
+                    pending.insert(pending.begin(), j);
+                }
+                cv.notify_all();
+                return;
+            }
+            if (any_done) cv.notify_all();
+            fill(mine);
+        }
+    }
+};
+
 /// One in-flight proof: a CUDA stream, its reduction workspace, pinned
 /// staging and profile counters. A context owns one lane per concurrent
 /// proof (lane 0 serves the single-call API).
@@ -457,6 +545,7 @@ struct Lane {
 /// The context is lane 0 itself; extra lanes (concurrent proofs) are
 /// created on demand and share the runtime-field state.
 struct dgkr_ctx : Lane {
+    AbsorbPool absorb_pool;  // output absorbs of the concurrent proofs of a stream
     std::mutex lanes_mu;
     std::vector<std::unique_ptr<Lane>> extra;  // lanes 1..
     cudaEvent_t user_ev[8] = {};

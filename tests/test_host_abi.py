@@ -91,3 +91,30 @@ def test_replicate_matches_definition():
     for k in range(4):
         sv = sub.evaluate(vals[k * insz:(k + 1) * insz], 97)[-1]
         assert out[k * 8:(k + 1) * 8] == sv
+
+
+@pytest.mark.parametrize("k,n,threads", [(1, 5, 1), (2, 100, 1), (3, 33, 1), (4, 64, 1), (7, 17, 1),
+                                         (5, 70000, 5), (9, 40000, 9), (3, 1, 3)])
+def test_absorb_multi_equals_separate_chains(k, n, threads):
+    """k transcripts absorbing k element streams interleaved (multi-buffer
+    SHA-NI), and through the stream's combining absorb scheduler with one
+    thread per transcript (chunk hand-offs at 2^15), equal k separate absorbs."""
+    import ctypes as C
+
+    from paper_2404_10404_b200._lib import Transcript_t, check
+
+    f = P.Field.bn254()
+    data = [W.random_inputs(f.p, n, 50 + j) for j in range(k)]
+    want = []
+    for j in range(k):
+        t = P.Transcript(f, "multi", [j])
+        t.absorb_elems(data[j].tobytes())
+        want.append(t.state)
+    ts = [Transcript_t() for _ in range(k)]
+    for j in range(k):
+        ts[j] = P.Transcript(f, "multi", [j]).t
+    tptr = (C.POINTER(Transcript_t) * k)(*[C.pointer(t) for t in ts])
+    eptr = (C.c_void_p * k)(*[d.ctypes.data for d in data])
+    check(lib().dgkr_transcript_absorb_elems_multi(f.handle, tptr, C.c_size_t(k), eptr, C.c_size_t(n),
+                                                   C.c_int(threads)))
+    assert [bytes(t.state) for t in ts] == want
