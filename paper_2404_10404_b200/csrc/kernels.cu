@@ -1430,7 +1430,7 @@ static void launch_round_tma_t(const RoundTmaParams& p, int grid, cudaStream_t s
 static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, int lp, cudaStream_t st) {
     const std::uint64_t P = a.n_out_pairs;
     const std::uint64_t lim = tuning().tma_min_pairs;
-    if (lim == 0 || P < lim || P % kTmaConsumers != 0 || a.np != 1 || !a.has_g || !a.in_host ||
+    if (lim == 0 || P < lim || P % kTmaTile != 0 || a.np != 1 || !a.has_g || !a.in_host ||
         (a.mode != kScan && !a.out_host))
         return false;
     RoundTmaParams p{};
@@ -1442,7 +1442,8 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
     p.result = ws.result;
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const std::uint64_t elems = a.mode == kScan ? 2 * P : 4 * P;
-    const int box = a.mode == kScan ? kTmaConsumers / 2 : (a.mode == kFoldNat ? kTmaConsumers : kTmaConsumers / 4);
+    const int box = a.mode == kScan ? TmaShape<kScan>::kBoxRows
+                    : (a.mode == kFoldNat ? TmaShape<kFoldNat>::kBoxRows : TmaShape<kFoldRev>::kBoxRows);
     for (int t = 0; t < 3; ++t) {
         if (!encode_table_map(&p.map[t], a.in_host[t], elems, box)) return false;
         p.out[t] = a.mode == kScan ? nullptr : a.out_host[t];
@@ -1466,7 +1467,7 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
         return d;
     }();
     p.dbg = dbg;
-    const std::uint64_t tiles = P / kTmaConsumers;
+    const std::uint64_t tiles = (P / kTmaTile + kTmaWarps - 1) / kTmaWarps;  // CTAs with work for every warp
     const int grid = static_cast<int>(std::min<std::uint64_t>(tiles, static_cast<std::uint64_t>(2 * ws.num_sms)));
     DISPATCH_FIELD(k, F, {
         if (a.mode == kScan) {

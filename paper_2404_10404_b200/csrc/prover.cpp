@@ -867,8 +867,15 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         if (!comm || comm->rank == root) {
             const double t0 = now_ms();
-            if (pool && w == 32) pool->run(tr.state_bytes(), out + 4, n_out);  // interleaved with other proofs' chains
-            else tr.absorb_many(out + 4, n_out, w);
+            // DGKR_DIAG_SKIP_OUTPUT_ABSORB=1: bottleneck diagnosis only (tools/diag_stream.py):
+            // skips the absorb, so the proof is NOT the reference's; never set for a bench
+            static const bool diag_skip = std::getenv("DGKR_DIAG_SKIP_OUTPUT_ABSORB") != nullptr;
+            if (diag_skip) {
+            } else if (pool && w == 32) {
+                pool->run(tr.state_bytes(), out + 4, n_out);  // interleaved with other proofs' chains
+            } else {
+                tr.absorb_many(out + 4, n_out, w);
+            }
             const double dt = now_ms() - t0;
             ctx->prof.output_absorb_ms += dt;
             ctx->prof.host_transcript_ms += dt;

@@ -5,13 +5,13 @@
 // Why: the register-fed k_round runs at 2 CTAs/SM (112 registers) with one
 // output pair in flight per thread, so HBM latency is exposed (ncu r1: 24%
 // warps active, 35-53% issue active, long-scoreboard the top stall on the
-// fold rounds). Here a producer warp streams each tile's tables into a
-// shared-memory ring with cp.async.bulk.tensor (TMA) while 8 consumer warps
-// fold and sum the previous tiles from shared memory, so the loads are in
-// flight during the field arithmetic without costing registers. The producer
-// is thread 0 of the CTA (not a dedicated warp): a 9th warp would cap the
-// registers at 96 (5 warps on some SM sub-partitions) and spill; with 8 warps
-// x 2 CTAs per SM every thread keeps 128.
+// fold rounds). Here every warp streams its own tables into its own
+// shared-memory ring with cp.async.bulk.tensor (TMA): lane 0 refills a stage
+// as soon as the warp has read it, so loads run ahead of the field
+// arithmetic without costing registers and no warp ever waits for another.
+// (A CTA-wide ring refilled by one thread measured slower: the refill had
+// to wait for the slowest warp. A dedicated producer warp would cap the
+// registers at 96 -- 5 warps on some SM sub-partitions -- and spill.)
 //
 // Layout: every table is viewed as a 2-D tensor of 128-byte rows (4 field
 // elements) with the 128-byte swizzle, so each consumer's 16-byte shared
@@ -20,27 +20,30 @@
 //   kFoldNat  (round 2)   index i = elements 4i..4i+3:   tile = 256 rows
 //   kFoldRev  (rounds>=3) index i = elements i, i+P, i+2P, i+3P of the
 //                         bit-reversed table: 4 boxes of 64 rows per tile
-// One ring stage holds one table's part of one tile; a tile is ntab stages.
+// A warp-tile is 32 output pairs; one ring stage holds one table's part of a
+// warp-tile, so a warp-tile is ntab stages.
 #pragma once
 
 #include <cuda.h>  // CUtensorMap (the map is built on the host by cuTensorMapEncodeTiled)
 
-constexpr int kTmaConsumers = 256;                 // one output pair per thread per tile
-constexpr int kTmaThreads = kTmaConsumers;
-constexpr int kTmaRingBytes = 96 * 1024;           // 3 stages of a fold tile (6 of a scan tile)
+constexpr int kTmaWarps = 8;
+constexpr int kTmaThreads = 32 * kTmaWarps;
+constexpr int kTmaWarpRing = 12 * 1024;  // per warp: 3 fold stages of 4 KB (6 scan stages of 2 KB)
+constexpr int kTmaRingBytes = kTmaWarps * kTmaWarpRing;
 constexpr int kTmaMaxTabs = 3;
+constexpr int kTmaTile = 32;  // output pairs per warp-tile
 
 struct RoundTmaParams {
     CUtensorMap map[kTmaMaxTabs];  // input tables, 2-D {32 x u32, rows}, SWIZZLE_128B
     Fe* out[kTmaMaxTabs];          // fold outputs (unused by kScan)
-    std::uint64_t n_out_pairs;     // P (a multiple of kTmaConsumers)
+    std::uint64_t n_out_pairs;     // P (a multiple of kTmaTile)
     int log_p;
     int ntab;
     Fe* partials;
     unsigned* counter;
     Fe* result;
     FoldConst k;  // fold challenge (kernel-parameter space: IMAD constant operands)
-    // debug (DGKR_TMA_VERIFY=1): every staged element is compared with a
+    // debug (DGKR_TMA_VERIFY): every staged element is compared with a
     // direct global load of in[t]; mismatches counted in dbg[0], first one in dbg[1..4]
     const Fe* in[kTmaMaxTabs];
     unsigned* dbg;
@@ -54,9 +57,6 @@ __device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
     asm volatile(
@@ -84,11 +84,11 @@ __device__ __forceinline__ uint4 lds128(std::uint32_t addr) {
     return v;
 }
 
-/// element at (row, first 16-byte chunk c0) of a SWIZZLE_128B tile at shared
-/// address `tile` (1024-aligned): chunk c of row r sits at chunk c ^ (r & 7)
-__device__ __forceinline__ Fe lds_fe_swz(std::uint32_t tile, std::uint32_t row, std::uint32_t c0) {
+/// element at (row, first 16-byte chunk c0) of a SWIZZLE_128B box at shared
+/// address `box` (1024-aligned): chunk c of row r sits at chunk c ^ (r & 7)
+__device__ __forceinline__ Fe lds_fe_swz(std::uint32_t box, std::uint32_t row, std::uint32_t c0) {
     const std::uint32_t sw = row & 7;
-    const std::uint32_t r = tile + row * 128;
+    const std::uint32_t r = box + row * 128;
     const uint4 lo = lds128(r + ((c0 ^ sw) << 4));
     const uint4 hi = lds128(r + (((c0 + 1) ^ sw) << 4));
     Fe x;
@@ -99,14 +99,12 @@ __device__ __forceinline__ Fe lds_fe_swz(std::uint32_t tile, std::uint32_t row, 
 
 template <int MODE>
 struct TmaShape {
-    static constexpr int kStageBytes = MODE == kScan ? kTmaConsumers * 64 : kTmaConsumers * 128;
-    static constexpr int kStages = kTmaRingBytes / kStageBytes;
-    static constexpr int kBoxRows = MODE == kScan ? kTmaConsumers / 2 : (MODE == kFoldNat ? kTmaConsumers : kTmaConsumers / 4);
+    static constexpr int kStageBytes = MODE == kScan ? kTmaTile * 64 : kTmaTile * 128;
+    static constexpr int kStages = kTmaWarpRing / kStageBytes;
+    // rows of one TMA box: kScan 2 pairs per row, kFoldNat 1, kFoldRev 4 boxes of 4 elements per row
+    static constexpr int kBoxRows = MODE == kScan ? kTmaTile / 2 : (MODE == kFoldNat ? kTmaTile : kTmaTile / 4);
 };
 
-/// Consumer view of one table of one tile: the pair (x0, x1) of index
-/// i = tile * 256 + tid, folded with the challenge unless kScan; fold outputs
-/// are stored as in load_pair (kFoldNat writes bit-reversed).
 __device__ __noinline__ void tma_verify(const RoundTmaParams& a, int t, std::uint64_t gi, const Fe& x, int mode) {
     const Fe y = fe_load(a.in[t] + gi);
     bool ok = true;
@@ -120,12 +118,15 @@ __device__ __noinline__ void tma_verify(const RoundTmaParams& a, int t, std::uin
     }
 }
 
+/// Lane view of one table of one warp-tile: the pair (x0, x1) of output index
+/// i = wtile * 32 + lane, folded with the challenge unless kScan; fold outputs
+/// are stored as in load_pair (kFoldNat writes bit-reversed).
 template <class F, int MODE>
-__device__ __forceinline__ void tma_pair(std::uint32_t st, int tid, std::uint64_t i, const RoundTmaParams& a,
+__device__ __forceinline__ void tma_pair(std::uint32_t st, int lane, std::uint64_t i, const RoundTmaParams& a,
                                          Fe* dst, Fe& x0, Fe& x1, int t) {
     const std::uint64_t P = a.n_out_pairs;
     if (MODE == kScan) {
-        const std::uint32_t row = tid >> 1, cb = (tid & 1) * 4;
+        const std::uint32_t row = lane >> 1, cb = (lane & 1) * 4;
         x0 = lds_fe_swz(st, row, cb);
         x1 = lds_fe_swz(st, row, cb + 2);
         if (a.dbg) {
@@ -133,8 +134,8 @@ __device__ __forceinline__ void tma_pair(std::uint32_t st, int tid, std::uint64_
             tma_verify(a, t, 2 * i + 1, x1, MODE);
         }
     } else if (MODE == kFoldNat) {
-        const Fe a0 = lds_fe_swz(st, tid, 0), a1 = lds_fe_swz(st, tid, 2);
-        const Fe b0 = lds_fe_swz(st, tid, 4), b1 = lds_fe_swz(st, tid, 6);
+        const Fe a0 = lds_fe_swz(st, lane, 0), a1 = lds_fe_swz(st, lane, 2);
+        const Fe b0 = lds_fe_swz(st, lane, 4), b1 = lds_fe_swz(st, lane, 6);
         if (a.dbg) {
             tma_verify(a, t, 4 * i, a0, MODE);
             tma_verify(a, t, 4 * i + 1, a1, MODE);
@@ -147,8 +148,8 @@ __device__ __forceinline__ void tma_pair(std::uint32_t st, int tid, std::uint64_
         fe_store(dst + s, x0);
         fe_store(dst + s + P, x1);
     } else {
-        const std::uint32_t row = tid >> 2, cb = (tid & 3) * 2;
-        constexpr int seg = kTmaConsumers * 32;  // one box: 256 elements
+        const std::uint32_t row = lane >> 2, cb = (lane & 3) * 2;
+        constexpr int seg = kTmaTile * 32;  // one box: 32 elements, 1 KB
         const Fe a0 = lds_fe_swz(st, row, cb), b0 = lds_fe_swz(st + seg, row, cb);
         const Fe a1 = lds_fe_swz(st + 2 * seg, row, cb), b1 = lds_fe_swz(st + 3 * seg, row, cb);
         if (a.dbg) {
@@ -166,8 +167,8 @@ __device__ __forceinline__ void tma_pair(std::uint32_t st, int tid, std::uint64_
 
 /// One round over the layer tables (V, H, G): S0 = sum V0 H0 + G0,
 /// S2 = sum dV dH (and S1 = sum V1 H1 + G1 when S1). Grid: persistent CTAs
-/// (<= 2 per SM), each striding over tiles of 256 output pairs; a CTA's
-/// units (tile, table) stream through a ring of kStages shared-memory stages.
+/// (<= 2 per SM) of 8 independent warps; warp g of G strides over warp-tiles
+/// g, g + G, ...; its units (warp-tile, table) stream through its own ring.
 template <class F, int MODE, bool S1>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_constant__ RoundTmaParams a) {
     using Shape = TmaShape<MODE>;
@@ -175,40 +176,40 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     constexpr int kStages = Shape::kStages;
     constexpr bool kWide = MODE == kScan && !S1;  // round 1: unreduced products, one REDC per CTA
     extern __shared__ std::uint8_t smem_raw[];
-    __shared__ std::uint64_t full[kStages], empty[kStages];
-    // the ring as a 32-bit shared-window address, 1024-aligned for the swizzle
-    const std::uint32_t ring = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    __shared__ std::uint64_t full_all[kTmaWarps][kStages];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    std::uint64_t* full = full_all[warp];
+    // this warp's ring as a 32-bit shared-window address, 1024-aligned for the swizzle
+    const std::uint32_t ring = ((smem_u32(smem_raw) + 1023u) & ~1023u) + warp * kTmaWarpRing;
     const std::uint64_t P = a.n_out_pairs;
-    const std::uint64_t n_tiles = P / kTmaConsumers;
-    const std::uint64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const std::uint64_t n_units = my_tiles * a.ntab;
-    // unit u = (tile blockIdx.x + (u / ntab) * gridDim.x, table u % ntab) -> ring stage s
+    const std::uint64_t n_wt = P / kTmaTile;
+    const std::uint64_t G = static_cast<std::uint64_t>(gridDim.x) * kTmaWarps;
+    const std::uint64_t g = static_cast<std::uint64_t>(blockIdx.x) * kTmaWarps + warp;
+    const std::uint64_t my_wt = g < n_wt ? (n_wt - g + G - 1) / G : 0;
+    const std::uint64_t n_units = my_wt * a.ntab;
+    // unit u = (warp-tile g + (u / ntab) G, table u % ntab) -> stage s (lane 0 only)
     auto issue = [&](std::uint64_t u, int s) {
-        const std::uint64_t tile = blockIdx.x + (u / a.ntab) * gridDim.x;
+        const std::uint64_t wt = g + (u / a.ntab) * G;
         const int t = static_cast<int>(u % a.ntab);
         const std::uint32_t dst = ring + s * Shape::kStageBytes;
         mbar_expect_tx(&full[s], Shape::kStageBytes);
         if (MODE == kScan) {
-            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(tile * (kTmaConsumers / 2)));
+            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(wt * (kTmaTile / 2)));
         } else if (MODE == kFoldNat) {
-            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(tile * kTmaConsumers));
+            tma_load_2d(dst, &a.map[t], &full[s], 0, static_cast<int>(wt * kTmaTile));
         } else {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                tma_load_2d(dst + q * (kTmaConsumers * 32), &a.map[t], &full[s], 0,
-                            static_cast<int>((tile * kTmaConsumers + q * P) >> 2));
+                tma_load_2d(dst + q * (kTmaTile * 32), &a.map[t], &full[s], 0,
+                            static_cast<int>((wt * kTmaTile + q * P) >> 2));
         }
     };
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTmaConsumers / 32);
-        }
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int s = 0; s < kStages && static_cast<std::uint64_t>(s) < n_units; ++s) issue(s, s);
     }
-    __syncthreads();
+    __syncwarp();
     std::conditional_t<kWide, Acc, Fe> w[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -218,17 +219,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     int s = 0;
     std::uint32_t ph = 0;
     std::uint64_t u = 0;
-    // consume unit u from stage s; thread 0 refills the stage with unit
-    // u + kStages once all 8 warps have released it
+    // consume unit u from stage s; once the whole warp has read it, lane 0
+    // refills the stage with unit u + kStages
     auto next = [&](Fe* dst, std::uint64_t i, Fe& x0, Fe& x1, int t) {
         mbar_wait(&full[s], ph);
-        tma_pair<F, MODE>(ring + s * Shape::kStageBytes, tid, i, a, dst, x0, x1, t);
+        tma_pair<F, MODE>(ring + s * Shape::kStageBytes, lane, i, a, dst, x0, x1, t);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && u + kStages < n_units) {
-            mbar_wait(&empty[s], ph);
-            // the generic-proxy reads of this stage are ordered before the
-            // async-proxy (TMA) writes that refill it
+        if (lane == 0 && u + kStages < n_units) {
+            // the warp's generic-proxy reads of this stage before the async-proxy (TMA) refill
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(u + kStages, s);
         }
@@ -238,8 +236,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
             ph ^= 1;
         }
     };
-    for (std::uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const std::uint64_t i = tile * kTmaConsumers + tid;
+    for (std::uint64_t k = 0; k < my_wt; ++k) {
+        const std::uint64_t i = (g + k * G) * kTmaTile + lane;
         Fe f0, f1, g0, g1;
         next(a.out[0], i, f0, f1, 0);
         next(a.out[1], i, g0, g1, 1);
