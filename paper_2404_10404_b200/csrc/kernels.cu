@@ -526,6 +526,61 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(const __grid_cons
     }
 }
 
+// Row-pair bookkeeping with round 1 fused (BookkeepLaunch::pseg). Phase 1:
+// rows x = 2j, 2j+1 of H (= slot out) and G; phase 2: rows y of MA and C.
+// The two rows' CSR entries are visited interleaved (two independent gathers
+// in flight); round-1 sums are kept unreduced (Acc) and reduced once per CTA,
+// exactly as k_round's kScan does on the stored tables.
+template <class F, int PHASE>
+__global__ void __launch_bounds__(kThreads) k_bookkeep_pairs(const __grid_constant__ BookkeepLaunch a,
+                                                             const __grid_constant__ FoldConst vxk) {
+    const SlotDesc sd = a.slots[0];
+    const int lp = static_cast<int>(sd.log_stride) - 1;
+    const std::uint64_t pmask = (std::uint64_t{1} << lp) - 1;
+    Acc w[2];
+    acc_zero(w[0]);
+    acc_zero(w[1]);
+    for (std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; t < (a.T >> 1);
+         t += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t c = t >> lp;
+        const uint4 ps = a.pseg[t & pmask];
+        const std::uint64_t x0 = (c << sd.log_stride) | ps.w;
+        Fe h[2] = {fe_zero(), fe_zero()}, gs[2] = {fe_zero(), fe_zero()};
+        const std::uint32_t n = ps.y > ps.z ? ps.y : ps.z;
+        for (std::uint32_t e = 0; e < n; ++e) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (e >= (r ? ps.z : ps.y)) continue;
+                const uint4 en = sd.ent[ps.x + (r ? ps.y : 0) + e];
+                const Fe wg = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
+                Fe prod, base;
+                if (PHASE == 1) {  // mul: H += w V[y]    add: H += w, G += w V[y]
+                    base = wg;
+                    prod = fe_mul<F>(wg, fe_load_nc(sd.V + ((c << sd.log_stride) | en.y)));
+                } else {  // cx = w chi_x(u); mul: MA += cx V(u)   add: MA += cx, C += cx V(u)
+                    base = fe_mul<F>(wg, fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y)));
+                    prod = fe_mul_fold<F>(base, vxk);
+                }
+                const bool mul = en.z >> 31;
+                h[r] = fe_add<F>(h[r], fe_select<F>(mul, prod, base));
+                gs[r] = fe_select<F>(mul, gs[r], fe_add<F>(gs[r], prod));
+            }
+        }
+        fe_store(sd.out + x0, h[0]);
+        fe_store(sd.out + x0 + 1, h[1]);
+        fe_store(a.G + x0, gs[0]);
+        fe_store(a.G + x0 + 1, gs[1]);
+        // round 1 of the phase (sumcheck.hpp:118-137 over the pair (V, H) + G)
+        const Fe v0 = fe_load_nc(sd.V + x0), v1 = fe_load_nc(sd.V + x0 + 1);
+        acc_mad(w[0], v0, h[0]);
+        acc_add_hi(w[0], gs[0]);
+        acc_mad(w[1], fe_sub_lazy<F>(v1, v0), fe_sub_lazy<F>(h[1], h[0]));
+    }
+    Fe s[2];
+    block_sum_wide<F, 2>(w, s);
+    grid_finish<F, 2>(s, a.r1.partials, a.r1.counter, a.r1.result, true);
+}
+
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) {
     for (std::uint64_t x = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; x < a.T;
@@ -1408,8 +1463,9 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0};
+        Tuning v{kSmallRoundPairs, 0, 1};
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
         return v;
     }();
@@ -1613,6 +1669,12 @@ void launch_bookkeep_heavy(FieldKind k, const BookkeepLaunch& a, int phase, cuda
 
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
+    if (a.pseg) {
+        const int gp = grid_for(a.T / 2, kThreads, a.r1.max_blocks);
+        DISPATCH_FIELD(k, F, (k_bookkeep_pairs<F, 1><<<gp, kThreads, 0, st>>>(a, FoldConst{})));
+        check_launch("bookkeep_pairs(1)");
+        return;
+    }
     if (a.perm && a.n_slots == 1 && a.gate_w) {
         DISPATCH_FIELD(k, F, (k_bookkeep1_sorted<F><<<g, kThreads, 0, st>>>(a)));
     } else {
@@ -1624,6 +1686,14 @@ void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t s
 
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st) {
     const int g = grid_for(a.T, kThreads, 148 * 16);
+    if (a.pseg) {
+        FoldConst vk{};
+        std::memcpy(&vk, a.vx_const, sizeof(FoldConst));
+        const int gp = grid_for(a.T / 2, kThreads, a.r1.max_blocks);
+        DISPATCH_FIELD(k, F, (k_bookkeep_pairs<F, 2><<<gp, kThreads, 0, st>>>(a, vk)));
+        check_launch("bookkeep_pairs(2)");
+        return;
+    }
     if (a.perm && a.n_slots == 1 && a.gate_w && a.eq_u && a.vx_const) {
         FoldConst vk{};
         std::memcpy(&vk, a.vx_const, sizeof(FoldConst));

@@ -78,6 +78,7 @@ constexpr std::uint64_t kSmallRoundPairs = 256;
 struct Tuning {
     std::uint64_t small_round_pairs;
     std::uint64_t tma_min_pairs;
+    std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
 };
 Tuning& tuning();
 
@@ -160,7 +161,16 @@ struct BookkeepLaunch {
     std::uint32_t heavy_min = 0xffffffffu;
     Fe* heavy_h = nullptr;  // scratch [n_heavy] per-item H_m / MA_m partials
     Fe* heavy_g = nullptr;  // scratch [n_heavy] per-item G / C partials
+    // Row-pair path with the phase's first sum-check round fused in (single
+    // slot, no heavy rows): one thread builds rows (2j, 2j+1) of a copy, the
+    // pairs visited in a static order sorted by the larger row degree; then
+    // it adds V0 H0 + G0 and (V1 - V0)(H1 - H0) of its pair to round 1's
+    // (S0, S2) -- the sums k_round's kScan would re-read the tables for.
+    const uint4* pseg = nullptr;  // [2^(log_stride-1)] {entry start of row 2j, count 2j, count 2j+1, 2j}
+    ReduceWs r1{};                // round-1 sums land in r1.result[0..2)
 };
+/// Phase 1 / phase 2 bookkeeping; with a.pseg set (and no heavy rows) also
+/// round 1 of the phase's sum-check: returns true if it was fused.
 void launch_bookkeep_phase1(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
 void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t st);
 

@@ -94,7 +94,7 @@ struct SumcheckRun {
 /// computed on the device); nullptr = derive every round from the tables.
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                        RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr, const U256* claim = nullptr,
-                       const Fe* const* base_host = nullptr);
+                       const Fe* const* base_host = nullptr, bool r1_done = false);
 
 /// Distributed form (cluster.hpp:228-320 generalised to the layer
 /// sum-check): `nv` local variables per rank, rank = high variables. Local
@@ -105,10 +105,11 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
 /// equals the single-GPU one byte for byte.
 SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                             RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, DistTail& dt,
-                            const U256* claim = nullptr, const Fe* const* base_host = nullptr) {
+                            const U256* claim = nullptr, const Fe* const* base_host = nullptr,
+                            bool r1_done = false) {
     const int ntab = 2 * np + (has_g ? 1 : 0);
     const int world = comm->world;
-    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim, base_host);
+    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim, base_host, r1_done);
     // boundary: gather every rank's final table values
     std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
     for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
@@ -138,7 +139,9 @@ SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, 
 
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                        RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim,
-                       const Fe* const* base_host) {
+                       const Fe* const* base_host, bool r1_done) {
+    // r1_done: round 1's (S0, S2) are already in ws.result (bookkeeping with
+    // the first round fused, k_bookkeep_pairs); the round-1 launch is skipped
     const HostField& F = f->f;
     const bool skip_s1 = claim != nullptr;
     const int nres = skip_s1 ? 2 : 3;  // device sums per round: (S0, S2) or (S0, S1, S2)
@@ -179,9 +182,13 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         rl.n_out_pairs = size0 >> j;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
         const std::uint64_t small_pairs = tuning().small_round_pairs;
-        if (rl.n_out_pairs <= small_pairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
-        else launch_round(kind, rl, ctx->ws, ctx->st);
-        ctx->launched();
+        if (j == 1 && r1_done) {
+            if (!skip_s1) fail(DGKR_LOGIC_ERROR, "fused round 1 computes (S0, S2) only");
+        } else {
+            if (rl.n_out_pairs <= small_pairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
+            else launch_round(kind, rl, ctx->ws, ctx->st);
+            ctx->launched();
+        }
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev1, ctx->st));
         if (comm) {
             // every rank's partial round sums (cluster.hpp:272-278), summed on every rank
@@ -196,7 +203,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             ctx->d2h(ctx->h_small + 1, ctx->ws.result, nres * sizeof(Fe));
             ctx->sync();
         }
-        if (ctx->profile_on) {
+        if (ctx->profile_on && !(j == 1 && r1_done)) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.round_ms += ms;
@@ -354,6 +361,7 @@ struct dgkr_circuit {
         DBuf<uint4> nested;
         DBuf<std::uint32_t> xperm, yperm;  // single-slot: degree-sorted rows
         DBuf<uint2> xseg, yseg;
+        DBuf<uint4> xpseg, ypseg;          // single-slot: row pairs, sorted by the larger degree (fused round 1)
         DBuf<uint4> xheavy, yheavy;        // heavy-row items {slot, copy, row, 0}, sorted by table row
         std::uint32_t n_xheavy = 0, n_yheavy = 0;
     };
@@ -376,6 +384,8 @@ namespace {
 
 /// CSR rows with more entries than this are reduced by a CTA, not a thread
 constexpr std::uint32_t kHeavyMin = 64;
+
+bool fuse_round1() { return tuning().fuse_round1 != 0; }
 
 /// GeneralCircuit::validate (circuit.hpp:103-152) on the sub-circuit plus
 /// the data-parallel preconditions; builds all device-side structures.
@@ -553,6 +563,26 @@ void build_circuit(Lane* ctx, dgkr_circuit& c, const std::uint64_t* lgs, const s
             };
             sorted(xoff, C.xperm, C.xseg);
             sorted(yoff, C.yperm, C.yseg);
+            // row pairs (2j, 2j+1) for the bookkeeping kernel with round 1 fused
+            auto pairs = [&](const std::vector<std::uint32_t>& off, DBuf<uint4>& dps) {
+                if (S < 2) return;
+                const std::uint64_t np = S / 2;
+                std::vector<std::uint32_t> order(np);
+                auto deg = [&](std::uint64_t r) { return off[r + 1] - off[r]; };
+                for (std::uint64_t j = 0; j < np; ++j) order[j] = static_cast<std::uint32_t>(j);
+                std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+                    return std::max(deg(2 * a), deg(2 * a + 1)) > std::max(deg(2 * b), deg(2 * b + 1));
+                });
+                std::vector<uint4> ps(np);
+                for (std::uint64_t k = 0; k < np; ++k) {
+                    const std::uint32_t j = order[k];
+                    ps[k] = make_uint4(off[2 * j], deg(2 * j), deg(2 * j + 1), 2 * j);
+                }
+                dps.ensure(np);
+                CK(cudaMemcpy(dps.p, ps.data(), np * sizeof(uint4), cudaMemcpyHostToDevice));
+            };
+            pairs(xoff, C.xpseg);
+            pairs(yoff, C.ypseg);
         }
         C.xoff.ensure(xoff.size());
         C.yoff.ensure(yoff.size());
@@ -992,6 +1022,11 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.heavy_g = W.heavy_scr.p + std::max<std::uint32_t>(c.max_heavy, 1);
         bk.heavy = C.xheavy.p;
         bk.n_heavy = C.n_xheavy;
+        // row pairs with round 1 fused: single slot, no heavy rows, a full pair table
+        const bool fuse1 = fuse_round1() && C.xpseg.p && C.n_xheavy == 0 && ns == 1 && side >= 2 &&
+                           c.sub_log[C.slots[0]] + c.log_copies == side;
+        bk.pseg = fuse1 ? C.xpseg.p : nullptr;
+        bk.r1 = ctx->ws;
         launch_bookkeep_phase1(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -1003,9 +1038,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         SumcheckRun p1 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
-                                   &combined.value, WC.base_host.data())
+                                   &combined.value, WC.base_host.data(), fuse1)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
-                              &combined.value, WC.base_host.data());
+                              &combined.value, WC.base_host.data(), fuse1);
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
@@ -1033,6 +1068,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         bk.seg = C.yseg.p;
         bk.heavy = C.yheavy.p;
         bk.n_heavy = C.n_yheavy;
+        const bool fuse2 = fuse_round1() && C.ypseg.p && C.n_yheavy == 0 && ns == 1 && side >= 2 &&
+                           c.sub_log[C.slots[0]] + c.log_copies == side && bk.vx_const;
+        bk.pseg = fuse2 ? C.ypseg.p : nullptr;
         launch_bookkeep_phase2(kind, bk, ctx->st);
         ctx->launched();
         if (ctx->profile_on) {
@@ -1044,9 +1082,9 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         }
         SumcheckRun p2 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
-                                   &p1.claim_end, WC.base_host.data())
+                                   &p1.claim_end, WC.base_host.data(), fuse2)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
-                              &p1.claim_end, WC.base_host.data());
+                              &p1.claim_end, WC.base_host.data(), fuse2);
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;
@@ -2351,6 +2389,7 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         const std::string n = name ? name : "";
         if (n == "small_round_pairs") tuning().small_round_pairs = value;
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
+        else if (n == "fuse_round1") tuning().fuse_round1 = value;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }
@@ -2360,6 +2399,7 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         const std::string n = name ? name : "";
         if (n == "small_round_pairs") *value = tuning().small_round_pairs;
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
+        else if (n == "fuse_round1") *value = tuning().fuse_round1;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }

@@ -77,3 +77,42 @@ def test_tma_round_distributed(ctx, tma_everywhere, world):
 def test_tuning_rejects_unknown_knob():
     with pytest.raises(P.prover.InvalidArgument):
         P.set_tuning("no_such_knob", 1)
+
+
+# ---------------------------------------------------------------------------
+# bookkeeping by row pairs with round 1 fused (k_bookkeep_pairs)
+# ---------------------------------------------------------------------------
+def _prove_fuse(ctx, f, insz, flat, copies, inputs, label, fuse):
+    old = P.get_tuning("fuse_round1")
+    P.set_tuning("fuse_round1", 1 if fuse else 0)
+    try:
+        circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+        tr = P.Transcript(f, label)
+        return P.gkr_prove(ctx, circ, inputs, tr), tr.state
+    finally:
+        P.set_tuning("fuse_round1", old)
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, O.GOLDILOCKS_P, 97])
+@pytest.mark.parametrize("log_w,copies,depth", [(1, 1, 3), (2, 2, 3), (8, 1, 3), (10, 8, 3)])
+def test_fused_round1_equals_separate(ctx, p, log_w, copies, depth):
+    f = P.Field(p)
+    insz, flat = W.layered_circuit(900 + log_w, log_w, depth)
+    inputs = W.random_inputs(f.p, insz * copies, 3 + log_w)
+    assert _prove_fuse(ctx, f, insz, flat, copies, inputs, "fuse", True) == \
+        _prove_fuse(ctx, f, insz, flat, copies, inputs, "fuse", False)
+
+
+def test_fused_round1_equals_reference(ctx):
+    assert P.get_tuning("fuse_round1") == 1  # the default path
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(5151, 7, 5)
+    copies = 4
+    inputs = W.random_inputs(f.p, insz * copies, 8)
+    circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+    tr = P.Transcript(f, "fuse.ref")
+    proof = P.gkr_prove(ctx, circ, inputs, tr)
+    full_in, full_flat = W.replicate(insz, flat, copies)
+    want, want_state = R.gkr_prove(O.BN254, "fuse.ref", [], O.Circuit.from_flat(full_in, *full_flat),
+                                   O.BN254.elems_from_bytes(inputs.tobytes()), flat=full_flat)
+    assert proof == want and tr.state == want_state
