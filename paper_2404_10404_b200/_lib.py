@@ -8,7 +8,9 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgkr_b200.so")
+# DGKR_LIB: an alternative in-tree build of the same library (A/B experiments of
+# compile-time variants, e.g. build/variants/); the default is the product build
+LIB_PATH = os.environ.get("DGKR_LIB") or os.path.join(_HERE, "libdgkr_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dgkr_b200.h")
 
 _lib = None

@@ -104,7 +104,8 @@ def test_fused_round1_equals_separate(ctx, p, log_w, copies, depth):
 
 
 def test_fused_round1_equals_reference(ctx):
-    assert P.get_tuning("fuse_round1") == 1  # the default path
+    old = P.get_tuning("fuse_round1")
+    P.set_tuning("fuse_round1", 1)
     f = P.Field.bn254()
     insz, flat = W.layered_circuit(5151, 7, 5)
     copies = 4
@@ -115,4 +116,5 @@ def test_fused_round1_equals_reference(ctx):
     full_in, full_flat = W.replicate(insz, flat, copies)
     want, want_state = R.gkr_prove(O.BN254, "fuse.ref", [], O.Circuit.from_flat(full_in, *full_flat),
                                    O.BN254.elems_from_bytes(inputs.tobytes()), flat=full_flat)
+    P.set_tuning("fuse_round1", old)
     assert proof == want and tr.state == want_state
