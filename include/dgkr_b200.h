@@ -48,6 +48,7 @@ extern "C" {
 typedef struct dgkr_ctx dgkr_ctx;
 typedef struct dgkr_field dgkr_field;
 typedef struct dgkr_circuit dgkr_circuit;
+typedef struct dgkr_pairsum dgkr_pairsum;
 
 /* Transcript value: replaces the private members of dgkr::Transcript
  * (transcript.hpp:127-129). */
@@ -117,6 +118,23 @@ int dgkr_ctx_device_info(dgkr_ctx* ctx, int* sm_count, int* cc_major, int* cc_mi
  * (sumcheck.hpp:51-61). */
 int dgkr_prove_product_sum(dgkr_ctx* ctx, const dgkr_field* f, size_t n_pairs, size_t vars, const uint8_t* tables,
                            dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+/* ---- PairSumSession (sumcheck.hpp:152-221) --------------------------------------
+ * The product sum-check's steps as separate calls (the cluster runtime drives
+ * one session per worker, cluster.hpp:250-316). tables = f_0 g_0 f_1 g_1 ...,
+ * each 2^vars canonical elements; copied to the device at begin (:168).
+ * round: the round polynomial {c0, c1, c2, c3 = 0} of the current tables
+ * (4 elements). fold: bind the next variable to r (canonical). finals: after
+ * all folds, [f_0(r), g_0(r), f_1(r), ...] (2 n_pairs elements). Errors: the
+ * reference's -- INVALID_ARGUMENT (no pairs), LOGIC_ERROR ("sumcheck session
+ * exhausted" / "still has unbound variables"). */
+int dgkr_pairsum_begin(dgkr_ctx* ctx, const dgkr_field* f, size_t n_pairs, size_t vars, const uint8_t* tables,
+                       dgkr_pairsum** out);                                   /* PairSumSession ctor :154-171 */
+void dgkr_pairsum_end(dgkr_pairsum* s);
+size_t dgkr_pairsum_vars_left(const dgkr_pairsum* s);                        /* vars_left() :174 */
+int dgkr_pairsum_total(dgkr_pairsum* s, uint8_t* out);                       /* total() :177-186 */
+int dgkr_pairsum_round(dgkr_pairsum* s, uint8_t* out4);                      /* round_poly() :188-193 */
+int dgkr_pairsum_fold(dgkr_pairsum* s, const uint8_t* r);                    /* fold(r) :195-201 */
+int dgkr_pairsum_finals(dgkr_pairsum* s, uint8_t* out);                      /* final_values() :204-215 */
 
 /* ---- layer sum-check -------------------------------------------------------
  * prove_layer_sum (sumcheck.hpp:342-448). wire_meta: n_wires x {is_mul,

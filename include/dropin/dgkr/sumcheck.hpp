@@ -1,6 +1,10 @@
-// Drop-in dgkr/sumcheck.hpp: the reference header with prove_product_sum
-// (sumcheck.hpp:226) and prove_layer_sum (:342) on the B200 prover. Same
-// names, signatures, proofs (bit-exact) and exception types.
+// Drop-in dgkr/sumcheck.hpp: the reference header with PairSumSession
+// (sumcheck.hpp:152-221), prove_product_sum (:226) and prove_layer_sum (:342)
+// on the B200 prover. Same names, signatures, proofs (bit-exact) and
+// exception types. The reference's own PairSumSession is renamed
+// PairSumSessionCpuReference (it still backs the renamed CPU provers), so
+// reference code that drives sessions itself -- cluster::dist_sumcheck
+// (cluster.hpp:250-316) -- runs one device session per worker.
 #pragma once
 #include <cstdint>
 #include <span>
@@ -14,13 +18,87 @@
 
 #define prove_product_sum prove_product_sum_cpu_reference
 #define prove_layer_sum prove_layer_sum_cpu_reference
+#define PairSumSession PairSumSessionCpuReference
 #include_next <dgkr/sumcheck.hpp>
 #undef prove_product_sum
 #undef prove_layer_sum
+#undef PairSumSession
+
+#include <memory>
 
 #include "dgkr/b200_dropin_core.hpp"
 
 namespace dgkr::sumcheck {
+
+/// PairSumSession (sumcheck.hpp:152-221) on the device (dgkr_pairsum_*):
+/// the tables are copied to the GPU at construction; round_poly / fold /
+/// final_values / total are device launches. Copies share one session.
+class PairSumSession {
+public:
+    explicit PairSumSession(std::span<const ProductPair> pairs) {
+        namespace B = dgkr::b200_dropin;
+        if (pairs.empty()) throw std::invalid_argument("product sum needs at least one pair");  // :155-157
+        cfg_ = pairs.front().f.config();
+        const std::size_t vars = pairs.front().f.num_vars();
+        std::vector<std::uint8_t> tabs;
+        for (const auto& p : pairs) {  // :160-169
+            if (p.f.num_vars() != vars || p.g.num_vars() != vars)
+                throw std::invalid_argument("mixed table sizes in product sum");
+            if (p.f.config()->modulus() != cfg_->modulus() || p.g.config()->modulus() != cfg_->modulus())
+                throw std::invalid_argument("mixed field configs in product sum");
+            auto a = B::canonical(p.f.evals()), b = B::canonical(p.g.evals());
+            tabs.insert(tabs.end(), a.begin(), a.end());
+            tabs.insert(tabs.end(), b.begin(), b.end());
+        }
+        n_pairs_ = pairs.size();
+        B::Device& dev = B::device(cfg_);
+        dgkr_pairsum* h = nullptr;
+        B::check(dgkr_pairsum_begin(dev.ctx(), dev.field(), n_pairs_, vars, tabs.data(), &h));
+        h_ = std::shared_ptr<dgkr_pairsum>(h, dgkr_pairsum_end);
+    }
+
+    const FieldConfigPtr& config() const { return cfg_; }
+    std::size_t vars_left() const { return dgkr_pairsum_vars_left(h_.get()); }
+    std::size_t pair_count() const { return n_pairs_; }
+
+    FieldElement total() const {
+        std::vector<std::uint8_t> b(cfg_->byte_width());
+        dgkr::b200_dropin::check(dgkr_pairsum_total(h_.get(), b.data()));
+        const std::uint8_t* p = b.data();
+        return dgkr::b200_dropin::take_elem(p, cfg_);
+    }
+
+    RoundPolynomial round_poly() const {
+        std::vector<std::uint8_t> b(4 * cfg_->byte_width());
+        dgkr::b200_dropin::check(dgkr_pairsum_round(h_.get(), b.data()));
+        const std::uint8_t* p = b.data();
+        FieldElement c0 = dgkr::b200_dropin::take_elem(p, cfg_);
+        FieldElement c1 = dgkr::b200_dropin::take_elem(p, cfg_);
+        FieldElement c2 = dgkr::b200_dropin::take_elem(p, cfg_);
+        FieldElement c3 = dgkr::b200_dropin::take_elem(p, cfg_);
+        return RoundPolynomial{{c0, c1, c2, c3}};
+    }
+
+    void fold(const FieldElement& r) {
+        std::vector<std::uint8_t> b;
+        r.append_bytes(b);
+        dgkr::b200_dropin::check(dgkr_pairsum_fold(h_.get(), b.data()));
+    }
+
+    std::vector<FieldElement> final_values() const {
+        std::vector<std::uint8_t> b(2 * n_pairs_ * cfg_->byte_width());
+        dgkr::b200_dropin::check(dgkr_pairsum_finals(h_.get(), b.data()));
+        const std::uint8_t* p = b.data();
+        std::vector<FieldElement> out;
+        for (std::size_t i = 0; i < 2 * n_pairs_; ++i) out.push_back(dgkr::b200_dropin::take_elem(p, cfg_));
+        return out;
+    }
+
+private:
+    FieldConfigPtr cfg_;
+    std::size_t n_pairs_ = 0;
+    std::shared_ptr<dgkr_pairsum> h_;
+};
 
 inline SumcheckProof prove_product_sum(std::span<const ProductPair> pairs, Transcript& transcript) {
     namespace B = dgkr::b200_dropin;

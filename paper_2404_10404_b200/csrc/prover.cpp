@@ -1528,6 +1528,192 @@ int dgkr_prove_product_sum(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_pai
     });
 }
 
+// ===========================================================================
+// PairSumSession (sumcheck.hpp:152-221): the product sum-check's steps as
+// separate calls, so a caller (cluster.hpp:250-316 drives one per worker and
+// one for the master tail) can run the protocol itself. The tables live on
+// the device; fold(r) is the fused fold + next-round kernel (k_round), so
+// the round polynomial of the folded tables is ready when fold returns.
+// ===========================================================================
+struct dgkr_pairsum {
+    dgkr_ctx* ctx = nullptr;
+    const dgkr_field* f = nullptr;
+    int np = 0;
+    int vars_left = 0;
+    int layout = 0;  // 0: natural order (before the first fold), 1: bit-reversed (k_round kFoldNat/kFoldRev outputs)
+    std::uint64_t size = 0;  // current table size 2^vars_left
+    DBuf<Fe> tabs;
+    DBuf<const Fe*> base;
+    RoundBuffers rb;
+    const Fe* const* cur = nullptr;
+    int cur_buf = -1;  // -1 base tables, 0 rb.A, 1 rb.B
+    bool have_sums = false;
+    U256 sums[3]{};     // (S0, S1, S2) of the current tables
+    std::vector<U256> finals;
+};
+
+namespace {
+
+void pairsum_scan(dgkr_pairsum* s) {
+    // round sums of the natural-order initial tables (k_round kScan, all three sums)
+    Lane* L = s->ctx;
+    RoundLaunch rl;
+    rl.np = s->np;
+    rl.has_g = false;
+    rl.mode = 0;
+    rl.in = s->cur;
+    rl.n_out_pairs = s->size / 2;
+    rl.need_s1 = true;
+    const FieldKind kind = L->use(s->f);
+    if (rl.n_out_pairs <= tuning().small_round_pairs) launch_round_small(kind, rl, L->ws, L->st);
+    else launch_round(kind, rl, L->ws, L->st);
+    L->launched();
+    L->d2h(L->h_small + 1, L->ws.result, 3 * sizeof(Fe));
+    L->sync();
+    for (int k = 0; k < 3; ++k) s->sums[k] = to_u256(L->h_small[1 + k]);
+    s->have_sums = true;
+}
+
+}  // namespace
+
+int dgkr_pairsum_begin(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_pairs, std::size_t vars,
+                       const std::uint8_t* tables, dgkr_pairsum** out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "product sum needs at least one pair");  // sumcheck.hpp:155-157
+        if (vars > 40) fail(DGKR_INVALID_ARGUMENT, "table too large");
+        auto s = std::make_unique<dgkr_pairsum>();
+        s->ctx = ctx;
+        s->f = f;
+        s->np = static_cast<int>(n_pairs);
+        s->vars_left = static_cast<int>(vars);
+        s->size = std::uint64_t{1} << vars;
+        const int ntab = 2 * s->np;
+        s->tabs.ensure(static_cast<std::size_t>(ntab) * s->size);
+        DBuf<std::uint8_t> stage;
+        ctx->upload_elems(f, tables, static_cast<std::uint64_t>(ntab) * s->size, s->tabs.p, stage);  // copies the tables (:168)
+        std::vector<const Fe*> hp(ntab);
+        for (int t = 0; t < ntab; ++t) hp[t] = s->tabs.p + t * s->size;
+        s->base.ensure(ntab);
+        ctx->h2d(s->base.p, hp.data(), ntab * sizeof(const Fe*));
+        s->cur = s->base.p;
+        s->rb.ensure(ntab, s->size, ctx->st);
+        CK(cudaStreamSynchronize(ctx->st));
+        *out = s.release();
+    });
+}
+
+void dgkr_pairsum_end(dgkr_pairsum* s) { delete s; }
+
+std::size_t dgkr_pairsum_vars_left(const dgkr_pairsum* s) { return s ? static_cast<std::size_t>(s->vars_left) : 0; }
+
+int dgkr_pairsum_total(dgkr_pairsum* s, std::uint8_t* out) {
+    return guard([&] {
+        Lane* L = s->ctx;
+        CK(cudaSetDevice(L->device));
+        U256 tot{};
+        if (s->vars_left == 0) {  // 1-element tables: the finals
+            for (int k = 0; k < s->np; ++k) tot = s->f->f.add(tot, s->f->f.mul(s->finals[2 * k], s->finals[2 * k + 1]));
+        } else {  // sum_k sum_b f_k(b) g_k(b) (:177-186; layout-independent)
+            launch_pair_total(L->use(s->f), s->cur, s->np, s->size, L->ws, L->st);
+            L->launched();
+            L->d2h(L->h_small + 1, L->ws.result, sizeof(Fe));
+            L->sync();
+            tot = to_u256(L->h_small[1]);
+        }
+        s->f->f.to_bytes(tot, out);
+    });
+}
+
+int dgkr_pairsum_round(dgkr_pairsum* s, std::uint8_t* out4) {
+    return guard([&] {
+        if (s->vars_left == 0) fail(DGKR_LOGIC_ERROR, "sumcheck session exhausted");  // sumcheck.hpp:188-191
+        CK(cudaSetDevice(s->ctx->device));
+        if (!s->have_sums) pairsum_scan(s);
+        const HostField& F = s->f->f;
+        const U256 c0 = s->sums[0], c2 = s->sums[2];
+        const U256 c1 = F.sub(F.sub(s->sums[1], c0), c2);  // c1 = sum f0 dg + g0 df
+        const std::size_t w = F.width();
+        F.to_bytes(c0, out4);
+        F.to_bytes(c1, out4 + w);
+        F.to_bytes(c2, out4 + 2 * w);
+        F.to_bytes(U256{}, out4 + 3 * w);  // c3 = 0 (sumcheck.hpp:18-37)
+    });
+}
+
+int dgkr_pairsum_fold(dgkr_pairsum* s, const std::uint8_t* r_canon) {
+    return guard([&] {
+        if (s->vars_left == 0) fail(DGKR_LOGIC_ERROR, "sumcheck session exhausted");  // sumcheck.hpp:195-198
+        Lane* L = s->ctx;
+        CK(cudaSetDevice(L->device));
+        const HostField& F = s->f->f;
+        const U256 r = F.from_bytes(r_canon);
+        const FieldKind kind = L->use(s->f);
+        const int ntab = 2 * s->np;
+        if (s->vars_left == 1) {  // 2-element tables -> the final values
+            L->h_small[0] = to_fe(r);
+            L->h2d(L->d_small.p, L->h_small, sizeof(Fe));
+            launch_fold_final(kind, s->cur, const_cast<Fe* const*>(s->rb.F()), ntab, L->d_small.p, L->st);
+            L->launched();
+            Fe* hf = L->h_small + Lane::kFinalsOff;
+            if (ntab > static_cast<int>(Lane::kGatherOff - Lane::kFinalsOff)) fail(DGKR_UNSUPPORTED, "too many pairs");
+            L->d2h(hf, s->rb.finals.p, ntab * sizeof(Fe));
+            L->sync();
+            s->finals.clear();
+            for (int t = 0; t < ntab; ++t) s->finals.push_back(to_u256(hf[t]));
+            s->vars_left = 0;
+            s->size = 1;
+            s->have_sums = false;
+            return;
+        }
+        // fold with r and compute the next round's sums in one launch (mle.hpp:75-85 + sumcheck.hpp:118-137)
+        U256 fk[9];
+        s->f->fold_const(r, fk);
+        RoundLaunch rl;
+        rl.np = s->np;
+        rl.has_g = false;
+        rl.mode = s->layout == 0 ? 1 : 2;
+        rl.in = s->cur;
+        const int nb = s->cur_buf == 0 ? 1 : 0;
+        const Fe* const* nxt = nb == 0 ? s->rb.A() : s->rb.B();
+        rl.out = const_cast<Fe* const*>(nxt);
+        rl.n_out_pairs = s->size / 4;
+        rl.fold_const = fk;
+        rl.need_s1 = true;
+        if (rl.n_out_pairs <= tuning().small_round_pairs) launch_round_small(kind, rl, L->ws, L->st);
+        else launch_round(kind, rl, L->ws, L->st);
+        L->launched();
+        L->d2h(L->h_small + 1, L->ws.result, 3 * sizeof(Fe));
+        L->sync();  // ws.result is shared by every session of the context: read it now
+        for (int k = 0; k < 3; ++k) s->sums[k] = to_u256(L->h_small[1 + k]);
+        s->have_sums = true;
+        s->cur = nxt;
+        s->cur_buf = nb;
+        s->layout = 1;
+        s->size /= 2;
+        s->vars_left -= 1;
+    });
+}
+
+int dgkr_pairsum_finals(dgkr_pairsum* s, std::uint8_t* out) {
+    return guard([&] {
+        if (s->vars_left != 0) fail(DGKR_LOGIC_ERROR, "sumcheck session still has unbound variables");  // :204-207
+        if (s->finals.empty()) {  // a 0-variable session: the 1-element tables themselves
+            Lane* L = s->ctx;
+            CK(cudaSetDevice(L->device));
+            std::vector<const Fe*> hp(2 * s->np);
+            CK(cudaMemcpy(hp.data(), s->cur, hp.size() * sizeof(const Fe*), cudaMemcpyDeviceToHost));
+            for (const Fe* p : hp) {
+                Fe v;
+                CK(cudaMemcpy(&v, p, sizeof(Fe), cudaMemcpyDeviceToHost));
+                s->finals.push_back(to_u256(v));
+            }
+        }
+        const std::size_t w = s->f->f.width();
+        for (std::size_t t = 0; t < s->finals.size(); ++t) s->f->f.to_bytes(s->finals[t], out + t * w);
+    });
+}
+
 int dgkr_prove_layer_sum(dgkr_ctx* ctx, const dgkr_field* f, std::size_t side_vars, std::size_t n_slots,
                          const std::uint8_t* slot_tables, std::size_t n_wires, const std::uint32_t* wire_meta,
                          const std::uint64_t* wire_idx, const std::uint8_t* wire_weights, const std::uint8_t* claimed,

@@ -44,3 +44,17 @@ def test_reference_epoch_pipeline_on_the_gpu_prover(args):
     assert a.returncode == 0 and b.returncode == 0, (a.stderr + b.stderr)[-3000:]
     assert a.stdout == b.stdout
     assert ('"all_accepted":true' in a.stdout) == (len(args) <= 4)
+
+
+def test_pairsum_session_and_reference_dist_sumcheck_on_device_sessions():
+    """PairSumSession (sumcheck.hpp:152-221) on the device through the drop-in,
+    step by step against the reference's own session, and the reference's OWN
+    dist_sumcheck (cluster.hpp:228-320) driving one device session per worker:
+    byte-equal to the single-machine reference proof and to the C-ABI
+    dist_sumcheck, N = 1..8, three fields (tests/cpp/pairsum_dropin_test.cpp)"""
+    exe = os.path.join(ROOT, "oracle", "_ref", "pairsum_dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("pairsum drop-in test not built (make -C oracle, needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert ", 0 failures" in r.stdout

@@ -351,3 +351,50 @@ def test_pcs_rejects_ragged_rows(ctx):
         P.pcs_commit(ctx, f, [a[:-1]])
     with pytest.raises(InvalidArgument):
         P.pcs_open(ctx, f, [a, b], [1, 2], P.Transcript(f, "x"))
+
+
+@pytest.mark.parametrize("p", FIELDS)
+@pytest.mark.parametrize("vars_,n_pairs", [(0, 1), (1, 2), (4, 1), (9, 3)])
+def test_pairsum_session_steps_match_oracle(ctx, p, vars_, n_pairs):
+    """dgkr_pairsum_* (PairSumSession, sumcheck.hpp:152-221) driven step by
+    step reproduces prove_product_sum's transcript and proof bytes."""
+    import ctypes as C
+
+    from paper_2404_10404_b200._lib import LogicError, check, lib
+
+    rng = np.random.default_rng(7000 + vars_ + 10 * n_pairs + p % 97)
+    f, of = P.Field(p), O.Field(p)
+    pairs = _pairs(of, n_pairs, vars_, rng)
+    tabs = b"".join(f.encode(x) for pr in pairs for x in pr)
+    h = C.c_void_p()
+    check(lib().dgkr_pairsum_begin(ctx.handle, f.handle, C.c_size_t(n_pairs), C.c_size_t(vars_), tabs, C.byref(h)))
+    try:
+        w = f.width
+        tr = P.Transcript(f, "sess", [1])
+        buf = C.create_string_buffer(4 * w)
+        check(lib().dgkr_pairsum_total(h, buf))
+        out = buf.raw[:w]
+        tr.absorb_bytes(buf.raw[:w])
+        lib().dgkr_pairsum_vars_left.restype = C.c_size_t
+        assert lib().dgkr_pairsum_vars_left(h) == vars_
+        for _ in range(vars_):
+            check(lib().dgkr_pairsum_round(h, buf))
+            rp = buf.raw[:4 * w]
+            for k in range(4):
+                tr.absorb_bytes(rp[k * w:(k + 1) * w])
+            out += rp
+            r = tr.challenge()
+            check(lib().dgkr_pairsum_fold(h, f.encode([r])))
+        fin = C.create_string_buffer(2 * n_pairs * w)
+        check(lib().dgkr_pairsum_finals(h, fin))
+        with pytest.raises(LogicError):
+            check(lib().dgkr_pairsum_round(h, buf))
+    finally:
+        lib().dgkr_pairsum_end(h)
+    otr = O.Transcript("sess", of, [1])
+    want = O.prove_product_sum(pairs, otr).to_bytes(of)
+    n = len(want)
+    # SumcheckProof bytes = claimed || u32 rounds || 4w per round || u32 finals || finals (sumcheck.hpp:51-61)
+    got = out[:w] + vars_.to_bytes(4, "little") + out[w:] + (2 * n_pairs).to_bytes(4, "little") + fin.raw
+    assert got == want and len(got) == n
+    assert tr.state == otr.state
