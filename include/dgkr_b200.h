@@ -399,6 +399,15 @@ int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, size_t n_workers, size_t n_c
                 const uint8_t* rows, const uint8_t* r, size_t r_len, size_t spot_checks, uint8_t* roots_out,
                 size_t* n_roots, uint8_t* open_out, size_t cap, size_t* open_len, uint8_t* combined_out,
                 char* traffic_json, size_t json_cap);
+/* The same over several device contexts: cluster c is committed and opened
+ * on context c mod n_ctx, every cluster on its own lane (stream + host
+ * thread), so the K leaders hash and open concurrently (their transcripts
+ * are independent, cluster.hpp:445-449); the open reuses the matrix and the
+ * Merkle tree its commit built. Output bytes equal dgkr_distpc's. */
+int dgkr_distpc_multi(dgkr_ctx* const* ctxs, size_t n_ctx, const dgkr_field* f, size_t n_workers, size_t n_clusters,
+                      size_t row_vars, const uint8_t* rows, const uint8_t* r, size_t r_len, size_t spot_checks,
+                      uint8_t* roots_out, size_t* n_roots, uint8_t* open_out, size_t cap, size_t* open_len,
+                      uint8_t* combined_out, char* traffic_json, size_t json_cap);
 
 #ifdef __cplusplus
 }

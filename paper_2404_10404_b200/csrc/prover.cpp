@@ -1157,9 +1157,12 @@ std::size_t pcs_opening_size(std::size_t w, std::size_t r_len, std::size_t rows,
 /// pcs::open (pcs.hpp:212-254), written straight into `out` (cap bytes):
 /// the combined row lands in place by one D2H and is absorbed from there.
 /// Returns the opening's length.
+/// resident: d.m and d.nodes already hold this matrix and its tree (the
+/// commit of the same rows just before, as in DistPc::commit -> open); the
+/// reference rebuilds them (pcs.hpp:241-244), which gives the same bytes.
 std::size_t pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t rows, std::size_t cols,
                      const std::uint8_t* data, const std::vector<U256>& r, std::size_t q, Transcript& tr,
-                     U256* value_out, std::uint8_t* out, std::size_t cap) {
+                     U256* value_out, std::uint8_t* out, std::size_t cap, bool resident = false) {
     check_matrix(rows, cols);
     const HostField& F = f->f;
     const FieldKind kind = ctx->use(f);
@@ -1168,37 +1171,41 @@ std::size_t pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t r
     if (r.size() != row_vars + index_vars) fail(DGKR_INVALID_ARGUMENT, "opening point has wrong dimension");
     const std::size_t total = pcs_opening_size(w, r.size(), rows, cols, q);
     if (total > cap) fail(DGKR_CAPACITY, "output buffer too small");
-    d.m.ensure(rows * cols);
-    ctx->upload_elems(f, data, rows * cols, d.m.p, d.stage);
+    if (!resident) {
+        d.m.ensure(rows * cols);
+        ctx->upload_elems(f, data, rows * cols, d.m.p, d.stage);
+    }
     std::vector<U256> r_low(r.begin(), r.begin() + row_vars), r_high(r.begin() + row_vars, r.end());
     std::vector<U256> beta(rows);
     for (std::size_t i = 0; i < rows; ++i) beta[i] = chi_eval_host(i, r_high, F);  // pcs.hpp:161-170
-    // row evaluations (dense MLE at r_low) with split-eq tables
-    DBuf<Fe> eqt;
-    DBuf<EqJob> jobs;
-    eqt.ensure(2 * ((std::size_t{1} << ((row_vars + 1) / 2)) + (std::size_t{1} << (row_vars / 2))) + 8);
-    SplitEq e = build_split_eq(ctx, f, {r_low}, {F.one()}, eqt.p, jobs, 16);
-    std::vector<U256> row_evals(rows);
-    U256 value{};
+    // row evaluations (dense MLE at r_low, split-eq tables): one launch per
+    // row, each result copied out behind its launch, one sync for all rows
+    d.eqt.ensure(2 * ((std::size_t{1} << ((row_vars + 1) / 2)) + (std::size_t{1} << (row_vars / 2))) + 8);
+    SplitEq e = build_split_eq(ctx, f, {r_low}, {F.one()}, d.eqt.p, d.jobs, 16);
+    if (rows > Lane::kGatherOff - Lane::kFinalsOff) fail(DGKR_UNSUPPORTED, "too many matrix rows");
+    Fe* hre = ctx->h_small + Lane::kFinalsOff;
     for (std::size_t i = 0; i < rows; ++i) {
         launch_dense_eval(kind, d.m.p + i * cols, cols, e, ctx->ws, ctx->st);
         ctx->launched();
-        ctx->d2h(ctx->h_small + 1, ctx->ws.result, sizeof(Fe));
-        ctx->sync();
-        row_evals[i] = to_u256(ctx->h_small[1]);
-        value = F.add(value, F.mul(beta[i], row_evals[i]));
+        ctx->d2h(hre + i, ctx->ws.result, sizeof(Fe));
     }
     // combined row (pcs.hpp:233-239)
-    DBuf<Fe> comb, dbeta;
-    comb.ensure(cols);
-    dbeta.ensure(rows);
+    d.comb.ensure(cols);
+    d.beta.ensure(rows);
     std::vector<Fe> hb(rows);
     for (std::size_t i = 0; i < rows; ++i) hb[i] = to_fe(beta[i]);
-    ctx->h2d(dbeta.p, hb.data(), rows * sizeof(Fe));
-    launch_beta_combine(kind, d.m.p, cols, static_cast<int>(rows), dbeta.p, comb.p, ctx->st);
+    ctx->h2d(d.beta.p, hb.data(), rows * sizeof(Fe));
+    launch_beta_combine(kind, d.m.p, cols, static_cast<int>(rows), d.beta.p, d.comb.p, ctx->st);
     ctx->launched();
     // leaves + tree (pcs.hpp:241-244)
-    pcs_build_tree(ctx, f, d, rows, cols);
+    if (!resident) pcs_build_tree(ctx, f, d, rows, cols);
+    ctx->sync();
+    std::vector<U256> row_evals(rows);
+    U256 value{};
+    for (std::size_t i = 0; i < rows; ++i) {
+        row_evals[i] = to_u256(hre[i]);
+        value = F.add(value, F.mul(beta[i], row_evals[i]));
+    }
     // Opening::to_bytes head (pcs.hpp:135-156): |r|, r, value, M, row evals, cols, combined row
     std::size_t pos = 0;
     auto put_u32 = [&](std::uint32_t v) {
@@ -1216,9 +1223,9 @@ std::size_t pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t r
     put_u32(static_cast<std::uint32_t>(cols));
     std::uint8_t* combined = out + pos;
     d.stage.ensure(cols * w);
-    launch_to_canonical(kind, comb.p, d.stage.p, static_cast<int>(w), cols, ctx->st);
+    launch_to_canonical(kind, d.comb.p, d.stage.p, static_cast<int>(w), cols, ctx->st);
     ctx->launched();
-    ctx->d2h(combined, d.stage.p, cols * w);
+    ctx->d2h_large(combined, d.stage.p, cols * w);
     pos += cols * w;
     Digest root;
     ctx->d2h(root.data(), d.nodes.p + 32, 32);
@@ -1244,22 +1251,34 @@ std::size_t pcs_open(Lane* ctx, const dgkr_field* f, PcsDevice& d, std::size_t r
         }
     }
     ctx->prof.host_transcript_ms += now_ms() - t0;
-    // spot checks: column + Merkle path (merkle.hpp:34-45) each
+    // spot checks: column + Merkle path (merkle.hpp:34-45) each; all path
+    // digests gathered on the device into one buffer, one copy back
+    const std::size_t depth = log2_exact(cols);
+    std::vector<std::uint64_t> nodes;
+    nodes.reserve(idx.size() * depth);
+    for (std::uint64_t j : idx)
+        for (std::size_t node = cols + j; node > 1; node >>= 1) nodes.push_back(node ^ 1);
+    std::vector<std::uint8_t> paths(nodes.size() * 32);
+    if (!nodes.empty()) {
+        d.path_idx.ensure(nodes.size());
+        d.path_out.ensure(nodes.size() * 32);
+        ctx->h2d(d.path_idx.p, nodes.data(), nodes.size() * sizeof(std::uint64_t));
+        launch_gather32(d.nodes.p, d.path_idx.p, nodes.size(), d.path_out.p, ctx->st);
+        ctx->launched();
+        ctx->d2h(paths.data(), d.path_out.p, paths.size());
+        ctx->sync();
+    }
     put_u32(static_cast<std::uint32_t>(idx.size()));
-    for (std::uint64_t j : idx) {
+    for (std::size_t s = 0; s < idx.size(); ++s) {
+        const std::uint64_t j = idx[s];
         put_u32(static_cast<std::uint32_t>(j));
         for (std::size_t i = 0; i < rows; ++i) {
             std::memcpy(out + pos, data + (i * cols + j) * w, w);
             pos += w;
         }
-        std::size_t node = cols + j;
-        while (node > 1) {
-            ctx->d2h(out + pos, d.nodes.p + (node ^ 1) * 32, 32);
-            pos += 32;
-            node >>= 1;
-        }
+        std::memcpy(out + pos, paths.data() + s * depth * 32, depth * 32);
+        pos += depth * 32;
     }
-    ctx->sync();
     if (pos != total) fail(DGKR_LOGIC_ERROR, "opening size mismatch");
     if (value_out) *value_out = value;
     return pos;
@@ -2675,62 +2694,104 @@ int dgkr_dist_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers
     });
 }
 
-int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::size_t n_clusters,
-                std::size_t row_vars, const std::uint8_t* rows, const std::uint8_t* r, std::size_t r_len,
-                std::size_t q, std::uint8_t* roots_out, std::size_t* n_roots, std::uint8_t* open_out, std::size_t cap,
-                std::size_t* open_len, std::uint8_t* combined_out, char* traffic_json, std::size_t json_cap) {
+/// DistPc::commit + open (cluster.hpp:336-412) over the K = plan(N) clusters,
+/// spread over the given contexts (devices): cluster c runs on context
+/// c mod n_ctx, on its own lane (stream + host thread), so clusters commit
+/// and open concurrently -- the leaders hash in parallel and the K opening
+/// transcripts (independent by construction, cluster.hpp:445-449) run on K
+/// host threads. Member rows land in the leader's device buffer (the
+/// mempool, metered as mempool bytes, cluster.hpp:349-361); the open reuses
+/// the matrix and tree its commit built.
+int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field* f, std::size_t n_workers,
+                      std::size_t n_clusters, std::size_t row_vars, const std::uint8_t* rows, const std::uint8_t* r,
+                      std::size_t r_len, std::size_t q, std::uint8_t* roots_out, std::size_t* n_roots,
+                      std::uint8_t* open_out, std::size_t cap, std::size_t* open_len, std::uint8_t* combined_out,
+                      char* traffic_json, std::size_t json_cap) {
     return guard([&] {
-        ctx->begin_call();
-        CK(cudaSetDevice(ctx->device));
+        if (!ctxs || n_ctx == 0) fail(DGKR_INVALID_ARGUMENT, "no device context");
+        for (std::size_t i = 0; i < n_ctx; ++i) ctxs[i]->begin_call();
         const HostField& F = f->f;
         const std::size_t K = plan_clusters(n_workers, n_clusters);
         const std::size_t M = n_workers / K;
+        if (row_vars > 40) fail(DGKR_INVALID_ARGUMENT, "rows too large");
         const std::size_t cols = std::size_t{1} << row_vars;
         const std::size_t w = F.width();
         const std::size_t row_bytes = cols * w;
-        Traffic ts;
-        ts.cur = "commit";
-        // mempool writes (cluster.hpp:349-361): every worker row lands in its
-        // cluster leader's buffer; rows of one cluster are contiguous here.
-        for (std::size_t i = 0; i < n_workers; ++i) {
-            for (std::size_t e = 0; e < cols; ++e) F.from_bytes(rows + i * row_bytes + e * w);
-            ts.mempool(row_bytes);
-        }
-        auto& dev = ctx->nttws().pcs_clusters;
-        while (dev.size() < K) dev.push_back(std::make_unique<PcsDevice>());
-        for (std::size_t c = 0; c < K; ++c) {
-            const Digest root = pcs_commit(ctx, f, *dev[c], M, cols, rows + c * M * row_bytes);
-            std::memcpy(roots_out + 32 * c, root.data(), 32);
-            ts.msg(c * M, 0, 0, 32);
-        }
-        *n_roots = K;
-        ts.cur = "open";
         std::size_t member_vars = log2_exact(M), cluster_vars = log2_exact(K);
         if (r_len != row_vars + member_vars + cluster_vars) fail(DGKR_INVALID_ARGUMENT, "opening point has wrong dimension");
         std::vector<U256> pt(r_len);
         for (std::size_t i = 0; i < r_len; ++i) pt[i] = F.from_bytes(r + i * w);
-        std::vector<U256> r_local(pt.begin(), pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars));
-        std::vector<U256> r_top(pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars), pt.end());
+        const std::vector<U256> r_local(pt.begin(), pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars));
+        const std::vector<U256> r_top(pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars), pt.end());
+        const std::size_t osz = pcs_opening_size(w, r_local.size(), M, cols, q);
+        std::vector<std::vector<std::uint8_t>> ops(K, std::vector<std::uint8_t>(osz));
+        std::vector<std::size_t> op_len(K, 0);
+        std::vector<U256> values(K);
+        std::vector<Digest> roots(K);
+        std::vector<int> codes(K, DGKR_OK);
+        std::vector<std::string> errs(K);
+        // cluster c -> (context c mod n_ctx, lane c / n_ctx); a worker thread per lane
+        const std::size_t n_threads = std::min<std::size_t>(K, std::max<std::size_t>(n_ctx, std::min<std::size_t>(K, 16)));
+        auto work = [&](std::size_t th) {
+            for (std::size_t c = th; c < K; c += n_threads) {
+                try {
+                    dgkr_ctx* cx = ctxs[c % n_ctx];
+                    CK(cudaSetDevice(cx->device));
+                    Lane* L = cx->lane(static_cast<int>((c / n_ctx) % 16));
+                    PcsDevice& d = L->nttws().pcs;
+                    const std::uint8_t* mine = rows + c * M * row_bytes;  // the cluster's mempool
+                    roots[c] = pcs_commit(L, f, d, M, cols, mine);
+                    Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
+                    tr.absorb_u64(c);
+                    op_len[c] = pcs_open(L, f, d, M, cols, mine, r_local, q, tr, &values[c], ops[c].data(), osz, true);
+                } catch (const Error& e) {
+                    codes[c] = e.code;
+                    errs[c] = e.what();
+                } catch (const std::exception& e) {
+                    codes[c] = DGKR_LOGIC_ERROR;
+                    errs[c] = e.what();
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (std::size_t t = 1; t < n_threads; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& t : pool) t.join();
+        for (std::size_t c = 0; c < K; ++c)
+            if (codes[c] != DGKR_OK) fail(codes[c], "cluster " + std::to_string(c) + ": " + errs[c]);
+        // TrafficStats in the reference's order (cluster.hpp:349-361, :368-371, :402-404)
+        Traffic ts;
+        ts.cur = "commit";
+        for (std::size_t i = 0; i < n_workers; ++i) ts.mempool(row_bytes);
+        for (std::size_t c = 0; c < K; ++c) {
+            std::memcpy(roots_out + 32 * c, roots[c].data(), 32);
+            ts.msg(c * M, 0, 0, 32);
+        }
+        *n_roots = K;
+        ts.cur = "open";
         std::vector<std::uint8_t> all;
         U256 combined{};
         for (std::size_t c = 0; c < K; ++c) {
-            Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
-            tr.absorb_u64(c);
-            U256 value;
-            const std::size_t osz = pcs_opening_size(w, r_local.size(), M, cols, q);
-            const std::size_t at = all.size();
-            all.resize(at + 4 + osz);
-            const std::size_t n_op =
-                pcs_open(ctx, f, *dev[c], M, cols, rows + c * M * row_bytes, r_local, q, tr, &value, all.data() + at + 4, osz);
-            for (int i = 0; i < 4; ++i) all[at + i] = static_cast<std::uint8_t>(n_op >> (8 * i));
+            const std::size_t n_op = op_len[c];
+            for (int i = 0; i < 4; ++i) all.push_back(static_cast<std::uint8_t>(n_op >> (8 * i)));
+            all.insert(all.end(), ops[c].begin(), ops[c].begin() + static_cast<std::ptrdiff_t>(n_op));
             ts.msg(c * M, 0, 0, n_op);
-            combined = F.add(combined, F.mul(chi_eval_host(c, r_top, F), value));
+            combined = F.add(combined, F.mul(chi_eval_host(c, r_top, F), values[c]));
         }
         F.to_bytes(combined, combined_out);
         write_json(ts.json(), traffic_json, json_cap);
-        ctx->end_call();
+        for (std::size_t i = 0; i < n_ctx; ++i) ctxs[i]->end_call();
         emit(all, open_out, cap, open_len);
     });
+}
+
+int dgkr_distpc(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers, std::size_t n_clusters,
+                std::size_t row_vars, const std::uint8_t* rows, const std::uint8_t* r, std::size_t r_len,
+                std::size_t q, std::uint8_t* roots_out, std::size_t* n_roots, std::uint8_t* open_out, std::size_t cap,
+                std::size_t* open_len, std::uint8_t* combined_out, char* traffic_json, std::size_t json_cap) {
+    dgkr_ctx* one[1] = {ctx};
+    return dgkr_distpc_multi(one, 1, f, n_workers, n_clusters, row_vars, rows, r, r_len, q, roots_out, n_roots,
+                             open_out, cap, open_len, combined_out, traffic_json, json_cap);
 }
 
 }  // extern "C"

@@ -169,6 +169,10 @@ struct PcsDevice {
     DBuf<Fe> m;                // rows x cols Montgomery
     DBuf<std::uint8_t> nodes;  // 2*cols digests
     DBuf<std::uint8_t> stage;
+    DBuf<Fe> comb, beta, eqt;  // open: combined row, beta weights, split-eq tables
+    DBuf<EqJob> jobs;
+    DBuf<std::uint64_t> path_idx;  // open: node indexes of every spot check's Merkle path
+    DBuf<std::uint8_t> path_out;
 };
 
 /// device buffers of the NTT / RS / FRI entry points, kept across calls
@@ -181,9 +185,8 @@ struct NttWs {
     DBuf<std::uint64_t> didx;
     // beacon tree (config C3)
     DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
-    // polynomial commitment (pcs_commit / pcs_open) and DistPc's clusters
+    // polynomial commitment (pcs_commit / pcs_open; a DistPc cluster on this lane)
     PcsDevice pcs;
-    std::vector<std::unique_ptr<PcsDevice>> pcs_clusters;
 };
 
 /// Combining scheduler for the serial output absorbs of concurrent proofs

@@ -628,10 +628,11 @@ def dist_sumcheck(ctx: Context, n_workers: int, pairs, tr: Transcript):
     return out.raw[: ln.value], js.value.decode()
 
 
-def distpc(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], spot_checks: int = 32,
+def distpc(ctx, field: Field, rows: Sequence[Elems], r: Sequence[int], spot_checks: int = 32,
            n_clusters: int = 0):
     """DistPc::commit + open (cluster.hpp:336-412) -> (roots, cluster opening
-    bytes, combined value, TrafficStats json)"""
+    bytes, combined value, TrafficStats json). ctx: a Context, or a list of
+    Contexts (one per device) the clusters are spread over (dgkr_distpc_multi)."""
     N = len(rows)
     data = b"".join(field.encode(x) for x in rows)
     cols = len(field.encode(rows[0])) // field.width
@@ -642,10 +643,12 @@ def distpc(ctx: Context, field: Field, rows: Sequence[Elems], r: Sequence[int], 
     out, ln = _out(cap)
     comb = C.create_string_buffer(field.width)
     js = C.create_string_buffer(8192)
-    check(lib().dgkr_distpc(ctx.handle, field.handle, C.c_size_t(N), C.c_size_t(n_clusters), C.c_size_t(row_vars),
-                            C.c_char_p(data), C.c_char_p(field.encode(r)), C.c_size_t(len(r)),
-                            C.c_size_t(spot_checks), roots, C.byref(nr), out, C.c_size_t(cap), C.byref(ln), comb, js,
-                            C.c_size_t(8192)))
+    ctxs = list(ctx) if isinstance(ctx, (list, tuple)) else [ctx]
+    handles = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+    check(lib().dgkr_distpc_multi(handles, C.c_size_t(len(ctxs)), field.handle, C.c_size_t(N), C.c_size_t(n_clusters),
+                                  C.c_size_t(row_vars), C.c_char_p(data), C.c_char_p(field.encode(r)),
+                                  C.c_size_t(len(r)), C.c_size_t(spot_checks), roots, C.byref(nr), out, C.c_size_t(cap),
+                                  C.byref(ln), comb, js, C.c_size_t(8192)))
     raw = out.raw[: ln.value]
     ops = []
     pos = 0

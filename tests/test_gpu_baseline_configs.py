@@ -167,3 +167,22 @@ def test_c5_distpc_n8_equals_reference(ctx):
     assert ops == w_ops
     assert comb == w_comb
     assert R.traffic_json_equal(js, w_js)
+
+
+@pytest.mark.parametrize("n_ctx", [2, 3])
+def test_c5_distpc_multi_context_equals_reference(ctx, n_ctx):
+    """clusters spread over several contexts (dgkr_distpc_multi; cluster c on
+    context c mod n_ctx, concurrently): the bytes of the single-context run and
+    of the reference"""
+    f = P.Field.bn254()
+    n_workers, row_vars = 8, 12
+    raw = W.random_inputs(f.p, n_workers << row_vars, 6)
+    rows = [FLD.elems_from_bytes(raw[i * (32 << row_vars):(i + 1) * (32 << row_vars)].tobytes())
+            for i in range(n_workers)]
+    r = O.random_elements(FLD, row_vars + 3, np.random.default_rng(10))
+    ctxs = [ctx] + [P.Context(0) for _ in range(n_ctx - 1)]
+    got = P.distpc(ctxs, f, rows, r)
+    want = R.distpc(FLD, rows, r)
+    assert got[0] == want[0] and got[1] == want[1] and got[2] == want[2]
+    assert R.traffic_json_equal(got[3], want[3])
+    assert P.distpc(ctx, f, rows, r, n_clusters=8)[0] == R.distpc(FLD, rows, r, k=8)[0]
