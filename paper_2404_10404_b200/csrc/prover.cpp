@@ -1631,7 +1631,7 @@ int dgkr_pairsum_total(dgkr_pairsum* s, std::uint8_t* out) {
         Lane* L = s->ctx;
         CK(cudaSetDevice(L->device));
         U256 tot{};
-        if (s->vars_left == 0) {  // 1-element tables: the finals
+        if (!s->finals.empty()) {  // folded down to the final values
             for (int k = 0; k < s->np; ++k) tot = s->f->f.add(tot, s->f->f.mul(s->finals[2 * k], s->finals[2 * k + 1]));
         } else {  // sum_k sum_b f_k(b) g_k(b) (:177-186; layout-independent)
             launch_pair_total(L->use(s->f), s->cur, s->np, s->size, L->ws, L->st);
