@@ -1134,13 +1134,28 @@ __global__ void __launch_bounds__(kThreads) k_bitrev_scale(const Fe* __restrict_
 // a chunk are exactly the inputs of its first b butterfly levels.
 constexpr int kNttLocalLog = 10;
 
+// The chunk (2^b consecutive elements, 32 KB at b = 10) is staged into shared
+// memory by one bulk asynchronous copy (cp.async.bulk global->shared, TMA
+// engine, completion on an mbarrier) instead of per-thread loads, and
+// written back by one bulk copy shared->global after the butterflies.
 template <class F>
 __global__ void __launch_bounds__(512) k_ntt_local(Fe* a, int log_n, int b, const Fe* __restrict__ tw) {
     extern __shared__ Fe sm[];
+    __shared__ std::uint64_t bar;
     const std::uint64_t m = std::uint64_t{1} << b;
     Fe* chunk = a + blockIdx.x * m;
-    for (std::uint64_t i = threadIdx.x; i < m; i += blockDim.x) sm[i] = fe_load(chunk + i);
+    const std::uint32_t bytes = static_cast<std::uint32_t>(m * sizeof(Fe));
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&bar, bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sm)),
+            "l"(chunk), "r"(bytes), "r"(smem_u32(&bar))
+            : "memory");
+    }
     __syncthreads();
+    mbar_wait(&bar, 0);
     for (int s = 1; s <= b; ++s) {
         const std::uint64_t half = std::uint64_t{1} << (s - 1);
         for (std::uint64_t t = threadIdx.x; t < m / 2; t += blockDim.x) {
@@ -1153,7 +1168,15 @@ __global__ void __launch_bounds__(512) k_ntt_local(Fe* a, int log_n, int b, cons
         }
         __syncthreads();
     }
-    for (std::uint64_t i = threadIdx.x; i < m; i += blockDim.x) fe_store(chunk + i, sm[i]);
+    if (threadIdx.x == 0) {
+        // the generic-proxy butterfly writes before the async-proxy bulk store
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(chunk), "r"(smem_u32(sm)),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // complete before the CTA (and its smem) retires
+    }
 }
 
 template <class F>

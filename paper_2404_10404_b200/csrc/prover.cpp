@@ -2724,7 +2724,9 @@ int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field
         const std::vector<U256> r_local(pt.begin(), pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars));
         const std::vector<U256> r_top(pt.begin() + static_cast<std::ptrdiff_t>(row_vars + member_vars), pt.end());
         const std::size_t osz = pcs_opening_size(w, r_local.size(), M, cols, q);
-        std::vector<std::vector<std::uint8_t>> ops(K, std::vector<std::uint8_t>(osz));
+        // every cluster opening has the same size: written in place, u32 length first
+        *open_len = K * (4 + osz);
+        if (*open_len > cap) fail(DGKR_CAPACITY, "output buffer too small");
         std::vector<std::size_t> op_len(K, 0);
         std::vector<U256> values(K);
         std::vector<Digest> roots(K);
@@ -2743,7 +2745,9 @@ int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field
                     roots[c] = pcs_commit(L, f, d, M, cols, mine);
                     Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
                     tr.absorb_u64(c);
-                    op_len[c] = pcs_open(L, f, d, M, cols, mine, r_local, q, tr, &values[c], ops[c].data(), osz, true);
+                    std::uint8_t* dst = open_out + c * (4 + osz);
+                    op_len[c] = pcs_open(L, f, d, M, cols, mine, r_local, q, tr, &values[c], dst + 4, osz, true);
+                    for (int i = 0; i < 4; ++i) dst[i] = static_cast<std::uint8_t>(op_len[c] >> (8 * i));
                 } catch (const Error& e) {
                     codes[c] = e.code;
                     errs[c] = e.what();
@@ -2769,19 +2773,14 @@ int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field
         }
         *n_roots = K;
         ts.cur = "open";
-        std::vector<std::uint8_t> all;
         U256 combined{};
         for (std::size_t c = 0; c < K; ++c) {
-            const std::size_t n_op = op_len[c];
-            for (int i = 0; i < 4; ++i) all.push_back(static_cast<std::uint8_t>(n_op >> (8 * i)));
-            all.insert(all.end(), ops[c].begin(), ops[c].begin() + static_cast<std::ptrdiff_t>(n_op));
-            ts.msg(c * M, 0, 0, n_op);
+            ts.msg(c * M, 0, 0, op_len[c]);
             combined = F.add(combined, F.mul(chi_eval_host(c, r_top, F), values[c]));
         }
         F.to_bytes(combined, combined_out);
         write_json(ts.json(), traffic_json, json_cap);
         for (std::size_t i = 0; i < n_ctx; ++i) ctxs[i]->end_call();
-        emit(all, open_out, cap, open_len);
     });
 }
 
