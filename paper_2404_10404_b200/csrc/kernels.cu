@@ -1001,21 +1001,25 @@ __global__ void __launch_bounds__(kThreads) k_beacon_verify(const std::uint8_t* 
         std::uint64_t node = idx[i];
         if (a < 64 && (node >> a) != 0) good = false;
         if (good) {
-            for (int k = 0; k < a; ++k) {
-                uint32_t s[8], t[8];
-                load_digest_words(sib + (i * a + k) * 32, s);
-                if (node & 1) hash_pair_words(s, h, t);
-                else hash_pair_words(h, s, t);
+            // one hash call site for both the active levels (sibling from the
+            // path, order by the node bit) and the zero-cache levels above the
+            // active subtree (beacon.hpp:159-178): a single inlined compression
+            // pair keeps the loop body in the instruction cache
+#pragma unroll 1
+            for (int k = 0; k < depth; ++k) {
+                uint32_t s[8], l[8], r[8], t[8];
+                const bool active = k < a;
+                load_digest_words(active ? sib + (i * a + k) * 32 : zc + 32 * k, s);
+                const bool right = active && (node & 1);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    l[j] = right ? s[j] : h[j];
+                    r[j] = right ? h[j] : s[j];
+                }
+                hash_pair_words(l, r, t);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) h[j] = t[j];
-                node >>= 1;
-            }
-            for (int k = a; k < depth; ++k) {
-                uint32_t z[8], t[8];
-                load_digest_words(zc + 32 * k, z);
-                hash_pair_words(h, z, t);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) h[j] = t[j];
+                if (active) node >>= 1;
             }
             uint32_t rt[8];
             load_digest_words(root, rt);
