@@ -388,9 +388,13 @@ def run_b200(args, cfg_name):
                      "traffic": traffic, "traffic_over_algorithmic": traffic_ratio, "peak_source": peak_src,
                      "note": "algorithmic bytes: fold reads 4 + writes 2 elements (32 B) per table per output pair"},
         "roofline_int": {"bound": "imad", "kernel": "k_round (fused fold+round)",
-                         "achieved": achieved_mps, "peak": mp.value, "unit": "BN254 mont-mul/s",
-                         "frac": (achieved_mps / mp.value) if achieved_mps else None,
-                         "peak_source": "measured: dgkr_bench_mul_peak (4 independent CIOS chains/thread)"},
+                         "achieved": achieved_mps, "unit": "BN254 mont-mul/s",
+                         "peak": HW_MUL_PEAK, "frac": (achieved_mps / HW_MUL_PEAK) if achieved_mps else None,
+                         "peak_source": HW_MUL_PEAK_SOURCE,
+                         "own_multiplier_peak": mp.value,
+                         "own_multiplier_frac": (achieved_mps / mp.value) if achieved_mps else None,
+                         "own_multiplier_source": "dgkr_bench_mul_peak: this repo's CIOS, 4 independent chains/thread "
+                                                  "(a software ceiling, not the hardware's)"},
         "roofline_proof": proof_roofline(n_copies, lw, depth, ms_per_step / lanes, mp.value),
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -402,6 +406,16 @@ def run_b200(args, cfg_name):
     return 0
 
 
+# Hardware integer roofline for BN254 Montgomery products: the IMAD issue rate
+# probed on this B200 (1.857e13 IMAD/s = 63.85 per clock per SM at 1965 MHz,
+# profiles/mulbench_r1.jsonl) over SURVEY.md §8(d)'s 256 IMAD per product.
+IMAD_PER_S = 1.857e13
+HW_MUL_PEAK = IMAD_PER_S / 256
+HW_MUL_PEAK_SOURCE = ("probed IMAD issue rate 1.857e13/s (profiles/mulbench_r1.jsonl) / 256 IMAD per BN254 "
+                      "Montgomery product (SURVEY.md 8(d)); the SASS of this repo's CIOS has 232 IMAD, the "
+                      "constant-multiplier fold 140")
+
+
 def proof_roofline(n_copies, lw, depth, ms_per_proof, mul_peak):
     """Whole-proof integer roofline with SURVEY.md §8(d)'s algorithmic count:
     sum over layers of (K_l + 13) T_l + 3 W_l, plus the evaluate mul wires and
@@ -411,7 +425,9 @@ def proof_roofline(n_copies, lw, depth, ms_per_proof, mul_peak):
     mults = sum((1 if l == depth else 2) * T + 13 * T + 3 * T for l in range(1, depth + 1)) + depth * T // 2 + T
     achieved = mults / (ms_per_proof * 1e-3)
     return {"bound": "imad", "unit": "BN254 mont-mul/s", "algorithmic_mults_per_proof": mults,
-            "ms_per_proof": ms_per_proof, "achieved": achieved, "peak": mul_peak, "frac": achieved / mul_peak,
+            "ms_per_proof": ms_per_proof, "achieved": achieved, "peak": HW_MUL_PEAK, "frac": achieved / HW_MUL_PEAK,
+            "peak_source": HW_MUL_PEAK_SOURCE, "own_multiplier_peak": mul_peak,
+            "own_multiplier_frac": achieved / mul_peak,
             "note": "survey count treats every fold as a full Montgomery multiplication"}
 
 

@@ -143,10 +143,17 @@ struct ShmComm : dgkr_comm {
         L->h2d(d_recv, bounce, static_cast<std::size_t>(world) * bytes);
         L->sync();
     }
+    /// chunked through the slots when larger than one (the early-boundary table gather)
     void allgather_to_host(const void* d_send, void* h_recv, std::size_t bytes, Lane* L) override {
-        need(bytes);
-        stage_send(d_send, bytes, L);
-        for (int r = 0; r < world; ++r) std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes, slot(r), bytes);
+        const std::size_t chunk = hdr->slot_bytes;
+        std::size_t off = 0;
+        do {
+            const std::size_t nb = std::min(chunk, bytes - off);
+            stage_send(static_cast<const std::uint8_t*>(d_send) + off, nb, L);
+            for (int r = 0; r < world; ++r)
+                std::memcpy(static_cast<std::uint8_t*>(h_recv) + r * bytes + off, slot(r), nb);
+            off += nb;
+        } while (off < bytes);
     }
     /// chunked through the slots (the claimed outputs exceed a slot): the
     /// segment stays small however large a rank's share of the outputs is

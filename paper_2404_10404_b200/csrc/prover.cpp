@@ -85,6 +85,10 @@ struct SumcheckRun {
     std::vector<U256> challenges;
     std::vector<U256> finals;  // per table, Montgomery
     U256 claim_end{};          // p_last(r_last) when run with a known claim
+    // stopped early (stop_after < nv): the tables folded with every challenge
+    // so far, 2^(nv - stop_after) elements each, bit-reversed when tail_bitrev
+    std::vector<const Fe*> tail_tables;
+    bool tail_bitrev = false;
 };
 
 /// tables: device pointer array `base` of ntab = 2*np + has_g tables of
@@ -94,7 +98,18 @@ struct SumcheckRun {
 /// computed on the device); nullptr = derive every round from the tables.
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                        RoundBuffers& rb, Transcript& tr, dgkr_comm* comm = nullptr, const U256* claim = nullptr,
-                       const Fe* const* base_host = nullptr, bool r1_done = false);
+                       const Fe* const* base_host = nullptr, bool r1_done = false, int stop_after = -1);
+
+inline std::size_t brev_bits(std::size_t x, int bits) {
+    std::size_t r = 0;
+    for (int i = 0; i < bits; ++i, x >>= 1) r = (r << 1) | (x & 1);
+    return r;
+}
+
+/// distributed sum-checks switch to redundant per-rank rounds once a rank's
+/// live tables are this small (2^kEarlyLog): one all-gather of the tables
+/// replaces the remaining per-round exchanges (SURVEY §7 "early boundary")
+constexpr int kEarlyLog = 10;
 
 /// Distributed form (cluster.hpp:228-320 generalised to the layer
 /// sum-check): `nv` local variables per rank, rank = high variables. Local
@@ -109,37 +124,59 @@ SumcheckRun run_rounds_dist(Lane* ctx, const dgkr_field* f, int np, bool has_g, 
                             bool r1_done = false) {
     const int ntab = 2 * np + (has_g ? 1 : 0);
     const int world = comm->world;
-    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim, base_host, r1_done);
-    // boundary: gather every rank's final table values
-    std::vector<Fe> mine(ntab), all(static_cast<std::size_t>(world) * ntab);
-    for (int t = 0; t < ntab; ++t) mine[t] = to_fe(loc.finals[t]);
-    dt.mine.ensure(ntab);
-    ctx->h2d(dt.mine.p, mine.data(), ntab * sizeof(Fe));
-    comm->allgather_to_host(dt.mine.p, all.data(), ntab * sizeof(Fe), ctx);
-    // world-sized tables, rank index = position (natural order)
-    dt.tabs.ensure(static_cast<std::size_t>(ntab) * world);
-    std::vector<Fe> h(static_cast<std::size_t>(ntab) * world);
-    for (int t = 0; t < ntab; ++t)
-        for (int r = 0; r < world; ++r) h[static_cast<std::size_t>(t) * world + r] = all[static_cast<std::size_t>(r) * ntab + t];
-    ctx->h2d(dt.tabs.p, h.data(), h.size() * sizeof(Fe));
-    std::vector<const Fe*> hp(ntab);
-    for (int t = 0; t < ntab; ++t) hp[t] = dt.tabs.p + static_cast<std::size_t>(t) * world;
-    dt.ptrs.ensure(ntab);
-    ctx->h2d(dt.ptrs.p, hp.data(), ntab * sizeof(const Fe*));
     int lw = 0;
     while ((1 << lw) < world) ++lw;
-    const U256 mid = (nv > 0 || !claim) ? loc.claim_end : *claim;
-    SumcheckRun tail = run_rounds(ctx, f, np, has_g, lw, dt.ptrs.p, dt.rb, tr, nullptr, claim ? &mid : nullptr);
+    // local rounds with a per-round all-gather of the sums, until the live
+    // tables have 2^kb elements; then ONE all-gather of those tables and every
+    // rank finishes the last kb + log2(world) rounds on the rebuilt global
+    // tables (rank = high bits), identically (cluster.hpp:289-318 with the
+    // boundary moved down: the same rounds, sums and transcript)
+    const int kb = std::min(nv, kEarlyLog);
+    SumcheckRun loc = run_rounds(ctx, f, np, has_g, nv, base, rb, tr, comm, claim, base_host, r1_done, nv - kb);
+    const std::size_t lsz = std::size_t{1} << kb;
+    std::vector<const Fe*> src = loc.tail_tables;
+    if (src.empty()) {  // no local round ran: the base tables themselves (natural order)
+        src.resize(ntab);
+        if (base_host) std::copy(base_host, base_host + ntab, src.begin());
+        else CK(cudaMemcpy(src.data(), base, ntab * sizeof(const Fe*), cudaMemcpyDeviceToHost));
+    }
+    dt.mine.ensure(static_cast<std::size_t>(ntab) * lsz);
+    for (int t = 0; t < ntab; ++t)
+        CK(cudaMemcpyAsync(dt.mine.p + t * lsz, src[t], lsz * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->st));
+    std::vector<Fe> all(static_cast<std::size_t>(world) * ntab * lsz);
+    comm->allgather_to_host(dt.mine.p, all.data(), ntab * lsz * sizeof(Fe), ctx);
+    // world-sized tables in natural order: global index = rank * 2^kb + logical local index
+    const std::size_t gsz = lsz * static_cast<std::size_t>(world);
+    std::vector<Fe> h(static_cast<std::size_t>(ntab) * gsz);
+    for (int r = 0; r < world; ++r)
+        for (int t = 0; t < ntab; ++t)
+            for (std::size_t l = 0; l < lsz; ++l) {
+                const std::size_t st = loc.tail_bitrev ? brev_bits(l, kb) : l;
+                h[static_cast<std::size_t>(t) * gsz + r * lsz + l] = all[(static_cast<std::size_t>(r) * ntab + t) * lsz + st];
+            }
+    dt.tabs.ensure(h.size());
+    ctx->h2d(dt.tabs.p, h.data(), h.size() * sizeof(Fe));
+    std::vector<const Fe*> hp(ntab);
+    for (int t = 0; t < ntab; ++t) hp[t] = dt.tabs.p + static_cast<std::size_t>(t) * gsz;
+    dt.ptrs.ensure(ntab);
+    ctx->h2d(dt.ptrs.p, hp.data(), ntab * sizeof(const Fe*));
+    const U256 mid = (nv - kb > 0 || !claim) ? loc.claim_end : *claim;
+    SumcheckRun tail = run_rounds(ctx, f, np, has_g, kb + lw, dt.ptrs.p, dt.rb, tr, nullptr, claim ? &mid : nullptr,
+                                  hp.data());
     loc.rounds.insert(loc.rounds.end(), tail.rounds.begin(), tail.rounds.end());
     loc.challenges.insert(loc.challenges.end(), tail.challenges.begin(), tail.challenges.end());
     loc.finals = tail.finals;
     loc.claim_end = tail.claim_end;
+    loc.tail_tables.clear();
     return loc;
 }
 
 SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int nv, const Fe* const* base,
                        RoundBuffers& rb, Transcript& tr, dgkr_comm* comm, const U256* claim,
-                       const Fe* const* base_host, bool r1_done) {
+                       const Fe* const* base_host, bool r1_done, int stop_after) {
+    // stop_after in [0, nv): run rounds 1..stop_after only, then fold the
+    // tables with the last challenge (the next round's fold, its sums unused)
+    // and return them in tail_tables instead of finals
     // r1_done: round 1's (S0, S2) are already in ws.result (bookkeeping with
     // the first round fused, k_bookkeep_pairs); the round-1 launch is skipped
     const HostField& F = f->f;
@@ -156,7 +193,8 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     const Fe* const* cur_h = base_host;  // host mirror of cur (null: no TMA round kernel)
     const U256 zero{};
     U256 fk[9] = {};
-    for (int j = 1; j <= nv; ++j) {
+    const int n_rounds = (stop_after >= 0 && stop_after < nv) ? stop_after : nv;
+    for (int j = 1; j <= n_rounds; ++j) {
         RoundLaunch rl;
         rl.np = np;
         rl.has_g = has_g;
@@ -235,6 +273,30 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
     }
     out.claim_end = run_claim;
+    if (n_rounds < nv) {
+        if (n_rounds == 0) return out;  // the base tables, untouched (natural order)
+        // fold with r_{n_rounds}: the round kernel of round n_rounds + 1 (its sums are not used)
+        const int j = n_rounds + 1;
+        RoundLaunch rl;
+        rl.np = np;
+        rl.has_g = has_g;
+        rl.fold_const = fk;
+        rl.need_s1 = !skip_s1;
+        rl.mode = (j == 2) ? 1 : 2;
+        rl.in = cur;
+        rl.in_host = cur_h;
+        const Fe* const* nxt = (j % 2 == 0) ? rb.A() : rb.B();
+        const Fe* const* nxt_h = (j % 2 == 0) ? rb.hA() : rb.hB();
+        rl.out = const_cast<Fe* const*>(nxt);
+        rl.out_host = cur_h ? const_cast<Fe* const*>(nxt_h) : nullptr;
+        rl.n_out_pairs = size0 >> j;
+        if (rl.n_out_pairs <= tuning().small_round_pairs) launch_round_small(kind, rl, ctx->ws, ctx->st);
+        else launch_round(kind, rl, ctx->ws, ctx->st);
+        ctx->launched();
+        out.tail_tables.assign(nxt_h, nxt_h + ntab);
+        out.tail_bitrev = true;
+        return out;
+    }
     // final fold of the 2-element tables (or read the 1-element tables)
     if (nv >= 1) {
         launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);

@@ -57,10 +57,13 @@ class ShmComm:
             pass
 
 
-def slot_bytes_for(circuit: P.Circuit, field: P.Field, cap: int = 8 << 20) -> int:
-    """per-rank slot: one rank's claimed outputs, capped (larger exchanges are
-    chunked through the slot), at least 4 KiB for the per-round sums"""
-    return max(min(circuit.output_size * field.width, cap), 4096)
+def slot_bytes_for(circuit: P.Circuit, field: P.Field, cap: int = 1 << 20) -> int:
+    """per-rank slot of a lane's segment: 1 MiB. The claimed-output gather is
+    chunked through it (a C2 rank share is 2^22/N x 32 B), and it holds the
+    early-boundary table gather (up to 31 tables x 2^10 elements x 32 B,
+    prover.cpp kEarlyLog). 64 lanes x 8 ranks x 1 MiB = 512 MiB of /dev/shm."""
+    del circuit, field
+    return cap
 
 
 def prove_dist_stream(ctx: P.Context, comms: Sequence, circuit: P.Circuit, field: P.Field, n: int, label: str,
