@@ -209,39 +209,47 @@ __device__ __forceinline__ Fe fe_sub_lazy(const Fe& b, const Fe& a) {
     return r;
 }
 
-/// Montgomery product a*b*R^{-1} mod p, fully reduced: CIOS with 64-bit C
-/// partial products. ptxas lowers a*b+t+c to IMAD.WIDE plus one add, which
-/// measured 7% faster than PTX mad.lo/madc.hi carry chains (IMAD + IADD3.X
-/// per product): 4.53 vs 4.23e10 mul/s on B200,
-/// profiles/mulbench_r1.jsonl. Inputs may be < 2p (lazy differences): the
-/// running value stays < 4p and the result < 2p since 4p < R.
+// ---- even/odd carry-chain rows (n = 8 limbs; a row uses x[off], x[off+2], ...) ----
+// A row x[off + 2j] * y puts lo at acc[2j] and hi at acc[2j+1]: rows of even
+// and of odd limbs never overlap within themselves, so each is ONE PTX
+// mad/madc carry chain (IMAD / IMAD.X / IMAD.HI.X on the FMA pipe) instead of
+// 64-bit partial products plus carry adds on the ALU pipe. All asm is
+// volatile: the carry flag links consecutive statements.
+__device__ __forceinline__ void eo_mul_row(uint32_t acc[8], const uint32_t* x, int off, uint32_t y) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        asm volatile("mul.lo.u32 %0, %2, %3;\n\tmul.hi.u32 %1, %2, %3;"
+                     : "=r"(acc[2 * j]), "=r"(acc[2 * j + 1])
+                     : "r"(x[off + 2 * j]), "r"(y));
+}
+/// acc += row; the carry out of acc[7] is left in the carry flag
+__device__ __forceinline__ void eo_mad_row(uint32_t acc[8], const uint32_t* x, int off, uint32_t y) {
+    asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.cc.u32 %1, %2, %3, %1;"
+                 : "+r"(acc[0]), "+r"(acc[1])
+                 : "r"(x[off]), "r"(y));
+#pragma unroll
+    for (int j = 1; j < 4; ++j)
+        asm volatile("madc.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.cc.u32 %1, %2, %3, %1;"
+                     : "+r"(acc[2 * j]), "+r"(acc[2 * j + 1])
+                     : "r"(x[off + 2 * j]), "r"(y));
+}
+/// dst[k] = row + src[k + 2] (src[8], src[9] = 0) + the carry flag at dst[0];
+/// the carry out of dst[7] is 0 (every intermediate value is < 2^288)
+__device__ __forceinline__ void eo_madc_row_rshift(uint32_t dst[8], const uint32_t* x, int off, uint32_t y,
+                                                   const uint32_t src[8]) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        asm volatile("madc.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.cc.u32 %1, %2, %3, %5;"
+                     : "=r"(dst[2 * j]), "=r"(dst[2 * j + 1])
+                     : "r"(x[off + 2 * j]), "r"(y), "r"(src[2 * j + 2]), "r"(src[2 * j + 3]));
+    asm volatile("madc.lo.cc.u32 %0, %2, %3, 0;\n\tmadc.hi.u32 %1, %2, %3, 0;"
+                 : "=r"(dst[6]), "=r"(dst[7])
+                 : "r"(x[off + 6]), "r"(y));
+}
+
+/// R < 2p -> R mod p (one conditional subtraction)
 template <class F>
-__device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
-    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        uint64_t c = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[j] + c;
-            t[j] = static_cast<uint32_t>(s);
-            c = s >> 32;
-        }
-        uint64_t s = static_cast<uint64_t>(t[8]) + c;
-        t[8] = static_cast<uint32_t>(s);
-        t[9] = static_cast<uint32_t>(s >> 32);
-        const uint32_t m = t[0] * F::np0();
-        c = (static_cast<uint64_t>(m) * F::p(0) + t[0]) >> 32;
-#pragma unroll
-        for (int j = 1; j < 8; ++j) {
-            const uint64_t s2 = static_cast<uint64_t>(m) * F::p(j) + t[j] + c;
-            t[j - 1] = static_cast<uint32_t>(s2);
-            c = s2 >> 32;
-        }
-        s = static_cast<uint64_t>(t[8]) + c;
-        t[7] = static_cast<uint32_t>(s);
-        t[8] = t[9] + static_cast<uint32_t>(s >> 32);
-    }
+__device__ __forceinline__ Fe fe_reduce_once(const uint32_t (&t)[8]) {
     Fe d;
     uint32_t borrow;
     asm("sub.cc.u32  %0, %9, %17;\n\t"
@@ -263,6 +271,56 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
     return r;
 }
 
+/// Montgomery product a*b*R^{-1} mod p, fully reduced: CIOS with even/odd
+/// split carry chains. The running value is T = E + O * 2^32 (E holds limb
+/// columns 0..7, O columns 1..8); a row adds the even limbs' products into E
+/// and the odd limbs' into O, the Montgomery row m*p likewise, and the
+/// one-limb shift of CIOS is folded into the next row (O becomes E with E[1]
+/// added at column 0; the rest of E, two limbs down, is the addend of the
+/// next odd row). ~137 IMAD + ~51 ALU SASS instructions against ~232 + ~210
+/// for 64-bit C partial products: 6.74 vs 4.53e10 products/s on B200, bit-exact
+/// over 2^20 random products (tools/mulbench/eobench.cu, profiles/r2/eobench.txt).
+/// Inputs may be < 2p (lazy differences): T stays < 2^288 and the result < 2p
+/// before the final subtraction since 4p < R (p < 2^254).
+template <class F>
+__device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
+    uint32_t P[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) P[k] = F::p(k);
+    const uint32_t np0 = F::np0();
+    uint32_t E[8], O[8], N[8];
+    eo_mul_row(E, a.v, 0, b.v[0]);
+    eo_mul_row(O, a.v, 1, b.v[0]);
+    {
+        const uint32_t m = E[0] * np0;
+        eo_mad_row(E, P, 0, m);
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(O[7]));  // E's carry: column 8
+        eo_mad_row(O, P, 1, m);
+    }
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(O[0]) : "r"(E[1]));  // shift: E[1] to column 0
+        eo_madc_row_rshift(N, a.v, 1, b.v[i], E);                            // next O: odd row + E[k+2]
+        eo_mad_row(O, a.v, 0, b.v[i]);                                       // next E: old O + even row
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(N[7]));
+        const uint32_t m = O[0] * np0;
+        eo_mad_row(O, P, 0, m);
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(N[7]));
+        eo_mad_row(N, P, 1, m);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            E[k] = O[k];
+            O[k] = N[k];
+        }
+    }
+    uint32_t R[8];  // final shift: R = O + E >> 32
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(O[0]), "r"(E[1]));
+#pragma unroll
+    for (int k = 1; k < 7; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(O[k]), "r"(E[k + 1]));
+    asm volatile("addc.u32 %0, %1, 0;" : "=r"(R[7]) : "r"(O[7]));
+    return fe_reduce_once<F>(R);
+}
+
 /// Multiplication by a per-launch constant r (the sum-check challenge of a
 /// fold), BN254 only. With c_k = r * 2^(32k+64) * R^-1 mod p precomputed on
 /// the host,  mont(x, r) = x r R^-1 = 2^-64 * sum_k x_k c_k  (mod p):
@@ -279,20 +337,27 @@ struct FoldConst {
 };
 
 __device__ __forceinline__ Fe fe_mul_const_bn254(const Fe& x, const FoldConst& K) {
-    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    // S = sum_k x_k c_k: eight rows (multiplicand c_k, scalar x_k), all at
+    // column 0, accumulated as even/odd carry chains: E (columns 0..7) and
+    // O (columns 1..8) plus one carry limb o8 (column 9; S < 8 * 2^32 * p < 2^289)
+    uint32_t E[8], O[8], o8 = 0;
+    eo_mul_row(E, K.c[0].v, 0, x.v[0]);
+    eo_mul_row(O, K.c[0].v, 1, x.v[0]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        uint64_t c = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint64_t s = static_cast<uint64_t>(x.v[k]) * K.c[k].v[j] + t[j] + c;
-            t[j] = static_cast<uint32_t>(s);
-            c = s >> 32;
-        }
-        const uint64_t s = static_cast<uint64_t>(t[8]) + c;
-        t[8] = static_cast<uint32_t>(s);
-        t[9] += static_cast<uint32_t>(s >> 32);
+    for (int k = 1; k < 8; ++k) {
+        eo_mad_row(E, K.c[k].v, 0, x.v[k]);
+        asm volatile("addc.cc.u32 %0, %0, 0;\n\taddc.u32 %1, %1, 0;" : "+r"(O[7]), "+r"(o8));
+        eo_mad_row(O, K.c[k].v, 1, x.v[k]);
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(o8));
     }
+    // merge into t[0..9]: t = E + O * 2^32
+    uint32_t t[10];
+    t[0] = E[0];
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(t[1]) : "r"(E[1]), "r"(O[0]));
+#pragma unroll
+    for (int k = 2; k < 8; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(t[k]) : "r"(E[k]), "r"(O[k - 1]));
+    asm volatile("addc.cc.u32 %0, %2, 0;\n\taddc.u32 %1, %3, 0;" : "=r"(t[8]), "=r"(t[9]) : "r"(O[7]), "r"(o8));
+    // two Montgomery steps (S < 2^289 -> < 2^225 + p < 2p, p > 2^253 + 2^224)
 #pragma unroll
     for (int st = 0; st < 2; ++st) {
         const uint32_t m = t[0] * Bn254::np0();
@@ -309,26 +374,10 @@ __device__ __forceinline__ Fe fe_mul_const_bn254(const Fe& x, const FoldConst& K
         t[8] = static_cast<uint32_t>(s);
         t[9] = 0;
     }
-    Fe d;
-    uint32_t borrow;
-    asm("sub.cc.u32  %0, %9, %17;\n\t"
-        "subc.cc.u32 %1, %10, %18;\n\t"
-        "subc.cc.u32 %2, %11, %19;\n\t"
-        "subc.cc.u32 %3, %12, %20;\n\t"
-        "subc.cc.u32 %4, %13, %21;\n\t"
-        "subc.cc.u32 %5, %14, %22;\n\t"
-        "subc.cc.u32 %6, %15, %23;\n\t"
-        "subc.cc.u32 %7, %16, %24;\n\t"
-        "subc.u32    %8, 0, 0;"
-        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
-          "=r"(d.v[7]), "=r"(borrow)
-        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(Bn254::p(0)),
-          "r"(Bn254::p(1)), "r"(Bn254::p(2)), "r"(Bn254::p(3)), "r"(Bn254::p(4)), "r"(Bn254::p(5)), "r"(Bn254::p(6)),
-          "r"(Bn254::p(7)));
-    Fe r;
+    uint32_t r8[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r.v[j] = borrow ? t[j] : d.v[j];
-    return r;
+    for (int j = 0; j < 8; ++j) r8[j] = t[j];
+    return fe_reduce_once<Bn254>(r8);
 }
 
 /// mont(x, r) for a fold challenge: constant-multiplier path for BN254,
