@@ -321,6 +321,43 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
     return fe_reduce_once<F>(R);
 }
 
+/// CIOS with 64-bit C partial products and a 10-limb accumulator: valid for
+/// ANY a < 2^256 when b < p (the running value stays < 2^257), which the
+/// even/odd fe_mul (a, b < 2p) is not. Used by acc_reduce, whose 256-bit
+/// remainder is not reduced.
+template <class F>
+__device__ __forceinline__ Fe fe_mul_any(const Fe& a, const Fe& b) {
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = static_cast<uint32_t>(s >> 32);
+        const uint32_t m = t[0] * F::np0();
+        c = (static_cast<uint64_t>(m) * F::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s2 = static_cast<uint64_t>(m) * F::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s2);
+            c = s2 >> 32;
+        }
+        s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        t[8] = t[9] + static_cast<uint32_t>(s >> 32);
+    }
+    uint32_t r8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r8[j] = t[j];
+    return fe_reduce_once<F>(r8);
+}
+
 /// Multiplication by a per-launch constant r (the sum-check challenge of a
 /// fold), BN254 only. With c_k = r * 2^(32k+64) * R^-1 mod p precomputed on
 /// the host,  mont(x, r) = x r R^-1 = 2^-64 * sum_k x_k c_k  (mod p):
@@ -564,8 +601,8 @@ __device__ Fe acc_reduce(const Acc& acc) {
     }
     hi.v[0] = t[16];
     one_raw.v[0] = 1;
-    const Fe lo_red = fe_mul<F>(fe_mul<F>(lo, r2), one_raw);  // X_lo mod p
-    const Fe hi_r = fe_mul<F>(hi, r2);                        // x_8 R mod p
+    const Fe lo_red = fe_mul<F>(fe_mul_any<F>(lo, r2), one_raw);  // X_lo mod p (X_lo: any 256-bit value)
+    const Fe hi_r = fe_mul<F>(hi, r2);                            // x_8 R mod p
     return fe_add<F>(lo_red, hi_r);
 }
 

@@ -137,6 +137,71 @@ __global__ void k_check(const Fe* a, const Fe* b, int n, unsigned* bad, Fe* firs
     }
 }
 
+// the previous constant multiplier (64-bit C partial products), the reference for field.cuh's
+__device__ __forceinline__ Fe const_old(const Fe& x, const FoldConst& K) {
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(x.v[k]) * K.c[k].v[j] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        const uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] += static_cast<uint32_t>(s >> 32);
+    }
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+        const uint32_t m = t[0] * Bn254::np0();
+        uint64_t c = (static_cast<uint64_t>(m) * Bn254::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(m) * Bn254::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        s = static_cast<uint64_t>(t[9]) + (s >> 32);
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = 0;
+    }
+    uint32_t r8[8];
+    for (int j = 0; j < 8; ++j) r8[j] = t[j];
+    return fe_reduce_once<Bn254>(r8);
+}
+
+__constant__ uint32_t c_pow[8][8];  // canonical 2^(32k+64) mod p
+
+/// field.cuh fe_mul on lazy inputs in [0, 2p) vs fe_mul_any; field.cuh's
+/// constant multiplier vs const_old on any 256-bit x (challenge r = b[i])
+__global__ void k_check2(const Fe* a, const Fe* b, int n, unsigned* bad) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        // lazy operands: a + p, b + p when they stay below 2p
+        Fe la = a[i], lb = b[i];
+        if (i & 1) la = fe_sub_lazy<Bn254>(a[i], fe_zero());  // a + p
+        if (i & 2) lb = fe_sub_lazy<Bn254>(b[i], fe_zero());
+        const Fe x = fe_mul<Bn254>(la, lb), y = fe_mul_any<Bn254>(la, lb);
+        bool eq = true;
+        for (int k = 0; k < 8; ++k) eq &= x.v[k] == y.v[k];
+        FoldConst K;
+        for (int k = 0; k < 8; ++k) {
+            Fe pw;
+            for (int j = 0; j < 8; ++j) pw.v[j] = c_pow[k][j];
+            K.c[k] = fe_mul_any<Bn254>(b[i], pw);
+        }
+        K.r = b[i];
+        Fe xr = a[i];
+        xr.v[7] ^= (i & 4) ? 0xc0000000u : 0u;  // any 256-bit input
+        const Fe u = fe_mul_const_bn254(xr, K), v = const_old(xr, K);
+        for (int k = 0; k < 8; ++k) eq &= u.v[k] == v.v[k];
+        if (!eq) atomicAdd(bad, 1u);
+    }
+}
+
 template <int V>
 __global__ void __launch_bounds__(256) k_peak(int iters, Fe* sink, unsigned never) {
     Fe a[4], b;
@@ -185,6 +250,25 @@ int main() {
     unsigned bad = 0;
     CK(cudaMemcpy(&bad, dbad, sizeof(unsigned), cudaMemcpyDeviceToHost));
     std::printf("{\"check\": \"fe_mul_eo vs fe_mul on %d random products\", \"mismatches\": %u}\n", n, bad);
+    {
+        const uint32_t pw[8][8] = {
+            {0x00000000u, 0x00000000u, 0x00000001u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u},
+            {0x00000000u, 0x00000000u, 0x00000000u, 0x00000001u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u},
+            {0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000001u, 0x00000000u, 0x00000000u, 0x00000000u},
+            {0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000001u, 0x00000000u, 0x00000000u},
+            {0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000001u, 0x00000000u},
+            {0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000000u, 0x00000001u},
+            {0x4ffffffbu, 0xac96341cu, 0x9f60cd29u, 0x36fc7695u, 0x7879462eu, 0x666ea36fu, 0x9a07df2fu, 0x0e0a77c1u},
+            {0x15b8b9dau, 0x93e78865u, 0xb05ea154u, 0x16df2426u, 0x302ab839u, 0x1271b743u, 0xec6c226eu, 0x06bc037eu}};
+        CK(cudaMemcpyToSymbol(c_pow, pw, sizeof(pw)));
+        CK(cudaMemset(dbad, 0, sizeof(unsigned)));
+        k_check2<<<1184, 256>>>(da, db, n, dbad);
+        unsigned bad2 = 0;
+        CK(cudaMemcpy(&bad2, dbad, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        std::printf("{\"check\": \"field.cuh fe_mul on lazy [0,2p) operands vs 10-limb CIOS, and the constant "
+                    "multiplier vs the previous one on 256-bit inputs, %d cases\", \"mismatches\": %u}\n", n, bad2);
+        bad += bad2;
+    }
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int iters = 4096, blocks = sms * 8;
