@@ -292,9 +292,7 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
  * 256), "tma_min_pairs" = smallest round taking the TMA-staged round kernel
  * (default 0 = off: measured slower than the register-fed kernel on C2),
  * "fuse_round1" = 1 (default 0: measured slower) builds single-slot bookkeeping tables by row
- * pairs with round 1 of the phase fused in, "l2_prefetch" = 1 (default) has
- * each warp of the round kernel prefetch its next range of every table into
- * L2 (cp.async.bulk.prefetch.L2). Unknown names -> DGKR_INVALID_ARGUMENT. */
+ * pairs with round 1 of the phase fused in. Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);
 

@@ -111,21 +111,9 @@ __device__ __forceinline__ void block_sum_wide(Acc (&s)[K], Fe (&out)[K]) {
 #pragma unroll
             for (int k = 0; k < K; ++k) acc_add(s[k], acc_shfl_down(s[k], off));
         }
-        // lane k reduces accumulator k (the K reductions run side by side,
-        // not one after another in lane 0 while the CTA waits at the barrier)
-        __shared__ Fe red[K];
-        Acc mine;
-        acc_zero(mine);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const Acc b = acc_shfl(s[k], 0);
-            if (lane == k) mine = b;
-        }
-        if (lane < K) red[lane] = acc_reduce<F>(mine);
-        __syncwarp();
         if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) out[k] = red[k];
+            for (int k = 0; k < K; ++k) out[k] = acc_reduce<F>(s[k]);
         }
     }
     __syncthreads();
@@ -215,7 +203,6 @@ struct RoundParams {
     unsigned* counter;
     Fe* result;
     FoldConst k;                // fold challenge (kernel-parameter space: IMAD constant operands)
-    int prefetch;               // L2 bulk prefetch of the next grid-stride range (prefetch_next)
 };
 
 // Table layouts of the round engine (P = output pairs of this round):
@@ -292,37 +279,9 @@ __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i
     }
 }
 
-/// Lane 0 of each warp asks L2 for the warp's NEXT grid-stride range of every
-/// table (cp.async.bulk.prefetch.L2: no registers, no completion to wait for),
-/// so the loads of the next iteration hit L2 instead of paying the DRAM
-/// latency the fold rounds are bound by (ncu r2: long-scoreboard stalls).
-template <int MODE>
-__device__ __forceinline__ void prefetch_next(const RoundParams& a, int ntab, std::uint64_t i_next) {
-    if ((threadIdx.x & 31) != 0 || i_next >= a.n_out_pairs) return;
-    const std::uint64_t P = a.n_out_pairs;
-    const std::uint64_t cnt = P - i_next < 32 ? P - i_next : 32;  // warp-contiguous indexes
-    for (int t = 0; t < ntab; ++t) {
-        const Fe* src = a.in[t];
-        if (MODE == kScan) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + 2 * i_next),
-                         "r"(static_cast<unsigned>(cnt * 64)) : "memory");
-        } else if (MODE == kFoldNat) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + 4 * i_next),
-                         "r"(static_cast<unsigned>(cnt * 128)) : "memory");
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + i_next + q * P),
-                             "r"(static_cast<unsigned>(cnt * 32)) : "memory");
-        }
-    }
-}
-
 template <class F, int NP, bool HAS_G, int MODE, bool S1, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant__ RoundParams a) {
     constexpr int NS = S1 ? 3 : 2;
-    const int ntab = 2 * (NP > 0 ? NP : a.np) + (HAS_G ? 1 : 0);
-    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
     if constexpr (MODE == kScan && !S1) {
         // Round 1 (no fold): the two general products per index are the
         // whole cost, so the sums are kept unreduced (Acc) and reduced once
@@ -332,8 +291,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant_
 #pragma unroll
         for (int k = 0; k < NS; ++k) acc_zero(w[k]);
         for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-             i < a.n_out_pairs; i += stride) {
-            if (a.prefetch) prefetch_next<MODE>(a, ntab, (i & ~std::uint64_t{31}) + stride);
+             i < a.n_out_pairs; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
             round_body<F, NP, HAS_G, MODE, S1>(a, i, w);
         }
         Fe s[NS];
@@ -344,8 +302,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_round(const __grid_constant_
 #pragma unroll
         for (int k = 0; k < NS; ++k) s[k] = fe_zero();
         for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-             i < a.n_out_pairs; i += stride) {
-            if (a.prefetch) prefetch_next<MODE>(a, ntab, (i & ~std::uint64_t{31}) + stride);
+             i < a.n_out_pairs; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
             round_body<F, NP, HAS_G, MODE, S1>(a, i, s);
         }
         grid_finish<F, NS>(s, a.partials, a.counter, a.result);
@@ -1533,8 +1490,7 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0, 0, 1};  // fused round 1: measured slower on C2
-        if (const char* e = std::getenv("DGKR_L2_PREFETCH")) v.l2_prefetch = std::strtoull(e, nullptr, 10);
+        Tuning v{kSmallRoundPairs, 0, 0};  // fused round 1: measured slower on C2
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
@@ -1623,10 +1579,9 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
-    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}, 0};
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}};
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
-    p.prefetch = tuning().l2_prefetch ? 1 : 0;
     if (launch_round_tma(k, a, ws, lp, st)) return;
     const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
     // 2 CTAs/SM (<= 128 registers); forcing 3 (80 registers, small spill) measured no faster
@@ -1653,7 +1608,7 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
 void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
-    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}, 0};
+    RoundParams p{a.in, a.out, a.np, a.n_out_pairs, lp, ws.partials, ws.counter, ws.result, FoldConst{}};
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     const unsigned threads = a.n_out_pairs <= 32 ? 32u : (a.n_out_pairs <= 128 ? 128u : kThreads);

@@ -79,7 +79,6 @@ struct Tuning {
     std::uint64_t small_round_pairs;
     std::uint64_t tma_min_pairs;
     std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
-    std::uint64_t l2_prefetch;  // k_round: L2 bulk prefetch of the next grid-stride range
 };
 Tuning& tuning();
 

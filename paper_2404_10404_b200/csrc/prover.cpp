@@ -2657,7 +2657,6 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         if (n == "small_round_pairs") tuning().small_round_pairs = value;
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
-        else if (n == "l2_prefetch") tuning().l2_prefetch = value;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }
@@ -2668,7 +2667,6 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         if (n == "small_round_pairs") *value = tuning().small_round_pairs;
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
-        else if (n == "l2_prefetch") *value = tuning().l2_prefetch;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }
