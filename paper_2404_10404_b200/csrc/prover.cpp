@@ -936,8 +936,12 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             if (c.sub_size[l] != c.sub_size[0] || c.sub_size[l] != c.sub_padded[l])
                 fail(DGKR_INVALID_ARGUMENT, "distributed proving needs a uniform power-of-two layer width");
     }
-    if (inputs) evaluate_circuit(ctx, c, W, f, inputs);  // gkr.hpp:186
-    else evaluate_layers(ctx, c, W, f);
+    NvtxRange nv_prove("dgkr.gkr_prove");
+    {
+        NvtxRange nv("dgkr.evaluate");
+        if (inputs) evaluate_circuit(ctx, c, W, f, inputs);  // gkr.hpp:186
+        else evaluate_layers(ctx, c, W, f);
+    }
 
     // absorb the padded output table (gkr.hpp:189-190): D2H canonical, serial SHA chain
     const std::uint32_t out_layer = c.depth;
@@ -958,6 +962,7 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             ctx->sync();
         }
         if (!comm || comm->rank == root) {
+            NvtxRange nv("dgkr.output_absorb");
             const double t0 = now_ms();
             // DGKR_DIAG_SKIP_OUTPUT_ABSORB=1: bottleneck diagnosis only (tools/diag_stream.py):
             // skips the absorb, so the proof is NOT the reference's; never set for a bench
@@ -1028,6 +1033,8 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
     for (std::uint32_t layer = out_layer; layer >= 1; --layer) {
         auto& C = *c.cons[layer];
         auto& WC = *W.cons[layer];
+        const std::string nv_name = "dgkr.layer " + std::to_string(layer);
+        NvtxRange nv_layer(nv_name.c_str());
         std::vector<U256> alphas;
         const double th = now_ms();
         LayerClaim combined = combine_claims(std::move(registry[layer]), tr, F, &alphas);  // gkr.hpp:206-207
@@ -1098,11 +1105,13 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
+        nvtxRangePushA("dgkr.phase1 rounds");
         SumcheckRun p1 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
                                    &combined.value, WC.base_host.data(), fuse1)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
                               &combined.value, WC.base_host.data(), fuse1);
+        nvtxRangePop();
         std::vector<U256> vx(ns);
         for (int m = 0; m < ns; ++m) vx[m] = p1.finals[2 * m];
         // phase 2 (sumcheck.hpp:407-431): chi_x(u) split tables + V_m(u)
@@ -1142,11 +1151,13 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
             CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
             ctx->prof.bookkeep_ms += ms;
         }
+        nvtxRangePushA("dgkr.phase2 rounds");
         SumcheckRun p2 =
             comm ? run_rounds_dist(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, comm, W.dist,
                                    &p1.claim_end, WC.base_host.data(), fuse2)
                  : run_rounds(ctx, f, ns, true, static_cast<int>(side), WC.base_ptrs.p, W.rb, tr, nullptr,
                               &p1.claim_end, WC.base_host.data(), fuse2);
+        nvtxRangePop();
         std::vector<U256> finals = vx;
         for (int m = 0; m < ns; ++m) finals.push_back(p2.finals[2 * m]);
         std::vector<RoundPoly> rounds = p1.rounds;

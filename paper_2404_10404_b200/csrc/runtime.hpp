@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a profiler injects a tool
+
 #include "dgkr_b200.h"
 #include "fe.hpp"
 #include "host_core.hpp"
@@ -35,6 +37,15 @@ namespace dgkr_b200 {
 
 /// last error message of a C-ABI call on this thread (dgkr_last_error)
 inline thread_local std::string g_err;
+
+/// NVTX range for nsys / ncu --nvtx timelines: gkr_prove, evaluate, the
+/// output absorb, each layer and each sum-check phase are named ranges
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class Fn>
 int guard(Fn&& fn) {
