@@ -79,6 +79,7 @@ struct Tuning {
     std::uint64_t small_round_pairs;
     std::uint64_t tma_min_pairs;
     std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
+    std::uint64_t absorb_chains;  // output absorbs interleaved per host thread in a proof stream (1..4)
 };
 Tuning& tuning();
 

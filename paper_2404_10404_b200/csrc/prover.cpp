@@ -1547,6 +1547,7 @@ int dgkr_transcript_absorb_elems_multi(const dgkr_field* f, dgkr_transcript* con
         // one host thread per transcript through the combining scheduler of
         // the proof stream (AbsorbPool): the same bytes, whatever the grouping
         AbsorbPool pool;
+        pool.max_k = AbsorbPool::kMaxK;
         std::vector<std::thread> th;
         for (std::size_t j = 0; j < k; ++j) th.emplace_back([&, j] { pool.run(ts[j]->state, elems[j], n); });
         for (auto& x : th) x.join();
@@ -2419,6 +2420,7 @@ int dgkr_gkr_prove_stream(dgkr_ctx* ctx, dgkr_circuit* c, const dgkr_field* f, s
             std::memset(&lanes[i]->prof, 0, sizeof(dgkr_profile));
         }
         ctx->use(f);  // upload runtime-field constants once, before concurrency
+        ctx->absorb_pool.max_k = static_cast<int>(std::clamp<std::uint64_t>(tuning().absorb_chains, 1, AbsorbPool::kMaxK));
         std::vector<std::string> errs(n);
         std::vector<int> codes(n, DGKR_OK);
         // host inputs: a work queue (any lane may take any proof); resident
@@ -2488,6 +2490,7 @@ int dgkr_gkr_prove_dist_stream(dgkr_ctx* ctx, dgkr_comm* const* comms, std::size
             workspace(*c, static_cast<int>(i));
         }
         ctx->use(f);
+        ctx->absorb_pool.max_k = static_cast<int>(std::clamp<std::uint64_t>(tuning().absorb_chains, 1, AbsorbPool::kMaxK));
         std::vector<int> codes(n, DGKR_OK);
         std::vector<std::string> errs(n);
         // static assignment: lane l proves l, l+L, l+2L, ... in order on every
@@ -2668,6 +2671,10 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         if (n == "small_round_pairs") tuning().small_round_pairs = value;
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
+        else if (n == "absorb_chains") {
+            if (value < 1 || value > 4) fail(DGKR_INVALID_ARGUMENT, "absorb_chains must be 1..4");
+            tuning().absorb_chains = value;
+        }
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }
@@ -2678,6 +2685,7 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         if (n == "small_round_pairs") *value = tuning().small_round_pairs;
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
+        else if (n == "absorb_chains") *value = tuning().absorb_chains;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
 }

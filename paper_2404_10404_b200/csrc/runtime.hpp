@@ -204,14 +204,14 @@ struct NttWs {
 /// (gkr.hpp:189-190: state <- SHA256(state || out_i) for every padded
 /// output). One chain is bound by SHA-NI round latency; K chains interleaved
 /// in one thread (absorb_chain32_multi) run ~1.5x (one core) to ~2.3x (all
-/// cores busy) the absorbs per core (tools/absorb, profiles/absorb_r2.txt).
-/// A lane that reaches its absorb queues its job; if its job is not being
-/// processed it becomes a processor: it owns its job plus up to kMaxK - 1
-/// queued ones and advances them together chunk by chunk, topping up free
-/// slots at chunk boundaries. When its own job is done it hands the others
-/// back (their state and position travel with the job) and returns; a lane
-/// whose job is owned elsewhere sleeps until it is done or handed back. Every
-/// chain's bytes are exactly absorb_chain32's.
+/// cores busy) the absorbs per core (tools/absorb, profiles/r2/absorb_probe.txt).
+/// A lane that reaches its absorb queues its job. If a running processor has
+/// a free slot, the lane sleeps: that processor takes the job at its next
+/// chunk boundary (2^15 absorbs, a few ms) and advances it interleaved with
+/// its own. Otherwise the lane becomes a processor itself. A processor whose
+/// own job is done hands the others back (state and position travel with the
+/// job) and returns; one of their lanes takes over. Every chain's bytes are
+/// exactly absorb_chain32's. max_k = 1 disables the interleaving.
 struct AbsorbPool {
     struct Job {
         std::uint8_t* state;
@@ -223,9 +223,11 @@ struct AbsorbPool {
     };
     static constexpr std::size_t kChunk = std::size_t{1} << 15;
     static constexpr int kMaxK = 4;
+    int max_k = 2;     // chains per processor (tuning "absorb_chains")
     std::mutex mu;
     std::condition_variable cv;
     std::vector<Job*> pending;  // unowned and unfinished, FIFO
+    int spare = 0;              // free slots of the running processors
 
     void run(std::uint8_t* state, const std::uint8_t* data, std::size_t n) {
         Job me{state, data, n};
@@ -234,10 +236,11 @@ struct AbsorbPool {
         pending.push_back(&me);
         for (;;) {
             if (me.done) return;
-            if (!me.owned) {
+            if (!me.owned && spare == 0) {
                 std::vector<Job*> mine;
                 take(&me, mine);
                 fill(mine);
+                spare += max_k - static_cast<int>(mine.size());
                 lk.unlock();
                 process(mine, &me);
                 lk.lock();
@@ -254,7 +257,7 @@ private:
         mine.push_back(j);
     }
     void fill(std::vector<Job*>& mine) {  // mu held
-        while (static_cast<int>(mine.size()) < kMaxK && !pending.empty()) take(pending.front(), mine);
+        while (static_cast<int>(mine.size()) < max_k && !pending.empty()) take(pending.front(), mine);
     }
     void process(std::vector<Job*> mine, Job* me) {
         std::uint8_t* st[kMaxK];
@@ -268,6 +271,7 @@ private:
             }
             absorb_chain32_multi(st, in, mine.size(), m);
             std::lock_guard<std::mutex> lk(mu);
+            spare -= max_k - static_cast<int>(mine.size());  // this processor's slots, re-added below
             bool any_done = false;
             for (Job* j : mine) {
                 j->pos += m;
@@ -282,8 +286,9 @@ private:
                 cv.notify_all();
                 return;
             }
-            if (any_done) cv.notify_all();
             fill(mine);
+            spare += max_k - static_cast<int>(mine.size());
+            if (any_done) cv.notify_all();
         }
     }
 };
