@@ -292,7 +292,9 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
  * 256), "tma_min_pairs" = smallest round taking the TMA-staged round kernel
  * (default 0 = off: measured slower than the register-fed kernel on C2),
  * "fuse_round1" = 1 (default 0: measured slower) builds single-slot bookkeeping tables by row
- * pairs with round 1 of the phase fused in. Unknown names -> DGKR_INVALID_ARGUMENT. */
+ * pairs with round 1 of the phase fused in, "absorb_chains" = 1..4 (default
+ * 1: measured best) output absorbs a host thread interleaves in a proof
+ * stream. Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);
 
