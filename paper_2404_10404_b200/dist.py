@@ -117,7 +117,14 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
     # proofs in flight: the serial output absorb (~0.5 s of host time per C2
     # proof, spread over the ranks) caps throughput at lanes / 0.5 s, so lanes
     # grow with N; per-lane device memory shrinks as 1/N
-    lanes = args.lanes or min(64, 32 * world)
+    # DGKR_TRANSPORT: "shm" (default: one POSIX shared-memory segment per lane;
+    # the per-round payloads are host-resident already) or "nccl" (one NCCL
+    # communicator per lane over NVLink; communicator setup is heavier, so the
+    # default lane count is lower)
+    transport = os.environ.get("DGKR_TRANSPORT", "shm")
+    if transport not in ("shm", "nccl"):
+        raise SystemExit(f"DGKR_TRANSPORT={transport}: expected shm or nccl")
+    lanes = args.lanes or (min(64, 32 * world) if transport == "shm" else min(16, 8 * world))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     if lanes * local_world > (os.cpu_count() or 1) and "DGKR_SPIN_US" not in os.environ:
         # more lane threads than host cores: spin briefly, then block, so
@@ -139,9 +146,15 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
     all_inputs = W.random_inputs(field.p, insz * n_copies, input_seed)
     per = insz * n_local * field.width
     mine = np.ascontiguousarray(all_inputs[rank * per:(rank + 1) * per])
-    token = [secrets.token_hex(6) if rank == 0 else None]
-    dist.broadcast_object_list(token, src=0)
-    comms = [ShmComm(ctx, f"/dgkr_{token[0]}_{l}", rank, world, slot_bytes_for(circ, field)) for l in range(lanes)]
+    if transport == "shm":
+        token = [secrets.token_hex(6) if rank == 0 else None]
+        dist.broadcast_object_list(token, src=0)
+        comms = [ShmComm(ctx, f"/dgkr_{token[0]}_{l}", rank, world, slot_bytes_for(circ, field))
+                 for l in range(lanes)]
+    else:
+        uids = [[P.Comm.nccl_unique_id() for _ in range(lanes)] if rank == 0 else None]
+        dist.broadcast_object_list(uids, src=0)
+        comms = [P.Comm(ctx, uids[0][l], rank, world) for l in range(lanes)]
     for l in range(lanes):
         P.load_inputs_lane(ctx, circ, field, l, mine)
     cap = circ.proof_bound(field) + (world - 1) * circ.output_size * field.width + 4096
@@ -203,7 +216,8 @@ def run_bench_rank(args, cfg_name, configs, circuit_seed, input_seed, helpers=No
             "data": "synthetic",
             "config": {"workload": desc, "field": "bn254", "n_copies": n_copies, "copies_per_gpu": n_local,
                        "gates_per_layer_per_copy": 1 << lw, "depth": depth, "gates": gates,
-                       "parallelism": f"dp{world} (rank = top log2(N) variables)", "transport": "shm per lane",
+                       "parallelism": f"dp{world} (rank = top log2(N) variables)",
+                       "transport": "shm per lane" if transport == "shm" else "NCCL communicator per lane",
                        "output_absorb": "proof i on rank i mod N",
                        "l2": "no flush: layer tables exceed L2"},
             "lanes": lanes, "proof_latency_ms": 1e3 * lat,
