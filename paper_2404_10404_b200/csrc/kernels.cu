@@ -1577,6 +1577,11 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
     return true;
 }
 
+#ifndef DGKR_ROUND_MINB
+#define DGKR_ROUND_MINB 2
+#endif
+constexpr int kRoundMinBlocks = DGKR_ROUND_MINB;
+
 void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st) {
     int lp = 0;
     while ((std::uint64_t{1} << lp) < a.n_out_pairs) ++lp;
@@ -1589,7 +1594,7 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
 #define LAUNCH_ROUND(NP, HG, MD)                                                   \
     do {                                                                           \
         if (a.need_s1) k_round<F, NP, HG, MD, true, 2><<<g, kThreads, 0, st>>>(p); \
-        else k_round<F, NP, HG, MD, false, 2><<<g, kThreads, 0, st>>>(p);          \
+        else k_round<F, NP, HG, MD, false, kRoundMinBlocks><<<g, kThreads, 0, st>>>(p); \
     } while (0)
 #define BY_MODE(NP, HG)                                   \
     do {                                                  \
