@@ -206,6 +206,11 @@ def run_reference_arm(args, cfg_name):
         "cpu_baseline": {"value": value, "unit": "gates/s", "cores": threads, "kind": "reference", "sample": sample,
                          "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "sample_vs_workload": (
+            "measured on one core of this host (tools/ref_scaling.py, profiles/r2/reference_scaling.jsonl): "
+            "12.9 us/gate for the 2^16 x 2 sample, 13.3 for one full 2^16 x 24 sub-circuit, growing ~0.7-0.9 us "
+            "per extra variable (SURVEY 8(a) a5: (3s+30) mults/gate); at C2's s = 22 the reference pays ~16-18 "
+            "us/gate, so this sample overstates its C2 throughput by ~1.25-1.4x" if cfg_name == "c2" else None),
     }
     print(json.dumps(line))
     return 0
