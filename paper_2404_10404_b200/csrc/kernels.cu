@@ -1535,7 +1535,11 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
     }
     // DGKR_TMA_VERIFY=1: check after every launch (synchronous); =2: count
     // asynchronously, report at exit (keeps the launch concurrency)
+#ifdef DGKR_TMA_DEBUG
     static const int verify = std::getenv("DGKR_TMA_VERIFY") ? std::atoi(std::getenv("DGKR_TMA_VERIFY")) : 0;
+#else
+    static const int verify = 0;  // the staged-element check is compiled in only with -DDGKR_TMA_DEBUG
+#endif
     static unsigned* dbg = [] {
         unsigned* d = nullptr;
         if (verify) {

@@ -105,6 +105,7 @@ struct TmaShape {
     static constexpr int kBoxRows = MODE == kScan ? kTmaTile / 2 : (MODE == kFoldNat ? kTmaTile : kTmaTile / 4);
 };
 
+#ifdef DGKR_TMA_DEBUG
 __device__ __noinline__ void tma_verify(const RoundTmaParams& a, int t, std::uint64_t gi, const Fe& x, int mode) {
     const Fe y = fe_load(a.in[t] + gi);
     bool ok = true;
@@ -117,6 +118,13 @@ __device__ __noinline__ void tma_verify(const RoundTmaParams& a, int t, std::uin
         a.dbg[4] = blockIdx.x;
     }
 }
+#define TMA_VERIFY(...) \
+    if (a.dbg) {        \
+        __VA_ARGS__;    \
+    }
+#else
+#define TMA_VERIFY(...)
+#endif
 
 /// Lane view of one table of one warp-tile: the pair (x0, x1) of output index
 /// i = wtile * 32 + lane, folded with the challenge unless kScan; fold outputs
@@ -129,19 +137,12 @@ __device__ __forceinline__ void tma_pair(std::uint32_t st, int lane, std::uint64
         const std::uint32_t row = lane >> 1, cb = (lane & 1) * 4;
         x0 = lds_fe_swz(st, row, cb);
         x1 = lds_fe_swz(st, row, cb + 2);
-        if (a.dbg) {
-            tma_verify(a, t, 2 * i, x0, MODE);
-            tma_verify(a, t, 2 * i + 1, x1, MODE);
-        }
+        TMA_VERIFY(tma_verify(a, t, 2 * i, x0, MODE); tma_verify(a, t, 2 * i + 1, x1, MODE))
     } else if (MODE == kFoldNat) {
         const Fe a0 = lds_fe_swz(st, lane, 0), a1 = lds_fe_swz(st, lane, 2);
         const Fe b0 = lds_fe_swz(st, lane, 4), b1 = lds_fe_swz(st, lane, 6);
-        if (a.dbg) {
-            tma_verify(a, t, 4 * i, a0, MODE);
-            tma_verify(a, t, 4 * i + 1, a1, MODE);
-            tma_verify(a, t, 4 * i + 2, b0, MODE);
-            tma_verify(a, t, 4 * i + 3, b1, MODE);
-        }
+        TMA_VERIFY(tma_verify(a, t, 4 * i, a0, MODE); tma_verify(a, t, 4 * i + 1, a1, MODE);
+                   tma_verify(a, t, 4 * i + 2, b0, MODE); tma_verify(a, t, 4 * i + 3, b1, MODE))
         x0 = foldk<F>(a0, a1, a.k);
         x1 = foldk<F>(b0, b1, a.k);
         const std::uint64_t s = a.log_p ? (__brevll(i) >> (64 - a.log_p)) : 0;
@@ -152,12 +153,8 @@ __device__ __forceinline__ void tma_pair(std::uint32_t st, int lane, std::uint64
         constexpr int seg = kTmaTile * 32;  // one box: 32 elements, 1 KB
         const Fe a0 = lds_fe_swz(st, row, cb), b0 = lds_fe_swz(st + seg, row, cb);
         const Fe a1 = lds_fe_swz(st + 2 * seg, row, cb), b1 = lds_fe_swz(st + 3 * seg, row, cb);
-        if (a.dbg) {
-            tma_verify(a, t, i, a0, MODE);
-            tma_verify(a, t, i + P, b0, MODE);
-            tma_verify(a, t, i + 2 * P, a1, MODE);
-            tma_verify(a, t, i + 3 * P, b1, MODE);
-        }
+        TMA_VERIFY(tma_verify(a, t, i, a0, MODE); tma_verify(a, t, i + P, b0, MODE);
+                   tma_verify(a, t, i + 2 * P, a1, MODE); tma_verify(a, t, i + 3 * P, b1, MODE))
         x0 = foldk<F>(a0, a1, a.k);
         x1 = foldk<F>(b0, b1, a.k);
         fe_store(dst + i, x0);
@@ -238,15 +235,25 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_round_tma(const __grid_const
     };
     for (std::uint64_t k = 0; k < my_wt; ++k) {
         const std::uint64_t i = (g + k * G) * kTmaTile + lane;
-        Fe f0, f1, g0, g1;
-        next(a.out[0], i, f0, f1, 0);
-        next(a.out[1], i, g0, g1, 1);
-        sum_prod<F>(w[0], f0, g0);
-        if constexpr (S1) sum_prod<F>(w[1], f1, g1);
-        sum_prod<F>(w[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0));
-        next(a.out[2], i, g0, g1, 2);
-        sum_val<F>(w[0], g0);
-        if constexpr (S1) sum_val<F>(w[1], g1);
+        Fe f0, f1;
+        // one (rolled) copy of the staged fold for the three tables keeps
+        // the loop body small in the instruction cache
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+            Fe x0, x1;
+            next(a.out[t], i, x0, x1, t);
+            if (t == 0) {
+                f0 = x0;
+                f1 = x1;
+            } else if (t == 1) {
+                sum_prod<F>(w[0], f0, x0);
+                if constexpr (S1) sum_prod<F>(w[1], f1, x1);
+                sum_prod<F>(w[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(x1, x0));
+            } else {
+                sum_val<F>(w[0], x0);
+                if constexpr (S1) sum_val<F>(w[1], x1);
+            }
+        }
     }
     Fe sums[NS];
     if constexpr (kWide) {
