@@ -2776,13 +2776,13 @@ int dgkr_dist_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, std::size_t n_workers
 }
 
 /// DistPc::commit + open (cluster.hpp:336-412) over the K = plan(N) clusters,
-/// spread over the given contexts (devices): cluster c runs on context
-/// c mod n_ctx, on its own lane (stream + host thread), so clusters commit
-/// and open concurrently -- the leaders hash in parallel and the K opening
-/// transcripts (independent by construction, cluster.hpp:445-449) run on K
-/// host threads. Member rows land in the leader's device buffer (the
-/// mempool, metered as mempool bytes, cluster.hpp:349-361); the open reuses
-/// the matrix and tree its commit built.
+/// spread over the given contexts (devices): worker i's row lives on context
+/// i mod n_ctx, cluster c is assembled on its leader's (worker c*M) context
+/// by peer copies of the member rows (the mempool, metered as mempool bytes,
+/// cluster.hpp:349-361), each cluster on its own lane (stream + host thread),
+/// so the leaders hash in parallel and the K opening transcripts
+/// (independent by construction, cluster.hpp:445-449) run on K host threads;
+/// the open reuses the matrix and tree its commit built.
 int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field* f, std::size_t n_workers,
                       std::size_t n_clusters, std::size_t row_vars, const std::uint8_t* rows, const std::uint8_t* r,
                       std::size_t r_len, std::size_t q, std::uint8_t* roots_out, std::size_t* n_roots,
@@ -2813,17 +2813,53 @@ int dgkr_distpc_multi(dgkr_ctx* const* ctxs, std::size_t n_ctx, const dgkr_field
         std::vector<Digest> roots(K);
         std::vector<int> codes(K, DGKR_OK);
         std::vector<std::string> errs(K);
-        // cluster c -> (context c mod n_ctx, lane c / n_ctx); a worker thread per lane
-        const std::size_t n_threads = std::min<std::size_t>(K, std::max<std::size_t>(n_ctx, std::min<std::size_t>(K, 16)));
+        // Placement: worker i holds its row on context i mod n_ctx (its own
+        // lane there); cluster c's leader is worker c*M (cluster.hpp:24-36), so
+        // the cluster is assembled, committed and opened on context
+        // (c*M) mod n_ctx. Member rows move device to device (peer copies)
+        // into the leader's matrix: the mempool writes (cluster.hpp:349-361).
+        for (std::size_t i = 0; i < n_ctx; ++i)  // direct peer copies (NVLink) where the devices allow
+            for (std::size_t j = 0; j < n_ctx; ++j) {
+                const int di = ctxs[i]->device, dj = ctxs[j]->device;
+                int can = 0;
+                if (di == dj || cudaDeviceCanAccessPeer(&can, di, dj) != cudaSuccess || !can) continue;
+                CK(cudaSetDevice(di));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(dj, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                (void)cudaGetLastError();
+            }
+        const std::size_t n_threads = std::min<std::size_t>(K, 16);
         auto work = [&](std::size_t th) {
             for (std::size_t c = th; c < K; c += n_threads) {
                 try {
-                    dgkr_ctx* cx = ctxs[c % n_ctx];
-                    CK(cudaSetDevice(cx->device));
-                    Lane* L = cx->lane(static_cast<int>((c / n_ctx) % 16));
+                    dgkr_ctx* cx = ctxs[(c * M) % n_ctx];
+                    Lane* L = cx->lane(static_cast<int>(1 + c));
                     PcsDevice& d = L->nttws().pcs;
-                    const std::uint8_t* mine = rows + c * M * row_bytes;  // the cluster's mempool
-                    roots[c] = pcs_commit(L, f, d, M, cols, mine);
+                    const std::uint8_t* mine = rows + c * M * row_bytes;  // the cluster's rows (for the openings' columns)
+                    check_matrix(M, cols);
+                    // (1) every member uploads its own row on its own device
+                    std::vector<const Fe*> src(M);
+                    std::vector<int> src_dev(M);
+                    for (std::size_t m = 0; m < M; ++m) {
+                        const std::size_t wi = c * M + m;
+                        dgkr_ctx* wc = ctxs[wi % n_ctx];
+                        CK(cudaSetDevice(wc->device));
+                        Lane* WL = wc->lane(static_cast<int>(1 + K + wi));
+                        NttWs& ws = WL->nttws();
+                        ws.worker_row.ensure(cols);
+                        WL->upload_elems(f, rows + wi * row_bytes, cols, ws.worker_row.p, ws.worker_stage);  // synced
+                        src[m] = ws.worker_row.p;
+                        src_dev[m] = wc->device;
+                    }
+                    // (2) the leader pulls the member rows into its matrix (peer copies over NVLink
+                    //     when the members sit on other GPUs), then commits (pcs.hpp:105-113)
+                    CK(cudaSetDevice(cx->device));
+                    d.m.ensure(M * cols);
+                    for (std::size_t m = 0; m < M; ++m)
+                        CK(cudaMemcpyPeerAsync(d.m.p + m * cols, cx->device, src[m], src_dev[m], cols * sizeof(Fe), L->st));
+                    pcs_build_tree(L, f, d, M, cols);
+                    L->d2h(roots[c].data(), d.nodes.p + 32, 32);
+                    L->sync();
                     Transcript tr(&f->f, "dgkr.pc.cluster");  // cluster.hpp:445-449
                     tr.absorb_u64(c);
                     std::uint8_t* dst = open_out + c * (4 + osz);

@@ -198,6 +198,10 @@ struct NttWs {
     DBuf<std::uint8_t> b_recs, b_nodes, b_leaves, b_sib, b_zc, b_ok, b_root;
     // polynomial commitment (pcs_commit / pcs_open; a DistPc cluster on this lane)
     PcsDevice pcs;
+    // DistPc worker row resident on this lane's device (Montgomery), the
+    // source of the peer copy into its cluster leader's matrix
+    DBuf<Fe> worker_row;
+    DBuf<std::uint8_t> worker_stage;
 };
 
 /// Combining scheduler for the serial output absorbs of concurrent proofs
