@@ -393,6 +393,15 @@ int dgkr_beacon_verify(dgkr_ctx* ctx, const uint8_t* root, const uint8_t* record
 int dgkr_dist_sumcheck(dgkr_ctx* ctx, const dgkr_field* f, size_t n_workers, size_t n_pairs, size_t vars,
                        const uint8_t* tables, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len,
                        char* traffic_json, size_t json_cap);
+/* dist_sumcheck over real devices: this rank's share (rows [rank 2^lv, (rank+1) 2^lv) of
+ * every table, f_0 g_0 f_1 g_1 ..., shard_pairs cluster.hpp:190-217) on its own GPU;
+ * round sums all-gathered over `comm` (NCCL / shared memory), the early boundary, tail
+ * rounds redundant on every rank. Every rank returns the single-machine proof bytes. */
+int dgkr_dist_sumcheck_comm(dgkr_ctx* ctx, dgkr_comm* comm, const dgkr_field* f, size_t n_pairs, size_t local_vars,
+                            const uint8_t* local_tables, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
+/* the same with `world` ranks as host threads on lanes of one GPU (full tables in) */
+int dgkr_dist_sumcheck_emulated(dgkr_ctx* ctx, const dgkr_field* f, int world, size_t n_pairs, size_t vars,
+                                const uint8_t* tables, dgkr_transcript* t, uint8_t* proof, size_t cap, size_t* len);
 /* DistPc commit + open (cluster.hpp:336-412): K roots (32 B each), cluster
  * openings as u32 len || Opening::to_bytes, combined value, and traffic json
  * (phases "commit", "open"). n_clusters = 0 selects ClusterTopology::plan's

@@ -375,6 +375,42 @@ std::vector<std::uint8_t> product_sumcheck(Lane* ctx, const dgkr_field* f, std::
     return sumcheck_bytes(F, claimed, run.rounds, run.finals);
 }
 
+/// One rank's share of a distributed product sum-check (cluster.hpp:228-320
+/// over real devices): the rank holds f_k^(rank), g_k^(rank) -- rows
+/// [rank * 2^lv, (rank + 1) * 2^lv) of every table, the rank index being the
+/// high variables (shard_pairs, cluster.hpp:190-217). Claimed sum = sum of the
+/// ranks' totals (an all-gather); then the layer engine's distributed rounds:
+/// per-round all-gather of the round sums, the early boundary, redundant tail
+/// rounds on every rank. Byte-identical to prove_product_sum over the
+/// concatenated tables on every rank.
+std::vector<std::uint8_t> product_sumcheck_dist(Lane* ctx, const dgkr_field* f, std::size_t n_pairs,
+                                                std::size_t local_vars, const std::uint8_t* local_tables,
+                                                Transcript& tr, dgkr_comm* comm, DistTail& dt, DBuf<Fe>& tabs,
+                                                RoundBuffers& rb) {
+    if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "nothing to shard");
+    if (local_vars > 40) fail(DGKR_INVALID_ARGUMENT, "table too large");
+    const HostField& F = f->f;
+    const std::uint64_t n = std::uint64_t{1} << local_vars;
+    const int ntab = static_cast<int>(2 * n_pairs);
+    DBuf<std::uint8_t> stage;
+    tabs.ensure(static_cast<std::size_t>(ntab) * n);
+    ctx->upload_elems(f, local_tables, static_cast<std::uint64_t>(ntab) * n, tabs.p, stage);
+    std::vector<const Fe*> hp(ntab);
+    for (int t = 0; t < ntab; ++t) hp[t] = tabs.p + t * n;
+    DBuf<const Fe*> base;
+    base.ensure(ntab);
+    ctx->h2d(base.p, hp.data(), ntab * sizeof(const Fe*));
+    launch_pair_total(ctx->use(f), base.p, static_cast<int>(n_pairs), n, ctx->ws, ctx->st);  // local total (:258-262)
+    ctx->launched();
+    comm->allgather_to_host(ctx->ws.result, ctx->h_small + Lane::kGatherOff, sizeof(Fe), ctx);
+    U256 claimed{};
+    for (int r = 0; r < comm->world; ++r) claimed = F.add(claimed, to_u256(ctx->h_small[Lane::kGatherOff + r]));
+    tr.absorb(claimed);  // :264-265
+    SumcheckRun run = run_rounds_dist(ctx, f, static_cast<int>(n_pairs), false, static_cast<int>(local_vars), base.p,
+                                      rb, tr, comm, dt, &claimed, hp.data());
+    return sumcheck_bytes(F, claimed, run.rounds, run.finals);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -2737,6 +2773,94 @@ int dgkr_pcs_open(dgkr_ctx* ctx, const dgkr_field* f, std::size_t rows, std::siz
         std::memcpy(t->state, tr.state().data(), 32);
         t->draws = tr.draws();
         ctx->end_call();
+    });
+}
+
+int dgkr_dist_sumcheck_comm(dgkr_ctx* ctx, dgkr_comm* comm, const dgkr_field* f, std::size_t n_pairs,
+                            std::size_t local_vars, const std::uint8_t* local_tables, dgkr_transcript* t,
+                            std::uint8_t* proof, std::size_t cap, std::size_t* len) {
+    return guard([&] {
+        ctx->begin_call();
+        CK(cudaSetDevice(ctx->device));
+        if (!comm) fail(DGKR_INVALID_ARGUMENT, "no communicator");
+        if ((comm->world & (comm->world - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "world size must be a power of two");
+        Transcript tr(&f->f, t->state, t->draws);
+        DistTail dt;
+        DBuf<Fe> tabs;
+        RoundBuffers rb;
+        auto bytes = product_sumcheck_dist(ctx, f, n_pairs, local_vars, local_tables, tr, comm, dt, tabs, rb);
+        std::memcpy(t->state, tr.state().data(), 32);
+        t->draws = tr.draws();
+        ctx->end_call();
+        emit(bytes, proof, cap, len);
+    });
+}
+
+int dgkr_dist_sumcheck_emulated(dgkr_ctx* ctx, const dgkr_field* f, int world, std::size_t n_pairs, std::size_t vars,
+                                const std::uint8_t* tables, dgkr_transcript* t, std::uint8_t* proof, std::size_t cap,
+                                std::size_t* len) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (world < 1 || world > 64 || (world & (world - 1)) != 0) fail(DGKR_INVALID_ARGUMENT, "world must be 1..64, pow2");
+        if (n_pairs == 0) fail(DGKR_INVALID_ARGUMENT, "nothing to shard");
+        const std::uint64_t total = std::uint64_t{1} << vars;
+        if (total % static_cast<std::uint64_t>(world) != 0)
+            fail(DGKR_INVALID_ARGUMENT, "worker count must divide table size");  // cluster.hpp:196-198
+        const std::size_t lv = vars - log2_exact(static_cast<std::uint64_t>(world));
+        const std::size_t w = f->f.width();
+        const std::size_t chunk = (std::size_t{1} << lv) * w;
+        // shard_pairs (cluster.hpp:200-215): rank r's slice of every table, f_0 g_0 f_1 g_1 ...
+        std::vector<std::vector<std::uint8_t>> shares(world, std::vector<std::uint8_t>(2 * n_pairs * chunk));
+        for (int r = 0; r < world; ++r)
+            for (std::size_t tb = 0; tb < 2 * n_pairs; ++tb)
+                std::memcpy(shares[r].data() + tb * chunk, tables + tb * total * w + r * chunk, chunk);
+        std::vector<Lane*> lanes(world);
+        for (int r = 0; r < world; ++r) lanes[r] = ctx->lane(r);
+        ctx->use(f);
+        ThreadGroup group;
+        group.world = world;
+        std::vector<ThreadComm> comms(world);
+        std::vector<std::vector<std::uint8_t>> outs(world);
+        std::vector<dgkr_transcript> ts(world, *t);
+        std::vector<int> codes(world, DGKR_OK);
+        std::vector<std::string> errs(world);
+        for (int r = 0; r < world; ++r) {
+            comms[r].rank = r;
+            comms[r].world = world;
+            comms[r].g = &group;
+        }
+        auto work = [&](int r) {
+            try {
+                CK(cudaSetDevice(ctx->device));
+                Lane* L = lanes[r];
+                Transcript tr(&f->f, ts[r].state, ts[r].draws);
+                DistTail dt;
+                DBuf<Fe> tabs;
+                RoundBuffers rb;
+                outs[r] = product_sumcheck_dist(L, f, n_pairs, lv, shares[r].data(), tr, &comms[r], dt, tabs, rb);
+                std::memcpy(ts[r].state, tr.state().data(), 32);
+                ts[r].draws = tr.draws();
+            } catch (const Error& e) {
+                codes[r] = e.code;
+                errs[r] = e.what();
+                group.abort();
+            } catch (const std::exception& e) {
+                codes[r] = DGKR_LOGIC_ERROR;
+                errs[r] = e.what();
+                group.abort();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int r = 1; r < world; ++r) th.emplace_back(work, r);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int r = 0; r < world; ++r)
+            if (codes[r] != DGKR_OK) fail(codes[r], "rank " + std::to_string(r) + ": " + errs[r]);
+        for (int r = 1; r < world; ++r)
+            if (outs[r] != outs[0] || std::memcmp(ts[r].state, ts[0].state, 32) != 0)
+                fail(DGKR_LOGIC_ERROR, "ranks disagree on the proof");
+        *t = ts[0];
+        emit(outs[0], proof, cap, len);
     });
 }
 

@@ -628,6 +628,22 @@ def dist_sumcheck(ctx: Context, n_workers: int, pairs, tr: Transcript):
     return out.raw[: ln.value], js.value.decode()
 
 
+def dist_sumcheck_emulated(ctx: Context, world: int, pairs, tr: Transcript) -> bytes:
+    """dist_sumcheck on `world` ranks (host threads on lanes of one GPU, each
+    holding its shard_pairs slice, cluster.hpp:190-217) exchanging round sums
+    through a communicator (dgkr_dist_sumcheck_emulated) -> proof bytes"""
+    f = tr.field
+    tabs = [f.encode(x) for pair in pairs for x in pair]
+    n = len(tabs[0]) // f.width
+    vars_ = max(0, n.bit_length() - 1)
+    cap = 64 + (vars_ + 2) * 4 * f.width + 2 * len(pairs) * f.width + 64
+    out, ln = _out(cap)
+    check(lib().dgkr_dist_sumcheck_emulated(ctx.handle, f.handle, C.c_int(world), C.c_size_t(len(pairs)),
+                                            C.c_size_t(vars_), C.c_char_p(b"".join(tabs)), C.byref(tr.t), out,
+                                            C.c_size_t(cap), C.byref(ln)))
+    return out.raw[: ln.value]
+
+
 def distpc(ctx, field: Field, rows: Sequence[Elems], r: Sequence[int], spot_checks: int = 32,
            n_clusters: int = 0):
     """DistPc::commit + open (cluster.hpp:336-412) -> (roots, cluster opening

@@ -73,3 +73,20 @@ def test_nccl_transport_world1(ctx):
     tr2 = P.Transcript(f, "nccl")
     got = P.gkr_prove_dist(ctx, comm, P.Circuit(ctx, insz, *flat, n_copies=4), inputs, tr2)
     assert got == want and tr2.state == tr1.state
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, O.GOLDILOCKS_P, 97])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("vars_,n_pairs", [(3, 1), (7, 2), (12, 3)])
+def test_dist_sumcheck_over_comm_equals_single(ctx, p, world, vars_, n_pairs):
+    """dist_sumcheck with the ranks' shards exchanging round sums through a
+    communicator (dgkr_dist_sumcheck_comm's code path, ranks as threads):
+    the single-machine prove_product_sum bytes on every rank (cluster.hpp:219-227)"""
+    rng = np.random.default_rng(900 + world + 10 * vars_ + p % 91)
+    f, of = P.Field(p), O.Field(p)
+    pairs = [(O.random_elements(of, 1 << vars_, rng), O.random_elements(of, 1 << vars_, rng)) for _ in range(n_pairs)]
+    t1 = P.Transcript(f, "dsc", [world])
+    single = P.prove_product_sum(ctx, pairs, t1)
+    t2 = P.Transcript(f, "dsc", [world])
+    assert P.prover.dist_sumcheck_emulated(ctx, world, pairs, t2) == single
+    assert t2.state == t1.state
