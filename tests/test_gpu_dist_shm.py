@@ -76,3 +76,25 @@ def test_two_process_shm_spread_absorb(ctx, tmp_path):
                 assert proof == want
             else:
                 assert proof[n_out_bytes:] == want[n_out_bytes:] and not any(proof[4:n_out_bytes])
+
+
+@pytest.mark.parametrize("world,vars_,n_pairs", [(2, 9, 2), (4, 13, 1)])
+def test_dist_sumcheck_processes_over_shm(ctx, tmp_path, world, vars_, n_pairs):
+    """dgkr_dist_sumcheck_comm with one process per rank (all on this GPU),
+    round sums and the early-boundary table gather through shared memory
+    (4 KiB slots: chunked): every rank returns the single-machine proof"""
+    token = secrets.token_hex(4)
+    out = str(tmp_path / "dsc")
+    worker = os.path.join(ROOT, "tools", "dsc_shm_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), token, str(vars_), str(n_pairs), out],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    logs = [p.communicate(timeout=300)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(logs)
+    f = P.Field.bn254()
+    tabs = [W.random_inputs(f.p, 1 << vars_, 300 + t).tobytes() for t in range(2 * n_pairs)]
+    pairs = [(tabs[2 * k], tabs[2 * k + 1]) for k in range(n_pairs)]
+    tr = P.Transcript(f, "dsc.shm")
+    want = P.prove_product_sum(ctx, pairs, tr)
+    for r in range(world):
+        raw = open(f"{out}.{r}", "rb").read()
+        assert raw[:-32] == want and raw[-32:] == tr.state
