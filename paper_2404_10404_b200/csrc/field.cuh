@@ -559,6 +559,13 @@ __device__ __forceinline__ void acc_add(Acc& a, const Acc& b) {
     a.v[16] += b.v[16];
 }
 
+__device__ __forceinline__ Acc acc_shfl(const Acc& a, int src) {
+    Acc r;
+#pragma unroll
+    for (int i = 0; i < 17; ++i) r.v[i] = __shfl_sync(0xffffffffu, a.v[i], src);
+    return r;
+}
+
 __device__ __forceinline__ Acc acc_shfl_down(const Acc& a, int off) {
     Acc r;
 #pragma unroll

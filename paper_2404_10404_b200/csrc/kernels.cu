@@ -111,9 +111,20 @@ __device__ __forceinline__ void block_sum_wide(Acc (&s)[K], Fe (&out)[K]) {
 #pragma unroll
             for (int k = 0; k < K; ++k) acc_add(s[k], acc_shfl_down(s[k], off));
         }
+        // lane k reduces accumulator k: the K reductions side by side
+        __shared__ Fe red[K];
+        Acc mine;
+        acc_zero(mine);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const Acc b = acc_shfl(s[k], 0);
+            if (lane == k) mine = b;
+        }
+        if (lane < K) red[lane] = acc_reduce<F>(mine);
+        __syncwarp();
         if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) out[k] = acc_reduce<F>(s[k]);
+            for (int k = 0; k < K; ++k) out[k] = red[k];
         }
     }
     __syncthreads();
@@ -1581,6 +1592,11 @@ static bool launch_round_tma(FieldKind k, const RoundLaunch& a, const ReduceWs& 
     return true;
 }
 
+#ifndef DGKR_SCAN_ONE_WAVE
+#define DGKR_SCAN_ONE_WAVE 1
+#endif
+constexpr bool kScanOneWave = DGKR_SCAN_ONE_WAVE;
+
 #ifndef DGKR_ROUND_MINB
 #define DGKR_ROUND_MINB 2
 #endif
@@ -1593,7 +1609,10 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
     static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
     if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
     if (launch_round_tma(k, a, ws, lp, st)) return;
-    const int g = grid_for(a.n_out_pairs, kThreads, ws.max_blocks);
+    // round 1 with unreduced sums: one wave of resident CTAs (2 per SM), so
+    // each CTA's single REDC epilogue is amortised over ~4x more pairs
+    const int g = grid_for(a.n_out_pairs, kThreads,
+                           (a.mode == kScan && !a.need_s1 && kScanOneWave) ? 2 * ws.num_sms : ws.max_blocks);
     // 2 CTAs/SM (<= 128 registers); forcing 3 (80 registers, small spill) measured no faster
 #define LAUNCH_ROUND(NP, HG, MD)                                                   \
     do {                                                                           \
