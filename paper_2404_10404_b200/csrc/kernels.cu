@@ -525,9 +525,7 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(const __grid_cons
         for (std::uint32_t e = sg.x; e < sg.x + n_e; ++e) {
             const uint4 en = sd.ent[e];
             const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
-            const std::uint64_t xg = (c << sd.log_stride) | en.y;
-            // chi_x(u): the dense table, or on the fly from its split halves (L1/L2-resident)
-            const Fe eu = a.eq_u ? fe_load_nc(a.eq_u + xg) : split_eq<F>(a.u, xg);
+            const Fe eu = fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y));
             const Fe cx = fe_mul<F>(w, eu);
             const Fe prod = fe_mul_fold<F>(cx, vxk);  // V(u) is a per-launch constant
             const bool mul = en.z >> 31;
@@ -1503,8 +1501,7 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0, 0, 1, 0};
-        if (const char* e = std::getenv("DGKR_EQ_ON_THE_FLY")) v.eq_on_the_fly = std::strtoull(e, nullptr, 10);  // fused round 1, interleaved absorbs: measured slower on C2
+        Tuning v{kSmallRoundPairs, 0, 0, 1};  // fused round 1, interleaved absorbs: measured slower on C2
         if (const char* e = std::getenv("DGKR_ABSORB_CHAINS")) v.absorb_chains = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);
@@ -1753,7 +1750,7 @@ void launch_bookkeep_phase2(FieldKind k, const BookkeepLaunch& a, cudaStream_t s
         check_launch("bookkeep_pairs(2)");
         return;
     }
-    if (a.perm && a.n_slots == 1 && a.gate_w && a.vx_const) {
+    if (a.perm && a.n_slots == 1 && a.gate_w && a.eq_u && a.vx_const) {
         FoldConst vk{};
         std::memcpy(&vk, a.vx_const, sizeof(FoldConst));
         DISPATCH_FIELD(k, F, (k_bookkeep2_sorted<F><<<g, kThreads, 0, st>>>(a, vk)));

@@ -80,7 +80,6 @@ struct Tuning {
     std::uint64_t tma_min_pairs;
     std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
     std::uint64_t absorb_chains;  // output absorbs interleaved per host thread in a proof stream (1..4)
-    std::uint64_t eq_on_the_fly;  // phase-2 bookkeeping computes chi_x(u) per wire from split tables
 };
 Tuning& tuning();
 

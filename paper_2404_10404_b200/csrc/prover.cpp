@@ -1165,19 +1165,12 @@ std::size_t gkr_prove(Lane* ctx, dgkr_circuit& c, CircuitWs& W, const dgkr_field
         f->fold_const(vx[0], vxk);
         bk.vx_const = vxk;
         if (ctx->profile_on) CK(cudaEventRecord(ctx->ev0, ctx->st));
-        if (tuning().eq_on_the_fly) {
-            // chi_x(u) computed per wire from the split tables inside the
-            // bookkeeping kernel: no dense 2^side table written and re-read
-            equ_n = 0;
-            bk.eq_u = nullptr;
-        } else {
-            const std::uint8_t* fp_u = eq_fold_pow(f, W, uq);
-            launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st, fp_u, W.eq_hc.p);  // chi_x(u), sumcheck.hpp:415
-            equ_point = p1.challenges;
-            equ_n = T;
-            ctx->launched();
-            bk.eq_u = W.EqU.p;
-        }
+        const std::uint8_t* fp_u = eq_fold_pow(f, W, uq);
+        launch_split_eq_expand(kind, uq, T, W.EqU.p, ctx->st, fp_u, W.eq_hc.p);  // chi_x(u), sumcheck.hpp:415
+        equ_point = p1.challenges;
+        equ_n = T;
+        ctx->launched();
+        bk.eq_u = W.EqU.p;
         bk.perm = C.yperm.p;
         bk.seg = C.yseg.p;
         bk.heavy = C.yheavy.p;
@@ -2714,7 +2707,6 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         if (n == "small_round_pairs") tuning().small_round_pairs = value;
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
-        else if (n == "eq_on_the_fly") tuning().eq_on_the_fly = value;
         else if (n == "absorb_chains") {
             if (value < 1 || value > 4) fail(DGKR_INVALID_ARGUMENT, "absorb_chains must be 1..4");
             tuning().absorb_chains = value;
@@ -2729,7 +2721,6 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         if (n == "small_round_pairs") *value = tuning().small_round_pairs;
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
-        else if (n == "eq_on_the_fly") *value = tuning().eq_on_the_fly;
         else if (n == "absorb_chains") *value = tuning().absorb_chains;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });
