@@ -30,6 +30,7 @@ __constant__ RtFieldConst c_rt_field;
 
 struct Bn254 {
     static constexpr bool kRuntime = false;
+    static constexpr bool kWide = false;
     __device__ __forceinline__ static uint32_t p(int i) {
         constexpr uint32_t P[8] = {0xf0000001u, 0x43e1f593u, 0x79b97091u, 0x2833e848u,
                                    0x8181585du, 0xb85045b6u, 0xe131a029u, 0x30644e72u};
@@ -50,10 +51,19 @@ struct Bn254 {
 
 struct Rt {
     static constexpr bool kRuntime = true;
+    static constexpr bool kWide = false;
     __device__ __forceinline__ static uint32_t p(int i) { return c_rt_field.p[i]; }
     __device__ __forceinline__ static uint32_t np0() { return c_rt_field.np0; }
     __device__ __forceinline__ static uint32_t r2(int i) { return c_rt_field.r2[i]; }
     __device__ __forceinline__ static uint32_t one(int i) { return c_rt_field.one[i]; }
+};
+
+/// Runtime modulus with 2^254 <= p < 2^256 (the reference accepts any prime,
+/// field.hpp:26-40): a + b may carry out of 256 bits and 4p > 2^256, so adds
+/// are carry-aware, differences are fully reduced and products use the
+/// 10-limb CIOS with a 257-bit final comparison.
+struct RtW : Rt {
+    static constexpr bool kWide = true;
 };
 
 // ---------------------------------------------------------------------------
@@ -104,9 +114,49 @@ __device__ __forceinline__ void fe_store(Fe* p, const Fe& x) {
     q[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
 }
 
+/// a + b mod p for 2^254 <= p < 2^256: the sum's carry-out takes part in the comparison
+template <class F>
+__device__ __forceinline__ Fe fe_add_wide(const Fe& a, const Fe& b) {
+    Fe s, t;
+    uint32_t carry, borrow;
+    asm("add.cc.u32  %0, %9, %17;\n\t"
+        "addc.cc.u32 %1, %10, %18;\n\t"
+        "addc.cc.u32 %2, %11, %19;\n\t"
+        "addc.cc.u32 %3, %12, %20;\n\t"
+        "addc.cc.u32 %4, %13, %21;\n\t"
+        "addc.cc.u32 %5, %14, %22;\n\t"
+        "addc.cc.u32 %6, %15, %23;\n\t"
+        "addc.cc.u32 %7, %16, %24;\n\t"
+        "addc.u32    %8, 0, 0;"
+        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]),
+          "=r"(s.v[7]), "=r"(carry)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    asm("sub.cc.u32  %0, %9, %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(t.v[0]), "=r"(t.v[1]), "=r"(t.v[2]), "=r"(t.v[3]), "=r"(t.v[4]), "=r"(t.v[5]), "=r"(t.v[6]),
+          "=r"(t.v[7]), "=r"(borrow)
+        : "r"(s.v[0]), "r"(s.v[1]), "r"(s.v[2]), "r"(s.v[3]), "r"(s.v[4]), "r"(s.v[5]), "r"(s.v[6]), "r"(s.v[7]),
+          "r"(F::p(0)), "r"(F::p(1)), "r"(F::p(2)), "r"(F::p(3)), "r"(F::p(4)), "r"(F::p(5)), "r"(F::p(6)),
+          "r"(F::p(7)));
+    const bool keep = borrow && !carry;  // s < p and no carry: s is reduced
+    Fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.v[i] = keep ? s.v[i] : t.v[i];
+    return r;
+}
+
 /// r = a + b mod p (a, b < p < 2^254: the raw sum never carries out).
 template <class F>
 __device__ __forceinline__ Fe fe_add(const Fe& a, const Fe& b) {
+    if constexpr (F::kWide) return fe_add_wide<F>(a, b);
     Fe s, t;
     asm("add.cc.u32  %0, %8, %16;\n\t"
         "addc.cc.u32 %1, %9, %17;\n\t"
@@ -183,6 +233,7 @@ __device__ __forceinline__ Fe fe_sub(const Fe& a, const Fe& b) {
 /// the constant-multiplier path accepts any 256-bit input.
 template <class F>
 __device__ __forceinline__ Fe fe_sub_lazy(const Fe& b, const Fe& a) {
+    if constexpr (F::kWide) return fe_sub<F>(b, a);  // b - a + p may not fit 256 bits
     Fe r;
     asm("sub.cc.u32  %0, %8, %16;\n\t"
         "subc.cc.u32 %1, %9, %17;\n\t"
@@ -271,6 +322,58 @@ __device__ __forceinline__ Fe fe_reduce_once(const uint32_t (&t)[8]) {
     return r;
 }
 
+/// Montgomery product for 2^254 <= p < 2^256 (RtW): CIOS with a 10-limb
+/// running value (< 2p < 2^257 between rows, < 2^289 inside a row) and a
+/// final comparison that includes the 257th bit. Inputs < p.
+template <class F>
+__device__ __forceinline__ Fe fe_mul_wide(const Fe& a, const Fe& b) {
+    uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint64_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t s = static_cast<uint64_t>(a.v[j]) * b.v[i] + t[j] + c;
+            t[j] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        uint64_t s = static_cast<uint64_t>(t[8]) + c;
+        t[8] = static_cast<uint32_t>(s);
+        t[9] = static_cast<uint32_t>(s >> 32);
+        const uint32_t m = t[0] * F::np0();
+        c = (static_cast<uint64_t>(m) * F::p(0) + t[0]) >> 32;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const uint64_t s2 = static_cast<uint64_t>(m) * F::p(j) + t[j] + c;
+            t[j - 1] = static_cast<uint32_t>(s2);
+            c = s2 >> 32;
+        }
+        s = static_cast<uint64_t>(t[8]) + c;
+        t[7] = static_cast<uint32_t>(s);
+        t[8] = t[9] + static_cast<uint32_t>(s >> 32);
+    }
+    Fe d;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9, %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(F::p(0)),
+          "r"(F::p(1)), "r"(F::p(2)), "r"(F::p(3)), "r"(F::p(4)), "r"(F::p(5)), "r"(F::p(6)), "r"(F::p(7)));
+    const bool keep = borrow && t[8] == 0;  // the 257-bit value is below p
+    Fe r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = keep ? t[j] : d.v[j];
+    return r;
+}
+
 /// Montgomery product a*b*R^{-1} mod p, fully reduced: CIOS with even/odd
 /// split carry chains. The running value is T = E + O * 2^32 (E holds limb
 /// columns 0..7, O columns 1..8); a row adds the even limbs' products into E
@@ -284,6 +387,7 @@ __device__ __forceinline__ Fe fe_reduce_once(const uint32_t (&t)[8]) {
 /// before the final subtraction since 4p < R (p < 2^254).
 template <class F>
 __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
+    if constexpr (F::kWide) return fe_mul_wide<F>(a, b);
     uint32_t P[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) P[k] = F::p(k);
@@ -327,6 +431,7 @@ __device__ __forceinline__ Fe fe_mul(const Fe& a, const Fe& b) {
 /// remainder is not reduced.
 template <class F>
 __device__ __forceinline__ Fe fe_mul_any(const Fe& a, const Fe& b) {
+    if constexpr (F::kWide) return fe_mul_wide<F>(a, b);
     uint32_t t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {

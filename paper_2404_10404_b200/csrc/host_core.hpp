@@ -33,7 +33,7 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
 // ---------------------------------------------------------------------------
-// Field: runtime odd modulus p < 2^254, Montgomery form with R = 2^256.
+// Field: runtime odd modulus p < 2^256, Montgomery form with R = 2^256.
 // ---------------------------------------------------------------------------
 struct U256 {
     std::uint64_t w[4] = {0, 0, 0, 0};
@@ -89,7 +89,7 @@ public:
                 break;
             }
         }
-        if (bits_ > 254) fail(DGKR_UNSUPPORTED, "GPU prover supports moduli below 2^254");
+        if (bits_ > 256) fail(DGKR_UNSUPPORTED, "modulus wider than 256 bits");
         if ((p_.w[0] & 1) == 0) fail(DGKR_UNSUPPORTED, "GPU prover needs an odd modulus");
         if (bits_ < 2) fail(DGKR_INVALID_ARGUMENT, "modulus must be at least 2");
         width_ = (bits_ + 7) / 8;
@@ -124,8 +124,9 @@ public:
 
     U256 add(const U256& a, const U256& b) const {
         U256 r, s;
-        add_to(r, a, b);  // < 2^255, no carry
-        return sub_to(s, r, p_) ? r : s;
+        const std::uint64_t carry = add_to(r, a, b);  // a carry-out only for p >= 2^255
+        const std::uint64_t borrow = sub_to(s, r, p_);
+        return (borrow && !carry) ? r : s;
     }
     U256 sub(const U256& a, const U256& b) const {
         U256 r;
@@ -160,7 +161,8 @@ public:
             t[4] = t[5] + static_cast<std::uint64_t>(c >> 64);
         }
         U256 r{{t[0], t[1], t[2], t[3]}}, s;
-        return sub_to(s, r, p_) ? r : s;
+        const std::uint64_t borrow = sub_to(s, r, p_);
+        return (borrow && t[4] == 0) ? r : s;  // t[4]: the 257th bit (p close to 2^256)
     }
 
     U256 to_mont(const U256& canonical) const { return mul(canonical, r2_); }

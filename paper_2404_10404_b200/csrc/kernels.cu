@@ -1437,15 +1437,18 @@ __global__ void __launch_bounds__(kThreads) k_bitchange(std::uint64_t first, std
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
-#define DISPATCH_FIELD(kind, F, ...)    \
-    do {                                \
-        if ((kind) == FieldKind::Bn254) { \
-            using F = Bn254;            \
-            __VA_ARGS__;                \
-        } else {                        \
-            using F = Rt;               \
-            __VA_ARGS__;                \
-        }                               \
+#define DISPATCH_FIELD(kind, F, ...)              \
+    do {                                          \
+        if ((kind) == FieldKind::Bn254) {         \
+            using F = Bn254;                      \
+            __VA_ARGS__;                          \
+        } else if ((kind) == FieldKind::Runtime) { \
+            using F = Rt;                         \
+            __VA_ARGS__;                          \
+        } else {                                  \
+            using F = RtW;                        \
+            __VA_ARGS__;                          \
+        }                                         \
     } while (0)
 
 void upload_rt_field(const RtFieldHost& f, cudaStream_t st) {

@@ -11,9 +11,11 @@ namespace dgkr_b200 {
 
 struct Fe;  // 8 x u32 Montgomery limbs (fe.hpp)
 
-/// Which field policy a launch uses: the BN254 specialisation or the
-/// runtime-modulus path (constants uploaded with upload_rt_field()).
-enum class FieldKind : int { Bn254 = 0, Runtime = 1 };
+/// Which field policy a launch uses: the BN254 specialisation, the
+/// runtime-modulus path for p < 2^254 (constants uploaded with
+/// upload_rt_field()), or the wide runtime path for 2^254 <= p < 2^256
+/// (carry-aware adds, no lazy differences, 10-limb products).
+enum class FieldKind : int { Bn254 = 0, Runtime = 1, RuntimeWide = 2 };
 
 struct RtFieldHost {
     std::uint32_t p[8];

@@ -1483,7 +1483,7 @@ int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out
                                             0x79, 0x48, 0xe8, 0x33, 0x28, 0x5d, 0x58, 0x81, 0x81, 0xb6, 0x45,
                                             0x50, 0xb8, 0x29, 0xa0, 0x31, 0xe1, 0x72, 0x4e, 0x64, 0x30};
         HostField bnf(bn, 32);
-        f->kind = f->f.same(bnf) ? FieldKind::Bn254 : FieldKind::Runtime;
+        f->kind = f->f.same(bnf) ? FieldKind::Bn254 : (f->f.bits() > 254 ? FieldKind::RuntimeWide : FieldKind::Runtime);
         for (int i = 0; i < 4; ++i) {
             f->rt.p[2 * i] = static_cast<std::uint32_t>(f->f.p().w[i]);
             f->rt.p[2 * i + 1] = static_cast<std::uint32_t>(f->f.p().w[i] >> 32);

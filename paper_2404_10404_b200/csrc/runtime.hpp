@@ -377,7 +377,7 @@ struct Lane {
     }
 
     FieldKind use(const dgkr_field* f) {
-        if (f->kind == FieldKind::Runtime) {
+        if (f->kind != FieldKind::Bn254) {
             std::lock_guard<std::mutex> lk(rt->mu);
             if (!rt->valid || std::memcmp(&rt->cur, &f->rt, sizeof(RtFieldHost)) != 0) {
                 upload_rt_field(f->rt, st);

@@ -43,9 +43,27 @@ def test_field_widths(p):
 
 def test_field_rejects_unsupported_moduli():
     with pytest.raises(P._lib.DgkrError):
-        P.Field(2**255 + 95)  # > 254 bits: outside the GPU path
+        P.Field(2**256 + 297)  # 257 bits: wider than the 256-bit limbs
     with pytest.raises(P._lib.DgkrError):
         P.Field(1 << 20)  # even
+
+
+@pytest.mark.parametrize("p", [2**255 - 19, 2**256 - 2**32 - 977])
+def test_wide_moduli_host_field_matches_oracle(p):
+    """255- and 256-bit primes (the reference accepts any prime, field.hpp:26-40):
+    the host field's carry-aware add and 257-bit Montgomery reduction drive the
+    transcript exactly like the oracle"""
+    rng = np.random.default_rng(p % 1009)
+    f, of = P.Field(p), O.Field(p)
+    assert (f.width, f.bits) == (of.width, of.bits)
+    t, ot = P.Transcript(f, "wide", [3]), O.Transcript("wide", of, [3])
+    el = [p - 1, p - 2, 0, 1] + O.random_elements(of, 12, rng)
+    t.absorb_elems(el)
+    for e in el:
+        ot.absorb(e)
+    for _ in range(20):
+        assert t.challenge() == ot.challenge()
+    assert t.state == ot.state
 
 
 @pytest.mark.parametrize("p", [O.BN254_P, 97, O.GOLDILOCKS_P])
