@@ -4,7 +4,8 @@ byte for byte, over three families (a GPU box with oracle/_ref built):
   * data-parallel layered circuits of 2^13..2^17 gates per layer, so the BN254
     constant-multiplier chi expansion (k_split_eq_expand_const, klo >= 8) and
     the lazy-difference round kernels run at size;
-  * general circuits over the runtime-modulus path (p = 97, Goldilocks);
+  * general circuits over the runtime-modulus path (p = 97, Goldilocks) and
+    the wide path (255- and 256-bit primes);
   * the distributed prover (emulated ranks 2/4/8) against the single proof;
   * pcs commit roots and openings (M rows, random sizes, BN254/Goldilocks).
 usage: python tools/fuzz_parity.py [general_cases] [layered_cases] [seconds]
@@ -136,6 +137,8 @@ general(O.BN254, n_general, "gen")
 layered(n_layered)
 general(O.Field(O.GOLDILOCKS_P), n_general // 3, "gen")
 general(O.Field(97), n_general // 3, "gen")
+general(O.Field(2**255 - 19), n_general // 6, "gen")           # wide runtime policy (255 bits)
+general(O.Field(2**256 - 2**32 - 977), n_general // 6, "gen")  # wide runtime policy (256 bits)
 distributed(max(8, n_layered))
 pcs(max(20, n_layered * 2))
 print("total mismatches", bad)
