@@ -294,7 +294,10 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
  * "fuse_round1" = 1 (default 0: measured slower) builds single-slot bookkeeping tables by row
  * pairs with round 1 of the phase fused in, "absorb_chains" = 1..4 (default
  * 1: measured best) output absorbs a host thread interleaves in a proof
- * stream. Unknown names -> DGKR_INVALID_ARGUMENT. */
+ * stream, "tail_pairs" = the last rounds of a sum-check with <= this many
+ * output pairs run in one launch that trades sums and challenges with the
+ * host through a mapped-memory mailbox (default 256; 0 = one launch per
+ * round). Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);
 

@@ -231,23 +231,31 @@ __device__ __forceinline__ Fe foldk(const Fe& a, const Fe& b, const FoldConst& K
     return fe_add<F>(a, fe_mul_fold<F>(fe_sub_lazy<F>(b, a), K));
 }
 
-template <class F, int MODE>
+// CG: read through L2 only (ld.global.cg) -- for tables written earlier in
+// the same launch (k_round_tail), where the non-coherent path may be stale
+template <bool CG>
+__device__ __forceinline__ Fe fe_load_tab(const Fe* p) {
+    if constexpr (CG) return fe_ldcg(p);
+    else return fe_load_nc(p);
+}
+
+template <class F, int MODE, bool CG = false>
 __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __restrict__ dst, std::uint64_t i,
                                           std::uint64_t P, int log_p, const FoldConst& K, Fe& x0, Fe& x1) {
     if (MODE == kScan) {
-        x0 = fe_load_nc(src + 2 * i);
-        x1 = fe_load_nc(src + 2 * i + 1);
+        x0 = fe_load_tab<CG>(src + 2 * i);
+        x1 = fe_load_tab<CG>(src + 2 * i + 1);
     } else if (MODE == kFoldNat) {
-        const Fe a0 = fe_load_nc(src + 4 * i), a1 = fe_load_nc(src + 4 * i + 1);
-        const Fe b0 = fe_load_nc(src + 4 * i + 2), b1 = fe_load_nc(src + 4 * i + 3);
+        const Fe a0 = fe_load_tab<CG>(src + 4 * i), a1 = fe_load_tab<CG>(src + 4 * i + 1);
+        const Fe b0 = fe_load_tab<CG>(src + 4 * i + 2), b1 = fe_load_tab<CG>(src + 4 * i + 3);
         x0 = foldk<F>(a0, a1, K);
         x1 = foldk<F>(b0, b1, K);
         const std::uint64_t s = log_p ? (__brevll(i) >> (64 - log_p)) : 0;
         fe_store(dst + s, x0);
         fe_store(dst + s + P, x1);
     } else {
-        const Fe a0 = fe_load_nc(src + i), a1 = fe_load_nc(src + i + 2 * P);
-        const Fe b0 = fe_load_nc(src + i + P), b1 = fe_load_nc(src + i + 3 * P);
+        const Fe a0 = fe_load_tab<CG>(src + i), a1 = fe_load_tab<CG>(src + i + 2 * P);
+        const Fe b0 = fe_load_tab<CG>(src + i + P), b1 = fe_load_tab<CG>(src + i + 3 * P);
         x0 = foldk<F>(a0, a1, K);
         x1 = foldk<F>(b0, b1, K);
         fe_store(dst + i, x0);
@@ -269,22 +277,22 @@ __device__ __forceinline__ void sum_val(Fe& s, const Fe& g) { s = fe_add<F>(s, g
 template <class F>
 __device__ __forceinline__ void sum_val(Acc& s, const Fe& g) { acc_add_hi(s, g); }
 
-template <class F, int NP, bool HAS_G, int MODE, bool S1, class A>
+template <class F, int NP, bool HAS_G, int MODE, bool S1, class A, bool CG = false>
 __device__ __forceinline__ void round_body(const RoundParams& a, std::uint64_t i, A (&s)[S1 ? 3 : 2]) {
     constexpr int NS = S1 ? 3 : 2;
     const int np = NP > 0 ? NP : a.np;
     const std::uint64_t P = a.n_out_pairs;
     for (int k = 0; k < np; ++k) {
         Fe f0, f1, g0, g1;
-        load_pair<F, MODE>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, a.k, f0, f1);
-        load_pair<F, MODE>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
+        load_pair<F, MODE, CG>(a.in[2 * k], MODE != kScan ? a.out[2 * k] : nullptr, i, P, a.log_p, a.k, f0, f1);
+        load_pair<F, MODE, CG>(a.in[2 * k + 1], MODE != kScan ? a.out[2 * k + 1] : nullptr, i, P, a.log_p, a.k, g0, g1);
         sum_prod<F>(s[0], f0, g0);
         if constexpr (S1) sum_prod<F>(s[1], f1, g1);
         sum_prod<F>(s[NS - 1], fe_sub_lazy<F>(f1, f0), fe_sub_lazy<F>(g1, g0));
     }
     if (HAS_G) {
         Fe g0, g1;
-        load_pair<F, MODE>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, a.k, g0, g1);
+        load_pair<F, MODE, CG>(a.in[2 * np], MODE != kScan ? a.out[2 * np] : nullptr, i, P, a.log_p, a.k, g0, g1);
         sum_val<F>(s[0], g0);
         if constexpr (S1) sum_val<F>(s[1], g1);
     }
@@ -350,6 +358,102 @@ __global__ void k_fold_final(const Fe* const* in, Fe* const* out, int n_tabs, co
     if (t >= n_tabs) return;
     const Fe r = fe_load(rp);
     fe_store(out[t], fold1<F>(fe_load(in[t]), fe_load(in[t] + 1), r));
+}
+
+// ---------------------------------------------------------------------------
+// Sum-check tail in one launch (kernels.hpp TailLaunch): the per-round host
+// round trip (launch, d2h of the sums, stream sync, h2d of the challenge)
+// becomes a pinned-memory mailbox exchange with a resident CTA.
+// ---------------------------------------------------------------------------
+struct TailParams {
+    const Fe* const* in;
+    Fe* const* buf_a;
+    Fe* const* buf_b;
+    Fe* const* fin;
+    int np;
+    int ntab;
+    int j0;
+    int nv;
+    TailMailbox* mb;
+    std::uint32_t tag;
+    std::uint64_t timeout_ns;
+    FoldConst k;
+};
+
+__device__ __forceinline__ std::uint64_t globaltimer_ns() {
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <class F, int NP, bool HAS_G, bool S1>
+__global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__ TailParams t) {
+    constexpr int NS = S1 ? 3 : 2;
+    __shared__ Fe sh[32][NS];
+    __shared__ RoundParams rp;
+    __shared__ int stop;
+    TailMailbox* mb = t.mb;
+    if (threadIdx.x == 0) {
+        rp.in = t.in;
+        rp.out = nullptr;
+        rp.np = t.np;
+        rp.k = t.k;
+        stop = 0;
+    }
+    for (int j = t.j0; j <= t.nv; ++j) {
+        if (threadIdx.x == 0) {
+            rp.out = j >= 2 ? ((j % 2 == 0) ? t.buf_a : t.buf_b) : nullptr;
+            rp.log_p = t.nv - j;
+            rp.n_out_pairs = std::uint64_t{1} << rp.log_p;
+        }
+        __syncthreads();
+        Fe s[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s[k] = fe_zero();
+        for (std::uint64_t i = threadIdx.x; i < rp.n_out_pairs; i += blockDim.x) {
+            if (j == 1) round_body<F, NP, HAS_G, kScan, S1, Fe, true>(rp, i, s);
+            else if (j == 2) round_body<F, NP, HAS_G, kFoldNat, S1, Fe, true>(rp, i, s);
+            else round_body<F, NP, HAS_G, kFoldRev, S1, Fe, true>(rp, i, s);
+        }
+        block_sum<F, NS>(s, sh);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+#pragma unroll
+                for (int w = 0; w < 8; ++w) reinterpret_cast<volatile std::uint32_t*>(mb->sums[k])[w] = s[k].v[w];
+            __threadfence_system();
+            mb->d_seq = t.tag | static_cast<std::uint32_t>(j);
+            // the challenge of round j (its fold constants drive round j + 1 / the final fold)
+            const std::uint64_t t0 = globaltimer_ns();
+            for (;;) {
+                const std::uint32_t h = mb->h_seq;
+                if (h == (t.tag | static_cast<std::uint32_t>(j))) break;
+                if (h == kTailAbort) {  // the host gave up on this proof
+                    stop = 1;
+                    break;
+                }
+                if (globaltimer_ns() - t0 > t.timeout_ns) {
+                    stop = 1;
+                    mb->d_seq = kTailAbort;
+                    break;
+                }
+            }
+            __threadfence_system();  // acquire: the payload reads below see the host's writes
+        }
+        __syncthreads();
+        if (stop) return;
+        // the fold constants: one uncached read of host memory per thread, all in flight together
+        {
+            const volatile std::uint32_t* src = reinterpret_cast<const volatile std::uint32_t*>(mb->k);
+            std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&rp.k);
+            for (int w = threadIdx.x; w < static_cast<int>(sizeof(FoldConst) / 4); w += blockDim.x) dst[w] = src[w];
+        }
+        if (threadIdx.x == 0 && j >= 2) rp.in = rp.out;
+        __syncthreads();
+    }
+    // final fold of the 2-element tables with the last challenge
+    for (int tb = threadIdx.x; tb < t.ntab; tb += blockDim.x)
+        fe_store(t.fin[tb], fold1<F>(fe_ldcg(rp.in[tb]), fe_ldcg(rp.in[tb] + 1), rp.k.r));
 }
 
 template <class F>
@@ -1504,11 +1608,12 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0, 0, 1};  // fused round 1, interleaved absorbs: measured slower on C2
+        Tuning v{kSmallRoundPairs, 0, 0, 1, kSmallRoundPairs};  // fused round 1, interleaved absorbs: measured slower on C2
         if (const char* e = std::getenv("DGKR_ABSORB_CHAINS")) v.absorb_chains = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("DGKR_TAIL_PAIRS")) v.tail_pairs = std::strtoull(e, nullptr, 10);
         return v;
     }();
     return t;
@@ -1657,6 +1762,29 @@ void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, c
 #undef LAUNCH_ROUND
 #undef BY_MODE
     check_launch("round_small");
+}
+
+void launch_round_tail(FieldKind k, const TailLaunch& a, cudaStream_t st) {
+    TailParams p{a.in, a.buf_a, a.buf_b, a.fin, a.np, 2 * a.np + (a.has_g ? 1 : 0), a.j0, a.nv, a.mb, a.tag,
+                 a.timeout_ns, FoldConst{}};
+    static_assert(sizeof(FoldConst) == kFoldConstBytes, "FoldConst layout");
+    static_assert(sizeof(TailMailbox::k) == sizeof(FoldConst), "mailbox layout");
+    if (a.fold_const) std::memcpy(&p.k, a.fold_const, sizeof(FoldConst));
+    const std::uint64_t p0 = std::uint64_t{1} << (a.nv - a.j0);  // pairs of the first (largest) tail round
+    // >= 72 threads: each reads one word of the fold constants from host memory
+    const unsigned threads = p0 <= 128 ? 128u : kThreads;
+#define LAUNCH_TAIL(NP, HG)                                                            \
+    do {                                                                               \
+        if (a.need_s1) k_round_tail<F, NP, HG, true><<<1, threads, 0, st>>>(p);        \
+        else k_round_tail<F, NP, HG, false><<<1, threads, 0, st>>>(p);                 \
+    } while (0)
+    DISPATCH_FIELD(k, F, {
+        if (a.np == 1 && a.has_g) LAUNCH_TAIL(1, true);
+        else if (a.has_g) LAUNCH_TAIL(0, true);
+        else LAUNCH_TAIL(0, false);
+    });
+#undef LAUNCH_TAIL
+    check_launch("round_tail");
 }
 
 /// the constant-multiplier path applies: BN254, one term, rows of >= 256

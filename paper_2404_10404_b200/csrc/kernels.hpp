@@ -73,6 +73,47 @@ void launch_round(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStr
 void launch_round_small(FieldKind k, const RoundLaunch& a, const ReduceWs& ws, cudaStream_t st);
 constexpr std::uint64_t kSmallRoundPairs = 256;
 
+/// Host <-> device mailbox of the tail kernel (pinned, mapped host memory,
+/// one per lane). The two directions sit on separate 128-byte lines; each
+/// side posts a tag (generation << 8 | round) after its payload and waits
+/// for the other side's tag of the same round.
+struct alignas(128) TailMailbox {
+    volatile std::uint32_t d_seq;  // device -> host: sums of round (d_seq & 255) posted; kTailAbort on timeout
+    std::uint32_t pad0[31];
+    std::uint32_t sums[3][8];      // (S0, S1, S2) or (S0, S2), Montgomery form
+    std::uint32_t pad1[8];
+    volatile std::uint32_t h_seq;  // host -> device: fold constants of the challenge of round (h_seq & 255) posted
+    std::uint32_t pad2[31];
+    std::uint8_t k[kFoldConstBytes];  // FoldConst of that challenge
+};
+constexpr std::uint32_t kTailAbort = 0xffffffffu;
+
+/// The last rounds of a sum-check (round j0..nv, every one with <=
+/// tuning().tail_pairs output pairs) and the final fold in ONE launch of one
+/// CTA: after each round the CTA posts its sums to `mb`, spins until the
+/// host posts the fold constants of the challenge, and goes on (no launch,
+/// copy or stream sync per round). Round j0's constants come in `fold_const`
+/// (unused when j0 == 1). Tables ping-pong in A/B exactly like the
+/// per-round launches (round j writes A when j is even), finals go to fin.
+/// The kernel gives up after timeout_ns without a host answer (posts
+/// kTailAbort and exits).
+struct TailLaunch {
+    const Fe* const* in = nullptr;
+    Fe* const* buf_a = nullptr;
+    Fe* const* buf_b = nullptr;
+    Fe* const* fin = nullptr;
+    int np = 0;
+    bool has_g = false;
+    bool need_s1 = true;
+    int j0 = 1;
+    int nv = 1;
+    const void* fold_const = nullptr;
+    TailMailbox* mb = nullptr;
+    std::uint32_t tag = 0;  // generation << 8
+    std::uint64_t timeout_ns = 0;
+};
+void launch_round_tail(FieldKind k, const TailLaunch& a, cudaStream_t st);
+
 /// Process-wide launch tuning (dgkr_set_tuning; env DGKR_SMALL_PAIRS /
 /// DGKR_TMA_MIN_PAIRS give the start values): rounds of <= small_round_pairs
 /// output pairs run on one CTA; rounds of >= tma_min_pairs take the
@@ -82,6 +123,7 @@ struct Tuning {
     std::uint64_t tma_min_pairs;
     std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
     std::uint64_t absorb_chains;  // output absorbs interleaved per host thread in a proof stream (1..4)
+    std::uint64_t tail_pairs;     // rounds of <= tail_pairs output pairs run in one mailbox launch (0: off)
 };
 Tuning& tuning();
 

@@ -194,7 +194,39 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     const U256 zero{};
     U256 fk[9] = {};
     const int n_rounds = (stop_after >= 0 && stop_after < nv) ? stop_after : nv;
-    for (int j = 1; j <= n_rounds; ++j) {
+    // host side of a round: round polynomial from the device sums in
+    // h_small[1..], transcript, challenge, next fold constants (fk)
+    auto host_round = [&]() -> U256 {
+        const double t0 = now_ms();
+        const U256 s0 = to_u256(ctx->h_small[1]);
+        const U256 s1 = skip_s1 ? F.sub(run_claim, s0) : to_u256(ctx->h_small[2]);  // p(0) + p(1) = claim
+        const U256 s2 = to_u256(ctx->h_small[nres]);
+        RoundPoly rp;
+        rp.c[0] = s0;
+        rp.c[2] = s2;
+        rp.c[1] = F.sub(F.sub(s1, s0), s2);
+        for (int k = 0; k < 3; ++k) tr.absorb(rp.c[k]);
+        tr.absorb(zero);
+        const U256 r = tr.challenge();
+        if (skip_s1) run_claim = F.add(rp.c[0], F.mul(r, F.add(rp.c[1], F.mul(r, rp.c[2]))));  // p(r)
+        ctx->prof.host_transcript_ms += now_ms() - t0;
+        ctx->prof.rounds += 1;
+        out.rounds.push_back(rp);
+        out.challenges.push_back(r);
+        f->fold_const(r, fk);  // next round's fold constants (kernel parameters)
+        return r;
+    };
+    // the rounds with <= tail_pairs output pairs and the final fold run in one
+    // mailbox launch (launch_round_tail) where the sum-check runs to the end
+    // on this lane alone
+    int j_tail = n_rounds + 1;
+    if (const std::uint64_t tp = tuning().tail_pairs; tp && !comm && n_rounds == nv && nv >= 1) {
+        int j = 1;
+        while (j <= nv && (size0 >> j) > tp) ++j;
+        if (j == 1 && r1_done) j = 2;
+        if (j <= nv) j_tail = j;
+    }
+    for (int j = 1; j < j_tail; ++j) {
         RoundLaunch rl;
         rl.np = np;
         rl.has_g = has_g;
@@ -252,25 +284,63 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             ctx->prof.round_bytes += pairs * ntabs * 32 * (rl.mode ? 6 : 2);
             ctx->prof.round_mults += pairs * (nres * np + (rl.mode ? 2 * ntabs : 0));
         }
-        const double t0 = now_ms();
-        const U256 s0 = to_u256(ctx->h_small[1]);
-        const U256 s1 = skip_s1 ? F.sub(run_claim, s0) : to_u256(ctx->h_small[2]);  // p(0) + p(1) = claim
-        const U256 s2 = to_u256(ctx->h_small[nres]);
-        RoundPoly rp;
-        rp.c[0] = s0;
-        rp.c[2] = s2;
-        rp.c[1] = F.sub(F.sub(s1, s0), s2);
-        for (int k = 0; k < 3; ++k) tr.absorb(rp.c[k]);
-        tr.absorb(zero);
-        const U256 r = tr.challenge();
-        if (skip_s1) run_claim = F.add(rp.c[0], F.mul(r, F.add(rp.c[1], F.mul(r, rp.c[2]))));  // p(r)
-        ctx->prof.host_transcript_ms += now_ms() - t0;
-        ctx->prof.rounds += 1;
-        out.rounds.push_back(rp);
-        out.challenges.push_back(r);
-        f->fold_const(r, fk);  // next round's fold constants (kernel parameters)
+        const U256 r = host_round();
         ctx->h_small[0] = to_fe(r);
         ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
+    }
+    if (j_tail <= n_rounds) {
+        TailMailbox* mb = ctx->tail_mb;
+        ctx->tail_gen = ctx->tail_gen % 0xfffffeu + 1;  // tags never 0 nor kTailAbort
+        const std::uint32_t tag = ctx->tail_gen << 8;
+        TailLaunch tl;
+        tl.in = j_tail == 1 ? base : cur;
+        tl.buf_a = const_cast<Fe* const*>(rb.A());
+        tl.buf_b = const_cast<Fe* const*>(rb.B());
+        tl.fin = const_cast<Fe* const*>(rb.F());
+        tl.np = np;
+        tl.has_g = has_g;
+        tl.need_s1 = !skip_s1;
+        tl.j0 = j_tail;
+        tl.nv = nv;
+        tl.fold_const = fk;
+        tl.mb = ctx->tail_mb_dev;
+        tl.tag = tag;
+        tl.timeout_ns = 30ull * 1000 * 1000 * 1000;
+        std::uint32_t* d_seq = const_cast<std::uint32_t*>(&mb->d_seq);
+        std::uint32_t* h_seq = const_cast<std::uint32_t*>(&mb->h_seq);
+        __atomic_store_n(d_seq, 0u, __ATOMIC_RELEASE);
+        __atomic_store_n(h_seq, 0u, __ATOMIC_RELEASE);  // clear a previous abort
+        launch_round_tail(kind, tl, ctx->st);
+        ctx->launched();
+        try {
+            for (int j = j_tail; j <= nv; ++j) {
+                const std::uint32_t want = tag | static_cast<std::uint32_t>(j);
+                const double t0 = now_ms();
+                for (std::uint32_t spin = 1;; ++spin) {
+                    const std::uint32_t v = __atomic_load_n(d_seq, __ATOMIC_ACQUIRE);
+                    if (v == want) break;
+                    if (v == kTailAbort) fail(DGKR_CUDA_ERROR, "sum-check tail kernel timed out waiting for the host");
+                    if ((spin & 4095) == 0) {
+                        const cudaError_t q = cudaStreamQuery(ctx->st);
+                        if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
+                        if (q == cudaSuccess && __atomic_load_n(d_seq, __ATOMIC_ACQUIRE) != want)
+                            fail(DGKR_CUDA_ERROR, "sum-check tail kernel ended without posting round sums");
+                        if (now_ms() - t0 > 60e3) fail(DGKR_CUDA_ERROR, "sum-check tail kernel: no round sums in 60 s");
+                    }
+                }
+                std::memcpy(ctx->h_small + 1, mb->sums, nres * sizeof(Fe));
+                const U256 r = host_round();
+                std::memcpy(mb->k, fk, kFoldConstBytes);
+                __atomic_store_n(h_seq, want, __ATOMIC_RELEASE);
+                if (j == nv) {  // d_small[0] holds the last challenge, as after the per-round path
+                    ctx->h_small[0] = to_fe(r);
+                    ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
+                }
+            }
+        } catch (...) {
+            __atomic_store_n(h_seq, kTailAbort, __ATOMIC_RELEASE);  // release the CTA
+            throw;
+        }
     }
     out.claim_end = run_claim;
     if (n_rounds < nv) {
@@ -299,8 +369,10 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     }
     // final fold of the 2-element tables (or read the 1-element tables)
     if (nv >= 1) {
-        launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
-        ctx->launched();
+        if (j_tail > nv) {  // else the tail kernel folded them
+            launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
+            ctx->launched();
+        }
         Fe* hf = ctx->h_small + Lane::kFinalsOff;
         ctx->d2h(hf, rb.finals.p, ntab * sizeof(Fe));
         ctx->sync();
@@ -2707,6 +2779,7 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         if (n == "small_round_pairs") tuning().small_round_pairs = value;
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
+        else if (n == "tail_pairs") tuning().tail_pairs = value;
         else if (n == "absorb_chains") {
             if (value < 1 || value > 4) fail(DGKR_INVALID_ARGUMENT, "absorb_chains must be 1..4");
             tuning().absorb_chains = value;
@@ -2721,6 +2794,7 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         if (n == "small_round_pairs") *value = tuning().small_round_pairs;
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
+        else if (n == "tail_pairs") *value = tuning().tail_pairs;
         else if (n == "absorb_chains") *value = tuning().absorb_chains;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });

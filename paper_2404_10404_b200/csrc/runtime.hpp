@@ -313,6 +313,9 @@ struct Lane {
     DBuf<int> d_err;
     DBuf<int> d_flag;       // kernel-raised predicate flags (distinct checks)
     Fe* h_small = nullptr;  // pinned mirror of d_small
+    TailMailbox* tail_mb = nullptr;      // pinned, mapped: the tail kernel's mailbox (host view)
+    TailMailbox* tail_mb_dev = nullptr;  // its device address
+    std::uint32_t tail_gen = 0;          // generation of the last tail launch (mailbox tags)
     // pinned staging layout (Fe units): [0] challenge, [1..4) reduction
     // results, [16, 8192) eq-table points/seeds, [8192, 12288) slot values,
     // [12288, 16384) round finals.
@@ -357,6 +360,9 @@ struct Lane {
         CK(cudaMemset(d_err.p, 0, sizeof(int)));
         d_flag.ensure(2);
         CK(cudaMallocHost(reinterpret_cast<void**>(&h_small), kSmall * sizeof(Fe)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&tail_mb), sizeof(TailMailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(static_cast<void*>(tail_mb), 0, sizeof(TailMailbox));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&tail_mb_dev), tail_mb, 0));
         CK(cudaEventCreate(&ev0));
         CK(cudaEventCreate(&ev1));
         CK(cudaEventCreateWithFlags(&ev_sync, cudaEventBlockingSync | cudaEventDisableTiming));
@@ -371,6 +377,7 @@ struct Lane {
         if (up_ring) cudaFreeHost(up_ring);
         if (ev_sync) cudaEventDestroy(ev_sync);
         if (h_small) cudaFreeHost(h_small);
+        if (tail_mb) cudaFreeHost(tail_mb);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st) cudaStreamDestroy(st);

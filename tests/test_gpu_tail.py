@@ -1,0 +1,114 @@
+"""GPU: the sum-check tail in one launch (kernels.cu k_round_tail, tuning
+"tail_pairs"). The last rounds of every sum-check and the final fold run on a
+resident CTA that trades round sums and challenges with the host through a
+mapped-memory mailbox. Whatever the threshold -- 0 (a launch per round), 1,
+4, the default 256, or so large that whole sum-checks run in the tail from
+round 1 (scan, natural fold and bit-reversed folds all inside the kernel) --
+proofs and transcripts must be byte-identical to the compiled reference and
+the Python oracle, on BN254, Goldilocks, p = 97 and a 255-bit modulus."""
+import numpy as np
+import pytest
+
+import paper_2404_10404_b200 as P
+from oracle import dgkr_oracle as O
+from oracle import refbind as R
+from paper_2404_10404_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+THRESHOLDS = [0, 1, 4, 256, 1 << 22]
+
+
+@pytest.fixture
+def tail_knob():
+    old = P.get_tuning("tail_pairs")
+    yield lambda v: P.set_tuning("tail_pairs", v)
+    P.set_tuning("tail_pairs", old)
+
+
+def test_tail_knob_roundtrip(tail_knob):
+    assert P.get_tuning("tail_pairs") == 256  # the default
+    tail_knob(17)
+    assert P.get_tuning("tail_pairs") == 17
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, O.GOLDILOCKS_P, 97, 2**255 - 19])
+@pytest.mark.parametrize("log_w,copies,depth", [(4, 1, 3), (9, 4, 3), (12, 2, 2)])
+def test_tail_gkr_any_threshold(ctx, tail_knob, p, log_w, copies, depth):
+    f = P.Field(p)
+    insz, flat = W.layered_circuit(500 + log_w, log_w, depth)
+    inputs = W.random_inputs(f.p, insz * copies, log_w + copies)
+    circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+    got = set()
+    for tp in THRESHOLDS:
+        tail_knob(tp)
+        tr = P.Transcript(f, "tail.gkr")
+        got.add((P.gkr_prove(ctx, circ, inputs, tr), tr.state))
+    assert len(got) == 1
+
+
+def test_tail_gkr_equals_reference(ctx, tail_knob):
+    assert R.available()
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(4343, 9, 4)
+    copies = 8
+    inputs = W.random_inputs(f.p, insz * copies, 6)
+    full_in, full_flat = W.replicate(insz, flat, copies)
+    want, want_state = R.gkr_prove(O.BN254, "tail.ref", [], O.Circuit.from_flat(full_in, *full_flat),
+                                   O.BN254.elems_from_bytes(inputs.tobytes()), flat=full_flat)
+    circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+    for tp in (256, 1 << 22):
+        tail_knob(tp)
+        tr = P.Transcript(f, "tail.ref")
+        assert P.gkr_prove(ctx, circ, inputs, tr) == want
+        assert tr.state == want_state
+
+
+@pytest.mark.parametrize("p", [O.BN254_P, 97])
+@pytest.mark.parametrize("vars_,n_pairs", [(1, 1), (2, 3), (9, 2), (13, 1)])
+def test_tail_product_sum(ctx, tail_knob, p, vars_, n_pairs):
+    """need_s1 = true (no prover-side claim): all three sums cross the mailbox."""
+    rng = np.random.default_rng(vars_ * 11 + n_pairs)
+    f, of = P.Field(p), O.Field(p)
+    pairs = [(O.random_elements(of, 1 << vars_, rng), O.random_elements(of, 1 << vars_, rng))
+             for _ in range(n_pairs)]
+    otr = O.Transcript("tail.sc", of, [3])
+    want = O.prove_product_sum(pairs, otr).to_bytes(of)
+    for tp in THRESHOLDS:
+        tail_knob(tp)
+        tr = P.Transcript(f, "tail.sc", [3])
+        assert P.prove_product_sum(ctx, pairs, tr) == want
+        assert tr.state == otr.state
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_tail_distributed_tail_rounds(ctx, tail_knob, world):
+    """The distributed prover's redundant tail rounds (after the early
+    boundary) run through the mailbox kernel; proofs equal the single GPU's."""
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(91, 11, 2)
+    copies = 16
+    inputs = W.random_inputs(f.p, insz * copies, 4)
+    tail_knob(0)
+    tr = P.Transcript(f, "tail.dist")
+    single = P.gkr_prove(ctx, P.Circuit(ctx, insz, *flat, n_copies=copies), inputs, tr)
+    tail_knob(256)
+    tr2 = P.Transcript(f, "tail.dist")
+    got = P.gkr_prove_dist_emulated(ctx, P.Circuit(ctx, insz, *flat, n_copies=copies // world), world, inputs, tr2)
+    assert got == single and tr2.state == tr.state
+
+
+def test_tail_stream_lanes(ctx, tail_knob):
+    """Concurrent lanes each run their own mailbox: a proof stream over 8
+    lanes with distinct inputs equals the single proofs."""
+    tail_knob(256)
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(2024, 10, 3)
+    copies = 4
+    circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+    ins = [W.random_inputs(f.p, insz * copies, 40 + i) for i in range(8)]
+    singles = []
+    for x in ins:
+        tr = P.Transcript(f, "tail.lanes")
+        singles.append(P.gkr_prove(ctx, circ, x, tr))
+    trs = [P.Transcript(f, "tail.lanes") for _ in ins]
+    assert P.gkr_prove_batch(ctx, circ, ins, trs) == singles
