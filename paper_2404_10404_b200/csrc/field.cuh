@@ -114,6 +114,56 @@ __device__ __forceinline__ void fe_store(Fe* p, const Fe& x) {
     q[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
 }
 
+// One 256-bit access per element (LDG/STG .ENL2.256, new on sm_100) for
+// tables in global memory, whose elements are 32-byte aligned (cudaMalloc
+// bases, Fe-strided offsets): half the load/store instructions of the
+// two-uint4 forms above. DGKR_V8=0 builds the uint4 forms (A/B).
+#ifndef DGKR_V8
+#define DGKR_V8 1
+#endif
+__device__ __forceinline__ Fe fe_load_nc32(const Fe* p) {
+#if DGKR_V8
+    Fe r;
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]),
+          "=r"(r.v[7])
+        : "l"(p));
+    return r;
+#else
+    return fe_load_nc(p);
+#endif
+}
+
+/// L2-only (coherent within a launch) 256-bit load
+__device__ __forceinline__ Fe fe_ldcg32(const Fe* p) {
+    Fe r;
+#if DGKR_V8
+    asm volatile("ld.global.cg.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                   "=r"(r.v[6]), "=r"(r.v[7])
+                 : "l"(p)
+                 : "memory");
+#else
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 a = __ldcg(q), b = __ldcg(q + 1);
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+#endif
+    return r;
+}
+
+// no "memory" clobber, so later table loads can still be hoisted above it:
+// nothing in a launch reads these stores back except through fe_ldcg32
+// (volatile, ordered after it) or after a grid-wide sync
+__device__ __forceinline__ void fe_store32(Fe* p, const Fe& x) {
+#if DGKR_V8
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(x.v[0]), "r"(x.v[1]),
+                 "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]), "r"(x.v[7]));
+#else
+    fe_store(p, x);
+#endif
+}
+
 /// a + b mod p for 2^254 <= p < 2^256: the sum's carry-out takes part in the comparison
 template <class F>
 __device__ __forceinline__ Fe fe_add_wide(const Fe& a, const Fe& b) {

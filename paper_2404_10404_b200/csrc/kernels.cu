@@ -235,8 +235,8 @@ __device__ __forceinline__ Fe foldk(const Fe& a, const Fe& b, const FoldConst& K
 // the same launch (k_round_tail), where the non-coherent path may be stale
 template <bool CG>
 __device__ __forceinline__ Fe fe_load_tab(const Fe* p) {
-    if constexpr (CG) return fe_ldcg(p);
-    else return fe_load_nc(p);
+    if constexpr (CG) return fe_ldcg32(p);
+    else return fe_load_nc32(p);
 }
 
 template <class F, int MODE, bool CG = false>
@@ -251,15 +251,15 @@ __device__ __forceinline__ void load_pair(const Fe* __restrict__ src, Fe* __rest
         x0 = foldk<F>(a0, a1, K);
         x1 = foldk<F>(b0, b1, K);
         const std::uint64_t s = log_p ? (__brevll(i) >> (64 - log_p)) : 0;
-        fe_store(dst + s, x0);
-        fe_store(dst + s + P, x1);
+        fe_store32(dst + s, x0);
+        fe_store32(dst + s + P, x1);
     } else {
         const Fe a0 = fe_load_tab<CG>(src + i), a1 = fe_load_tab<CG>(src + i + 2 * P);
         const Fe b0 = fe_load_tab<CG>(src + i + P), b1 = fe_load_tab<CG>(src + i + 3 * P);
         x0 = foldk<F>(a0, a1, K);
         x1 = foldk<F>(b0, b1, K);
-        fe_store(dst + i, x0);
-        fe_store(dst + i + P, x1);
+        fe_store32(dst + i, x0);
+        fe_store32(dst + i + P, x1);
     }
 }
 
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_total(const Fe* const* tabs, 
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         for (int k = 0; k < np; ++k) {
-            s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc(tabs[2 * k] + i), fe_load_nc(tabs[2 * k + 1] + i)));
+            s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc32(tabs[2 * k] + i), fe_load_nc32(tabs[2 * k + 1] + i)));
         }
     }
     grid_finish<F, 1>(s, partials, counter, result);
@@ -495,10 +495,10 @@ template <class F>
 __device__ __forceinline__ Fe split_eq(const SplitEq& e, std::uint64_t g) {
     g += e.offset;
     const std::uint64_t lo = g & ((std::uint64_t{1} << e.klo) - 1), hi = g >> e.klo;
-    Fe w = fe_mul<F>(fe_load_nc(e.A + lo), fe_load_nc(e.B + hi));
+    Fe w = fe_mul<F>(fe_load_nc32(e.A + lo), fe_load_nc32(e.B + hi));
     for (int t = 1; t < e.K; ++t) {
-        w = fe_add<F>(w, fe_mul<F>(fe_load_nc(e.A + (static_cast<std::uint64_t>(t) << e.klo) + lo),
-                                   fe_load_nc(e.B + (static_cast<std::uint64_t>(t) << e.khi) + hi)));
+        w = fe_add<F>(w, fe_mul<F>(fe_load_nc32(e.A + (static_cast<std::uint64_t>(t) << e.klo) + lo),
+                                   fe_load_nc32(e.B + (static_cast<std::uint64_t>(t) << e.khi) + hi)));
     }
     return w;
 }
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kThreads) k_split_eq_expand_add(SplitEq e, std
                                                                   const Fe* __restrict__ dense, Fe* __restrict__ out) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        fe_store(out + i, fe_add<F>(fe_load_nc(dense + i), split_eq<F>(e, i)));
+        fe_store32(out + i, fe_add<F>(fe_load_nc32(dense + i), split_eq<F>(e, i)));
     }
 }
 
@@ -517,7 +517,7 @@ template <class F>
 __global__ void __launch_bounds__(kThreads) k_split_eq_expand(SplitEq e, std::uint64_t n, Fe* __restrict__ out) {
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        fe_store(out + i, split_eq<F>(e, i));
+        fe_store32(out + i, split_eq<F>(e, i));
     }
 }
 
@@ -563,9 +563,9 @@ __global__ void __launch_bounds__(kThreads) k_split_eq_expand_const(const Fe* __
             cur = h;
         }
         const std::uint64_t i = (q << 8) + threadIdx.x;
-        Fe w = fe_mul_const_bn254(fe_load_nc(A + ((g0 + threadIdx.x) & mask)), K);
-        if (dense) w = fe_add<Bn254>(fe_load_nc(dense + i), w);
-        fe_store(out + i, w);
+        Fe w = fe_mul_const_bn254(fe_load_nc32(A + ((g0 + threadIdx.x) & mask)), K);
+        if (dense) w = fe_add<Bn254>(fe_load_nc32(dense + i), w);
+        fe_store32(out + i, w);
     }
 }
 
@@ -600,15 +600,15 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep1_sorted(BookkeepLaunch a)
         Fe h = fe_zero(), gacc = fe_zero();
         for (std::uint32_t e = sg.x; e < sg.x + n_e; ++e) {
             const uint4 en = sd.ent[e];
-            const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
-            const Fe vy = fe_load_nc(sd.V + ((c << sd.log_stride) | en.y));
+            const Fe w = fe_load_nc32(a.gate_w + ((c << a.log_gcons) | en.x));
+            const Fe vy = fe_load_nc32(sd.V + ((c << sd.log_stride) | en.y));
             const Fe prod = fe_mul<F>(w, vy);
             const bool mul = en.z >> 31;
             h = fe_add<F>(h, fe_select<F>(mul, prod, w));
             gacc = fe_select<F>(mul, gacc, fe_add<F>(gacc, prod));
         }
-        fe_store(sd.out + x, h);
-        fe_store(a.G + x, gacc);
+        fe_store32(sd.out + x, h);
+        fe_store32(a.G + x, gacc);
     }
 }
 
@@ -628,16 +628,16 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep2_sorted(const __grid_cons
         Fe ma = fe_zero(), cacc = fe_zero();
         for (std::uint32_t e = sg.x; e < sg.x + n_e; ++e) {
             const uint4 en = sd.ent[e];
-            const Fe w = fe_load_nc(a.gate_w + ((c << a.log_gcons) | en.x));
-            const Fe eu = fe_load_nc(a.eq_u + ((c << sd.log_stride) | en.y));
+            const Fe w = fe_load_nc32(a.gate_w + ((c << a.log_gcons) | en.x));
+            const Fe eu = fe_load_nc32(a.eq_u + ((c << sd.log_stride) | en.y));
             const Fe cx = fe_mul<F>(w, eu);
             const Fe prod = fe_mul_fold<F>(cx, vxk);  // V(u) is a per-launch constant
             const bool mul = en.z >> 31;
             ma = fe_add<F>(ma, fe_select<F>(mul, prod, cx));
             cacc = fe_select<F>(mul, cacc, fe_add<F>(cacc, prod));
         }
-        fe_store(sd.out + y, ma);
-        fe_store(a.G + y, cacc);
+        fe_store32(sd.out + y, ma);
+        fe_store32(a.G + y, cacc);
     }
 }
 
@@ -711,21 +711,21 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase1(BookkeepLaunch a) 
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
-                    const Fe w = a.wire_w   ? fe_load_nc(a.wire_w + en.w)
-                                 : a.gate_w ? fe_load_nc(a.gate_w + g)
+                    const Fe w = a.wire_w   ? fe_load_nc32(a.wire_w + en.w)
+                                 : a.gate_w ? fe_load_nc32(a.gate_w + g)
                                             : split_eq<F>(a.w, g);
                     const std::uint32_t ys = en.z & 0x7fffffffu;
                     const SlotDesc sy = a.slots[ys];
-                    const Fe vy = fe_load_nc(sy.V + ((c << sy.log_stride) | en.y));
+                    const Fe vy = fe_load_nc32(sy.V + ((c << sy.log_stride) | en.y));
                     const Fe prod = fe_mul<F>(w, vy);
                     const bool mul = en.z >> 31;
                     h = fe_add<F>(h, fe_select<F>(mul, prod, w));
                     gacc = fe_select<F>(mul, gacc, fe_add<F>(gacc, prod));
                 }
             }
-            fe_store(sd.out + x, h);
+            fe_store32(sd.out + x, h);
         }
-        fe_store(a.G + x, gacc);
+        fe_store32(a.G + x, gacc);
     }
 }
 
@@ -744,12 +744,12 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
                 for (std::uint32_t e = e0; e < e1; ++e) {
                     const uint4 en = sd.ent[e];
                     const std::uint64_t g = (c << a.log_gcons) | en.x;
-                    const Fe w = a.wire_w   ? fe_load_nc(a.wire_w + en.w)
-                                 : a.gate_w ? fe_load_nc(a.gate_w + g)
+                    const Fe w = a.wire_w   ? fe_load_nc32(a.wire_w + en.w)
+                                 : a.gate_w ? fe_load_nc32(a.gate_w + g)
                                             : split_eq<F>(a.w, g);
                     const std::uint32_t xs = en.z & 0x7fffffffu;
                     const std::uint64_t x = (c << a.slots[xs].log_stride) | en.y;
-                    const Fe cx = fe_mul<F>(w, a.eq_u ? fe_load_nc(a.eq_u + x) : split_eq<F>(a.u, x));
+                    const Fe cx = fe_mul<F>(w, a.eq_u ? fe_load_nc32(a.eq_u + x) : split_eq<F>(a.u, x));
                     const Fe vx = fe_load(a.vx + xs);
                     const Fe prod = fe_mul<F>(cx, vx);
                     const bool mul = en.z >> 31;
@@ -757,9 +757,9 @@ __global__ void __launch_bounds__(kThreads) k_bookkeep_phase2(BookkeepLaunch a) 
                     cacc = fe_select<F>(mul, cacc, fe_add<F>(cacc, prod));
                 }
             }
-            fe_store(sd.out + y, ma);
+            fe_store32(sd.out + y, ma);
         }
-        fe_store(a.G + y, cacc);
+        fe_store32(a.G + y, cacc);
     }
 }
 
@@ -771,7 +771,7 @@ constexpr int kHeavyThreads = 128;
 template <class F>
 __device__ __forceinline__ Fe bk_weight(const BookkeepLaunch& a, std::uint64_t c, const uint4& en) {
     const std::uint64_t g = (c << a.log_gcons) | en.x;
-    return a.wire_w ? fe_load_nc(a.wire_w + en.w) : a.gate_w ? fe_load_nc(a.gate_w + g) : split_eq<F>(a.w, g);
+    return a.wire_w ? fe_load_nc32(a.wire_w + en.w) : a.gate_w ? fe_load_nc32(a.gate_w + g) : split_eq<F>(a.w, g);
 }
 
 template <class F, int PHASE>
@@ -847,12 +847,12 @@ __global__ void __launch_bounds__(kThreads) k_evaluate(EvalLaunch a) {
             for (std::uint32_t k = k0; k < k1; ++k) {
                 const uint4 e = a.nested[k];
                 const std::uint32_t ll = (e.x >> 1) & 0x7fffu, rl = e.x >> 16;
-                const Fe va = fe_load_nc(a.layer_vals[ll] + ((c << a.layer_log_stride[ll]) | e.y));
-                const Fe vb = fe_load_nc(a.layer_vals[rl] + ((c << a.layer_log_stride[rl]) | e.z));
+                const Fe va = fe_load_nc32(a.layer_vals[ll] + ((c << a.layer_log_stride[ll]) | e.y));
+                const Fe vb = fe_load_nc32(a.layer_vals[rl] + ((c << a.layer_log_stride[rl]) | e.z));
                 acc = fe_add<F>(acc, (e.x & 1) ? fe_mul<F>(va, vb) : fe_add<F>(va, vb));
             }
         }
-        fe_store(a.out + gw, acc);
+        fe_store32(a.out + gw, acc);
     }
 }
 
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_eval(const Fe* __restrict__ 
     Fe s[1] = {fe_zero()};
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc(t + i), split_eq<F>(e, i)));
+        s[0] = fe_add<F>(s[0], fe_mul<F>(fe_load_nc32(t + i), split_eq<F>(e, i)));
     }
     grid_finish<F, 1>(s, partials, counter, result);
 }
