@@ -387,7 +387,9 @@ def run_b200(args, cfg_name):
             "host_transcript_total_per_proof": phase["host_transcript_ms"] / args.steps / lanes,
             "round_kernels": prof["round_ms"], "bookkeeping_kernels": prof["bookkeep_ms"],
             "evaluate_kernels": prof["evaluate_ms"], "rounds_per_proof": phase["rounds"] // (args.steps * lanes),
-            "note": "kernel times from one profiled single proof (per-launch CUDA events)"},
+            "tail_launches_incl_host_exchange": prof["tail_ms"], "tail_rounds_per_proof": prof["tail_rounds"],
+            "note": "kernel times from one profiled single proof (per-launch CUDA events); round_kernels and the "
+                    "roofline cover the rounds with > 256 pairs, the smaller ones run inside the tail launches"},
         "roofline": {"bound": "hbm", "kernel": "k_round (fused fold+round)", "achieved": achieved_gbs,
                      "peak": peak_gbs, "unit": "GB/s", "frac": (achieved_gbs / peak_gbs) if achieved_gbs else None,
                      "traffic": traffic, "traffic_over_algorithmic": traffic_ratio, "peak_source": peak_src,

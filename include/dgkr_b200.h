@@ -75,14 +75,18 @@ typedef struct dgkr_profile {
     double ntt_ms;              /* NTT / RS-encode kernels (bit-reverse + butterflies) */
     double merkle_ms;           /* leaf digests + Merkle tree kernels (PCS, FRI) */
     double fold_ms;             /* FRI fold kernels */
+    double tail_ms;             /* sum-check tail launches (k_round_tail), incl. the host's
+                                   transcript work between their rounds */
+    uint64_t tail_rounds;       /* rounds run inside tail launches (not in round_ms / round_bytes) */
 } dgkr_profile;
 
 const char* dgkr_last_error(void);
 int dgkr_abi_version(void); /* 2 */
 
 /* ---- field (field.hpp:23-80) ------------------------------------------- */
-/* modulus: little-endian bytes. The GPU path supports odd p < 2^254
- * (BN254 Fr is specialised; other moduli take the runtime-modulus path). */
+/* modulus: little-endian bytes. The GPU path supports any odd p < 2^256
+ * (BN254 Fr is specialised; other moduli take the runtime-modulus path,
+ * 2^254 <= p the wide variant of it). */
 int dgkr_field_create(const uint8_t* modulus_le, size_t len, dgkr_field** out);
 void dgkr_field_destroy(dgkr_field* f);
 size_t dgkr_field_width(const dgkr_field* f);   /* field.hpp:67 byte_width() */

@@ -109,6 +109,8 @@ class Profile_t(C.Structure):
         ("ntt_ms", C.c_double),
         ("merkle_ms", C.c_double),
         ("fold_ms", C.c_double),
+        ("tail_ms", C.c_double),
+        ("tail_rounds", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -310,6 +310,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         std::uint32_t* h_seq = const_cast<std::uint32_t*>(&mb->h_seq);
         __atomic_store_n(d_seq, 0u, __ATOMIC_RELEASE);
         __atomic_store_n(h_seq, 0u, __ATOMIC_RELEASE);  // clear a previous abort
+        ctx->tbeg();
         launch_round_tail(kind, tl, ctx->st);
         ctx->launched();
         try {
@@ -341,6 +342,8 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             __atomic_store_n(h_seq, kTailAbort, __ATOMIC_RELEASE);  // release the CTA
             throw;
         }
+        ctx->tend(ctx->prof.tail_ms);
+        ctx->prof.tail_rounds += static_cast<std::uint64_t>(nv - j_tail + 1);
     }
     out.claim_end = run_claim;
     if (n_rounds < nv) {
