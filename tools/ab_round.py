@@ -14,7 +14,8 @@ from paper_2404_10404_b200 import workloads as W  # noqa: E402
 from paper_2404_10404_b200._lib import check, lib  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-settings = [int(x) for x in sys.argv[2:]] or [0, 1 << 14]
+# settings: integers (tma_min_pairs) or knob=value
+settings = [x if "=" in x else int(x) for x in sys.argv[2:]] or [0, 1 << 14]
 n_copies, lw, depth = {"c2": (64, 16, 24), "c1": (1, 12, 16), "small": (4, 12, 4)}[cfg]
 ctx = P.Context(0)
 f = P.Field.bn254()
@@ -27,7 +28,11 @@ buf = C.create_string_buffer(cap)
 ln = C.c_size_t()
 states = set()
 for tma in settings:
-    P.set_tuning("tma_min_pairs", tma)
+    if isinstance(tma, str):
+        knob, val = tma.split("=")
+        P.set_tuning(knob, int(val))
+    else:
+        P.set_tuning("tma_min_pairs", tma)
     for prof in (False, True, True):
         ctx.set_profile(prof)
         tr = P.Transcript(f, "dgkr.bench.c2")
@@ -35,7 +40,7 @@ for tma in settings:
                                             C.byref(ln)))
     pr = ctx.profile()
     states.add(tr.state.hex())
-    print(json.dumps({"cfg": cfg, "tma_min_pairs": tma, "round_ms": pr["round_ms"], "bookkeep_ms": pr["bookkeep_ms"],
+    print(json.dumps({"cfg": cfg, "setting": tma, "round_ms": pr["round_ms"], "bookkeep_ms": pr["bookkeep_ms"],
                       "evaluate_ms": pr["evaluate_ms"], "total_ms": pr["total_ms"],
                       "round_GBps": pr["round_bytes"] / pr["round_ms"] / 1e6, "state": tr.state.hex()[:16]}),
           flush=True)
