@@ -78,6 +78,7 @@ typedef struct dgkr_profile {
     double tail_ms;             /* sum-check tail launches (k_round_tail), incl. the host's
                                    transcript work between their rounds */
     uint64_t tail_rounds;       /* rounds run inside tail launches (not in round_ms / round_bytes) */
+    uint64_t tail_aborts;       /* tail launches that gave up waiting for the host (rest run per round) */
 } dgkr_profile;
 
 const char* dgkr_last_error(void);
@@ -301,7 +302,10 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
  * stream, "tail_pairs" = the last rounds of a sum-check with <= this many
  * output pairs run in one launch that trades sums and challenges with the
  * host through a mapped-memory mailbox (default 256; 0 = one launch per
- * round). Unknown names -> DGKR_INVALID_ARGUMENT. */
+ * round), "tail_timeout_us" = how long that launch waits for a challenge
+ * before it hands the remaining rounds back to per-round launches (default
+ * 20000; a profiler that serialises launches hits it once per sum-check).
+ * Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);
 

@@ -111,6 +111,7 @@ class Profile_t(C.Structure):
         ("fold_ms", C.c_double),
         ("tail_ms", C.c_double),
         ("tail_rounds", C.c_uint64),
+        ("tail_aborts", C.c_uint64),
     ]
 
     def as_dict(self):

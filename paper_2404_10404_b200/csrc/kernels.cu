@@ -434,6 +434,8 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
                 }
                 if (globaltimer_ns() - t0 > t.timeout_ns) {
                     stop = 1;
+                    mb->abort_round = static_cast<std::uint32_t>(j);
+                    __threadfence_system();
                     mb->d_seq = kTailAbort;
                     break;
                 }
@@ -454,6 +456,11 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
     // final fold of the 2-element tables with the last challenge
     for (int tb = threadIdx.x; tb < t.ntab; tb += blockDim.x)
         fe_store(t.fin[tb], fold1<F>(fe_ldcg(rp.in[tb]), fe_ldcg(rp.in[tb] + 1), rp.k.r));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        mb->d_seq = t.tag | static_cast<std::uint32_t>(t.nv + 1);  // no host fallback needed
+    }
 }
 
 template <class F>
@@ -1608,7 +1615,7 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0, 0, 1, kSmallRoundPairs};  // fused round 1, interleaved absorbs: measured slower on C2
+        Tuning v{kSmallRoundPairs, 0, 0, 1, kSmallRoundPairs, kTailTimeoutUs};  // fused round 1, interleaved absorbs: measured slower on C2
         if (const char* e = std::getenv("DGKR_ABSORB_CHAINS")) v.absorb_chains = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);

@@ -78,8 +78,10 @@ constexpr std::uint64_t kSmallRoundPairs = 256;
 /// side posts a tag (generation << 8 | round) after its payload and waits
 /// for the other side's tag of the same round.
 struct alignas(128) TailMailbox {
-    volatile std::uint32_t d_seq;  // device -> host: sums of round (d_seq & 255) posted; kTailAbort on timeout
-    std::uint32_t pad0[31];
+    volatile std::uint32_t d_seq;  // device -> host: sums of round (d_seq & 255) posted (nv + 1: finals
+                                   // folded); kTailAbort when the CTA gave up waiting
+    volatile std::uint32_t abort_round;  // with kTailAbort: the round whose challenge it waited for
+    std::uint32_t pad0[30];
     std::uint32_t sums[3][8];      // (S0, S1, S2) or (S0, S2), Montgomery form
     std::uint32_t pad1[8];
     volatile std::uint32_t h_seq;  // host -> device: fold constants of the challenge of round (h_seq & 255) posted
@@ -87,6 +89,11 @@ struct alignas(128) TailMailbox {
     std::uint8_t k[kFoldConstBytes];  // FoldConst of that challenge
 };
 constexpr std::uint32_t kTailAbort = 0xffffffffu;
+/// how long the tail CTA waits for a challenge before it gives up (the host
+/// then runs the remaining rounds as per-round launches): long against the
+/// host's microseconds per round, short enough that a profiler serialising
+/// launches (the host cannot answer while the kernel runs) costs little
+constexpr std::uint64_t kTailTimeoutUs = 20000;
 
 /// The last rounds of a sum-check (round j0..nv, every one with <=
 /// tuning().tail_pairs output pairs) and the final fold in ONE launch of one
@@ -96,7 +103,8 @@ constexpr std::uint32_t kTailAbort = 0xffffffffu;
 /// (unused when j0 == 1). Tables ping-pong in A/B exactly like the
 /// per-round launches (round j writes A when j is even), finals go to fin.
 /// The kernel gives up after timeout_ns without a host answer (posts
-/// kTailAbort and exits).
+/// abort_round and kTailAbort and exits); after the final fold it posts
+/// tag | (nv + 1).
 struct TailLaunch {
     const Fe* const* in = nullptr;
     Fe* const* buf_a = nullptr;
@@ -124,6 +132,7 @@ struct Tuning {
     std::uint64_t fuse_round1;  // bookkeeping with round 1 fused (k_bookkeep_pairs) where it applies
     std::uint64_t absorb_chains;  // output absorbs interleaved per host thread in a proof stream (1..4)
     std::uint64_t tail_pairs;     // rounds of <= tail_pairs output pairs run in one mailbox launch (0: off)
+    std::uint64_t tail_timeout_us;  // the tail CTA's wait for a challenge before it hands back to the host
 };
 Tuning& tuning();
 

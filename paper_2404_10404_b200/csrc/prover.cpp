@@ -226,7 +226,16 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         if (j == 1 && r1_done) j = 2;
         if (j <= nv) j_tail = j;
     }
-    for (int j = 1; j < j_tail; ++j) {
+    // one round as its own launch + sums readback (the path for large rounds,
+    // distributed rounds, and the rounds after a tail launch gave up)
+    auto buffer_after = [&](int j) -> const Fe* const* {  // tables as round j left them
+        return j >= 2 ? ((j % 2 == 0) ? rb.A() : rb.B()) : base;
+    };
+    auto buffer_after_h = [&](int j) -> const Fe* const* {
+        if (!base_host) return nullptr;
+        return j >= 2 ? ((j % 2 == 0) ? rb.hA() : rb.hB()) : base_host;
+    };
+    auto launch_round_j = [&](int j) {
         RoundLaunch rl;
         rl.np = np;
         rl.has_g = has_g;
@@ -242,7 +251,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             rl.mode = (j == 2) ? 1 : 2;  // fold natural -> bit-reversed, then bit-reversed -> bit-reversed
             rl.in = cur;
             rl.in_host = cur_h;
-            const Fe* const* nxt = (j % 2 == 0) ? rb.A() : rb.B();
+            const Fe* const* nxt = buffer_after(j);
             const Fe* const* nxt_h = (j % 2 == 0) ? rb.hA() : rb.hB();
             rl.out = const_cast<Fe* const*>(nxt);
             rl.out_host = cur_h ? const_cast<Fe* const*>(nxt_h) : nullptr;
@@ -287,7 +296,9 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         const U256 r = host_round();
         ctx->h_small[0] = to_fe(r);
         ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
-    }
+    };
+    for (int j = 1; j < j_tail; ++j) launch_round_j(j);
+    bool tail_folded = false;  // the tail launch wrote the finals
     if (j_tail <= n_rounds) {
         TailMailbox* mb = ctx->tail_mb;
         ctx->tail_gen = ctx->tail_gen % 0xfffffeu + 1;  // tags never 0 nor kTailAbort
@@ -305,7 +316,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         tl.fold_const = fk;
         tl.mb = ctx->tail_mb_dev;
         tl.tag = tag;
-        tl.timeout_ns = 30ull * 1000 * 1000 * 1000;
+        tl.timeout_ns = tuning().tail_timeout_us * 1000;
         std::uint32_t* d_seq = const_cast<std::uint32_t*>(&mb->d_seq);
         std::uint32_t* h_seq = const_cast<std::uint32_t*>(&mb->h_seq);
         __atomic_store_n(d_seq, 0u, __ATOMIC_RELEASE);
@@ -313,21 +324,48 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
         ctx->tbeg();
         launch_round_tail(kind, tl, ctx->st);
         ctx->launched();
+        // If the CTA gives up waiting for a challenge (the host thread was
+        // descheduled, or a profiler serialises launches so the host cannot
+        // answer while the kernel runs), the rounds it did not finish run as
+        // per-round launches from where it stopped: same tables, same bytes.
+        int resume = 0;
         try {
-            for (int j = j_tail; j <= nv; ++j) {
+            for (int j = j_tail; j <= nv + 1; ++j) {  // j = nv + 1: the final fold's acknowledgement
                 const std::uint32_t want = tag | static_cast<std::uint32_t>(j);
                 const double t0 = now_ms();
+                std::uint32_t v = 0;
                 for (std::uint32_t spin = 1;; ++spin) {
-                    const std::uint32_t v = __atomic_load_n(d_seq, __ATOMIC_ACQUIRE);
-                    if (v == want) break;
-                    if (v == kTailAbort) fail(DGKR_CUDA_ERROR, "sum-check tail kernel timed out waiting for the host");
+                    v = __atomic_load_n(d_seq, __ATOMIC_ACQUIRE);
+                    if (v == want || v == kTailAbort) break;
                     if ((spin & 4095) == 0) {
                         const cudaError_t q = cudaStreamQuery(ctx->st);
                         if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
-                        if (q == cudaSuccess && __atomic_load_n(d_seq, __ATOMIC_ACQUIRE) != want)
-                            fail(DGKR_CUDA_ERROR, "sum-check tail kernel ended without posting round sums");
-                        if (now_ms() - t0 > 60e3) fail(DGKR_CUDA_ERROR, "sum-check tail kernel: no round sums in 60 s");
+                        v = __atomic_load_n(d_seq, __ATOMIC_ACQUIRE);
+                        if (v == want || v == kTailAbort) break;
+                        if (q == cudaSuccess) fail(DGKR_CUDA_ERROR, "sum-check tail kernel ended without posting");
+                        if (now_ms() - t0 > 60e3) fail(DGKR_CUDA_ERROR, "sum-check tail kernel: no post in 60 s");
                     }
+                }
+                if (v == kTailAbort) {
+                    const int ar = static_cast<int>(__atomic_load_n(const_cast<std::uint32_t*>(&mb->abort_round),
+                                                                    __ATOMIC_ACQUIRE));
+                    if (ar == j && j <= nv) {  // round j's sums are posted; its challenge was not taken
+                        std::memcpy(ctx->h_small + 1, mb->sums, nres * sizeof(Fe));
+                        const U256 r = host_round();
+                        ctx->h_small[0] = to_fe(r);
+                        ctx->h2d(d_r, ctx->h_small, sizeof(Fe));
+                        resume = j + 1;
+                    } else if (ar == j - 1) {  // stopped before round j
+                        resume = j;
+                    } else {
+                        fail(DGKR_LOGIC_ERROR, "sum-check tail: inconsistent abort round");
+                    }
+                    ctx->prof.tail_aborts += 1;
+                    break;
+                }
+                if (j == nv + 1) {
+                    tail_folded = true;
+                    break;
                 }
                 std::memcpy(ctx->h_small + 1, mb->sums, nres * sizeof(Fe));
                 const U256 r = host_round();
@@ -343,7 +381,14 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
             throw;
         }
         ctx->tend(ctx->prof.tail_ms);
-        ctx->prof.tail_rounds += static_cast<std::uint64_t>(nv - j_tail + 1);
+        if (resume) {
+            cur = buffer_after(resume - 1);
+            cur_h = buffer_after_h(resume - 1);
+            ctx->prof.tail_rounds += static_cast<std::uint64_t>(resume - j_tail);
+            for (int j = resume; j <= nv; ++j) launch_round_j(j);
+        } else {
+            ctx->prof.tail_rounds += static_cast<std::uint64_t>(nv - j_tail + 1);
+        }
     }
     out.claim_end = run_claim;
     if (n_rounds < nv) {
@@ -372,7 +417,7 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
     }
     // final fold of the 2-element tables (or read the 1-element tables)
     if (nv >= 1) {
-        if (j_tail > nv) {  // else the tail kernel folded them
+        if (!tail_folded) {
             launch_fold_final(kind, cur, const_cast<Fe* const*>(rb.F()), ntab, d_r, ctx->st);
             ctx->launched();
         }
@@ -2783,6 +2828,7 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         else if (n == "tma_min_pairs") tuning().tma_min_pairs = value;
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
         else if (n == "tail_pairs") tuning().tail_pairs = value;
+        else if (n == "tail_timeout_us") tuning().tail_timeout_us = value;
         else if (n == "absorb_chains") {
             if (value < 1 || value > 4) fail(DGKR_INVALID_ARGUMENT, "absorb_chains must be 1..4");
             tuning().absorb_chains = value;
@@ -2798,6 +2844,7 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         else if (n == "tma_min_pairs") *value = tuning().tma_min_pairs;
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
         else if (n == "tail_pairs") *value = tuning().tail_pairs;
+        else if (n == "tail_timeout_us") *value = tuning().tail_timeout_us;
         else if (n == "absorb_chains") *value = tuning().absorb_chains;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });

@@ -112,3 +112,52 @@ def test_tail_stream_lanes(ctx, tail_knob):
         singles.append(P.gkr_prove(ctx, circ, x, tr))
     trs = [P.Transcript(f, "tail.lanes") for _ in ins]
     assert P.gkr_prove_batch(ctx, circ, ins, trs) == singles
+
+
+@pytest.fixture
+def timeout_knob():
+    old = P.get_tuning("tail_timeout_us")
+    yield lambda v: P.set_tuning("tail_timeout_us", v)
+    P.set_tuning("tail_timeout_us", old)
+
+
+@pytest.mark.parametrize("timeout_us", [0, 1, 5])
+@pytest.mark.parametrize("p", [O.BN254_P, 97])
+def test_tail_gives_up_and_host_finishes(ctx, tail_knob, timeout_knob, timeout_us, p):
+    """A tail CTA that stops waiting for the host (here: a timeout of 0-5 us,
+    so it gives up at varying rounds, before or after posting sums) hands the
+    remaining rounds and the final fold back to per-round launches; proofs
+    stay byte-identical and the profile counts the hand-backs."""
+    f = P.Field(p)
+    insz, flat = W.layered_circuit(808, 10, 3)
+    copies = 4
+    inputs = W.random_inputs(f.p, insz * copies, 12)
+    circ = P.Circuit(ctx, insz, *flat, n_copies=copies)
+    tail_knob(0)
+    tr = P.Transcript(f, "tail.abort")
+    want = P.gkr_prove(ctx, circ, inputs, tr)
+    for tp in (256, 1 << 22):
+        tail_knob(tp)
+        timeout_knob(timeout_us)
+        ctx.set_profile(True)
+        tr2 = P.Transcript(f, "tail.abort")
+        got = P.gkr_prove(ctx, circ, inputs, tr2)
+        prof = ctx.profile()
+        ctx.set_profile(False)
+        timeout_knob(20000)
+        assert got == want and tr2.state == tr.state
+        if timeout_us == 0:
+            assert prof["tail_aborts"] > 0
+
+
+def test_tail_profile_counts(ctx, tail_knob):
+    f = P.Field.bn254()
+    insz, flat = W.layered_circuit(909, 10, 2)
+    circ = P.Circuit(ctx, insz, *flat, n_copies=2)
+    inputs = W.random_inputs(f.p, insz * 2, 1)
+    tail_knob(256)
+    ctx.set_profile(True)
+    P.gkr_prove(ctx, circ, inputs, P.Transcript(f, "tail.prof"))
+    prof = ctx.profile()
+    ctx.set_profile(False)
+    assert prof["tail_rounds"] > 0 and prof["tail_aborts"] == 0 and prof["tail_ms"] > 0
