@@ -304,7 +304,9 @@ int dgkr_bench_mul_peak(dgkr_ctx* ctx, double* mults_per_s);
  * host through a mapped-memory mailbox (default 256; 0 = one launch per
  * round), "tail_timeout_us" = how long that launch waits for a challenge
  * before it hands the remaining rounds back to per-round launches (default
- * 20000; a profiler that serialises launches hits it once per sum-check).
+ * 20000; a profiler that serialises launches hits it once per sum-check),
+ * "spin_yield" = 1 makes host threads waiting on the GPU yield their core
+ * between polls (default 0: measured no faster).
  * Unknown names -> DGKR_INVALID_ARGUMENT. */
 int dgkr_set_tuning(const char* name, uint64_t value);
 int dgkr_get_tuning(const char* name, uint64_t* value);

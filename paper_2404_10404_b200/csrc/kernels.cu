@@ -1615,12 +1615,13 @@ Tuning& tuning() {
     static Tuning t = [] {
         // the TMA-staged round kernel measured slower than k_round on C2
         // (DESIGN.md §11), so it is off unless asked for
-        Tuning v{kSmallRoundPairs, 0, 0, 1, kSmallRoundPairs, kTailTimeoutUs};  // fused round 1, interleaved absorbs: measured slower on C2
+        Tuning v{kSmallRoundPairs, 0, 0, 1, kSmallRoundPairs, kTailTimeoutUs, 0};  // fused round 1, interleaved absorbs: measured slower on C2
         if (const char* e = std::getenv("DGKR_ABSORB_CHAINS")) v.absorb_chains = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_SMALL_PAIRS")) v.small_round_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_FUSE_ROUND1")) v.fuse_round1 = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TMA_MIN_PAIRS")) v.tma_min_pairs = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("DGKR_TAIL_PAIRS")) v.tail_pairs = std::strtoull(e, nullptr, 10);
+        if (const char* e = std::getenv("DGKR_SPIN_YIELD")) v.spin_yield = std::strtoull(e, nullptr, 10);
         return v;
     }();
     return t;

@@ -133,6 +133,7 @@ struct Tuning {
     std::uint64_t absorb_chains;  // output absorbs interleaved per host thread in a proof stream (1..4)
     std::uint64_t tail_pairs;     // rounds of <= tail_pairs output pairs run in one mailbox launch (0: off)
     std::uint64_t tail_timeout_us;  // the tail CTA's wait for a challenge before it hands back to the host
+    std::uint64_t spin_yield;       // host threads waiting on the GPU yield their core between polls
 };
 Tuning& tuning();
 

@@ -9,6 +9,7 @@
 #include <array>
 #include <cstdlib>
 #include <cstring>
+#include <sched.h>
 #include <memory>
 #include <set>
 #include <string>
@@ -334,9 +335,12 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
                 const std::uint32_t want = tag | static_cast<std::uint32_t>(j);
                 const double t0 = now_ms();
                 std::uint32_t v = 0;
+                const bool yield = tuning().spin_yield != 0;
                 for (std::uint32_t spin = 1;; ++spin) {
                     v = __atomic_load_n(d_seq, __ATOMIC_ACQUIRE);
                     if (v == want || v == kTailAbort) break;
+                    __builtin_ia32_pause();
+                    if (yield && (spin & 31) == 0) sched_yield();
                     if ((spin & 4095) == 0) {
                         const cudaError_t q = cudaStreamQuery(ctx->st);
                         if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
@@ -2829,6 +2833,7 @@ int dgkr_set_tuning(const char* name, std::uint64_t value) {
         else if (n == "fuse_round1") tuning().fuse_round1 = value;
         else if (n == "tail_pairs") tuning().tail_pairs = value;
         else if (n == "tail_timeout_us") tuning().tail_timeout_us = value;
+        else if (n == "spin_yield") tuning().spin_yield = value;
         else if (n == "absorb_chains") {
             if (value < 1 || value > 4) fail(DGKR_INVALID_ARGUMENT, "absorb_chains must be 1..4");
             tuning().absorb_chains = value;
@@ -2845,6 +2850,7 @@ int dgkr_get_tuning(const char* name, std::uint64_t* value) {
         else if (n == "fuse_round1") *value = tuning().fuse_round1;
         else if (n == "tail_pairs") *value = tuning().tail_pairs;
         else if (n == "tail_timeout_us") *value = tuning().tail_timeout_us;
+        else if (n == "spin_yield") *value = tuning().spin_yield;
         else if (n == "absorb_chains") *value = tuning().absorb_chains;
         else fail(DGKR_INVALID_ARGUMENT, "unknown tuning knob: " + n);
     });

@@ -2,6 +2,8 @@
 // ext.cpp): error guard, device buffers, field handle, lanes (stream +
 // workspace + pinned staging), the context, and the communicator interface.
 #pragma once
+
+#include <sched.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <fcntl.h>
@@ -407,6 +409,7 @@ struct Lane {
             if (q == cudaSuccess) return;
             if (q != cudaErrorNotReady) CK(q);
             if (now_ms() - t0 > spin_ms) break;
+            if (tuning().spin_yield) sched_yield();  // leave the core to a lane running its transcript
         }
         CK(cudaEventSynchronize(ev_sync));
     }
