@@ -7,7 +7,9 @@ byte for byte, over three families (a GPU box with oracle/_ref built):
   * general circuits over the runtime-modulus path (p = 97, Goldilocks) and
     the wide path (255- and 256-bit primes);
   * the distributed prover (emulated ranks 2/4/8) against the single proof;
-  * pcs commit roots and openings (M rows, random sizes, BN254/Goldilocks).
+  * pcs commit roots and openings (M rows, random sizes, BN254/Goldilocks);
+  every third general circuit runs with a random sum-check tail threshold and
+  hand-back timeout (the mailbox tail launch and its fallback).
 usage: python tools/fuzz_parity.py [general_cases] [layered_cases] [seconds]
 Prints one line per family and exits 1 on any mismatch."""
 import os
@@ -45,7 +47,16 @@ def general(fld, cases, tag):
         c = R.random_general_circuit(7000 + seed, insz, depth, 24, 3)
         inputs = O.random_elements(fld, insz, rng)
         want, _ = R.gkr_prove(fld, tag, [seed], c, inputs)
-        got = P.gkr_prove(ctx, P.Circuit.from_oracle(ctx, c), inputs, P.Transcript(f, tag, [seed]))
+        # every third circuit: a random tail threshold and hand-back timeout
+        # (0-5 us makes the tail launch give up at varying rounds)
+        if seed % 3 == 2:
+            P.set_tuning("tail_pairs", [0, 1, 4, 256, 1 << 22][seed % 5])
+            P.set_tuning("tail_timeout_us", [0, 2, 5, 20000][seed % 4])
+        try:
+            got = P.gkr_prove(ctx, P.Circuit.from_oracle(ctx, c), inputs, P.Transcript(f, tag, [seed]))
+        finally:
+            P.set_tuning("tail_pairs", 256)
+            P.set_tuning("tail_timeout_us", 20000)
         if got != want:
             bad += 1
             print(f"MISMATCH {tag} p={fld.p} seed {seed}", flush=True)
