@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
                 }
                 if (globaltimer_ns() - t0 > t.timeout_ns) {
                     stop = 1;
-                    mb->abort_round = static_cast<std::uint32_t>(j);
+                    mb->abort_round = t.tag | static_cast<std::uint32_t>(j);
                     __threadfence_system();
                     mb->d_seq = kTailAbort;
                     break;

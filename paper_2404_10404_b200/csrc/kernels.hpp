@@ -80,7 +80,7 @@ constexpr std::uint64_t kSmallRoundPairs = 256;
 struct alignas(128) TailMailbox {
     volatile std::uint32_t d_seq;  // device -> host: sums of round (d_seq & 255) posted (nv + 1: finals
                                    // folded); kTailAbort when the CTA gave up waiting
-    volatile std::uint32_t abort_round;  // with kTailAbort: the round whose challenge it waited for
+    volatile std::uint32_t abort_round;  // with kTailAbort: tag | the round whose challenge it waited for
     std::uint32_t pad0[30];
     std::uint32_t sums[3][8];      // (S0, S1, S2) or (S0, S2), Montgomery form
     std::uint32_t pad1[8];

@@ -351,8 +351,10 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
                     }
                 }
                 if (v == kTailAbort) {
-                    const int ar = static_cast<int>(__atomic_load_n(const_cast<std::uint32_t*>(&mb->abort_round),
-                                                                    __ATOMIC_ACQUIRE));
+                    const std::uint32_t at = __atomic_load_n(const_cast<std::uint32_t*>(&mb->abort_round),
+                                                             __ATOMIC_ACQUIRE);
+                    if ((at & ~0xffu) != tag) fail(DGKR_LOGIC_ERROR, "sum-check tail: abort of another launch");
+                    const int ar = static_cast<int>(at & 0xffu);
                     if (ar == j && j <= nv) {  // round j's sums are posted; its challenge was not taken
                         std::memcpy(ctx->h_small + 1, mb->sums, nres * sizeof(Fe));
                         const U256 r = host_round();
@@ -381,7 +383,9 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
                 }
             }
         } catch (...) {
-            __atomic_store_n(h_seq, kTailAbort, __ATOMIC_RELEASE);  // release the CTA
+            // release the CTA and let it exit before the mailbox is reused
+            __atomic_store_n(h_seq, kTailAbort, __ATOMIC_RELEASE);
+            (void)cudaStreamSynchronize(ctx->st);
             throw;
         }
         ctx->tend(ctx->prof.tail_ms);
