@@ -2,6 +2,7 @@
 declares, and its host-side pieces (SHA-256, transcript, field encoding)
 match the oracle. No GPU compute is called here."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -136,3 +137,24 @@ def test_absorb_multi_equals_separate_chains(k, n, threads):
     check(lib().dgkr_transcript_absorb_elems_multi(f.handle, tptr, C.c_size_t(k), eptr, C.c_size_t(n),
                                                    C.c_int(threads)))
     assert [bytes(t.state) for t in ts] == want
+
+
+@pytest.mark.parametrize("knob,default", [("small_round_pairs", 256), ("tma_min_pairs", 0), ("fuse_round1", 0),
+                                          ("absorb_chains", 1), ("tail_pairs", 256), ("tail_timeout_us", 20000),
+                                          ("spin_yield", 0)])
+def test_tuning_knobs_roundtrip(knob, default):
+    """Launch knobs are process-wide host state (no GPU involved): defaults,
+    set/get round trip, and the reference-style error for unknown names."""
+    for env in ("DGKR_SMALL_PAIRS", "DGKR_TMA_MIN_PAIRS", "DGKR_FUSE_ROUND1", "DGKR_ABSORB_CHAINS",
+                "DGKR_TAIL_PAIRS", "DGKR_SPIN_YIELD"):
+        if env in os.environ:
+            pytest.skip(f"{env} overrides the default")
+    old = P.get_tuning(knob)
+    assert old == default
+    try:
+        P.set_tuning(knob, 3 if knob == "absorb_chains" else 7)
+        assert P.get_tuning(knob) == (3 if knob == "absorb_chains" else 7)
+    finally:
+        P.set_tuning(knob, old)
+    with pytest.raises(InvalidArgument):
+        P.set_tuning(knob + "_typo", 1)
