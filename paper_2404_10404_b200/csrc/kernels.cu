@@ -365,6 +365,11 @@ __global__ void k_fold_final(const Fe* const* in, Fe* const* out, int n_tabs, co
 // round trip (launch, d2h of the sums, stream sync, h2d of the challenge)
 // becomes a pinned-memory mailbox exchange with a resident CTA.
 // ---------------------------------------------------------------------------
+#ifndef DGKR_TAIL_SPLIT
+#define DGKR_TAIL_SPLIT 1
+#endif
+constexpr bool kTailSplit = DGKR_TAIL_SPLIT;
+
 struct TailParams {
     const Fe* const* in;
     Fe* const* buf_a;
@@ -384,6 +389,39 @@ __device__ __forceinline__ std::uint64_t globaltimer_ns() {
     std::uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// A tail round of a layer sum-check (np = 1 with G) on small tables with one
+// pair index spread over 4 lanes: lane q = 0 / 1 / 2 folds f / g / G, the
+// f and g lanes swap their outputs and take one product each, so the
+// per-round critical path is 2 folds + 1 product instead of 6 + 2 (these
+// rounds are latency-bound: a few dozen pairs on one CTA).
+// All 32 lanes of a warp must call it (shuffles); lanes past the last pair
+// pass active = false and contribute nothing.
+template <class F, int MODE, bool S1>
+__device__ __forceinline__ void round_body_split4(const RoundParams& a, std::uint64_t i, int q, bool active,
+                                                  Fe (&s)[S1 ? 3 : 2]) {
+    constexpr int NS = S1 ? 3 : 2;
+    Fe x0 = fe_zero(), x1 = fe_zero();
+    if (active && q < 3)
+        load_pair<F, MODE, true>(a.in[q], MODE != kScan ? a.out[q] : nullptr, i, a.n_out_pairs, a.log_p, a.k, x0,
+                                 x1);
+    Fe y0, y1;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        y0.v[w] = __shfl_xor_sync(0xffffffffu, x0.v[w], 1);
+        y1.v[w] = __shfl_xor_sync(0xffffffffu, x1.v[w], 1);
+    }
+    if (!active) return;
+    if (q == 0) {  // f0 g0 (and f1 g1)
+        sum_prod<F>(s[0], x0, y0);
+        if constexpr (S1) sum_prod<F>(s[1], x1, y1);
+    } else if (q == 1) {  // (g1 - g0)(f1 - f0)
+        sum_prod<F>(s[NS - 1], fe_sub_lazy<F>(x1, x0), fe_sub_lazy<F>(y1, y0));
+    } else if (q == 2) {  // G0 (and G1)
+        sum_val<F>(s[0], x0);
+        if constexpr (S1) sum_val<F>(s[1], x1);
+    }
 }
 
 template <class F, int NP, bool HAS_G, bool S1>
@@ -410,10 +448,19 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
         Fe s[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) s[k] = fe_zero();
-        for (std::uint64_t i = threadIdx.x; i < rp.n_out_pairs; i += blockDim.x) {
-            if (j == 1) round_body<F, NP, HAS_G, kScan, S1, Fe, true>(rp, i, s);
-            else if (j == 2) round_body<F, NP, HAS_G, kFoldNat, S1, Fe, true>(rp, i, s);
-            else round_body<F, NP, HAS_G, kFoldRev, S1, Fe, true>(rp, i, s);
+        if (NP == 1 && HAS_G && kTailSplit && 4 * rp.n_out_pairs <= blockDim.x) {
+            const std::uint64_t i = threadIdx.x >> 2;
+            const int q = threadIdx.x & 3;
+            const bool active = i < rp.n_out_pairs;
+            if (j == 1) round_body_split4<F, kScan, S1>(rp, i, q, active, s);
+            else if (j == 2) round_body_split4<F, kFoldNat, S1>(rp, i, q, active, s);
+            else round_body_split4<F, kFoldRev, S1>(rp, i, q, active, s);
+        } else {
+            for (std::uint64_t i = threadIdx.x; i < rp.n_out_pairs; i += blockDim.x) {
+                if (j == 1) round_body<F, NP, HAS_G, kScan, S1, Fe, true>(rp, i, s);
+                else if (j == 2) round_body<F, NP, HAS_G, kFoldNat, S1, Fe, true>(rp, i, s);
+                else round_body<F, NP, HAS_G, kFoldRev, S1, Fe, true>(rp, i, s);
+            }
         }
         block_sum<F, NS>(s, sh);
         if (threadIdx.x == 0) {
