@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
     __shared__ RoundParams rp;
     __shared__ int stop;
     TailMailbox* mb = t.mb;
+    std::uint64_t diag_start = globaltimer_ns(), diag_mark = diag_start, diag_wait = 0, diag_post = 0;
     if (threadIdx.x == 0) {
         rp.in = t.in;
         rp.out = nullptr;
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
             mb->d_seq = t.tag | static_cast<std::uint32_t>(j);
             // the challenge of round j (its fold constants drive round j + 1 / the final fold)
             const std::uint64_t t0 = globaltimer_ns();
+            diag_post += t0 - diag_mark;
             for (;;) {
                 const std::uint32_t h = mb->h_seq;
                 if (h == (t.tag | static_cast<std::uint32_t>(j))) break;
@@ -488,6 +490,8 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
                 }
             }
             __threadfence_system();  // acquire: the payload reads below see the host's writes
+            diag_mark = globaltimer_ns();
+            diag_wait += diag_mark - t0;
         }
         __syncthreads();
         if (stop) return;
@@ -505,6 +509,10 @@ __global__ void __launch_bounds__(kThreads) k_round_tail(const __grid_constant__
         fe_store(t.fin[tb], fold1<F>(fe_ldcg(rp.in[tb]), fe_ldcg(rp.in[tb] + 1), rp.k.r));
     __syncthreads();
     if (threadIdx.x == 0) {
+        volatile std::uint64_t* dg = mb->diag;
+        dg[0] = diag_wait;
+        dg[1] = diag_post;
+        dg[2] = globaltimer_ns() - diag_start;
         __threadfence_system();
         mb->d_seq = t.tag | static_cast<std::uint32_t>(t.nv + 1);  // no host fallback needed
     }

@@ -83,7 +83,7 @@ struct alignas(128) TailMailbox {
     volatile std::uint32_t abort_round;  // with kTailAbort: tag | the round whose challenge it waited for
     std::uint32_t pad0[30];
     std::uint32_t sums[3][8];      // (S0, S1, S2) or (S0, S2), Montgomery form
-    std::uint32_t pad1[8];
+    std::uint64_t diag[4];         // the launch's device time (ns): waiting for the host, computing + posting, total
     volatile std::uint32_t h_seq;  // host -> device: fold constants of the challenge of round (h_seq & 255) posted
     std::uint32_t pad2[31];
     std::uint8_t k[kFoldConstBytes];  // FoldConst of that challenge

@@ -371,6 +371,13 @@ SumcheckRun run_rounds(Lane* ctx, const dgkr_field* f, int np, bool has_g, int n
                 }
                 if (j == nv + 1) {
                     tail_folded = true;
+                    // DGKR_TAIL_DIAG=1: print the launch's device-side time split to stderr
+                    static const bool diag = std::getenv("DGKR_TAIL_DIAG") != nullptr;
+                    if (diag) {
+                        const volatile std::uint64_t* d = mb->diag;
+                        std::fprintf(stderr, "tail diag: rounds %d wait %.1f us compute+post %.1f us kernel %.1f us\n",
+                                     nv - j_tail + 1, d[0] * 1e-3, d[1] * 1e-3, d[2] * 1e-3);
+                    }
                     break;
                 }
                 std::memcpy(ctx->h_small + 1, mb->sums, nres * sizeof(Fe));
