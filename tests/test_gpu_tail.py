@@ -6,6 +6,8 @@ mapped-memory mailbox. Whatever the threshold -- 0 (a launch per round), 1,
 round 1 (scan, natural fold and bit-reversed folds all inside the kernel) --
 proofs and transcripts must be byte-identical to the compiled reference and
 the Python oracle, on BN254, Goldilocks, p = 97 and a 255-bit modulus."""
+import os
+
 import numpy as np
 import pytest
 
@@ -160,4 +162,9 @@ def test_tail_profile_counts(ctx, tail_knob):
     P.gkr_prove(ctx, circ, inputs, P.Transcript(f, "tail.prof"))
     prof = ctx.profile()
     ctx.set_profile(False)
-    assert prof["tail_rounds"] > 0 and prof["tail_aborts"] == 0 and prof["tail_ms"] > 0
+    assert prof["tail_rounds"] > 0 and prof["tail_ms"] > 0
+    # a tool that serialises launches (ncu, a tracer) keeps the host from
+    # answering while the kernel runs: then every tail launch hands back
+    traced = any(k in os.environ for k in ("CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+    if not traced:
+        assert prof["tail_aborts"] == 0
