@@ -82,7 +82,7 @@ typedef struct dgkr_profile {
 } dgkr_profile;
 
 const char* dgkr_last_error(void);
-int dgkr_abi_version(void); /* 2 */
+int dgkr_abi_version(void); /* 3 (round 2: dgkr_profile grew the tail_* fields) */
 
 /* ---- field (field.hpp:23-80) ------------------------------------------- */
 /* modulus: little-endian bytes. The GPU path supports any odd p < 2^256

@@ -1608,7 +1608,7 @@ std::size_t plan_clusters(std::size_t n, std::size_t k) {
 extern "C" {
 
 const char* dgkr_last_error(void) { return g_err.c_str(); }
-int dgkr_abi_version(void) { return 2; }
+int dgkr_abi_version(void) { return 3; }  // 3: dgkr_profile gained tail_ms / tail_rounds / tail_aborts
 
 int dgkr_field_create(const std::uint8_t* mod, std::size_t len, dgkr_field** out) {
     return guard([&] {

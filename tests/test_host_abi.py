@@ -21,7 +21,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_abi_version():
-    assert lib().dgkr_abi_version() == 2
+    assert lib().dgkr_abi_version() == 3
 
 
 @pytest.mark.parametrize("n", [0, 1, 3, 55, 56, 63, 64, 65, 119, 120, 1000])
